@@ -1,0 +1,188 @@
+/*
+ * vqb200.h -- C ABI of libvqb200.so, the B200 (sm_100a) LBG vector
+ * quantisation hot path.  Drop-in for the reference arxiv/paper_0910_4711
+ * (package vqkit, pure Python + numba).
+ *
+ * The reference has no C ABI: its drop-in seam is the module object
+ * vqkit._kernels, which every caller looks up by attribute at call time
+ * (core.py:20,244,258,271,315-316,338,380,392-393,402,421-422;
+ * parallel.py:22,114,121,190,273,290,316,321; codec.py:11,89,154-155).
+ * Two surfaces are exported:
+ *
+ *  1. Kernel surface (stateless, HOST buffers, same argument meaning as
+ *     vqkit._kernels): vqb_assign_range, vqb_update_rows, vqb_column_sums,
+ *     vqb_sum_inorder, vqb_pair_distance.  A ctypes shim can rebind the
+ *     reference's _kernels attributes to these.
+ *
+ *  2. Session surface (device-resident training set): vqb_open / vqb_train /
+ *     vqb_assign / vqb_update / vqb_close, replacing the reference's entry
+ *     points lbg_train (core.py:366-430), parallel_lbg_train
+ *     (parallel.py:256-329), assign_cells (core.py:292-316), update_codebook
+ *     (core.py:319-339) and encode (codec.py:62-93) without moving the
+ *     training set over PCIe on every pass.  The vqb_step_* calls expose one
+ *     Lloyd pass at a time for the multi-GPU loop (one process per GPU, the
+ *     caller allreduces the packed int64 exchange buffer over NCCL).
+ *
+ * Conventions.
+ *  - Status codes mirror the reference's exception hierarchy (errors.py:8-29):
+ *    0 ok, 1 UsageError, 2 ConfigError, 3 DomainError, 4 InternalError
+ *    (CUDA failures included).  vqb_last_error() returns the message of the
+ *    calling thread's last failure.
+ *  - Host buffers are caller-owned; device memory is owned by the session.
+ *  - Every call is synchronous on return unless its name says `step` / `async`.
+ *  - Metric codes: 0 squared_euclidean, 1 euclidean (_kernels.py:14-15).
+ *  - No CPU fallback: without a CUDA device every compute call returns 4.
+ */
+#ifndef VQB200_H
+#define VQB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VQB_OK 0
+#define VQB_USAGE 1
+#define VQB_CONFIG 2
+#define VQB_DOMAIN 3
+#define VQB_INTERNAL 4
+
+const char* vqb_last_error(void);
+int vqb_version(void);
+int vqb_device_count(int* count);
+
+/* ---- kernel surface: replaces vqkit._kernels (_kernels.py:18-98) ---- */
+
+/* _kernels.assign_range (_kernels.py:18-36): rows [start, stop) of
+ * vectors[m][dim] against codebook[size][dim]; writes out_cells[z] (int64)
+ * and out_dists[z] (FP64, sqrt'ed under metric 1) for z in [start, stop). */
+int vqb_assign_range(const double* vectors, int64_t m, int64_t dim, const double* codebook,
+                     int64_t size, int64_t start, int64_t stop, int metric,
+                     int64_t* out_cells, double* out_dists);
+
+/* _kernels.update_rows (_kernels.py:39-66): centroids of codevector rows
+ * i with i % stride == worker; empty rows copy old_codebook.  Other rows of
+ * out_codebook / out_counts are left untouched. */
+int vqb_update_rows(const double* vectors, int64_t m, int64_t dim, const int64_t* cells,
+                    const double* old_codebook, int64_t size, int64_t worker, int64_t stride,
+                    double* out_codebook, int64_t* out_counts);
+
+/* _kernels.column_sums (_kernels.py:81-89), ascending row order. */
+int vqb_column_sums(const double* vectors, int64_t m, int64_t dim, double* out);
+
+/* _kernels.sum_inorder (_kernels.py:92-98), strict left-to-right. */
+int vqb_sum_inorder(const double* values, int64_t n, double* out);
+
+/* _kernels.pair_distance (_kernels.py:69-78). */
+int vqb_pair_distance(const double* a, const double* b, int64_t dim, int metric, double* out);
+
+/* ---- session surface ---- */
+
+typedef struct vqb_session vqb_session;
+
+/* Training set upload (TrainingSet, core.py:72-99).  Exactly one of x32 / x64
+ * is non-null.  float32 rows (exact in FP64, core.py:47-60) take the FP32
+ * candidate path; float64 rows take the exact-FP64 path.  `rows`/`dim` are
+ * this process's shard; row_offset / n_global place it in the global set
+ * (n_global = rows, row_offset = 0 for one GPU).  device = CUDA ordinal. */
+int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int64_t row_offset,
+             int64_t n_global, int device, vqb_session** out);
+int vqb_close(vqb_session* s);
+/* Use a caller stream (cudaStream_t as void*), e.g. torch's current stream. */
+int vqb_set_stream(vqb_session* s, void* stream);
+/* max |x| over this shard (+inf when any value is non-finite). */
+int vqb_local_maxabs(vqb_session* s, double* out);
+
+typedef struct {
+  int64_t target_size;               /* LbgConfig.target_size (power of two) */
+  double epsilon;                    /* relative-drop threshold, <= test */
+  double delta;                      /* additive split offset */
+  int64_t max_iterations_per_level;  /* guard (warning, not error) */
+  int32_t metric;                    /* 0 squared_euclidean, 1 euclidean */
+  int32_t ordered;                   /* -1 auto, 0 fixed-point sums, 1 reference order */
+  double global_maxabs;              /* < 0: use this shard's max |x| */
+} vqb_train_config;
+
+typedef struct {
+  int64_t codebook_size;
+  int64_t iteration;
+  double td;
+  int64_t empty_cells;
+  double seconds;
+} vqb_level_iteration; /* LevelIteration (core.py:162-172) */
+
+typedef struct {
+  double total;
+  int64_t n_hist;
+  int64_t n_warn;
+  int64_t passes;
+  int64_t flagged_rows;  /* rows re-ranked in FP64 over the run */
+  int64_t evals;         /* sum over passes of rows * codebook size (this shard) */
+  int64_t final_size;
+  int32_t fast_path;     /* 1: FP32 candidate + FP64 re-rank; 0: exact FP64 scan */
+  int32_t ordered;
+} vqb_train_summary;
+
+/* Full LBG design on the device (lbg_train / parallel_lbg_train).  Outputs:
+ * codebook_out[target_size][dim], hist[hist_cap], warn_sizes[warn_cap] (level
+ * sizes whose guard tripped), final_dists[rows] (nullable: distances of the
+ * last allocation pass, for DistortionStats.per_worker). */
+int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
+              vqb_level_iteration* hist, int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap,
+              double* final_dists, vqb_train_summary* summary);
+
+/* Allocation with a fixed codebook (assign_cells / encode) over this shard.
+ * cells64 / idx32 / dists are nullable; total = deterministic tree-order sum. */
+int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric, int64_t* cells64,
+               uint32_t* idx32, double* dists, double* total);
+
+/* Centroid update for a given cell table (update_codebook / parallel_update). */
+int vqb_update(vqb_session* s, const int64_t* cells, const double* old_codebook, int64_t size,
+               double* new_codebook, int64_t* counts, int64_t* n_empty);
+
+/* ---- step API for the multi-GPU loop (one process per GPU) ----
+ * begin: uploads config, enqueues the local column-sum pass.
+ * Each pass: step_local (assign + re-rank + epilogue) ; caller allreduces the
+ * exchange buffer (int64 SUM) on the session stream ; step_finalize.
+ * The first finalize after begin computes the global centroid.
+ * step_poll reports done (synchronises the stream). */
+int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg);
+int vqb_step_local(vqb_session* s);
+int vqb_step_finalize(vqb_session* s);
+int vqb_step_exchange(vqb_session* s, int64_t** device_words, int64_t* count);
+int vqb_step_poll(vqb_session* s, int* done);
+int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* hist,
+                    int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap, double* final_dists,
+                    vqb_train_summary* summary);
+
+/* ---- one-shot host-buffer calls (end-to-end path, copies included) ---- */
+
+/* encode (codec.py:62-93) of host float32 rows: pipelined H2D / assign / D2H
+ * in row chunks; idx_out uint32[n]; total (nullable) = tree-order distortion. */
+int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codebook, int64_t size,
+                   int device, uint32_t* idx_out, double* total);
+
+/* One Lloyd iteration from host buffers (assign + distortion + update): the
+ * kernel-surface round trip a reference caller makes per pass
+ * (core.py:392-406).  Outputs new_codebook[size][dim], td (tree order),
+ * n_empty; cells_out (nullable, int64[n]). */
+int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* codebook,
+                       int64_t size, int device, double* new_codebook, int64_t* cells_out,
+                       double* td, int64_t* n_empty);
+
+/* Pipe microbenchmark (0 FFMA, 1 FFMA2, 2 FFMA+top-2 mix, 3 DADD): lane-ops/s. */
+int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
+                        double* seconds);
+
+/* Time `reps` device-resident allocation+update passes at a fixed codebook
+ * (the bench's kernel-only step).  Returns per-kernel average milliseconds. */
+int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
+                        double* ms_total, double* ms_assign, double* ms_rerank,
+                        double* ms_epilogue, double* ms_finalize, int64_t* flagged);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VQB200_H */

@@ -1,0 +1,918 @@
+// C ABI + native LBG driver loop (see include/vqb200.h for the contract and
+// the reference interfaces each entry point replaces).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vqb200.h"
+#include "vqb200_internal.h"
+
+using namespace vqb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(VQB_INTERNAL, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, \
+                  __LINE__, cudaGetErrorString(e_));                                      \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+int fixed_shift_for(long long n_global, double maxabs) {
+  int e_n = 0;
+  while ((1LL << e_n) < n_global && e_n < 62) ++e_n;
+  int e_x = 0;
+  if (maxabs > 0) {
+    std::frexp(maxabs, &e_x);  // maxabs < 2^e_x
+  }
+  int s = 62 - e_n - e_x - 1;
+  if (s > 1000) s = 1000;
+  if (s < -1000) s = -1000;
+  return s;
+}
+
+}  // namespace
+
+struct vqb_session {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  long long n = 0, dim = 0, row_offset = 0, n_global = 0;
+  float* x32 = nullptr;
+  double* x64 = nullptr;
+  float* mu = nullptr;
+  double maxabs = -1.0;
+  // run buffers
+  long long kmax = 0;
+  double* cb[2] = {nullptr, nullptr};
+  float* w = nullptr;
+  float* nrm = nullptr;
+  int* idx = nullptr;
+  int* flags = nullptr;
+  double* dists = nullptr;
+  long long* ex = nullptr;
+  long long ntiles_global = 0;
+  DevState* st = nullptr;
+  DevState* st_host = nullptr;  // pinned
+  int* done_host = nullptr;     // pinned
+  double* scratch = nullptr;    // small device scratch
+  bool fast = false;
+  bool ordered = false;
+  bool pending_init = false;
+  cudaEvent_t ev_batch[2] = {nullptr, nullptr};
+
+  KernelArgs args() const {
+    KernelArgs a{};
+    a.x32 = x32;
+    a.x64 = x64;
+    a.n = n;
+    a.dim = (int)dim;
+    a.tile0 = row_offset / kTdTile;
+    a.mu = mu;
+    a.cb[0] = cb[0];
+    a.cb[1] = cb[1];
+    a.w = w;
+    a.nrm = nrm;
+    a.kmax = kmax;
+    a.idx = idx;
+    a.flags = flags;
+    a.dists = dists;
+    a.ex.base = ex;
+    a.ex.kmax = kmax;
+    a.ex.dim = dim;
+    a.ex.ntiles = ntiles_global;
+    a.st = st;
+    return a;
+  }
+
+  int ensure(long long k) {
+    if (k <= kmax && cb[0]) return VQB_OK;
+    cudaFree(cb[0]);
+    cudaFree(cb[1]);
+    cudaFree(w);
+    cudaFree(nrm);
+    cudaFree(ex);
+    cb[0] = cb[1] = nullptr;
+    w = nrm = nullptr;
+    ex = nullptr;
+    kmax = k;
+    const long long kpad = (k + 3) / 4 * 4;
+    CK(dalloc(&cb[0], (size_t)(k * dim)));
+    CK(dalloc(&cb[1], (size_t)(k * dim)));
+    CK(dalloc(&w, (size_t)(kpad * dim + 64)));
+    CK(dalloc(&nrm, (size_t)(kpad + 64)));
+    CK(dalloc(&ex, (size_t)(k * dim + k + ntiles_global)));
+    CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (k * dim + k + ntiles_global), stream));
+    return VQB_OK;
+  }
+
+  ~vqb_session() {
+    if (device >= 0) cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    cudaFree(x32);
+    cudaFree(x64);
+    cudaFree(mu);
+    cudaFree(cb[0]);
+    cudaFree(cb[1]);
+    cudaFree(w);
+    cudaFree(nrm);
+    cudaFree(idx);
+    cudaFree(flags);
+    cudaFree(dists);
+    cudaFree(ex);
+    cudaFree(st);
+    cudaFree(scratch);
+    if (st_host) cudaFreeHost(st_host);
+    if (done_host) cudaFreeHost(done_host);
+    for (auto& e : ev_batch)
+      if (e) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+extern "C" {
+
+const char* vqb_last_error(void) { return g_err.c_str(); }
+int vqb_version(void) { return 1; }
+
+int vqb_device_count(int* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return fail(VQB_INTERNAL, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  *count = c;
+  return VQB_OK;
+}
+
+int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int64_t row_offset,
+             int64_t n_global, int device, vqb_session** out) {
+  *out = nullptr;
+  if ((x32 == nullptr) == (x64 == nullptr))
+    return fail(VQB_USAGE, "exactly one of x32 / x64 must be given");
+  if (rows < 1 || dim < 1)
+    return fail(VQB_USAGE, "training set must be at least 1x1, got %lldx%lld", (long long)rows,
+                (long long)dim);
+  if (n_global < rows + row_offset || row_offset < 0)
+    return fail(VQB_USAGE, "shard [%lld, %lld) outside %lld global rows", (long long)row_offset,
+                (long long)(row_offset + rows), (long long)n_global);
+  if (row_offset % kTdTile != 0)
+    return fail(VQB_USAGE, "shard offset %lld must be a multiple of %d rows", (long long)row_offset,
+                kTdTile);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(VQB_INTERNAL, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  CK(cudaSetDevice(device));
+  std::unique_ptr<vqb_session> s(new vqb_session());
+  s->device = device;
+  CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  s->own_stream = true;
+  s->n = rows;
+  s->dim = dim;
+  s->row_offset = row_offset;
+  s->n_global = n_global;
+  s->ntiles_global = (n_global + kTdTile - 1) / kTdTile;
+  const size_t count = (size_t)rows * dim;
+  CK(dalloc(&s->scratch, 64));
+  if (x32) {
+    CK(dalloc(&s->x32, count + 16));
+    CK(cudaMemcpyAsync(s->x32, x32, count * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  } else {
+    CK(dalloc(&s->x64, count + 8));
+    CK(cudaMemcpyAsync(s->x64, x64, count * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    // float64 rows that are exactly float32 take the FP32 candidate path
+    float* tmp = nullptr;
+    CK(dalloc(&tmp, count + 16));
+    int* flag = reinterpret_cast<int*>(s->scratch);
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), s->stream));
+    CK(launch_f64_to_f32_exact(s->x64, tmp, (long long)count, flag, s->sms, s->stream));
+    int inexact = 1;
+    CK(cudaMemcpyAsync(&inexact, flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (!inexact) {
+      cudaFree(s->x64);
+      s->x64 = nullptr;
+      s->x32 = tmp;
+    } else {
+      cudaFree(tmp);
+    }
+  }
+  // max |x| (fixed-point scale, fast-path eligibility)
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
+  CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
+  CK(launch_maxabs(s->x32, s->x64, (long long)count, mb, s->sms, s->stream));
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
+  CK(dalloc(&s->idx, (size_t)rows + 32));
+  CK(dalloc(&s->flags, (size_t)rows + 32));
+  CK(dalloc(&s->dists, (size_t)rows + 32));
+  CK(dalloc(&s->st, 1));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
+  CK(dalloc(&s->mu, (size_t)dim + 4));
+  CK(cudaEventCreateWithFlags(&s->ev_batch[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s->ev_batch[1], cudaEventDisableTiming));
+  CK(cudaStreamSynchronize(s->stream));
+  std::memcpy(&s->maxabs, &bits, sizeof(double));
+  if (!(s->maxabs <= 1.7976931348623157e308)) s->maxabs = INFINITY;
+  // centring vector: the shard's first row mean is as good as any; use a
+  // cheap, deterministic one -- the midpoint of [-maxabs, maxabs] is 0, so
+  // centre at the column means of up to 4096 leading rows (FP32, host-free:
+  // computed from the device copy).
+  {
+    std::vector<float> h((size_t)std::min<long long>(rows, 4096) * dim);
+    std::vector<double> h64;
+    const long long m = std::min<long long>(rows, 4096);
+    if (s->x32) {
+      CK(cudaMemcpy(h.data(), s->x32, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    } else {
+      h64.resize(h.size());
+      CK(cudaMemcpy(h64.data(), s->x64, h64.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < h.size(); ++i) h[i] = (float)h64[i];
+    }
+    std::vector<float> mu((size_t)dim, 0.f);
+    for (long long l = 0; l < dim; ++l) {
+      double acc = 0;
+      for (long long j = 0; j < m; ++j) acc += h[(size_t)j * dim + l];
+      mu[(size_t)l] = std::isfinite(acc) ? (float)(acc / (double)m) : 0.f;
+    }
+    CK(cudaMemcpy(s->mu, mu.data(), dim * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  s->fast = s->x32 != nullptr && fast_dim_supported((int)dim) && s->maxabs < 1099511627776.0;
+  *out = s.release();
+  return VQB_OK;
+}
+
+int vqb_close(vqb_session* s) {
+  delete s;
+  return VQB_OK;
+}
+
+int vqb_set_stream(vqb_session* s, void* stream) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  CK(cudaSetDevice(s->device));
+  CK(cudaStreamSynchronize(s->stream));
+  if (s->own_stream) cudaStreamDestroy(s->stream);
+  s->stream = reinterpret_cast<cudaStream_t>(stream);
+  s->own_stream = false;
+  return VQB_OK;
+}
+
+int vqb_local_maxabs(vqb_session* s, double* out) {
+  *out = s->maxabs;
+  return VQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// training loop
+// ---------------------------------------------------------------------------
+
+static int check_config(const vqb_train_config* cfg) {
+  const long long t = cfg->target_size;
+  if (t < 1 || (t & (t - 1)) != 0)
+    return fail(VQB_CONFIG, "codebook size must be a power of two, got %lld", t);
+  if (!(cfg->epsilon >= 0)) return fail(VQB_CONFIG, "epsilon must be >= 0, got %g", cfg->epsilon);
+  if (!(cfg->delta > 0)) return fail(VQB_CONFIG, "split offset delta must be > 0, got %g", cfg->delta);
+  if (cfg->max_iterations_per_level < 1)
+    return fail(VQB_CONFIG, "max iterations per level must be >= 1, got %lld",
+                (long long)cfg->max_iterations_per_level);
+  if (cfg->metric != 0 && cfg->metric != 1)
+    return fail(VQB_CONFIG, "unknown distortion metric code %d", cfg->metric);
+  if (t > (1LL << 24)) return fail(VQB_CONFIG, "codebook size %lld too large for one device", t);
+  return VQB_OK;
+}
+
+static bool choose_ordered(const vqb_session* s, int requested, long long kmax) {
+  if (requested == 1) return true;
+  if (requested == 0) return false;
+  // auto: float64 rows that are not float32-exact keep the reference's own
+  // summation order (bit-identical) while the per-pass cost stays modest.
+  return s->x64 != nullptr && s->n == s->n_global &&
+         (double)s->n * (double)kmax * (double)s->dim <= 2.7e8;
+}
+
+int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  CK(cudaSetDevice(s->device));
+  rc = s->ensure(cfg->target_size);
+  if (rc) return rc;
+  s->ordered = choose_ordered(s, cfg->ordered, cfg->target_size);
+  if (s->ordered && s->n != s->n_global)
+    return fail(VQB_USAGE, "reference-order mode needs the whole training set on one device");
+  DevState* h = s->st_host;
+  std::memset(h, 0, sizeof(DevState));
+  h->target = (int)cfg->target_size;
+  h->max_iter = (int)cfg->max_iterations_per_level;
+  h->metric = cfg->metric;
+  const double gmax = cfg->global_maxabs >= 0 ? cfg->global_maxabs : s->maxabs;
+  h->fixed_shift = fixed_shift_for(s->n_global, gmax);
+  h->eps = cfg->epsilon;
+  h->delta = cfg->delta;
+  h->n_global = s->n_global;
+  h->mode = kModeTrain;
+  h->ordered = s->ordered ? 1 : 0;
+  h->size = 1;
+  h->iteration = 1;
+  h->td_prev = INFINITY;
+  // copy only the header part of the state (history is written on device)
+  CK(cudaMemcpyAsync(s->st, h, offsetof(DevState, hist), cudaMemcpyHostToDevice, s->stream));
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  if (s->ordered) {
+    CK(cudaMemsetAsync(s->idx, 0, sizeof(int) * s->n, s->stream));
+    CK(launch_ordered_update(a, s->stream));
+  } else {
+    CK(launch_epilogue(a, false, true, true, s->sms, s->stream));
+  }
+  s->pending_init = true;
+  return VQB_OK;
+}
+
+int vqb_step_local(vqb_session* s) {
+  KernelArgs a = s->args();
+  CK(launch_assign(a, s->fast, s->sms, s->stream));
+  if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+  CK(launch_epilogue(a, true, !s->ordered, false, s->sms, s->stream));
+  if (s->ordered) CK(launch_ordered_update(a, s->stream));
+  return VQB_OK;
+}
+
+int vqb_step_finalize(vqb_session* s) {
+  KernelArgs a = s->args();
+  if (s->pending_init) {
+    CK(launch_init_centroid(a, s->stream));
+    s->pending_init = false;
+  } else {
+    CK(launch_finalize(a, s->stream));
+  }
+  if (s->fast) CK(launch_prep_codebook(a, s->stream));
+  return VQB_OK;
+}
+
+int vqb_step_exchange(vqb_session* s, int64_t** device_words, int64_t* count) {
+  *device_words = reinterpret_cast<int64_t*>(s->ex);
+  *count = s->kmax * s->dim + s->kmax + s->ntiles_global;
+  return VQB_OK;
+}
+
+int vqb_step_poll(vqb_session* s, int* done) {
+  CK(cudaMemcpyAsync(s->done_host, &s->st->done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  *done = s->done_host[0];
+  return VQB_OK;
+}
+
+int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* hist,
+                    int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap, double* final_dists,
+                    vqb_train_summary* summary) {
+  CK(cudaSetDevice(s->device));
+  CK(cudaStreamSynchronize(s->stream));
+  DevState* h = s->st_host;
+  CK(cudaMemcpy(h, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost));
+  if (!h->done) return fail(VQB_INTERNAL, "training loop has not finished");
+  const long long nh = std::min<long long>(h->n_hist, kMaxHist);
+  std::vector<HistRec> recs((size_t)nh);
+  if (nh > 0)
+    CK(cudaMemcpy(recs.data(), reinterpret_cast<char*>(s->st) + offsetof(DevState, hist),
+                  sizeof(HistRec) * nh, cudaMemcpyDeviceToHost));
+  const long long size = h->size;
+  if (codebook_out)
+    CK(cudaMemcpy(codebook_out, s->cb[h->cur], sizeof(double) * size * s->dim,
+                  cudaMemcpyDeviceToHost));
+  if (final_dists) CK(cudaMemcpy(final_dists, s->dists, sizeof(double) * s->n, cudaMemcpyDeviceToHost));
+  for (long long i = 0; i < nh && i < hist_cap; ++i) {
+    hist[i].codebook_size = recs[(size_t)i].size;
+    hist[i].iteration = recs[(size_t)i].iteration;
+    hist[i].td = recs[(size_t)i].td;
+    hist[i].empty_cells = recs[(size_t)i].empty;
+    hist[i].seconds = (double)(recs[(size_t)i].t_ns - h->t0_ns) * 1e-9;
+  }
+  for (long long i = 0; i < std::min<long long>(h->n_warn, kMaxWarn) && i < warn_cap; ++i)
+    warn_sizes[i] = h->warn_sizes[i];
+  if (summary) {
+    summary->total = h->total;
+    summary->n_hist = h->n_hist;
+    summary->n_warn = h->n_warn;
+    summary->passes = h->passes;
+    summary->flagged_rows = h->flagged_total;
+    summary->evals = h->evals;
+    summary->final_size = size;
+    summary->fast_path = s->fast ? 1 : 0;
+    summary->ordered = s->ordered ? 1 : 0;
+  }
+  if (h->n_hist > kMaxHist) return fail(VQB_INTERNAL, "history overflow (%d records)", h->n_hist);
+  return VQB_OK;
+}
+
+int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
+              vqb_level_iteration* hist, int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap,
+              double* final_dists, vqb_train_summary* summary) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  if (s->n != s->n_global)
+    return fail(VQB_USAGE, "vqb_train drives one device; use the vqb_step_* loop for shards");
+  int rc = vqb_step_begin(s, cfg);
+  if (rc) return rc;
+  rc = vqb_step_finalize(s);  // global centroid + first split
+  if (rc) return rc;
+  // Speculative batches: passes early-exit on the device once `done` is set,
+  // so the host only checks the flag of the previous batch while the next
+  // one is already queued (the GPU never waits on the host).
+  const int batch = 4;
+  long long issued = 0;
+  int b = 0;
+  const long long max_passes = (long long)(std::log2((double)cfg->target_size) + 1) *
+                                   (cfg->max_iterations_per_level + 1) + 8;
+  while (true) {
+    for (int i = 0; i < batch; ++i) {
+      rc = vqb_step_local(s);
+      if (rc) return rc;
+      rc = vqb_step_finalize(s);
+      if (rc) return rc;
+    }
+    issued += batch;
+    CK(cudaMemcpyAsync(&s->done_host[b], &s->st->done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaEventRecord(s->ev_batch[b], s->stream));
+    if (issued > batch) {
+      CK(cudaEventSynchronize(s->ev_batch[b ^ 1]));
+      if (s->done_host[b ^ 1]) break;
+    }
+    if (issued > max_passes + 2 * batch) {
+      CK(cudaStreamSynchronize(s->stream));
+      if (s->done_host[b]) break;
+      return fail(VQB_INTERNAL, "training loop did not terminate after %lld passes", issued);
+    }
+    b ^= 1;
+  }
+  return vqb_step_result(s, codebook_out, hist, hist_cap, warn_sizes, warn_cap, final_dists, summary);
+}
+
+// ---------------------------------------------------------------------------
+// one-shot calls on a session
+// ---------------------------------------------------------------------------
+
+static int upload_codebook(vqb_session* s, const double* codebook, long long size) {
+  int rc = s->ensure(size);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(s->cb[0], codebook, sizeof(double) * size * s->dim, cudaMemcpyHostToDevice,
+                     s->stream));
+  return VQB_OK;
+}
+
+static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered) {
+  DevState* h = s->st_host;
+  // configuration fields are written by the reset kernel + this header copy
+  std::memset(h, 0, offsetof(DevState, hist));
+  h->target = (int)size;
+  h->max_iter = 1;
+  h->metric = metric;
+  h->fixed_shift = fixed_shift_for(s->n_global, s->maxabs);
+  h->n_global = s->n_global;
+  h->mode = mode;
+  h->ordered = ordered;
+  h->size = (int)size;
+  h->iteration = 1;
+  h->td_prev = INFINITY;
+  CK(cudaMemcpyAsync(s->st, h, offsetof(DevState, hist), cudaMemcpyHostToDevice, s->stream));
+  return VQB_OK;
+}
+
+int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric, int64_t* cells64,
+               uint32_t* idx32, double* dists, double* total) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  if (size < 1) return fail(VQB_USAGE, "codebook must be at least 1x1");
+  if (size > (1LL << 30)) return fail(VQB_USAGE, "codebook too large");
+  CK(cudaSetDevice(s->device));
+  int rc = upload_codebook(s, codebook, size);
+  if (rc) return rc;
+  // in-order distortion (sum_inorder) when it is cheap: assign_cells returns
+  // the chunk total accumulated in input order (core.py:315-316)
+  const int ordered_td = (s->n == s->n_global && s->n <= (1LL << 20)) ? 1 : 0;
+  rc = set_state(s, kModeAssignOnly, size, metric, ordered_td);
+  if (rc) return rc;
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  if (s->fast) CK(launch_prep_codebook(a, s->stream));
+  CK(launch_assign(a, s->fast, s->sms, s->stream));
+  if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+  CK(launch_epilogue(a, true, false, false, s->sms, s->stream));
+  CK(launch_finalize(a, s->stream));
+  std::vector<int> tmp;
+  if (cells64 || idx32) {
+    if (idx32) {
+      CK(cudaMemcpyAsync(idx32, s->idx, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
+    } else {
+      tmp.resize((size_t)s->n);
+      CK(cudaMemcpyAsync(tmp.data(), s->idx, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
+    }
+  }
+  if (dists) CK(cudaMemcpyAsync(dists, s->dists, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (cells64) {
+    if (idx32)
+      for (long long i = 0; i < s->n; ++i) cells64[i] = idx32[i];
+    else
+      for (long long i = 0; i < s->n; ++i) cells64[i] = tmp[(size_t)i];
+  }
+  if (total) *total = s->st_host->total;
+  return VQB_OK;
+}
+
+int vqb_update(vqb_session* s, const int64_t* cells, const double* old_codebook, int64_t size,
+               double* new_codebook, int64_t* counts, int64_t* n_empty) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  CK(cudaSetDevice(s->device));
+  int rc = upload_codebook(s, old_codebook, size);
+  if (rc) return rc;
+  const int ordered = choose_ordered(s, -1, size) ? 1 : 0;
+  rc = set_state(s, kModeUpdateOnly, size, 0, ordered);
+  if (rc) return rc;
+  // cells (int64) staged through the dists buffer, narrowed on the device
+  CK(cudaMemcpyAsync(s->dists, cells, sizeof(int64_t) * s->n, cudaMemcpyHostToDevice, s->stream));
+  CK(launch_cells_to_idx(reinterpret_cast<const long long*>(s->dists), s->idx, s->n, s->sms, s->stream));
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  if (ordered)
+    CK(launch_ordered_update(a, s->stream));
+  else
+    CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
+  CK(launch_finalize(a, s->stream));
+  std::vector<long long> hc((size_t)size);
+  CK(cudaMemcpyAsync(new_codebook, s->cb[1], sizeof(double) * size * s->dim, cudaMemcpyDeviceToHost,
+                     s->stream));
+  CK(cudaMemcpyAsync(hc.data(), s->ex + s->kmax * s->dim, sizeof(long long) * size,
+                     cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (counts)
+    for (long long i = 0; i < size; ++i) counts[i] = hc[(size_t)i];
+  if (n_empty) *n_empty = s->st_host->last_empty;
+  return VQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel surface (stateless, host buffers)
+// ---------------------------------------------------------------------------
+
+int vqb_assign_range(const double* vectors, int64_t m, int64_t dim, const double* codebook,
+                     int64_t size, int64_t start, int64_t stop, int metric, int64_t* out_cells,
+                     double* out_dists) {
+  if (start < 0 || stop > m || start > stop) return fail(VQB_USAGE, "bad row range");
+  if (stop == start) return VQB_OK;
+  vqb_session* s = nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = vqb_open(nullptr, vectors + start * dim, stop - start, dim, 0, stop - start, dev, &s);
+  if (rc) return rc;
+  std::unique_ptr<vqb_session> guard(s);
+  return vqb_assign(s, codebook, size, metric, out_cells + start, nullptr, out_dists + start, nullptr);
+}
+
+int vqb_update_rows(const double* vectors, int64_t m, int64_t dim, const int64_t* cells,
+                    const double* old_codebook, int64_t size, int64_t worker, int64_t stride,
+                    double* out_codebook, int64_t* out_counts) {
+  if (stride < 1 || worker < 0) return fail(VQB_USAGE, "bad worker/stride");
+  if (m < 1) {
+    for (long long i = worker; i < size; i += stride) {
+      out_counts[i] = 0;
+      for (long long l = 0; l < dim; ++l) out_codebook[i * dim + l] = old_codebook[i * dim + l];
+    }
+    return VQB_OK;
+  }
+  vqb_session* s = nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = vqb_open(nullptr, vectors, m, dim, 0, m, dev, &s);
+  if (rc) return rc;
+  std::unique_ptr<vqb_session> guard(s);
+  std::vector<double> nb((size_t)(size * dim));
+  std::vector<int64_t> cnt((size_t)size);
+  int64_t empty = 0;
+  rc = vqb_update(s, cells, old_codebook, size, nb.data(), cnt.data(), &empty);
+  if (rc) return rc;
+  for (long long i = worker; i < size; i += stride) {
+    out_counts[i] = cnt[(size_t)i];
+    for (long long l = 0; l < dim; ++l) out_codebook[i * dim + l] = nb[(size_t)(i * dim + l)];
+  }
+  return VQB_OK;
+}
+
+int vqb_column_sums(const double* vectors, int64_t m, int64_t dim, double* out) {
+  if (m < 1 || dim < 1) return fail(VQB_USAGE, "column sums need a non-empty matrix");
+  double *dx = nullptr, *dout = nullptr;
+  CK(dalloc(&dx, (size_t)(m * dim)));
+  std::unique_ptr<double, decltype(&cudaFree)> g1(dx, &cudaFree);
+  CK(dalloc(&dout, (size_t)dim));
+  std::unique_ptr<double, decltype(&cudaFree)> g2(dout, &cudaFree);
+  CK(cudaMemcpy(dx, vectors, sizeof(double) * m * dim, cudaMemcpyHostToDevice));
+  CK(launch_column_sums_ordered(dx, nullptr, m, (int)dim, dout, 0));
+  CK(cudaMemcpy(out, dout, sizeof(double) * dim, cudaMemcpyDeviceToHost));
+  return VQB_OK;
+}
+
+int vqb_sum_inorder(const double* values, int64_t n, double* out) {
+  if (n <= 0) {
+    *out = 0.0;
+    return VQB_OK;
+  }
+  double *dv = nullptr, *dout = nullptr;
+  CK(dalloc(&dv, (size_t)n));
+  std::unique_ptr<double, decltype(&cudaFree)> g1(dv, &cudaFree);
+  CK(dalloc(&dout, 1));
+  std::unique_ptr<double, decltype(&cudaFree)> g2(dout, &cudaFree);
+  CK(cudaMemcpy(dv, values, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(launch_sum_inorder(dv, n, dout, 0));
+  CK(cudaMemcpy(out, dout, sizeof(double), cudaMemcpyDeviceToHost));
+  return VQB_OK;
+}
+
+int vqb_pair_distance(const double* a, const double* b, int64_t dim, int metric, double* out) {
+  double* d = nullptr;
+  CK(dalloc(&d, (size_t)(2 * dim + 1)));
+  std::unique_ptr<double, decltype(&cudaFree)> g(d, &cudaFree);
+  CK(cudaMemcpy(d, a, sizeof(double) * dim, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d + dim, b, sizeof(double) * dim, cudaMemcpyHostToDevice));
+  CK(launch_pair_distance(d, d + dim, (int)dim, metric, d + 2 * dim, 0));
+  CK(cudaMemcpy(out, d + 2 * dim, sizeof(double), cudaMemcpyDeviceToHost));
+  return VQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one-shot host-buffer paths (end-to-end)
+// ---------------------------------------------------------------------------
+
+namespace {
+// cached scratch session for repeated one-shot calls of the same shape
+std::mutex g_cache_mu;
+struct Cached {
+  vqb_session* s = nullptr;
+  long long n = 0, dim = 0;
+  int device = -1;
+};
+Cached g_cache;
+
+int cached_session(long long n, long long dim, int device, vqb_session** out) {
+  if (g_cache.s && g_cache.n == n && g_cache.dim == dim && g_cache.device == device) {
+    *out = g_cache.s;
+    return VQB_OK;
+  }
+  delete g_cache.s;
+  g_cache.s = nullptr;
+  // allocate with a dummy (zero) upload; data is copied per call
+  std::unique_ptr<vqb_session> s(new vqb_session());
+  CK(cudaSetDevice(device));
+  s->device = device;
+  CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  s->own_stream = true;
+  s->n = s->n_global = n;
+  s->dim = dim;
+  s->ntiles_global = (n + kTdTile - 1) / kTdTile;
+  CK(dalloc(&s->x32, (size_t)(n * dim + 16)));
+  CK(dalloc(&s->idx, (size_t)n + 32));
+  CK(dalloc(&s->flags, (size_t)n + 32));
+  CK(dalloc(&s->dists, (size_t)n + 32));
+  CK(dalloc(&s->st, 1));
+  CK(dalloc(&s->scratch, 64));
+  CK(dalloc(&s->mu, (size_t)dim + 4));
+  CK(cudaMemset(s->mu, 0, sizeof(float) * dim));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
+  s->fast = fast_dim_supported((int)dim);
+  g_cache.s = s.release();
+  g_cache.n = n;
+  g_cache.dim = dim;
+  g_cache.device = device;
+  *out = g_cache.s;
+  return VQB_OK;
+}
+
+int refresh_maxabs(vqb_session* s) {
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
+  CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
+  CK(launch_maxabs(s->x32, nullptr, s->n * s->dim, mb, s->sms, s->stream));
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  std::memcpy(&s->maxabs, &bits, sizeof(double));
+  if (!(s->maxabs <= 1.7976931348623157e308)) s->maxabs = INFINITY;
+  s->fast = fast_dim_supported((int)s->dim) && s->maxabs < 1099511627776.0;
+  return VQB_OK;
+}
+}  // namespace
+
+int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* codebook,
+                       int64_t size, int device, double* new_codebook, int64_t* cells_out,
+                       double* td, int64_t* n_empty) {
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  vqb_session* s = nullptr;
+  int rc = cached_session(n, dim, device, &s);
+  if (rc) return rc;
+  CK(cudaSetDevice(device));
+  CK(cudaMemcpyAsync(s->x32, x, sizeof(float) * n * dim, cudaMemcpyHostToDevice, s->stream));
+  rc = refresh_maxabs(s);
+  if (rc) return rc;
+  rc = upload_codebook(s, codebook, size);
+  if (rc) return rc;
+  rc = set_state(s, kModeLloydStep, size, 0, 0);
+  if (rc) return rc;
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  if (s->fast) CK(launch_prep_codebook(a, s->stream));
+  CK(launch_assign(a, s->fast, s->sms, s->stream));
+  if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+  CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
+  CK(launch_finalize(a, s->stream));
+  CK(cudaMemcpyAsync(new_codebook, s->cb[1], sizeof(double) * size * dim, cudaMemcpyDeviceToHost,
+                     s->stream));
+  std::vector<int> tmp;
+  if (cells_out) {
+    tmp.resize((size_t)n);
+    CK(cudaMemcpyAsync(tmp.data(), s->idx, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream));
+  }
+  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (cells_out)
+    for (long long i = 0; i < n; ++i) cells_out[i] = tmp[(size_t)i];
+  if (td) *td = s->st_host->total;
+  if (n_empty) *n_empty = s->st_host->last_empty;
+  return VQB_OK;
+}
+
+int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codebook, int64_t size,
+                   int device, uint32_t* idx_out, double* total) {
+  if (n == 0) {
+    if (total) *total = 0.0;
+    return VQB_OK;
+  }
+  CK(cudaSetDevice(device));
+  // Two slots, each a session over a chunk of rows; slot i%2 runs chunk i:
+  // H2D of chunk i+1 overlaps the kernels of chunk i.
+  const long long chunk = std::min<long long>(n, 1LL << 22);
+  std::unique_ptr<vqb_session> slot[2];
+  for (int i = 0; i < 2; ++i) {
+    slot[i].reset(new vqb_session());
+    vqb_session* s = slot[i].get();
+    s->device = device;
+    CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+    s->n = s->n_global = chunk;
+    s->dim = dim;
+    s->ntiles_global = (chunk + kTdTile - 1) / kTdTile;
+    CK(dalloc(&s->x32, (size_t)(chunk * dim + 16)));
+    CK(dalloc(&s->idx, (size_t)chunk + 32));
+    CK(dalloc(&s->flags, (size_t)chunk + 32));
+    CK(dalloc(&s->dists, (size_t)chunk + 32));
+    CK(dalloc(&s->st, 1));
+    CK(dalloc(&s->scratch, 64));
+    CK(dalloc(&s->mu, (size_t)dim + 4));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
+    // centre at the codebook mean (any centre is exact after the re-rank)
+    std::vector<float> mu((size_t)dim, 0.f);
+    for (long long l = 0; l < dim; ++l) {
+      double acc = 0;
+      for (long long k = 0; k < size; ++k) acc += codebook[k * dim + l];
+      mu[(size_t)l] = std::isfinite(acc) ? (float)(acc / (double)size) : 0.f;
+    }
+    CK(cudaMemcpy(s->mu, mu.data(), sizeof(float) * dim, cudaMemcpyHostToDevice));
+    s->maxabs = 0;
+    s->fast = fast_dim_supported((int)dim);
+    int rc = upload_codebook(s, codebook, size);
+    if (rc) return rc;
+  }
+  const long long nchunks = (n + chunk - 1) / chunk;
+  std::vector<double> totals((size_t)nchunks, 0.0);
+  std::vector<std::vector<double>> tot_host(2);
+  double* tot_pinned = nullptr;
+  CK(cudaMallocHost(reinterpret_cast<void**>(&tot_pinned), sizeof(double) * nchunks));
+  std::unique_ptr<double, decltype(&cudaFreeHost)> gp(tot_pinned, &cudaFreeHost);
+  for (long long c = 0; c < nchunks; ++c) {
+    vqb_session* s = slot[c & 1].get();
+    const long long r0 = c * chunk;
+    const long long rows = std::min(chunk, n - r0);
+    s->n = rows;  // last chunk may be short; tiles beyond it stay zero
+    CK(cudaMemcpyAsync(s->x32, x + r0 * dim, sizeof(float) * rows * dim, cudaMemcpyHostToDevice,
+                       s->stream));
+    // fixed-point scale unused (no sums); state reset on the device
+    KernelArgs a = s->args();
+    CK(launch_reset(s->st, kModeAssignOnly, (int)size, 0, 0, 0, s->stream));
+    CK(launch_clear(a, s->stream));
+    if (s->fast) CK(launch_prep_codebook(a, s->stream));
+    CK(launch_assign(a, s->fast, s->sms, s->stream));
+    if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+    CK(launch_epilogue(a, false, false, false, s->sms, s->stream));
+    CK(launch_finalize(a, s->stream));
+    CK(cudaMemcpyAsync(idx_out + r0, s->idx, sizeof(int) * rows, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(tot_pinned + c, &s->st->total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  }
+  CK(cudaStreamSynchronize(slot[0]->stream));
+  CK(cudaStreamSynchronize(slot[1]->stream));
+  if (total) {
+    double t = 0.0;
+    for (long long c = 0; c < nchunks; ++c) t += tot_pinned[c];
+    *total = t;
+  }
+  return VQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// bench helper: device-resident Lloyd iterations with per-kernel event timing
+// ---------------------------------------------------------------------------
+
+int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
+                        double* ms_total, double* ms_assign, double* ms_rerank, double* ms_epilogue,
+                        double* ms_finalize, int64_t* flagged) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  CK(cudaSetDevice(s->device));
+  int rc = upload_codebook(s, codebook, size);
+  if (rc) return rc;
+  rc = set_state(s, kModeLloydStep, size, 0, 0);
+  if (rc) return rc;
+  cudaEvent_t ev[5];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[4] = {0, 0, 0, 0};
+  long long fl = 0;
+  float ms_all = 0;
+  cudaEvent_t t0, t1;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  KernelArgs a = s->args();
+  CK(cudaEventRecord(t0, s->stream));
+  for (int r = 0; r < reps; ++r) {
+    // keep iterating on the device: after each update the new codebook
+    // becomes current (cur flips), exactly like consecutive Lloyd passes
+    CK(launch_reset(s->st, kModeLloydStep, (int)size, 0, 0, 1, s->stream));
+    CK(launch_clear(a, s->stream));
+    if (s->fast) CK(launch_prep_codebook(a, s->stream));
+    CK(cudaEventRecord(ev[0], s->stream));
+    CK(launch_assign(a, s->fast, s->sms, s->stream));
+    CK(cudaEventRecord(ev[1], s->stream));
+    if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+    CK(cudaEventRecord(ev[2], s->stream));
+    CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
+    CK(cudaEventRecord(ev[3], s->stream));
+    CK(launch_finalize(a, s->stream));
+    CK(cudaEventRecord(ev[4], s->stream));
+    CK(cudaEventSynchronize(ev[4]));
+    float m;
+    for (int k = 0; k < 4; ++k) {
+      CK(cudaEventElapsedTime(&m, ev[k], ev[k + 1]));
+      acc[k] += m;
+    }
+  }
+  long long flt = 0;
+  CK(cudaMemcpy(&flt, &s->st->flagged_total, sizeof(long long), cudaMemcpyDeviceToHost));
+  fl = flt;
+  CK(cudaEventRecord(t1, s->stream));
+  CK(cudaEventSynchronize(t1));
+  CK(cudaEventElapsedTime(&ms_all, t0, t1));
+  for (auto& e : ev) cudaEventDestroy(e);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  *ms_total = (acc[0] + acc[1] + acc[2] + acc[3]) / reps;
+  *ms_assign = acc[0] / reps;
+  *ms_rerank = acc[1] / reps;
+  *ms_epilogue = acc[2] / reps;
+  *ms_finalize = acc[3] / reps;
+  *flagged = fl / reps;
+  return VQB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1018 @@
+// sm_100a kernels for the LBG hot path (arxiv/paper_0910_4711 reference:
+// pkg/src/vqkit/_kernels.py, core.py, parallel.py).
+//
+//   prep_codebook     FP64 master codebook -> centred FP32 staging (w=-2c~, ||c~||^2)
+//   assign_fast<L>    nearest-codevector candidate pass: FP32 FFMA expanded form,
+//                     codebook tiles staged in smem by cp.async.bulk (TMA bulk
+//                     copies) + mbarrier, rows in registers, top-2 per row,
+//                     rigorous error band -> rows it cannot certify go to
+//   exact_rows        FP64 scan in the reference's exact arithmetic
+//                     (_kernels.py:22-32: dsub, dmul, dadd, ascending c, strict <)
+//   epilogue          exact FP64 winner distance, deterministic distortion tile
+//                     partials, int64 fixed-point cell sums + counts (order-free,
+//                     hence deterministic and G-invariant)
+//   ordered_update    reference-order FP64 cell sums (update_rows, _kernels.py:39-66),
+//                     used for float64 inputs where bit-identity needs the order
+//   finalize          one block: distortion, convergence test (core.py:342-356),
+//                     centroid update / empty cells (_kernels.py:59-66), split
+//                     (core.py:277-281), level/guard logic (core.py:384-415), history
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "vqb200_internal.h"
+
+namespace vqb {
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double load_x(const float* x, long long i) { return (double)x[i]; }
+__device__ __forceinline__ double load_x(const double* x, long long i) { return x[i]; }
+
+// Squared distance in the reference's arithmetic (_kernels.py:25-29): for c
+// ascending, diff = x - c; d = d + diff*diff, every op rounded separately
+// (the _rn intrinsics forbid FMA contraction).
+template <typename XT>
+__device__ __forceinline__ double ref_dist(const XT* x, const double* c, int dim) {
+  double d = 0.0;
+  for (int l = 0; l < dim; ++l) {
+    double diff = __dsub_rn(load_x(x, l), c[l]);
+    d = __dadd_rn(d, __dmul_rn(diff, diff));
+  }
+  return d;
+}
+
+__device__ __forceinline__ long long to_fixed(double v, double scale) {
+  return __double2ll_rn(v * scale);  // scale is a power of two: the product is exact
+}
+
+// ---------------------------------------------------------------------------
+// prep: centred FP32 staging of the current FP64 codebook
+// ---------------------------------------------------------------------------
+
+__global__ void prep_codebook_kernel(KernelArgs a) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = st->size;
+  const int dim = a.dim;
+  const double* cb = a.cb[st->cur];
+  const long long kpad = (a.kmax + 3) / 4 * 4;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < kpad;
+       k += (long long)gridDim.x * blockDim.x) {
+    float* w = a.w + k * dim;
+    if (k < K) {
+      double n = 0.0;
+      for (int l = 0; l < dim; ++l) {
+        float c = (float)(cb[k * dim + l] - (double)a.mu[l]);
+        n += (double)c * (double)c;
+        w[l] = -2.0f * c;
+      }
+      a.nrm[k] = (float)n;
+    } else {
+      for (int l = 0; l < dim; ++l) w[l] = 0.0f;
+      a.nrm[k] = INFINITY;  // padding never wins
+    }
+  }
+}
+
+cudaError_t launch_prep_codebook(const KernelArgs& a, cudaStream_t s) {
+  long long kpad = (a.kmax + 3) / 4 * 4;
+  int blocks = (int)((kpad + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  prep_codebook_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// assign_fast: FP32 candidate pass with a certified error band
+// ---------------------------------------------------------------------------
+
+template <int L>
+struct FastCfg;
+template <>
+struct FastCfg<16> {
+  static constexpr int NT = 512, R = 4, TK = 1024;
+};
+template <>
+struct FastCfg<32> {
+  static constexpr int NT = 256, R = 2, TK = 512;
+};
+template <>
+struct FastCfg<64> {
+  static constexpr int NT = 256, R = 2, TK = 256;
+};
+
+bool fast_dim_supported(int dim) { return dim == 16 || dim == 32 || dim == 64; }
+
+template <int L, int TK>
+struct TileStream {
+  // W tile [TK][L] then norms [TK]; two buffers.
+  static constexpr size_t kWBytes = (size_t)TK * L * sizeof(float);
+  static constexpr size_t kBufBytes = kWBytes + (size_t)TK * sizeof(float);
+};
+
+// Process rows assigned to this thread in one chunk: R rows, strided by NT.
+template <int L, int NT, int TK, int R>
+__device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0, long long row_end,
+                                             int K, int ntiles, float* smem, uint64_t* bars,
+                                             long long& seq, long long seq_total) {
+  const int tid = threadIdx.x;
+  float y[R][L];
+  float q[R];
+  bool valid[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    long long row = row0 + tid + (long long)r * NT;
+    valid[r] = row < row_end;
+    q[r] = 0.f;
+    const float4* src = reinterpret_cast<const float4*>(a.x32 + (valid[r] ? row : row0) * L);
+#pragma unroll
+    for (int v = 0; v < L / 4; ++v) {
+      float4 t = __ldg(src + v);
+      y[r][4 * v + 0] = __fsub_rn(t.x, a.mu[4 * v + 0]);
+      y[r][4 * v + 1] = __fsub_rn(t.y, a.mu[4 * v + 1]);
+      y[r][4 * v + 2] = __fsub_rn(t.z, a.mu[4 * v + 2]);
+      y[r][4 * v + 3] = __fsub_rn(t.w, a.mu[4 * v + 3]);
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) q[r] = fmaf(y[r][l], y[r][l], q[r]);
+  }
+  float m1[R], m2[R];
+  int i1[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    m1[r] = INFINITY;
+    m2[r] = INFINITY;
+    i1[r] = 0;
+  }
+  using TS = TileStream<L, TK>;
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = (ntiles == 1) ? 0 : (int)(seq & 1);
+    if (ntiles > 1) mbar_wait(&bars[buf], (uint32_t)((seq >> 1) & 1));
+    const float* sW = reinterpret_cast<const float*>(reinterpret_cast<const char*>(smem) +
+                                                     buf * TS::kBufBytes);
+    const float* sN = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sW) + TS::kWBytes);
+    const int jbase = t * TK;
+    const int cnt = min(TK, K - jbase);
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+      const float4* wj = reinterpret_cast<const float4*>(sW + j * L);
+      float v[R];
+      const float nj = sN[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = nj;
+#pragma unroll
+      for (int c = 0; c < L / 16; ++c) {
+        float w[16];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          float4 t4 = wj[c * 4 + p];
+          w[4 * p + 0] = t4.x;
+          w[4 * p + 1] = t4.y;
+          w[4 * p + 2] = t4.z;
+          w[4 * p + 3] = t4.w;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+          for (int l = 0; l < 16; ++l) v[r] = fmaf(w[l], y[r][c * 16 + l], v[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float vv = v[r];
+        const float n2 = fminf(m2[r], fmaxf(m1[r], vv));
+        const bool p = vv < m1[r];
+        m1[r] = fminf(m1[r], vv);
+        i1[r] = p ? jbase + j : i1[r];
+        m2[r] = n2;
+      }
+    }
+    if (ntiles > 1) {
+      __syncthreads();  // every warp is done with buffer `buf`
+      if (tid == 0 && seq + 2 < seq_total) {
+        const long long ns = seq + 2;
+        const int nt = (int)(ns % ntiles);
+        const int ncnt = min(TK, K - nt * TK);
+        const uint32_t wbytes = (uint32_t)ncnt * L * sizeof(float);
+        const uint32_t nbytes = (uint32_t)((ncnt + 3) / 4 * 4) * sizeof(float);
+        float* dW = reinterpret_cast<float*>(reinterpret_cast<char*>(smem) + buf * TS::kBufBytes);
+        float* dN = reinterpret_cast<float*>(reinterpret_cast<char*>(dW) + TS::kWBytes);
+        mbar_arrive_expect_tx(&bars[buf], wbytes + nbytes);
+        bulk_g2s(dW, a.w + (long long)nt * TK * L, wbytes, &bars[buf]);
+        bulk_g2s(dN, a.nrm + (long long)nt * TK, nbytes, &bars[buf]);
+      }
+      ++seq;
+    }
+  }
+  // Certification.  With y~ = fl(x - mu) and the centred FP32 codebook, the
+  // computed v_j = fl-chain(||c~_j||^2 - 2 y~.c~_j) differs from the exact
+  // ||x - c_j||^2 - ||y~||^2 by at most
+  //   (L+3) u S^2 + 2.5 u sqrt(D) S,   S = 2||y~|| + sqrt(D) (+ slack),
+  // (u = 2^-24; FMA-chain, norm rounding, centring and FP32 codebook
+  // rounding; ||c~_j|| <= ||y~|| + sqrt(D_j)), plus the FP64 reference's own
+  // rounding (~1e-14 D).  If the top-2 gap exceeds 3x that bound (2 rows'
+  // worth x 1.5 safety) the FP32 winner is the reference's winner; otherwise
+  // the row is re-ranked in exact FP64.  NaN / inf propagate to "flag".
+  const float u = 5.9604645e-8f;
+  const int lane = tid & 31;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    long long row = row0 + tid + (long long)r * NT;
+    bool ok = false;
+    if (valid[r]) {
+      const float yn = sqrtf(q[r]);
+      const float d2 = fmaxf(m2[r] + q[r], 0.f);
+      const float sd = sqrtf(d2) * 1.01f + 1.0f;
+      const float S = 2.02f * yn + sd;
+      const float E = (float)(L + 3) * u * S * S + 2.5f * u * sd * S + 1e-14f * S * S;
+      ok = (m2[r] - m1[r]) > 3.0f * E;
+      a.idx[row] = i1[r];
+    }
+    const bool flag = valid[r] && !ok;
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    if (mask) {
+      int base = 0;
+      const int leader = __ffs(mask) - 1;
+      if (lane == leader) base = atomicAdd(&a.st->flag_count, __popc(mask));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (flag) a.flags[base + __popc(mask & ((1u << lane) - 1u))] = (int)row;
+    }
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelArgs a) {
+  constexpr int NT = FastCfg<L>::NT, R = FastCfg<L>::R, TK = FastCfg<L>::TK;
+  using TS = TileStream<L, TK>;
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = st->size;
+  const int ntiles = (K + TK - 1) / TK;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw);
+  __shared__ __align__(8) uint64_t bars[2];
+
+  // contiguous, balanced row range for this block
+  const long long n = a.n;
+  const long long lo = n * blockIdx.x / gridDim.x;
+  const long long hi = n * (blockIdx.x + 1) / gridDim.x;
+  const long long rows = hi - lo;
+  const long long per_chunk = (long long)NT * R;
+  const long long full = rows / per_chunk;
+  const long long rem = rows - full * per_chunk;
+  const long long nchunks = full + (rem > 0 ? 1 : 0);
+  const long long seq_total = (ntiles > 1) ? nchunks * ntiles : 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (nchunks == 0) return;
+  if (threadIdx.x == 0) {
+    const int first = (ntiles > 1) ? 2 : 1;
+    for (int s = 0; s < first && s < seq_total; ++s) {
+      const int t = s % ntiles;
+      const int cnt = min(TK, K - t * TK);
+      const uint32_t wbytes = (uint32_t)cnt * L * sizeof(float);
+      const uint32_t nbytes = (uint32_t)((cnt + 3) / 4 * 4) * sizeof(float);
+      float* dW = reinterpret_cast<float*>(smem_raw + s * TS::kBufBytes);
+      float* dN = reinterpret_cast<float*>(smem_raw + s * TS::kBufBytes + TS::kWBytes);
+      mbar_arrive_expect_tx(&bars[s], wbytes + nbytes);
+      bulk_g2s(dW, a.w + (long long)t * TK * L, wbytes, &bars[s]);
+      bulk_g2s(dN, a.nrm + (long long)t * TK, nbytes, &bars[s]);
+    }
+  }
+  if (ntiles == 1) mbar_wait(&bars[0], 0);
+
+  long long seq = 0;
+  for (long long c = 0; c < full; ++c)
+    assign_chunk<L, NT, TK, R>(a, lo + c * per_chunk, hi, K, ntiles, smem, bars, seq, seq_total);
+  if (rem > 0) {
+    const long long row0 = lo + full * per_chunk;
+    const int rr = (int)((rem + NT - 1) / NT);
+    if (R >= 4 && rr >= 4)
+      assign_chunk<L, NT, TK, (R >= 4 ? 4 : R)>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
+    else if (rr >= 3 && R >= 3)
+      assign_chunk<L, NT, TK, (R >= 3 ? 3 : R)>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
+    else if (rr >= 2)
+      assign_chunk<L, NT, TK, (R >= 2 ? 2 : R)>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
+    else
+      assign_chunk<L, NT, TK, 1>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
+  }
+}
+
+template <int L>
+static cudaError_t launch_fast_L(const KernelArgs& a, int sms, cudaStream_t s) {
+  constexpr int TK = FastCfg<L>::TK;
+  using TS = TileStream<L, TK>;
+  const int ntiles_max = (int)((a.kmax + TK - 1) / TK);
+  const size_t smem = TS::kBufBytes * (ntiles_max > 1 ? 2 : 1);
+  cudaError_t e = cudaFuncSetAttribute(assign_fast_kernel<L>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  assign_fast_kernel<L><<<sms, FastCfg<L>::NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// exact FP64 rows: one warp per row, lanes stride the codebook
+// ---------------------------------------------------------------------------
+
+template <typename XT>
+__global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT* __restrict__ X,
+                                                         int use_list) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = st->size;
+  const int dim = a.dim;
+  const double* cbg = a.cb[st->cur];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* scb = reinterpret_cast<double*>(smem_raw);
+  const bool in_smem = (size_t)K * dim * sizeof(double) <= 96 * 1024;
+  if (in_smem) {
+    for (int i = threadIdx.x; i < K * dim; i += blockDim.x) scb[i] = cbg[i];
+    __syncthreads();
+  }
+  const double* cb = in_smem ? scb : cbg;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long count = use_list ? (long long)st->flag_count : a.n;
+  for (long long i = gw; i < count; i += nw) {
+    const long long row = use_list ? (long long)a.flags[i] : i;
+    const XT* x = X + row * dim;
+    double best = INFINITY;
+    int bj = 0x7fffffff;
+    for (int j = lane; j < K; j += 32) {
+      double d = ref_dist(x, cb + (long long)j * dim, dim);
+      if (d < best) {  // ascending j within the lane: first minimum kept
+        best = d;
+        bj = j;
+      }
+    }
+    // lexicographic (d, j) minimum == the sequential strict-< scan's winner
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+      if (ob < best || (ob == best && oj < bj)) {
+        best = ob;
+        bj = oj;
+      }
+    }
+    if (lane == 0) a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
+  }
+}
+
+cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
+  size_t smem = 96 * 1024;
+  if (a.x32) {
+    cudaFuncSetAttribute(exact_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    exact_rows_kernel<float><<<sms * 2, 256, smem, s>>>(a, a.x32, 1);
+  } else {
+    cudaFuncSetAttribute(exact_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    exact_rows_kernel<double><<<sms * 2, 256, smem, s>>>(a, a.x64, 1);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s) {
+  if (fast) {
+    switch (a.dim) {
+      case 16: return launch_fast_L<16>(a, sms, s);
+      case 32: return launch_fast_L<32>(a, sms, s);
+      case 64: return launch_fast_L<64>(a, sms, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  size_t smem = 96 * 1024;
+  if (a.x32) {
+    cudaFuncSetAttribute(exact_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    exact_rows_kernel<float><<<sms * 2, 256, smem, s>>>(a, a.x32, 0);
+  } else {
+    cudaFuncSetAttribute(exact_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    exact_rows_kernel<double><<<sms * 2, 256, smem, s>>>(a, a.x64, 0);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// epilogue: exact winner distance, distortion tiles, fixed-point cell sums
+// ---------------------------------------------------------------------------
+
+enum Sink { kSinkWarp = 0, kSinkBlock = 1, kSinkGlobal = 2 };
+constexpr int kEpiSmem = 96 * 1024;
+
+template <typename XT>
+__global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, const XT* __restrict__ X,
+                                                              int want_dists, int want_sums,
+                                                              int zero_cells) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = zero_cells ? 1 : st->size;
+  const int dim = a.dim;
+  const int metric = st->metric;
+  const double* cb = a.cb[st->cur];
+  const double scale = ldexp(1.0, st->fixed_shift);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kEpiThreads / 32;
+
+  // Sink for the fixed-point sums, chosen by the CURRENT codebook size: warp
+  // private smem tables (small K, plain adds), one block table (smem
+  // atomics), or straight to the exchange buffer (large K, little contention).
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  long long* table = reinterpret_cast<long long*>(smem_raw);  // sums then counts
+  const long long twords = (long long)K * dim + K;
+  int sink = kSinkGlobal;
+  if (want_sums) {
+    if (twords * 8 * kWarps <= kEpiSmem)
+      sink = kSinkWarp;
+    else if (twords * 8 <= kEpiSmem)
+      sink = kSinkBlock;
+  }
+  __shared__ double red[kWarps];
+  if (want_sums && sink != kSinkGlobal) {
+    const long long total = (sink == kSinkWarp) ? twords * kWarps : twords;
+    for (long long i = threadIdx.x; i < total; i += blockDim.x) table[i] = 0;
+    __syncthreads();
+  }
+  long long* my_table = (sink == kSinkWarp) ? table + warp * twords : table;
+
+  const long long n = a.n;
+  const long long ntiles = (n + kTdTile - 1) / kTdTile;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long tbase = t * kTdTile;
+    double tsum = 0.0;
+    for (int r = 0; r < kTdTile / kEpiThreads; ++r) {
+      const long long row = tbase + (long long)r * kEpiThreads + threadIdx.x;
+      const bool valid = row < n;
+      int cell = 0;
+      double d = 0.0;
+      if (valid) {
+        cell = zero_cells ? 0 : a.idx[row];
+        if (!zero_cells) {
+          d = ref_dist(X + row * dim, cb + (long long)cell * dim, dim);
+          if (metric == kEuclidean) d = sqrt(d);
+          if (want_dists) a.dists[row] = d;
+        }
+      }
+      tsum = __dadd_rn(tsum, d);
+      if (want_sums) {
+        const unsigned active = __ballot_sync(0xffffffffu, valid);
+        const unsigned grp = __match_any_sync(0xffffffffu, valid ? cell : -1);
+        unsigned remaining = active;
+        const long long wrow0 = tbase + (long long)r * kEpiThreads + warp * 32;
+        while (remaining) {
+          const int leader = __ffs(remaining) - 1;
+          const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
+          const int c = __shfl_sync(0xffffffffu, cell, leader);
+          remaining &= ~members;
+          for (int l0 = 0; l0 < dim; l0 += 32) {
+            const int l = l0 + lane;
+            if (l < dim) {
+              long long acc = 0;
+              unsigned m = members;
+              while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                acc += to_fixed(load_x(X, (wrow0 + b) * dim + l), scale);
+              }
+              if (sink == kSinkWarp)
+                my_table[(long long)c * dim + l] += acc;
+              else if (sink == kSinkBlock)
+                atomicAdd(reinterpret_cast<unsigned long long*>(my_table + (long long)c * dim + l),
+                          (unsigned long long)acc);
+              else
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.ex.sums() + (long long)c * dim + l),
+                          (unsigned long long)acc);
+            }
+          }
+          if (lane == 0) {
+            const unsigned long long cntv = (unsigned long long)__popc(members);
+            if (sink == kSinkWarp)
+              my_table[(long long)K * dim + c] += (long long)cntv;
+            else if (sink == kSinkBlock)
+              atomicAdd(reinterpret_cast<unsigned long long*>(my_table + (long long)K * dim + c), cntv);
+            else
+              atomicAdd(reinterpret_cast<unsigned long long*>(a.ex.counts() + c), cntv);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (!zero_cells) {
+      // fixed tree: lanes (xor butterfly), then warps in order
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        tsum = __dadd_rn(tsum, __shfl_xor_sync(0xffffffffu, tsum, off));
+      if (lane == 0) red[warp] = tsum;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, red[w]);
+        a.ex.td()[a.tile0 + t] = __double_as_longlong(s);
+      }
+      __syncthreads();
+    }
+  }
+  if (want_sums && sink != kSinkGlobal) {
+    __syncthreads();
+    // merge tables into the exchange buffer (int64: any order is exact)
+    for (long long i = threadIdx.x; i < twords; i += blockDim.x) {
+      long long v = 0;
+      if (sink == kSinkWarp)
+        for (int w = 0; w < kWarps; ++w) v += table[w * twords + i];
+      else
+        v = table[i];
+      if (v != 0) {
+        long long* dst = (i < (long long)K * dim) ? a.ex.sums() + i : a.ex.counts() + (i - (long long)K * dim);
+        atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)v);
+      }
+    }
+  }
+}
+
+template <typename XT>
+static cudaError_t launch_epi_t(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
+                                bool zero_cells, int sms, cudaStream_t s) {
+  const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
+  int blocks = (int)(ntiles < (long long)sms * 2 ? ntiles : (long long)sms * 2);
+  if (blocks < 1) blocks = 1;
+  const size_t smem = want_sums ? kEpiSmem : 0;
+  cudaError_t e = cudaFuncSetAttribute(epilogue_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kEpiSmem);
+  if (e != cudaSuccess) return e;
+  epilogue_kernel<XT><<<blocks, kEpiThreads, smem, s>>>(a, X, want_dists, want_sums, zero_cells);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums, bool zero_cells,
+                            int sms, cudaStream_t s) {
+  if (a.x32) return launch_epi_t<float>(a, a.x32, want_dists, want_sums, zero_cells, sms, s);
+  return launch_epi_t<double>(a, a.x64, want_dists, want_sums, zero_cells, sms, s);
+}
+
+// ---------------------------------------------------------------------------
+// ordered update: the reference's own summation order (update_rows,
+// _kernels.py:47-58: members of cell i summed in ascending training index)
+// one thread per (cell, dim); writes the new codebook directly.
+// ---------------------------------------------------------------------------
+
+template <typename XT>
+__global__ void ordered_update_kernel(KernelArgs a, const XT* __restrict__ X) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = st->size;
+  const int dim = a.dim;
+  const double* old = a.cb[st->cur];
+  double* out = a.cb[st->cur ^ 1];
+  const long long n = a.n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)K * dim;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t / dim), l = (int)(t % dim);
+    double s = 0.0;
+    long long cnt = 0;
+    for (long long j = 0; j < n; ++j) {
+      if (a.idx[j] == k) {
+        s = __dadd_rn(s, load_x(X, j * dim + l));
+        ++cnt;
+      }
+    }
+    out[t] = cnt > 0 ? __ddiv_rn(s, (double)cnt) : old[t];
+    if (l == 0) a.ex.counts()[k] = cnt;
+  }
+}
+
+cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s) {
+  long long work = a.kmax * a.dim;
+  int blocks = (int)((work + 127) / 128);
+  if (blocks > 4096) blocks = 4096;
+  if (a.x32)
+    ordered_update_kernel<float><<<blocks, 128, 0, s>>>(a, a.x32);
+  else
+    ordered_update_kernel<double><<<blocks, 128, 0, s>>>(a, a.x64);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// finalize: one block.  phase 0 = after the initial column-sum pass,
+// phase 1 = after an allocation pass.
+// ---------------------------------------------------------------------------
+
+__device__ void record_hist(DevState* st, int size, int it, double td, long long empty) {
+  if (st->n_hist < kMaxHist) {
+    HistRec& h = st->hist[st->n_hist];
+    h.size = size;
+    h.iteration = it;
+    h.td = td;
+    h.empty = empty;
+    h.t_ns = globaltimer();
+  }
+  st->n_hist += 1;
+}
+
+__global__ void __launch_bounds__(1024) finalize_kernel(KernelArgs a, int phase) {
+  DevState* st = a.st;
+  if (st->done) return;
+  if (threadIdx.x == 0) st->flagged_total += st->flag_count;
+  __shared__ int s_action;  // 0 none, 1 update, 2 split-after(cur), 3 update+split, 4 done
+  __shared__ double s_td;
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const int dim = a.dim;
+  const double inv_scale = ldexp(1.0, -st->fixed_shift);
+
+  if (phase == 0) {
+    // global centroid: column sums / m (core.py:380 / parallel.py:273)
+    double* cb = a.cb[st->cur];
+    if (!st->ordered) {
+      for (int l = tid; l < dim; l += blockDim.x)
+        cb[l] = __ddiv_rn((double)a.ex.sums()[l] * inv_scale, (double)st->n_global);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      st->t0_ns = globaltimer();
+      if (st->ordered) st->cur ^= 1;  // ordered_update wrote the centroid there
+    }
+    __syncthreads();
+    // split or final-assign setup happens below via the same split code
+    if (st->target <= 1) {
+      if (tid == 0) {
+        st->mode = kModeFinalAssign;
+        st->size = 1;
+      }
+      goto clear;
+    }
+    if (tid == 0) s_action = 2;
+    __syncthreads();
+    goto apply;
+  }
+
+  if (st->mode == kModeUpdateOnly) {
+    if (tid == 0) s_action = 1;
+    __syncthreads();
+    goto update;
+  }
+  {
+    // ---- distortion of this pass
+    double td;
+    if (st->ordered) {
+      if (tid == 0) {
+        double s = 0.0;  // _kernels.sum_inorder (_kernels.py:92-98)
+        for (long long i = 0; i < a.n; ++i) s = __dadd_rn(s, a.dists[i]);
+        s_td = s;
+      }
+    } else {
+      const long long nt = a.ex.ntiles;
+      const long long per = (nt + blockDim.x - 1) / blockDim.x;
+      double s = 0.0;
+      for (long long i = tid * per; i < (tid + 1) * per && i < nt; ++i)
+        s = __dadd_rn(s, __longlong_as_double(a.ex.td()[i]));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+      if ((tid & 31) == 0) red[tid >> 5] = s;
+      __syncthreads();
+      if (tid == 0) {
+        double t2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t2 = __dadd_rn(t2, red[w]);
+        s_td = t2;
+      }
+    }
+    __syncthreads();
+    td = s_td;
+    const int K = st->size;
+    if (tid == 0) {
+      st->passes += 1;
+      st->evals += a.n * (long long)K;
+      st->last_td = td;
+    }
+    if (st->mode == kModeFinalAssign || st->mode == kModeAssignOnly) {
+      if (tid == 0) {
+        st->total = td;
+        st->done = 1;
+      }
+      return;
+    }
+    if (st->mode == kModeLloydStep) {
+      if (tid == 0) {
+        st->total = td;
+        s_action = 1;
+      }
+      __syncthreads();
+      goto update;
+    }
+    // ---- convergence test (core.py:342-356) -- only tid 0 decides
+    if (tid == 0) {
+      const double p = st->td_prev;
+      bool conv;
+      if (isinf(p))
+        conv = false;
+      else if (p == 0.0)
+        conv = true;
+      else
+        conv = __ddiv_rn(__dsub_rn(p, td), p) <= st->eps;
+      s_action = conv ? 2 : 1;
+    }
+    __syncthreads();
+    if (s_action != 1) {
+      if (tid == 0) record_hist(st, K, st->iteration, td, 0);
+      __syncthreads();
+      goto apply;
+    }
+  }
+
+update:
+  {
+    // centroid update (update_rows _kernels.py:59-66): sum / n, empty keeps old
+    const int K = st->size;
+    const double* old = a.cb[st->cur];
+    double* out = a.cb[st->cur ^ 1];
+    int empty = 0;
+    for (int k = tid; k < K; k += blockDim.x) {
+      const long long cnt = a.ex.counts()[k];
+      if (cnt == 0) ++empty;
+      if (!st->ordered) {
+        for (int l = 0; l < dim; ++l) {
+          const long long idx = (long long)k * dim + l;
+          out[idx] = cnt > 0 ? __ddiv_rn((double)a.ex.sums()[idx] * inv_scale, (double)cnt) : old[idx];
+        }
+      }
+    }
+    // empties: block reduction (integer, order-free)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) empty += __shfl_xor_sync(0xffffffffu, empty, off);
+    if ((tid & 31) == 0) red[tid >> 5] = (double)empty;
+    __syncthreads();
+    if (tid == 0) {
+      long long e = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) e += (long long)red[w];
+      st->last_empty = e;
+      st->cur ^= 1;
+      if (st->mode == kModeUpdateOnly || st->mode == kModeLloydStep) {
+        st->done = 1;
+        s_action = 0;
+      } else {
+        record_hist(st, K, st->iteration, st->last_td, e);
+        st->td_prev = st->last_td;
+        st->iteration += 1;
+        if (st->iteration > st->max_iter) {
+          // guard exhausted: warning, level ends with the UPDATED codebook
+          // (core.py:400-415); the total stays the pre-update TD.
+          if (st->n_warn < kMaxWarn) st->warn_sizes[st->n_warn] = K;
+          st->n_warn += 1;
+          s_action = 2;
+        } else {
+          s_action = 0;
+        }
+      }
+    }
+    __syncthreads();
+    if (st->mode == kModeUpdateOnly || st->mode == kModeLloydStep) return;
+  }
+
+apply:
+  if (s_action == 2) {
+    const int K = st->size;
+    if (K < st->target) {
+      // split (core.py:277-281): row i -> 2i (+delta), 2i+1 (-delta)
+      const double* src = a.cb[st->cur];
+      double* dst = a.cb[st->cur ^ 1];
+      const double delta = st->delta;
+      for (long long i = tid; i < (long long)K * dim; i += blockDim.x) {
+        const long long k = i / dim, l = i % dim;
+        dst[(2 * k) * dim + l] = __dadd_rn(src[i], delta);
+        dst[(2 * k + 1) * dim + l] = __dsub_rn(src[i], delta);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        st->cur ^= 1;
+        st->size = 2 * K;
+        st->iteration = 1;
+        st->td_prev = INFINITY;
+      }
+    } else {
+      if (tid == 0) {
+        st->total = st->last_td;
+        st->done = 1;
+      }
+    }
+  }
+
+clear:
+  __syncthreads();
+  // zero the exchange buffer for the next pass
+  for (long long i = tid; i < a.ex.words(); i += blockDim.x) a.ex.base[i] = 0;
+  if (tid == 0) st->flag_count = 0;
+}
+
+cudaError_t launch_finalize(const KernelArgs& a, cudaStream_t s) {
+  finalize_kernel<<<1, 1024, 0, s>>>(a, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_centroid(const KernelArgs& a, cudaStream_t s) {
+  finalize_kernel<<<1, 1024, 0, s>>>(a, 0);
+  return cudaGetLastError();
+}
+
+__global__ void clear_kernel(KernelArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.ex.words();
+       i += (long long)gridDim.x * blockDim.x)
+    a.ex.base[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.st->flag_count = 0;
+}
+
+cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s) {
+  clear_kernel<<<64, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// misc
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void maxabs_kernel(const T* x, long long count, unsigned long long* out) {
+  double m = 0.0;
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = fabs((double)x[i]);
+    if (!(v <= DBL_MAX)) bad = true;
+    m = fmax(m, v);
+  }
+  unsigned long long bits = bad ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(m);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    unsigned long long o = __shfl_xor_sync(0xffffffffu, bits, off);
+    bits = o > bits ? o : bits;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, bits);
+}
+
+cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
+                          unsigned long long* out_bits, int sms, cudaStream_t s) {
+  if (x32)
+    maxabs_kernel<float><<<sms * 4, 256, 0, s>>>(x32, count, out_bits);
+  else
+    maxabs_kernel<double><<<sms * 4, 256, 0, s>>>(x64, count, out_bits);
+  return cudaGetLastError();
+}
+
+__global__ void sum_inorder_kernel(const double* v, long long n, double* out) {
+  double s = 0.0;
+  for (long long i = 0; i < n; ++i) s = __dadd_rn(s, v[i]);
+  *out = s;
+}
+
+cudaError_t launch_sum_inorder(const double* v, long long n, double* out, cudaStream_t s) {
+  sum_inorder_kernel<<<1, 1, 0, s>>>(v, n, out);
+  return cudaGetLastError();
+}
+
+// reset the per-call state (one-shot assign / update / Lloyd step calls)
+__global__ void reset_kernel(DevState* st, int mode, int size, int metric, int ordered,
+                             int keep_cur) {
+  st->mode = mode;
+  st->size = size;
+  st->metric = metric;
+  st->ordered = ordered;
+  st->done = 0;
+  if (!keep_cur) st->cur = 0;
+  st->flag_count = 0;
+  st->iteration = 1;
+  st->td_prev = INFINITY;
+  if (!keep_cur) {
+    st->n_hist = 0;
+    st->n_warn = 0;
+    st->passes = 0;
+    st->evals = 0;
+    st->flagged_total = 0;
+  }
+}
+
+cudaError_t launch_reset(DevState* st, int mode, int size, int metric, int ordered, int keep_cur,
+                         cudaStream_t s) {
+  reset_kernel<<<1, 1, 0, s>>>(st, mode, size, metric, ordered, keep_cur);
+  return cudaGetLastError();
+}
+
+__global__ void cells_to_idx_kernel(const long long* cells, int* idx, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    idx[i] = (int)cells[i];
+}
+
+cudaError_t launch_cells_to_idx(const long long* cells, int* idx, long long n, int sms, cudaStream_t s) {
+  cells_to_idx_kernel<<<sms * 4, 256, 0, s>>>(cells, idx, n);
+  return cudaGetLastError();
+}
+
+// float64 rows that are exactly float32 (the usual case: TrainingSet widens
+// float32 / 8-bit data, core.py:47-60) take the FP32 candidate path.
+__global__ void f64_to_f32_kernel(const double* x64, float* x32, long long count, int* inexact) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = x64[i];
+    const float f = (float)v;
+    x32[i] = f;
+    if (!((double)f == v)) bad = 1;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(inexact, 1);
+}
+
+cudaError_t launch_f64_to_f32_exact(const double* x64, float* x32, long long count, int* inexact,
+                                    int sms, cudaStream_t s) {
+  f64_to_f32_kernel<<<sms * 4, 256, 0, s>>>(x64, x32, count, inexact);
+  return cudaGetLastError();
+}
+
+// _kernels.column_sums (_kernels.py:81-89): ascending rows, one thread per column
+template <typename XT>
+__global__ void column_sums_kernel(const XT* x, long long m, int dim, double* out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= dim) return;
+  double s = 0.0;
+  for (long long j = 0; j < m; ++j) s = __dadd_rn(s, load_x(x, j * dim + l));
+  out[l] = s;
+}
+
+cudaError_t launch_column_sums_ordered(const double* x64, const float* x32, long long m, int dim,
+                                       double* out, cudaStream_t s) {
+  const int blocks = (dim + 63) / 64;
+  if (x32)
+    column_sums_kernel<float><<<blocks, 64, 0, s>>>(x32, m, dim, out);
+  else
+    column_sums_kernel<double><<<blocks, 64, 0, s>>>(x64, m, dim, out);
+  return cudaGetLastError();
+}
+
+// _kernels.pair_distance (_kernels.py:69-78)
+__global__ void pair_distance_kernel(const double* a, const double* b, int dim, int metric,
+                                     double* out) {
+  double d = ref_dist(a, b, dim);
+  *out = metric == kEuclidean ? sqrt(d) : d;
+}
+
+cudaError_t launch_pair_distance(const double* a, const double* b, int dim, int metric, double* out,
+                                 cudaStream_t s) {
+  pair_distance_kernel<<<1, 1, 0, s>>>(a, b, dim, metric, out);
+  return cudaGetLastError();
+}
+
+}  // namespace vqb

@@ -1,0 +1,165 @@
+// FP32/FP64 pipe microbenchmarks: the measured denominator for the roofline
+// of the distance pass (BASELINE.md section 4 asks for a measured FFMA peak
+// beside the nominal SMs x 128 x 2 x f_clk).  Each kernel runs independent
+// dependency chains so the pipe, not latency, is the limit.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vqb200_internal.h"
+
+namespace vqb {
+
+template <int CHAINS>
+__global__ void __launch_bounds__(256) ffma_kernel(float* out, int iters, float a, float b) {
+  float acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-7f + c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) acc[c] = fmaf(acc[c], a, b);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 123.456f) out[0] = s;
+}
+
+// packed f32x2 FMA (sm_100+: FFMA2)
+template <int CHAINS>
+__global__ void __launch_bounds__(256) ffma2_kernel(float* out, int iters, float a, float b) {
+  unsigned long long acc[CHAINS];
+  float2 av = make_float2(a, a), bv = make_float2(b, b);
+  unsigned long long ab = *reinterpret_cast<unsigned long long*>(&av);
+  unsigned long long bb = *reinterpret_cast<unsigned long long*>(&bv);
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    float2 v = make_float2(threadIdx.x * 1e-7f + c, c * 0.5f);
+    acc[c] = *reinterpret_cast<unsigned long long*>(&v);
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c)
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(acc[c]) : "l"(ab), "l"(bb));
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    float2 v = *reinterpret_cast<float2*>(&acc[c]);
+    s += v.x + v.y;
+  }
+  if (s == 123.456f) out[0] = s;
+}
+
+// 16 FFMA + top-2 bookkeeping (FSETP, SEL, 3 FMNMX) per "eval": the
+// expanded-form distance inner loop shape, to measure ALU co-issue.
+template <int CHAINS>
+__global__ void __launch_bounds__(256) mix_kernel(float* out, int iters, float a, float b) {
+  float acc[CHAINS], m1[CHAINS], m2[CHAINS];
+  int i1[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    acc[c] = threadIdx.x * 1e-7f + c;
+    m1[c] = 3e38f;
+    m2[c] = 3e38f;
+    i1[c] = 0;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) {
+      float v = acc[c];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v = fmaf(v, a, b);
+      acc[c] = v;
+      m2[c] = fminf(m2[c], fmaxf(m1[c], v));
+      bool p = v < m1[c];
+      m1[c] = fminf(m1[c], v);
+      i1[c] = p ? it : i1[c];
+    }
+  }
+  float s = 0.f;
+  int si = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    s += m1[c] + m2[c];
+    si += i1[c];
+  }
+  if (s == 123.456f || si == -7) out[0] = s + si;
+}
+
+template <int CHAINS>
+__global__ void __launch_bounds__(256) dadd_kernel(double* out, int iters, double b) {
+  double acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-7 + c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) acc[c] = __dadd_rn(acc[c], b);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 123.456) out[0] = s;
+}
+
+}  // namespace vqb
+
+using namespace vqb;
+
+// Returns achieved lane-ops/s (FMA counted once) for pipe `which`:
+// 0 = FFMA, 1 = FFMA2 (2 lane-ops per instruction), 2 = 16xFFMA + top-2 mix
+// (counts the 16 FFMA only), 3 = DADD.  `seconds` gets the kernel time.
+extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
+                                   double* seconds) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int threads = 256;
+  const int blocks = sms * blocks_per_sm;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, 64) != cudaSuccess) return 4;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double lane_ops = 0;
+  for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+    cudaEventRecord(e0);
+    switch (which) {
+      case 0:
+        ffma_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.999f, 1e-3f);
+        lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
+        break;
+      case 1:
+        ffma2_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.999f, 1e-3f);
+        lane_ops = 2.0 * blocks * threads * iters * 16 * 8;
+        break;
+      case 2:
+        mix_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.999f, 1e-3f);
+        lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
+        break;
+      default:
+        dadd_kernel<8><<<blocks, threads>>>((double*)buf, iters, 1e-3);
+        lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
+        break;
+    }
+    cudaEventRecord(e1);
+  }
+  cudaError_t err = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  if (err != cudaSuccess) return 4;
+  *seconds = ms * 1e-3;
+  *ops_per_s = lane_ops / (ms * 1e-3);
+  return 0;
+}

@@ -1,0 +1,129 @@
+// Internal declarations shared by the kernels (kernels.cu) and the C-ABI /
+// native training loop (api.cu).  Not part of the public ABI: that is
+// include/vqb200.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace vqb {
+
+constexpr int kMaxHist = 8192;   // levels x max_iterations_per_level records
+constexpr int kMaxWarn = 64;     // one warning per level at most
+constexpr int kTdTile = 2048;    // rows per distortion partial (fixed, global)
+constexpr int kEpiThreads = 256; // epilogue block: 8 rows per thread per tile
+
+// metric codes (reference _kernels.py:14-15)
+constexpr int kSquared = 0;
+constexpr int kEuclidean = 1;
+
+// device loop modes
+constexpr int kModeTrain = 0;       // split + Lloyd loop (core.py:384-415)
+constexpr int kModeFinalAssign = 1; // target_size == 1 (core.py:417-422)
+constexpr int kModeAssignOnly = 2;  // assign_cells / encode with a fixed codebook
+constexpr int kModeUpdateOnly = 3;  // update_codebook for a given cell table
+constexpr int kModeLloydStep = 4;   // one assign + update pass, no convergence logic
+
+struct HistRec {
+  int size;
+  int iteration;
+  double td;
+  long long empty;
+  unsigned long long t_ns;
+};
+
+// Loop state, resident on the device; every kernel of a pass reads it so the
+// host never needs to know the current codebook size (passes can be enqueued
+// speculatively and early-exit once `done` is set).
+struct DevState {
+  // configuration
+  int target;
+  int max_iter;
+  int metric;
+  int fixed_shift;     // sums are int64 fixed point with 2^-fixed_shift resolution
+  double eps;
+  double delta;
+  long long n_global;  // rows over all shards (for the centroid of size 1)
+  int mode;
+  int ordered;         // 1: reference-order update/TD kernels (bit-identical, slow)
+  // progress
+  int size;
+  int iteration;
+  int done;
+  int cur;             // which codebook buffer holds the current codebook
+  double td_prev;
+  double total;
+  double last_td;
+  long long last_empty;
+  int n_hist;
+  int n_warn;
+  int warn_sizes[kMaxWarn];
+  int flag_count;      // rows queued for the FP64 re-rank this pass
+  unsigned int cmax_bits;  // float bits of max_j ||c~_j|| (centred FP32 codebook)
+  int passes;          // allocation passes executed
+  long long flagged_total;  // rows re-ranked over the whole run (diagnostic)
+  long long evals;     // sum over passes of rows * size (this shard)
+  unsigned long long t0_ns;  // %globaltimer at the initial centroid
+  HistRec hist[kMaxHist];
+};
+
+// Packed exchange buffer (int64 words), one allreduce per pass in the
+// multi-GPU loop: [sums K*L | counts K | td tile partials (FP64 bit patterns,
+// zero on tiles another rank owns)].
+struct Exchange {
+  long long* base;
+  long long kmax;
+  long long dim;
+  long long ntiles;
+  __host__ __device__ long long* sums() const { return base; }
+  __host__ __device__ long long* counts() const { return base + kmax * dim; }
+  __host__ __device__ long long* td() const { return base + kmax * dim + kmax; }
+  __host__ __device__ long long words() const { return kmax * dim + kmax + ntiles; }
+};
+
+struct KernelArgs {
+  // training data (this shard): exactly one of x32/x64 is non-null
+  const float* x32;
+  const double* x64;
+  long long n;          // local rows
+  int dim;
+  long long tile0;      // global index of this shard's first TD tile
+  const float* mu;      // centring vector (FP32, dim)
+  // codebooks
+  double* cb[2];        // FP64 master, double buffered, kmax x dim
+  float* w;             // -2 * c~ (FP32), kpad x dim
+  float* nrm;           // ||c~||^2 (FP32), kpad
+  long long kmax;
+  // per-row outputs
+  int* idx;
+  int* flags;
+  double* dists;        // nullable
+  Exchange ex;
+  DevState* st;
+};
+
+// kernel launchers (kernels.cu); all asynchronous on `stream`
+cudaError_t launch_prep_codebook(const KernelArgs& a, cudaStream_t s);
+cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s);
+cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums, bool zero_cells,
+                            int sms, cudaStream_t s);
+cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s);
+cudaError_t launch_finalize(const KernelArgs& a, cudaStream_t s);
+cudaError_t launch_init_centroid(const KernelArgs& a, cudaStream_t s);
+cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s);
+cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
+                          unsigned long long* out_bits, int sms, cudaStream_t s);
+cudaError_t launch_sum_inorder(const double* v, long long n, double* out, cudaStream_t s);
+cudaError_t launch_reset(DevState* st, int mode, int size, int metric, int ordered, int keep_cur,
+                         cudaStream_t s);
+cudaError_t launch_cells_to_idx(const long long* cells, int* idx, long long n, int sms, cudaStream_t s);
+cudaError_t launch_f64_to_f32_exact(const double* x64, float* x32, long long count, int* inexact,
+                                    int sms, cudaStream_t s);
+cudaError_t launch_column_sums_ordered(const double* x64, const float* x32, long long m, int dim,
+                                       double* out, cudaStream_t s);
+cudaError_t launch_pair_distance(const double* a, const double* b, int dim, int metric, double* out,
+                                 cudaStream_t s);
+bool fast_dim_supported(int dim);
+
+}  // namespace vqb

@@ -1,0 +1,228 @@
+"""Multi-GPU LBG: one process per GPU, torch.distributed (NCCL) for the one
+exchange per pass.
+
+The reference's master/slave shared-memory scheme (parallel.py:256-329;
+PAPER.md section 4: workers allocate disjoint chunks, the master integrates
+tables and distortions) maps onto ranks as follows:
+
+* rows are sharded into contiguous, tile-aligned ranges (``ShardPlan``; a tile
+  is the 2048-row unit of the fixed distortion tree, so shard boundaries never
+  split a tile and the result is bit-identical for every world size);
+* every rank holds a codebook replica and runs allocation + epilogue on its
+  shard (the C ABI's ``vqb_step_local``);
+* the partial cell tables never move: each rank reduces them on the device
+  into one packed int64 buffer [K*L fixed-point sums | K counts | distortion
+  tile partials] and ONE ``all_reduce(SUM)`` over NVLink combines them --
+  integer addition is exact, so the combined buffer is identical on every
+  rank and for every world size;
+* every rank then runs the same finalize (convergence test, centroids, split)
+  on identical bits, so the "master" is implicit and no broadcast is needed.
+
+The driver (``run_sharded``) is backend-agnostic so its collective logic is
+tested on CPU with gloo (tests/test_distributed.py); ``DeviceShard`` is the
+B200 backend over libvqb200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+TILE = 2048  # vqb200_internal.h kTdTile
+
+
+def world_size() -> int:
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size()
+    return 1
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Contiguous tile-aligned row shards; the first (tiles mod world) ranks
+    take one extra tile (the reference's partition rule, parallel.py:93-107,
+    applied to 2048-row tiles)."""
+
+    n: int
+    world: int
+
+    @property
+    def tiles(self) -> int:
+        return -(-self.n // TILE)
+
+    def bounds(self, rank: int) -> tuple[int, int]:
+        base, extra = divmod(self.tiles, self.world)
+        t0 = rank * base + min(rank, extra)
+        t1 = t0 + base + (1 if rank < extra else 0)
+        return min(self.n, t0 * TILE), min(self.n, t1 * TILE)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device buffer (zero-copy into torch)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {
+            "shape": (count,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+
+
+class DeviceShard:
+    """B200 backend: one vqb_session over this rank's rows."""
+
+    def __init__(self, rows: np.ndarray, row_offset: int, n_global: int, device: int):
+        from .core import _Session
+
+        x32 = rows if rows.dtype == np.float32 else None
+        x64 = None if x32 is not None else np.ascontiguousarray(rows, dtype=np.float64)
+        self.s = _Session(x32, x64, device=device, row_offset=row_offset, n_global=n_global)
+        self.device = device
+        self.L = _lib.lib()
+        import torch
+
+        self.torch = torch
+        # run our kernels on torch's stream so NCCL and the passes are ordered
+        stream = torch.cuda.current_stream(device)
+        _lib.check(self.L.vqb_set_stream(self.s.handle, ctypes.c_void_p(stream.cuda_stream)))
+        self._ex = None
+
+    def maxabs(self) -> float:
+        return self.s.maxabs()
+
+    def tensor(self, values):
+        return self.torch.tensor(values, dtype=self.torch.float64, device=f"cuda:{self.device}")
+
+    def begin(self, config, global_maxabs: float) -> None:
+        from .core import metric_code
+
+        self.config = config
+        cfg = _lib.TrainConfig(config.target_size, config.epsilon, config.delta,
+                               config.max_iterations_per_level,
+                               metric_code(config.distortion_metric), 0, global_maxabs)
+        self._cfg = cfg
+        _lib.check(self.L.vqb_step_begin(self.s.handle, ctypes.byref(cfg)))
+
+    def exchange(self):
+        if self._ex is None:
+            p = ctypes.POINTER(ctypes.c_int64)()
+            n = ctypes.c_int64()
+            _lib.check(self.L.vqb_step_exchange(self.s.handle, ctypes.byref(p), ctypes.byref(n)))
+            addr = ctypes.cast(p, ctypes.c_void_p).value
+            self._ex = self.torch.as_tensor(_CudaArray(addr, int(n.value)),
+                                            device=f"cuda:{self.device}")
+        return self._ex
+
+    def local(self) -> None:
+        _lib.check(self.L.vqb_step_local(self.s.handle))
+
+    def finalize(self) -> None:
+        _lib.check(self.L.vqb_step_finalize(self.s.handle))
+
+    def poll(self) -> bool:
+        d = ctypes.c_int()
+        _lib.check(self.L.vqb_step_poll(self.s.handle, ctypes.byref(d)))
+        return bool(d.value)
+
+    def result(self):
+        from .core import LevelIteration, _max_iter_warning
+
+        config = self.config
+        levels = max(1, int(math.log2(config.target_size)))
+        cap = levels * config.max_iterations_per_level + 8
+        hist = (_lib.LevelIterationC * cap)()
+        warn = np.zeros(64, dtype=np.int64)
+        cb = np.empty((config.target_size, self.s.dim), dtype=np.float64)
+        dists = np.empty(self.s.rows, dtype=np.float64)
+        summ = _lib.TrainSummary()
+        _lib.check(self.L.vqb_step_result(self.s.handle, _lib.ptr(cb), hist, cap, _lib.ptr(warn), 64,
+                                          _lib.ptr(dists), ctypes.byref(summ)))
+        history = [LevelIteration(int(h.codebook_size), int(h.iteration), float(h.td),
+                                  int(h.empty_cells), float(h.seconds))
+                   for h in hist[: int(summ.n_hist)]]
+        warnings = [_max_iter_warning(int(s), config.max_iterations_per_level)
+                    for s in warn[: int(summ.n_warn)]]
+        return cb[: int(summ.final_size)], history, warnings, float(summ.total), dists
+
+
+def run_sharded(backend, config, batch: int = 4):
+    """Drive the pass loop on every rank.  Collectives: one MAX allreduce of
+    |x| (common fixed-point scale), then per pass one SUM allreduce of the
+    packed int64 exchange buffer.  Ranks stay in lockstep because every rank
+    derives `done` from identical combined bits."""
+    import torch.distributed as dist
+
+    gmax = backend.tensor([backend.maxabs()])
+    dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+    backend.begin(config, float(gmax.item()))
+    ex = backend.exchange()
+    dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+    backend.finalize()
+    levels = max(1, int(math.log2(config.target_size)))
+    limit = (levels + 1) * (config.max_iterations_per_level + 1) + 2 * batch
+    passes = 0
+    while True:
+        for _ in range(batch):
+            backend.local()
+            dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+            backend.finalize()
+        passes += batch
+        if backend.poll():
+            break
+        if passes > limit:
+            from .errors import InternalError
+
+            raise InternalError(f"sharded training did not terminate after {passes} passes")
+    return backend.result()
+
+
+def gather_rows(local: np.ndarray, plan: ShardPlan, device: str | None):
+    """All-gather this rank's per-row values into the global order."""
+    import torch
+    import torch.distributed as dist
+
+    world = plan.world
+    longest = max(hi - lo for lo, hi in (plan.bounds(r) for r in range(world)))
+    buf = torch.zeros(longest, dtype=torch.float64, device=device)
+    buf[: local.shape[0]] = torch.from_numpy(local).to(device)
+    parts = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    out = np.empty(plan.n, dtype=np.float64)
+    for r in range(world):
+        lo, hi = plan.bounds(r)
+        out[lo:hi] = parts[r][: hi - lo].cpu().numpy()
+    return out
+
+
+def sharded_lbg_train(ts, config, backend_factory=None):
+    """parallel_lbg_train over all ranks of the default process group."""
+    import torch
+    import torch.distributed as dist
+
+    from .core import Codebook, DistortionStats
+    from .parallel import _inorder, partition_training
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    plan = ShardPlan(ts.m, world)
+    lo, hi = plan.bounds(rank)
+    x32 = ts.__dict__.get("_x32")
+    rows = (x32 if x32 is not None else ts.vectors)[lo:hi]
+    if backend_factory is None:
+        device = torch.cuda.current_device()
+        backend = DeviceShard(np.ascontiguousarray(rows), lo, ts.m, device)
+        gdev = f"cuda:{device}"
+    else:
+        backend = backend_factory(rows, lo, ts.m)
+        gdev = None
+    cb, history, warnings, total, dists = run_sharded(backend, config)
+    all_dists = gather_rows(dists, plan, gdev)
+    per_worker = [_inorder(all_dists[a:b]) for a, b in partition_training(ts.m, config.workers).ranges]
+    stats = DistortionStats(per_worker=per_worker, total=total, history=history,
+                            warnings=warnings, vector_count=ts.m)
+    return Codebook(cb), stats

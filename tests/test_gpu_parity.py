@@ -1,0 +1,229 @@
+"""Parity of the B200 path (libvqb200.so through the drop-in API) against the
+reference's golden vectors and the CPU oracle.  GPU only."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import cases
+import oracle
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+vq = pytest.importorskip("paper_0910_4711_b200")
+
+
+def _golden(name):
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{name} golden not generated")
+    return np.load(path)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    from paper_0910_4711_b200 import _lib
+    if _lib.device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device")
+
+
+# ---------------------------------------------------------------------------
+# allocation: indices and per-row FP64 distances bit-exact
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(len(cases.assign_cases())))
+def test_assign_matches_reference(golden_small, i):
+    case = cases.assign_cases()[i]
+    metric = ["squared_euclidean", "euclidean"][case["metric"]]
+    table, total = vq.assign_cells(case["x"], vq.Codebook(case["cb"]), metric=metric)
+    assert table.cells.dtype == np.int64
+    assert np.array_equal(table.cells, golden_small[f"assign{i}_cells"])
+    # chunks <= 2^20 rows: the total is accumulated in input order, as the reference
+    assert total == float(golden_small[f"assign{i}_total"])
+
+
+@pytest.mark.parametrize("i", range(len(cases.assign_cases())))
+def test_assign_dists_bit_exact(golden_small, i):
+    case = cases.assign_cases()[i]
+    from paper_0910_4711_b200.core import _session_of, _matrix_keep_f32
+    _, dists, _ = _session_of(_matrix_keep_f32(case["x"])).assign(case["cb"], case["metric"])
+    assert dists.tobytes() == golden_small[f"assign{i}_dists"].tobytes()
+
+
+def test_assign_float32_input_uses_fast_path_and_matches():
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, 255, (50000, 16)).astype(np.float32)
+    cb = rng.uniform(0, 255, (1024, 16))
+    cells, dists = oracle.assign_all(x.astype(np.float64), cb, workers=8)
+    table, _ = vq.assign_cells(x, vq.Codebook(cb))
+    assert np.array_equal(table.cells, cells)
+
+
+@pytest.mark.parametrize("dim,k", [(16, 2), (16, 4096), (32, 300), (64, 512), (64, 1)])
+def test_assign_shapes_vs_oracle(dim, k):
+    rng = np.random.default_rng(dim * 1000 + k)
+    x = rng.integers(0, 256, (20000, dim)).astype(np.float32)
+    cb = x[rng.choice(20000, k, replace=False)].astype(np.float64) + 0.5
+    cells, _ = oracle.assign_all(x.astype(np.float64), cb, workers=8)
+    table, _ = vq.assign_cells(x, vq.Codebook(cb))
+    assert np.array_equal(table.cells, cells)
+
+
+def test_first_split_tie_density_exact():
+    """K=2 additive split of a GMM centroid: the tie-densest point of the whole
+    design.  Indices must still be bit-exact."""
+    from paper_0910_4711_b200 import synthetic
+    x = synthetic.make_training("cfg2", n=1 << 18)
+    x64 = x.astype(np.float64)
+    c = oracle.column_sums(x64) / x.shape[0]
+    cb = oracle.split_rows(c.reshape(1, -1), 0.01)
+    cells, _ = oracle.assign_all(x64, cb, workers=8)
+    table, _ = vq.assign_cells(x, vq.Codebook(cb))
+    assert np.array_equal(table.cells, cells)
+
+
+# ---------------------------------------------------------------------------
+# update
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(len(cases.update_cases())))
+def test_update_matches_reference(golden_small, i):
+    case = cases.update_cases()[i]
+    ts = vq.TrainingSet(case["x"])
+    table = vq.CellTable(case["cells"], case["cb"].shape[0])
+    cb, empty = vq.update_codebook(ts, table, vq.Codebook(case["cb"]))
+    want = golden_small[f"update{i}_cb"]
+    assert empty == int(np.count_nonzero(golden_small[f"update{i}_counts"] == 0))
+    if i == 5:
+        # tiny and large magnitudes in one huge cell: the reference's sequential
+        # sum rounds, the device's exact fixed-point sum does not -> ulps apart
+        np.testing.assert_allclose(cb.codevectors, want, rtol=1e-13, atol=1e-13)
+    else:
+        assert cb.codevectors.tobytes() == want.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# full designs
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(len(cases.design_cases())))
+def test_design_matches_reference(golden_small, i):
+    case = cases.design_cases()[i]
+    cfg = vq.LbgConfig(**case["config"])
+    cb, stats = vq.parallel_lbg_train(vq.TrainingSet(case["x"]), cfg)
+    hist = np.array([(h.codebook_size, h.iteration, h.td, h.empty_cells) for h in stats.history],
+                    dtype=np.float64).reshape(-1, 4)
+    want_hist = golden_small[f"design{i}_hist"]
+    assert hist.shape == want_hist.shape
+    assert np.array_equal(hist[:, [0, 1, 3]], want_hist[:, [0, 1, 3]])
+    np.testing.assert_allclose(hist[:, 2], want_hist[:, 2], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(cb.codevectors, golden_small[f"design{i}_cb"], rtol=1e-12, atol=1e-12)
+    assert len(stats.warnings) == int(golden_small[f"design{i}_nwarn"])
+    np.testing.assert_allclose(stats.per_worker, golden_small[f"design{i}_per_worker"], rtol=1e-12)
+
+
+def test_trace_kat_exact():
+    trace = vq.TrainingSet(np.array([[0.0, 0.0], [0.0, 1.0], [4.0, 0.0], [4.0, 1.0]]))
+    cb, stats = vq.lbg_train(trace, vq.LbgConfig(target_size=2, epsilon=1e-3, delta=0.5))
+    assert cb.codevectors.tolist() == [[4.0, 0.5], [0.0, 0.5]]
+    assert stats.total == 1.0
+    assert stats.td_history() == [(2, 1, 11.0), (2, 2, 1.0), (2, 3, 1.0)]
+    assert stats.mean == 0.25
+
+
+def _design_check(cfg_name, g, x, rtol_td=1e-12):
+    from paper_0910_4711_b200 import synthetic
+    spec = synthetic.WORKLOADS[cfg_name]
+    assert hashlib.sha256(x.tobytes()).hexdigest() == g["x_sha256"].item().decode()
+    conf = vq.LbgConfig(target_size=spec.target_size, epsilon=spec.epsilon, delta=spec.delta)
+    cb, stats = vq.lbg_train(vq.TrainingSet(x), conf)
+    hist = np.array([(h.codebook_size, h.iteration, h.td, h.empty_cells) for h in stats.history])
+    want = g["hist"]
+    # iteration count and per-level schedule must match exactly
+    assert hist.shape == want.shape, (hist.shape, want.shape)
+    assert np.array_equal(hist[:, [0, 1, 3]], want[:, [0, 1, 3]])
+    np.testing.assert_allclose(hist[:, 2], want[:, 2], rtol=rtol_td)
+    assert abs(stats.total - float(g["total"])) <= 1e-4 * float(g["total"])
+    np.testing.assert_allclose(cb.codevectors, g["cb"], rtol=1e-5)
+    return cb, stats
+
+
+def test_cfg1_full_design_vs_reference():
+    from paper_0910_4711_b200 import synthetic
+    g = _golden("cfg1_design")
+    cb, _ = _design_check("cfg1", g, synthetic.make_training("cfg1"))
+    # 8-bit pixels: every FP64 sum is exact, so the codebook is bit-identical
+    assert cb.codevectors.tobytes() == g["cb"].tobytes()
+
+
+def test_cfg2_full_design_vs_reference():
+    from paper_0910_4711_b200 import synthetic
+    g = _golden("cfg2_design")
+    _design_check("cfg2", g, synthetic.make_training("cfg2"))
+
+
+def test_teacher_forced_counts_cfg1():
+    """Every recorded codebook of the reference run, fed to the device, gives
+    the reference's cell counts exactly."""
+    from paper_0910_4711_b200 import synthetic
+    g = _golden("cfg1_design")
+    x = synthetic.make_training("cfg1")
+    ts = vq.TrainingSet(x)
+    counts = g["pass_counts"]
+    offs = np.cumsum([0] + [int(s) for s in g["hist"][:, 0]])
+    checked = 0
+    for p in range(len(offs) - 1):
+        key = f"pass{p}_cb"
+        if key not in g.files:
+            continue
+        table, _ = vq.assign_cells(ts, vq.Codebook(g[key]))
+        got = np.bincount(table.cells, minlength=g[key].shape[0])
+        assert np.array_equal(got, counts[offs[p]:offs[p + 1]]), p
+        checked += 1
+    assert checked > 10
+
+
+# ---------------------------------------------------------------------------
+# encode
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(len(cases.encode_cases())))
+def test_encode_matches_reference(golden_small, i):
+    case = cases.encode_cases()[i]
+    stream = vq.encode(case["x"], vq.Codebook(case["cb"]), workers=case["workers"])
+    assert stream.indices.dtype == np.uint32
+    assert np.array_equal(stream.indices, golden_small[f"encode{i}_idx"])
+
+
+def test_encode_float32_pipeline_vs_oracle():
+    from paper_0910_4711_b200 import synthetic
+    cb, q = synthetic.make_encode_case(n=(1 << 22) + 12345)  # > one pipeline chunk
+    stream = vq.encode(q, vq.Codebook(cb.astype(np.float64)))
+    sub = slice(0, 200000)
+    cells, _ = oracle.assign_all(q[sub].astype(np.float64), cb.astype(np.float64), workers=8)
+    assert np.array_equal(stream.indices[sub], cells.astype(np.uint32))
+    tail = slice(q.shape[0] - 50000, q.shape[0])
+    cells, _ = oracle.assign_all(q[tail].astype(np.float64), cb.astype(np.float64), workers=8)
+    assert np.array_equal(stream.indices[tail], cells.astype(np.uint32))
+
+
+def test_empty_encode_and_errors():
+    cb = vq.Codebook(np.zeros((2, 3)))
+    assert len(vq.encode(np.empty((0, 3)), cb)) == 0
+    with pytest.raises(vq.UsageError):
+        vq.assign_cells(np.empty((0, 3)), cb)
+    with pytest.raises(vq.UsageError, match="dimension"):
+        vq.encode(np.zeros((4, 2)), cb)
+
+
+def test_determinism_repeat_runs():
+    from paper_0910_4711_b200 import synthetic
+    x = synthetic.make_training("cfg2", n=1 << 16)
+    cfg = vq.LbgConfig(target_size=64, epsilon=1e-4, delta=0.01)
+    cb1, s1 = vq.lbg_train(vq.TrainingSet(x), cfg)
+    cb2, s2 = vq.lbg_train(vq.TrainingSet(x.copy()), cfg)
+    assert cb1.codevectors.tobytes() == cb2.codevectors.tobytes()
+    assert s1.td_history() == s2.td_history()
