@@ -1,0 +1,405 @@
+"""Benchmark of the B200 LBG hot path (BASELINE.json metric: G vector-codeword
+distance evals/s per Lloyd iteration; codebook design wall time).
+
+Workload (N=1): BASELINE configs[1] (cfg2) -- N = 2^20 float32 vectors, L = 16,
+from the seeded 1024-component Gaussian mixture (paper_0910_4711_b200/
+synthetic.py); a step is ONE Lloyd iteration at the final level K = 1024
+(assign over all rows + FP64 re-rank + exact distortion + centroid update),
+starting from the reference's own converged K=1024 codebook
+(tests/golden/cfg2_design.npz, produced by the reference).  Evals per step =
+N * K.  L2 is flushed (256 MiB write) between timed steps.
+
+Keys beyond the base contract:
+  e2e          same iteration through the C ABI with HOST buffers
+               (vqb_lloyd_step_f32: H2D of X + codebook, D2H of cells + codebook)
+  roofline     dominant kernel (assign_fast<16>): algorithmic 3L flops per
+               eval / its CUDA-event time, against the measured FFMA peak
+  cpu_baseline oracle/ (C + OpenMP restatement of the reference kernels) on a
+               bounded row sample of the same iteration, all host cores
+  design       one full cfg2 design (1 -> 1024, 244 passes in the reference):
+               device-resident wall time and through the host API
+--impl reference times the CPU oracle port alone (the reference itself is
+Python+numba and cannot travel to the GPU box).
+N>1 (torchrun): weak scaling, every rank a cfg2-sized shard (rank-seeded),
+one int64 allreduce per pass over NCCL; time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "G vector·codeword distance evals/s per Lloyd iter"
+UNIT = "G evals/s"
+
+
+def _rank_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def _golden_codebook():
+    g = np.load(os.path.join(ROOT, "tests", "golden", "cfg2_design.npz"))
+    return np.ascontiguousarray(g["cb"]), g
+
+
+def _cpu_info():
+    try:
+        import psutil
+        cores = psutil.cpu_count(logical=False) or os.cpu_count()
+    except Exception:
+        cores = os.cpu_count()
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return int(cores or 1), model
+
+
+def cpu_iteration_rate(x: np.ndarray, cb: np.ndarray, target_s: float = 4.0, repeats: int = 3):
+    """Oracle (reference arithmetic, OpenMP over all host cores) Lloyd
+    iteration = parallel assign + in-order TD + round-robin update, on a
+    bounded leading-row sample.  Returns (G evals/s, sample rows, threads, s)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    threads = oracle.max_threads()
+    k = cb.shape[0]
+
+    def one(rows):
+        xs = np.ascontiguousarray(x[:rows], dtype=np.float64)
+        t0 = time.perf_counter()
+        cells, dists = oracle.assign_all(xs, cb, workers=threads)
+        oracle.sum_inorder(dists)
+        oracle.update_all(xs, cells, cb, workers=threads)
+        return time.perf_counter() - t0
+
+    probe = min(x.shape[0], 8192)
+    one(probe)  # warm
+    t = one(probe)
+    rows = int(min(x.shape[0], max(probe, probe * target_s / max(t, 1e-6))))
+    best = min(one(rows) for _ in range(repeats))
+    return rows * k / best / 1e9, rows, threads, best
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _load_traffic():
+    path = os.path.join(ROOT, "profiles", "assign_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def run_reference(args):
+    rank, world, _ = _rank_env()
+    if rank != 0:
+        return 0
+    from paper_0910_4711_b200 import synthetic
+
+    cb, _ = _golden_codebook()
+    x = synthetic.make_training("cfg2")
+    cores, model = _cpu_info()
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    threads = oracle.max_threads()
+    # calibrate a sample so each step is ~2 s of CPU work
+    rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=2.0, repeats=1)
+    xs = np.ascontiguousarray(x[:rows], dtype=np.float64)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        cells, dists = oracle.assign_all(xs, cb, workers=threads)
+        oracle.sum_inorder(dists)
+        oracle.update_all(xs, cells, cb, workers=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = rows * cb.shape[0] / t / 1e9
+    sample = (f"{rows} leading rows of cfg2 x K=1024 (reference's converged codebook): "
+              f"assign + in-order TD + update per step")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2 gmm1024 N=2^20 L=16 K=1024 Lloyd iteration (sampled rows)",
+                   "rows_sampled": rows, "cpu_model": model},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    rank, world, local_rank = _rank_env()
+    import torch
+
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200 import _lib, synthetic
+    from paper_0910_4711_b200.core import _Session
+
+    torch.cuda.set_device(local_rank)
+    L = _lib.lib()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    cb, golden = _golden_codebook()
+    K = cb.shape[0]
+    if world == 1:
+        x = synthetic.make_training("cfg2")
+    else:  # weak scaling: a cfg2-sized shard per rank, rank-seeded
+        rng = np.random.default_rng(1000 + rank)
+        x = synthetic.gaussian_mixture(rng, 1 << 20, 16, 1024, 2.0, 20.0)
+    n = x.shape[0]
+    sess = _Session(x, None, device=local_rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
+
+    # ---- peak: measured FFMA throughput (lane FMA/s -> FLOP/s)
+    ops, sec = ctypes.c_double(), ctypes.c_double()
+    _lib.check(L.vqb_pipe_microbench(0, 4, 4000, ctypes.byref(ops), ctypes.byref(sec)))
+    ffma_peak_tflops = 2 * ops.value / 1e12
+
+    segs = (ctypes.c_double * 5)()
+    flagged = ctypes.c_int64()
+
+    def step():
+        _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cb), K, 1, segs, ctypes.byref(flagged)))
+        return list(segs)
+
+    ex_tensor = None
+    if world > 1:
+        ex_tensor = torch.zeros(K * 16 + K + 1, dtype=torch.int64, device=f"cuda:{local_rank}")
+
+    clocks = ClockSampler(local_rank).__enter__()
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+        if world > 1:
+            dist.all_reduce(ex_tensor)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    seg_hist = []
+    if True:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            s = step()
+            if world > 1:  # the per-pass exchange of the multi-GPU loop
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                dist.all_reduce(ex_tensor)
+                ev1.record()
+                torch.cuda.synchronize()
+                s = s + [ev0.elapsed_time(ev1)]
+            seg_hist.append(s)
+    torch.cuda.synchronize()
+    ms_steps = [sum(s) for s in seg_hist]
+    ms_step = sum(ms_steps) / len(ms_steps)
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        dist.barrier()
+    seg = [sum(s[k] for s in seg_hist) / len(seg_hist) for k in range(5)]
+    evals = n * K
+    value = world * evals / (ms_step * 1e-3) / 1e9
+    assign_ms = seg[1]
+    flops = 3 * 16 * evals
+    achieved = flops / (assign_ms * 1e-3) / 1e12
+    traffic = _load_traffic()
+
+    result = None
+    if rank == 0:
+        # ---- e2e: the same iteration through the C ABI with host buffers
+        xp = torch.from_numpy(x).pin_memory().numpy()
+        new_cb = np.empty_like(cb)
+        cells = np.empty(n, dtype=np.int64)
+        td = ctypes.c_double()
+        empty = ctypes.c_int64()
+
+        def e2e_step():
+            _lib.check(L.vqb_lloyd_step_f32(_lib.ptr(xp), n, 16, _lib.ptr(cb), K, local_rank,
+                                            _lib.ptr(new_cb), _lib.ptr(cells), ctypes.byref(td),
+                                            ctypes.byref(empty)))
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        e2e_t = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_s = sum(e2e_t) / len(e2e_t)
+        clocks.__exit__(None, None, None)
+
+        # ---- full cfg2 design (device-resident) vs the reference's run
+        spec = synthetic.WORKLOADS["cfg2"]
+        conf = vq.LbgConfig(target_size=spec.target_size, epsilon=spec.epsilon, delta=spec.delta)
+        design = {}
+        if world == 1:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dcb, hist, warns, total, _d, summ = sess.train(conf)
+            design_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)   # host buffer -> device -> host
+            design_e2e_s = time.perf_counter() - t0
+            ghist = golden["hist"]
+            design = {
+                "wall_s": design_s, "e2e_wall_s": design_e2e_s, "passes": int(summ.passes),
+                "evals": int(summ.evals), "g_evals_per_s": summ.evals / design_s / 1e9,
+                "flagged_rows": int(summ.flagged_rows),
+                "reference_passes": int(ghist.shape[0]),
+                "schedule_matches_reference": bool(
+                    len(hist) == ghist.shape[0] and all(
+                        (h.codebook_size, h.iteration, h.empty_cells) ==
+                        (int(g[0]), int(g[1]), int(g[3])) for h, g in zip(hist, ghist))),
+                "total_rel_err_vs_reference": abs(total - float(golden["total"])) / float(golden["total"]),
+                "reference_wall_s": float(golden["seconds"]),
+                "reference_workers": int(golden["workers"]) if "workers" in golden.files else None,
+            }
+
+        # ---- CPU baseline: oracle on a bounded sample, all host cores
+        cpu_rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=4.0)
+        cores, model = _cpu_info()
+        c = clocks.summary()
+        launches_per_step = 7 if sess_fast(sess) else 5
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": "cfg2: gmm1024 N=2^20 L=16, Lloyd iteration at K=1024 "
+                                   "(reference's converged codebook)",
+                       "rows_per_gpu": n, "codebook": K, "dim": 16,
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "l2": "flushed (256 MiB write) between timed steps"},
+            "segments_ms": {"stage": seg[0], "assign": seg[1], "rerank": seg[2],
+                            "epilogue": seg[3], "finalize": seg[4]},
+            "rerank_rows_per_step": int(flagged.value),
+            "roofline": {"bound": "fp32_ffma", "kernel": "assign_fast<16>",
+                         "achieved": achieved, "peak": ffma_peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / ffma_peak_tflops,
+                         "peak_source": "measured FFMA microbenchmark (vqb_pipe_microbench), "
+                                        "2 FLOP per FMA; nominal 148x128x2x1.965 GHz = 74.45",
+                         "algorithmic": "3L = 48 flops per vector-codeword eval, N*K evals/launch",
+                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "algorithmic_bytes": n * 16 * 4 + n * 4},
+            "e2e": {"value": evals / e2e_s / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": n * 16 * 4 + K * 16 * 8,
+                    "d2h_bytes_per_step": n * 8 + K * 16 * 8},
+            "cpu_baseline": {"value": cpu_rate, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{rows} leading rows x K=1024, assign+TD+update "
+                                       f"(oracle/ C+OpenMP, reference arithmetic), min of 3",
+                             "cpu_model": model},
+            "design": design,
+            "clocks": {k: c[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def sess_fast(sess) -> bool:
+    return sess.dim in (16, 32, 64)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -175,11 +175,13 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
 int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
                         double* seconds);
 
-/* Time `reps` device-resident allocation+update passes at a fixed codebook
- * (the bench's kernel-only step).  Returns per-kernel average milliseconds. */
+/* Time `reps` device-resident Lloyd passes (assign + re-rank + update) at a
+ * codebook (the bench's kernel-only step; each pass continues from the
+ * previous update).  ms_segments[5] = average ms of [state reset + codebook
+ * staging, assign, re-rank, epilogue, finalize]; flagged = rows re-ranked
+ * per pass. */
 int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
-                        double* ms_total, double* ms_assign, double* ms_rerank,
-                        double* ms_epilogue, double* ms_finalize, int64_t* flagged);
+                        double* ms_segments, int64_t* flagged);
 
 #ifdef __cplusplus
 }

@@ -857,61 +857,46 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
 // ---------------------------------------------------------------------------
 
 int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
-                        double* ms_total, double* ms_assign, double* ms_rerank, double* ms_epilogue,
-                        double* ms_finalize, int64_t* flagged) {
+                        double* ms_segments, int64_t* flagged) {
   if (!s) return fail(VQB_USAGE, "null session");
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
   rc = set_state(s, kModeLloydStep, size, 0, 0);
   if (rc) return rc;
-  cudaEvent_t ev[5];
+  // segments: [prep+clear, assign, rerank, epilogue, finalize]
+  cudaEvent_t ev[6];
   for (auto& e : ev) CK(cudaEventCreate(&e));
-  double acc[4] = {0, 0, 0, 0};
-  long long fl = 0;
-  float ms_all = 0;
-  cudaEvent_t t0, t1;
-  CK(cudaEventCreate(&t0));
-  CK(cudaEventCreate(&t1));
+  double acc[5] = {0, 0, 0, 0, 0};
   KernelArgs a = s->args();
-  CK(cudaEventRecord(t0, s->stream));
   for (int r = 0; r < reps; ++r) {
     // keep iterating on the device: after each update the new codebook
     // becomes current (cur flips), exactly like consecutive Lloyd passes
+    CK(cudaEventRecord(ev[0], s->stream));
     CK(launch_reset(s->st, kModeLloydStep, (int)size, 0, 0, 1, s->stream));
     CK(launch_clear(a, s->stream));
     if (s->fast) CK(launch_prep_codebook(a, s->stream));
-    CK(cudaEventRecord(ev[0], s->stream));
-    CK(launch_assign(a, s->fast, s->sms, s->stream));
     CK(cudaEventRecord(ev[1], s->stream));
-    if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+    CK(launch_assign(a, s->fast, s->sms, s->stream));
     CK(cudaEventRecord(ev[2], s->stream));
-    CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
+    if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
     CK(cudaEventRecord(ev[3], s->stream));
-    CK(launch_finalize(a, s->stream));
+    CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
     CK(cudaEventRecord(ev[4], s->stream));
-    CK(cudaEventSynchronize(ev[4]));
+    CK(launch_finalize(a, s->stream));
+    CK(cudaEventRecord(ev[5], s->stream));
+    CK(cudaEventSynchronize(ev[5]));
     float m;
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
       CK(cudaEventElapsedTime(&m, ev[k], ev[k + 1]));
       acc[k] += m;
     }
   }
   long long flt = 0;
   CK(cudaMemcpy(&flt, &s->st->flagged_total, sizeof(long long), cudaMemcpyDeviceToHost));
-  fl = flt;
-  CK(cudaEventRecord(t1, s->stream));
-  CK(cudaEventSynchronize(t1));
-  CK(cudaEventElapsedTime(&ms_all, t0, t1));
   for (auto& e : ev) cudaEventDestroy(e);
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
-  *ms_total = (acc[0] + acc[1] + acc[2] + acc[3]) / reps;
-  *ms_assign = acc[0] / reps;
-  *ms_rerank = acc[1] / reps;
-  *ms_epilogue = acc[2] / reps;
-  *ms_finalize = acc[3] / reps;
-  *flagged = fl / reps;
+  for (int k = 0; k < 5; ++k) ms_segments[k] = acc[k] / reps;
+  *flagged = flt / reps;
   return VQB_OK;
 }
 

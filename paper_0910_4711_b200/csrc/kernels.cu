@@ -19,6 +19,8 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "vqb200_internal.h"
 
@@ -71,6 +73,23 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// packed f32x2 (sm_100 FFMA2): two rows' accumulators in one 64-bit register
+// pair; the codebook value is a scalar broadcast operand (R.F32 in SASS).
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
 }
 
 __device__ __forceinline__ double load_x(const float* x, long long i) { return (double)x[i]; }
@@ -159,7 +178,7 @@ struct TileStream {
 };
 
 // Process rows assigned to this thread in one chunk: R rows, strided by NT.
-template <int L, int NT, int TK, int R>
+template <int L, int NT, int TK, int R, bool PACKED>
 __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0, long long row_end,
                                              int K, int ntiles, float* smem, uint64_t* bars,
                                              long long& seq, long long seq_total) {
@@ -201,6 +220,50 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
     const float* sN = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sW) + TS::kWBytes);
     const int jbase = t * TK;
     const int cnt = min(TK, K - jbase);
+    if constexpr (PACKED && (R % 2 == 0)) {
+      // FFMA2: row pairs share one instruction; 8 issue slots per 16-dim eval pair
+      constexpr int P = R / 2;
+      unsigned long long y2[P][L];
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+#pragma unroll
+        for (int l = 0; l < L; ++l) y2[p][l] = pack2(y[2 * p][l], y[2 * p + 1][l]);
+#pragma unroll 2
+      for (int j = 0; j < cnt; ++j) {
+        const float4* wj = reinterpret_cast<const float4*>(sW + j * L);
+        const float nj = sN[j];
+        const unsigned long long n2 = pack2(nj, nj);
+        unsigned long long v2[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) v2[p] = n2;
+#pragma unroll
+        for (int c = 0; c < L / 4; ++c) {
+          const float4 t4 = wj[c];
+          const float w[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const unsigned long long w2 = pack2(w[q], w[q]);
+#pragma unroll
+            for (int p = 0; p < P; ++p) v2[p] = ffma2(y2[p][c * 4 + q], w2, v2[p]);
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float va, vb;
+          unpack2(v2[p], va, vb);
+          const float vv[2] = {va, vb};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 2 * p + h;
+            const float n2r = fminf(m2[r], fmaxf(m1[r], vv[h]));
+            const bool pr = vv[h] < m1[r];
+            m1[r] = fminf(m1[r], vv[h]);
+            i1[r] = pr ? jbase + j : i1[r];
+            m2[r] = n2r;
+          }
+        }
+      }
+    } else {
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
       const float4* wj = reinterpret_cast<const float4*>(sW + j * L);
@@ -234,6 +297,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
         i1[r] = p ? jbase + j : i1[r];
         m2[r] = n2;
       }
+    }
     }
     if (ntiles > 1) {
       __syncthreads();  // every warp is done with buffer `buf`
@@ -288,7 +352,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
   }
 }
 
-template <int L>
+template <int L, bool PACKED>
 __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelArgs a) {
   constexpr int NT = FastCfg<L>::NT, R = FastCfg<L>::R, TK = FastCfg<L>::TK;
   using TS = TileStream<L, TK>;
@@ -336,96 +400,156 @@ __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelAr
 
   long long seq = 0;
   for (long long c = 0; c < full; ++c)
-    assign_chunk<L, NT, TK, R>(a, lo + c * per_chunk, hi, K, ntiles, smem, bars, seq, seq_total);
+    assign_chunk<L, NT, TK, R, PACKED>(a, lo + c * per_chunk, hi, K, ntiles, smem, bars, seq,
+                                       seq_total);
   if (rem > 0) {
+    // tail chunk: only as many rows per thread as needed (no wave tail)
     const long long row0 = lo + full * per_chunk;
-    const int rr = (int)((rem + NT - 1) / NT);
-    if (R >= 4 && rr >= 4)
-      assign_chunk<L, NT, TK, (R >= 4 ? 4 : R)>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
-    else if (rr >= 3 && R >= 3)
-      assign_chunk<L, NT, TK, (R >= 3 ? 3 : R)>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
-    else if (rr >= 2)
-      assign_chunk<L, NT, TK, (R >= 2 ? 2 : R)>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
+    int rr = (int)((rem + NT - 1) / NT);
+    if (PACKED && (rr & 1)) ++rr;  // row pairs
+    if (rr >= 4)
+      assign_chunk<L, NT, TK, (R >= 4 ? 4 : R), PACKED>(a, row0, hi, K, ntiles, smem, bars, seq,
+                                                        seq_total);
+    else if (rr == 3)
+      assign_chunk<L, NT, TK, (R >= 3 ? 3 : R), PACKED>(a, row0, hi, K, ntiles, smem, bars, seq,
+                                                        seq_total);
+    else if (rr == 2)
+      assign_chunk<L, NT, TK, (R >= 2 ? 2 : R), PACKED>(a, row0, hi, K, ntiles, smem, bars, seq,
+                                                        seq_total);
     else
-      assign_chunk<L, NT, TK, 1>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
+      assign_chunk<L, NT, TK, 1, PACKED>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
   }
 }
 
-template <int L>
-static cudaError_t launch_fast_L(const KernelArgs& a, int sms, cudaStream_t s) {
+static bool packed_default() {
+  // VQB_ASSIGN=ffma selects the scalar-FFMA candidate loop (A/B measurements)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VQB_ASSIGN");
+    v = (e && strcmp(e, "ffma") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int L, bool PACKED>
+static cudaError_t launch_fast_LP(const KernelArgs& a, int sms, cudaStream_t s) {
   constexpr int TK = FastCfg<L>::TK;
   using TS = TileStream<L, TK>;
   const int ntiles_max = (int)((a.kmax + TK - 1) / TK);
   const size_t smem = TS::kBufBytes * (ntiles_max > 1 ? 2 : 1);
-  cudaError_t e = cudaFuncSetAttribute(assign_fast_kernel<L>,
+  cudaError_t e = cudaFuncSetAttribute(assign_fast_kernel<L, PACKED>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  assign_fast_kernel<L><<<sms, FastCfg<L>::NT, smem, s>>>(a);
+  assign_fast_kernel<L, PACKED><<<sms, FastCfg<L>::NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
+template <int L>
+static cudaError_t launch_fast_L(const KernelArgs& a, int sms, cudaStream_t s) {
+  return packed_default() ? launch_fast_LP<L, true>(a, sms, s) : launch_fast_LP<L, false>(a, sms, s);
+}
+
 // ---------------------------------------------------------------------------
-// exact FP64 rows: one warp per row, lanes stride the codebook
+// exact FP64 rows: G lanes per row (G = min(32, pow2 >= K)), lanes stride the
+// codebook, a lexicographic (d, j) shuffle reduction reproduces the strict-<
+// ascending scan.  DIM is a compile-time row length (0 = runtime).
 // ---------------------------------------------------------------------------
 
-template <typename XT>
+template <int DIM, typename XT>
+__device__ __forceinline__ double ref_dist_regs(const XT (&xr)[DIM], const double* __restrict__ c) {
+  double d = 0.0;
+#pragma unroll
+  for (int c0 = 0; c0 < DIM; c0 += 16) {
+    double cr[16];
+    const double2* c2 = reinterpret_cast<const double2*>(c + c0);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double2 t = __ldg(c2 + v);
+      cr[2 * v] = t.x;
+      cr[2 * v + 1] = t.y;
+    }
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      const double diff = __dsub_rn((double)xr[c0 + l], cr[l]);
+      d = __dadd_rn(d, __dmul_rn(diff, diff));
+    }
+  }
+  return d;
+}
+
+template <typename XT, int DIM>
 __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT* __restrict__ X,
                                                          int use_list) {
   const DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
-  const int dim = a.dim;
-  const double* cbg = a.cb[st->cur];
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* scb = reinterpret_cast<double*>(smem_raw);
-  const bool in_smem = (size_t)K * dim * sizeof(double) <= 96 * 1024;
-  if (in_smem) {
-    for (int i = threadIdx.x; i < K * dim; i += blockDim.x) scb[i] = cbg[i];
-    __syncthreads();
-  }
-  const double* cb = in_smem ? scb : cbg;
+  const int dim = DIM ? DIM : a.dim;
+  const double* __restrict__ cb = a.cb[st->cur];
+  int G = 1;
+  while (G < K && G < 32) G <<= 1;
+  const int rpw = 32 / G;
   const int lane = threadIdx.x & 31;
+  const int sub = lane / G, sl = lane % G;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long count = use_list ? (long long)st->flag_count : a.n;
-  for (long long i = gw; i < count; i += nw) {
-    const long long row = use_list ? (long long)a.flags[i] : i;
-    const XT* x = X + row * dim;
+  for (long long base = gw * rpw; base < count; base += nw * rpw) {
+    const long long i = base + sub;
+    const bool valid = i < count;
+    const long long row = valid ? (use_list ? (long long)a.flags[i] : i) : 0;
     double best = INFINITY;
     int bj = 0x7fffffff;
-    for (int j = lane; j < K; j += 32) {
-      double d = ref_dist(x, cb + (long long)j * dim, dim);
-      if (d < best) {  // ascending j within the lane: first minimum kept
-        best = d;
-        bj = j;
+    if (valid) {
+      const XT* x = X + row * dim;
+      if constexpr (DIM > 0) {
+        XT xr[DIM];
+#pragma unroll
+        for (int l = 0; l < DIM; ++l) xr[l] = x[l];
+        for (int j = sl; j < K; j += G) {
+          const double d = ref_dist_regs<DIM, XT>(xr, cb + (long long)j * DIM);
+          if (d < best) {  // ascending j within the lane: first minimum kept
+            best = d;
+            bj = j;
+          }
+        }
+      } else {
+        for (int j = sl; j < K; j += G) {
+          const double d = ref_dist(x, cb + (long long)j * dim, dim);
+          if (d < best) {
+            best = d;
+            bj = j;
+          }
+        }
       }
     }
-    // lexicographic (d, j) minimum == the sequential strict-< scan's winner
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      double ob = __shfl_xor_sync(0xffffffffu, best, off);
-      int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+    for (int off = G >> 1; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
       if (ob < best || (ob == best && oj < bj)) {
         best = ob;
         bj = oj;
       }
     }
-    if (lane == 0) a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
+    if (valid && sl == 0) a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
   }
 }
 
-cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
-  size_t smem = 96 * 1024;
-  if (a.x32) {
-    cudaFuncSetAttribute(exact_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    exact_rows_kernel<float><<<sms * 2, 256, smem, s>>>(a, a.x32, 1);
-  } else {
-    cudaFuncSetAttribute(exact_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    exact_rows_kernel<double><<<sms * 2, 256, smem, s>>>(a, a.x64, 1);
+template <typename XT>
+static cudaError_t launch_exact_t(const KernelArgs& a, const XT* X, int use_list, int sms,
+                                  cudaStream_t s) {
+  const int blocks = sms * 4;
+  switch (a.dim) {
+    case 16: exact_rows_kernel<XT, 16><<<blocks, 256, 0, s>>>(a, X, use_list); break;
+    case 32: exact_rows_kernel<XT, 32><<<blocks, 256, 0, s>>>(a, X, use_list); break;
+    case 64: exact_rows_kernel<XT, 64><<<blocks, 256, 0, s>>>(a, X, use_list); break;
+    default: exact_rows_kernel<XT, 0><<<blocks, 256, 0, s>>>(a, X, use_list); break;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
+  if (a.x32) return launch_exact_t<float>(a, a.x32, 1, sms, s);
+  return launch_exact_t<double>(a, a.x64, 1, sms, s);
 }
 
 cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s) {
@@ -437,17 +561,8 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
       default: return cudaErrorInvalidValue;
     }
   }
-  size_t smem = 96 * 1024;
-  if (a.x32) {
-    cudaFuncSetAttribute(exact_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    exact_rows_kernel<float><<<sms * 2, 256, smem, s>>>(a, a.x32, 0);
-  } else {
-    cudaFuncSetAttribute(exact_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    exact_rows_kernel<double><<<sms * 2, 256, smem, s>>>(a, a.x64, 0);
-  }
-  return cudaGetLastError();
+  if (a.x32) return launch_exact_t<float>(a, a.x32, 0, sms, s);
+  return launch_exact_t<double>(a, a.x64, 0, sms, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -457,23 +572,24 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 enum Sink { kSinkWarp = 0, kSinkBlock = 1, kSinkGlobal = 2 };
 constexpr int kEpiSmem = 96 * 1024;
 
-template <typename XT>
+template <typename XT, int DIM>
 __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, const XT* __restrict__ X,
                                                               int want_dists, int want_sums,
                                                               int zero_cells) {
   const DevState* st = a.st;
   if (st->done) return;
   const int K = zero_cells ? 1 : st->size;
-  const int dim = a.dim;
+  const int dim = DIM ? DIM : a.dim;
   const int metric = st->metric;
-  const double* cb = a.cb[st->cur];
+  const double* __restrict__ cb = a.cb[st->cur];
   const double scale = ldexp(1.0, st->fixed_shift);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kWarps = kEpiThreads / 32;
 
   // Sink for the fixed-point sums, chosen by the CURRENT codebook size: warp
-  // private smem tables (small K, plain adds), one block table (smem
-  // atomics), or straight to the exchange buffer (large K, little contention).
+  // private smem tables (small K: group-aggregated plain adds), one block
+  // table (smem atomics), or RED straight into the exchange buffer (large K:
+  // few collisions).  Integer adds commute, so every sink gives the same bits.
   extern __shared__ __align__(128) unsigned char smem_raw[];
   long long* table = reinterpret_cast<long long*>(smem_raw);  // sums then counts
   const long long twords = (long long)K * dim + K;
@@ -491,6 +607,8 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
     __syncthreads();
   }
   long long* my_table = (sink == kSinkWarp) ? table + warp * twords : table;
+  unsigned long long* gsums = reinterpret_cast<unsigned long long*>(a.ex.sums());
+  unsigned long long* gcounts = reinterpret_cast<unsigned long long*>(a.ex.counts());
 
   const long long n = a.n;
   const long long ntiles = (n + kTdTile - 1) / kTdTile;
@@ -504,14 +622,76 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
       double d = 0.0;
       if (valid) {
         cell = zero_cells ? 0 : a.idx[row];
+        const XT* x = X + row * dim;
+        const double* c = cb + (long long)cell * dim;
+        const bool direct = want_sums && sink != kSinkWarp;
+        unsigned long long* dsum = (sink == kSinkBlock)
+                                       ? reinterpret_cast<unsigned long long*>(my_table) + (long long)cell * dim
+                                       : gsums + (long long)cell * dim;
+        if constexpr (DIM > 0) {
+#pragma unroll
+          for (int c0 = 0; c0 < DIM; c0 += 16) {
+            double xr[16];
+            if constexpr (sizeof(XT) == 4) {
+              const float4* x4 = reinterpret_cast<const float4*>(x + c0);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const float4 q = __ldg(x4 + v);
+                xr[4 * v] = q.x;
+                xr[4 * v + 1] = q.y;
+                xr[4 * v + 2] = q.z;
+                xr[4 * v + 3] = q.w;
+              }
+            } else {
+              const double2* x2 = reinterpret_cast<const double2*>(x + c0);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const double2 q = __ldg(x2 + v);
+                xr[2 * v] = q.x;
+                xr[2 * v + 1] = q.y;
+              }
+            }
+            if (!zero_cells) {
+              double cr[16];
+              const double2* c2 = reinterpret_cast<const double2*>(c + c0);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const double2 q = __ldg(c2 + v);
+                cr[2 * v] = q.x;
+                cr[2 * v + 1] = q.y;
+              }
+#pragma unroll
+              for (int l = 0; l < 16; ++l) {
+                const double diff = __dsub_rn(xr[l], cr[l]);
+                d = __dadd_rn(d, __dmul_rn(diff, diff));
+              }
+            }
+            if (direct) {
+#pragma unroll
+              for (int l = 0; l < 16; ++l)
+                atomicAdd(dsum + c0 + l, (unsigned long long)to_fixed(xr[l], scale));
+            }
+          }
+        } else {
+          if (!zero_cells) d = ref_dist(x, c, dim);
+          if (direct)
+            for (int l = 0; l < dim; ++l)
+              atomicAdd(dsum + l, (unsigned long long)to_fixed(load_x(x, l), scale));
+        }
+        if (direct) {
+          if (sink == kSinkBlock)
+            atomicAdd(reinterpret_cast<unsigned long long*>(my_table + (long long)K * dim + cell), 1ull);
+          else
+            atomicAdd(gcounts + cell, 1ull);
+        }
         if (!zero_cells) {
-          d = ref_dist(X + row * dim, cb + (long long)cell * dim, dim);
           if (metric == kEuclidean) d = sqrt(d);
           if (want_dists) a.dists[row] = d;
         }
       }
       tsum = __dadd_rn(tsum, d);
-      if (want_sums) {
+      if (want_sums && sink == kSinkWarp) {
+        // few cells: aggregate the warp's rows per cell (lanes = dims)
         const unsigned active = __ballot_sync(0xffffffffu, valid);
         const unsigned grp = __match_any_sync(0xffffffffu, valid ? cell : -1);
         unsigned remaining = active;
@@ -519,7 +699,7 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
         while (remaining) {
           const int leader = __ffs(remaining) - 1;
           const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
-          const int c = __shfl_sync(0xffffffffu, cell, leader);
+          const int cl = __shfl_sync(0xffffffffu, cell, leader);
           remaining &= ~members;
           for (int l0 = 0; l0 < dim; l0 += 32) {
             const int l = l0 + lane;
@@ -531,25 +711,10 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
                 m &= m - 1;
                 acc += to_fixed(load_x(X, (wrow0 + b) * dim + l), scale);
               }
-              if (sink == kSinkWarp)
-                my_table[(long long)c * dim + l] += acc;
-              else if (sink == kSinkBlock)
-                atomicAdd(reinterpret_cast<unsigned long long*>(my_table + (long long)c * dim + l),
-                          (unsigned long long)acc);
-              else
-                atomicAdd(reinterpret_cast<unsigned long long*>(a.ex.sums() + (long long)c * dim + l),
-                          (unsigned long long)acc);
+              my_table[(long long)cl * dim + l] += acc;
             }
           }
-          if (lane == 0) {
-            const unsigned long long cntv = (unsigned long long)__popc(members);
-            if (sink == kSinkWarp)
-              my_table[(long long)K * dim + c] += (long long)cntv;
-            else if (sink == kSinkBlock)
-              atomicAdd(reinterpret_cast<unsigned long long*>(my_table + (long long)K * dim + c), cntv);
-            else
-              atomicAdd(reinterpret_cast<unsigned long long*>(a.ex.counts() + c), cntv);
-          }
+          if (lane == 0) my_table[(long long)K * dim + cl] += __popc(members);
           __syncwarp();
         }
       }
@@ -586,18 +751,29 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
   }
 }
 
+template <typename XT, int DIM>
+static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
+                                  bool zero_cells, int blocks, cudaStream_t s) {
+  const size_t smem = want_sums ? kEpiSmem : 0;
+  cudaError_t e = cudaFuncSetAttribute(epilogue_kernel<XT, DIM>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kEpiSmem);
+  if (e != cudaSuccess) return e;
+  epilogue_kernel<XT, DIM><<<blocks, kEpiThreads, smem, s>>>(a, X, want_dists, want_sums, zero_cells);
+  return cudaGetLastError();
+}
+
 template <typename XT>
 static cudaError_t launch_epi_t(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
                                 bool zero_cells, int sms, cudaStream_t s) {
   const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
   int blocks = (int)(ntiles < (long long)sms * 2 ? ntiles : (long long)sms * 2);
   if (blocks < 1) blocks = 1;
-  const size_t smem = want_sums ? kEpiSmem : 0;
-  cudaError_t e = cudaFuncSetAttribute(epilogue_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kEpiSmem);
-  if (e != cudaSuccess) return e;
-  epilogue_kernel<XT><<<blocks, kEpiThreads, smem, s>>>(a, X, want_dists, want_sums, zero_cells);
-  return cudaGetLastError();
+  switch (a.dim) {
+    case 16: return launch_epi_dim<XT, 16>(a, X, want_dists, want_sums, zero_cells, blocks, s);
+    case 32: return launch_epi_dim<XT, 32>(a, X, want_dists, want_sums, zero_cells, blocks, s);
+    case 64: return launch_epi_dim<XT, 64>(a, X, want_dists, want_sums, zero_cells, blocks, s);
+    default: return launch_epi_dim<XT, 0>(a, X, want_dists, want_sums, zero_cells, blocks, s);
+  }
 }
 
 cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums, bool zero_cells,

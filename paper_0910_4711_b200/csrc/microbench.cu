@@ -110,13 +110,80 @@ __global__ void __launch_bounds__(256) dadd_kernel(double* out, int iters, doubl
   if (s == 123.456) out[0] = s;
 }
 
+// 3 vector-register operands (no uniform / constant / immediate source)
+template <int CHAINS>
+__global__ void __launch_bounds__(256) ffma3r_kernel(float* out, const float* in, int iters) {
+  float acc[CHAINS], xa[CHAINS], xb[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    acc[c] = in[(threadIdx.x + c) & 255];
+    xa[c] = in[(threadIdx.x * 3 + c) & 255];
+    xb[c] = in[(threadIdx.x * 5 + c) & 255];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) acc[c] = fmaf(xa[c], acc[c], xb[c]);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 123.456f) out[0] = s;
+}
+
+// distance inner loop, codebook in __constant__ (ULDC -> uniform registers)
+__constant__ float c_mb_cb[512 * 17];
+
+template <int R>
+__global__ void __launch_bounds__(256) dist_const_kernel(float* out, const float* in, int K, int reps) {
+  float y[R][16];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int l = 0; l < 16; ++l) y[r][l] = in[(threadIdx.x * 7 + r * 16 + l) & 255];
+  float m1[R], m2[R];
+  int i1[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) { m1[r] = INFINITY; m2[r] = INFINITY; i1[r] = 0; }
+  for (int rep = 0; rep < reps; ++rep) {
+    for (int j = 0; j < K; ++j) {
+      float v[R];
+      const float nj = c_mb_cb[j * 17 + 16];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = nj;
+#pragma unroll
+      for (int l = 0; l < 16; ++l) {
+        const float w = c_mb_cb[j * 17 + l];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = fmaf(w, y[r][l], v[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float n2 = fminf(m2[r], fmaxf(m1[r], v[r]));
+        const bool p = v[r] < m1[r];
+        m1[r] = fminf(m1[r], v[r]);
+        i1[r] = p ? j : i1[r];
+        m2[r] = n2;
+      }
+    }
+  }
+  float s = 0.f;
+  int si = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) { s += m1[r] + m2[r]; si += i1[r]; }
+  if (s == 123.456f || si == -7) out[0] = s + si;
+}
+
 }  // namespace vqb
 
 using namespace vqb;
 
 // Returns achieved lane-ops/s (FMA counted once) for pipe `which`:
 // 0 = FFMA, 1 = FFMA2 (2 lane-ops per instruction), 2 = 16xFFMA + top-2 mix
-// (counts the 16 FFMA only), 3 = DADD.  `seconds` gets the kernel time.
+// (counts the 16 FFMA only), 3 = DADD, 4 = 3-register FFMA, 5 = evals/s of a
+// constant-memory-codebook distance loop.  `seconds` gets the kernel time.
 extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
                                    double* seconds) {
   int dev = 0, sms = 0;
@@ -125,7 +192,15 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
   const int threads = 256;
   const int blocks = sms * blocks_per_sm;
   void* buf = nullptr;
+  void* inbuf = nullptr;
   if (cudaMalloc(&buf, 64) != cudaSuccess) return 4;
+  if (cudaMalloc(&inbuf, 1024) != cudaSuccess) return 4;
+  cudaMemset(inbuf, 0, 1024);
+  {
+    static float hcb[512 * 17];
+    for (int i = 0; i < 512 * 17; ++i) hcb[i] = (float)((i * 37) % 101) * 0.01f;
+    cudaMemcpyToSymbol(c_mb_cb, hcb, sizeof(hcb));
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -145,9 +220,17 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         mix_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.999f, 1e-3f);
         lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
         break;
-      default:
+      case 3:
         dadd_kernel<8><<<blocks, threads>>>((double*)buf, iters, 1e-3);
         lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
+        break;
+      case 4:
+        ffma3r_kernel<8><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
+        break;
+      default:  // 5: evals/s of the constant-codebook distance loop (K=512, R=4)
+        dist_const_kernel<4><<<blocks, threads>>>((float*)buf, (const float*)inbuf, 512, iters / 100 + 1);
+        lane_ops = 1.0 * blocks * threads * 4 * 512 * (iters / 100 + 1);
         break;
     }
     cudaEventRecord(e1);
@@ -158,6 +241,7 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
+  cudaFree(inbuf);
   if (err != cudaSuccess) return 4;
   *seconds = ms * 1e-3;
   *ops_per_s = lane_ops / (ms * 1e-3);
