@@ -80,6 +80,7 @@ struct vqb_session {
   int* flags = nullptr;
   double* dists = nullptr;
   long long* ex = nullptr;
+  long long* partials = nullptr;
   long long ntiles_global = 0;
   DevState* st = nullptr;
   DevState* st_host = nullptr;  // pinned
@@ -110,6 +111,7 @@ struct vqb_session {
     a.ex.kmax = kmax;
     a.ex.dim = dim;
     a.ex.ntiles = ntiles_global;
+    a.partials = partials;
     a.st = st;
     return a;
   }
@@ -121,9 +123,11 @@ struct vqb_session {
     cudaFree(w);
     cudaFree(nrm);
     cudaFree(ex);
+    cudaFree(partials);
     cb[0] = cb[1] = nullptr;
     w = nrm = nullptr;
     ex = nullptr;
+    partials = nullptr;
     kmax = k;
     const long long kpad = (k + 3) / 4 * 4;
     CK(dalloc(&cb[0], (size_t)(k * dim)));
@@ -131,6 +135,7 @@ struct vqb_session {
     CK(dalloc(&w, (size_t)(kpad * dim + 64)));
     CK(dalloc(&nrm, (size_t)(kpad + 64)));
     CK(dalloc(&ex, (size_t)(k * dim + k + ntiles_global)));
+    CK(dalloc(&partials, (size_t)sms * (size_t)(k * dim + k)));
     CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (k * dim + k + ntiles_global), stream));
     return VQB_OK;
   }
@@ -149,6 +154,7 @@ struct vqb_session {
     cudaFree(flags);
     cudaFree(dists);
     cudaFree(ex);
+    cudaFree(partials);
     cudaFree(st);
     cudaFree(scratch);
     if (st_host) cudaFreeHost(st_host);

@@ -480,20 +480,23 @@ __device__ __forceinline__ double ref_dist_regs(const XT (&xr)[DIM], const doubl
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT* __restrict__ X,
                                                          int use_list) {
+  // T threads per row (T = pow2 >= K, capped at the block): K=2 packs 128
+  // rows per block, K >= 256 gives one block per row.  Each thread scans
+  // j = t, t+T, ... (ascending) with the reference's strict <, then a
+  // lexicographic (d, j) reduction over the T threads.
   const DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
   const int dim = DIM ? DIM : a.dim;
   const double* __restrict__ cb = a.cb[st->cur];
-  int G = 1;
-  while (G < K && G < 32) G <<= 1;
-  const int rpw = 32 / G;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / G, sl = lane % G;
-  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  int T = 1;
+  while (T < K && T < (int)blockDim.x) T <<= 1;
+  const int rpb = blockDim.x / T;
+  const int sub = threadIdx.x / T, tl = threadIdx.x % T;
+  __shared__ double s_best[8];
+  __shared__ int s_bj[8];
   const long long count = use_list ? (long long)st->flag_count : a.n;
-  for (long long base = gw * rpw; base < count; base += nw * rpw) {
+  for (long long base = (long long)blockIdx.x * rpb; base < count; base += (long long)gridDim.x * rpb) {
     const long long i = base + sub;
     const bool valid = i < count;
     const long long row = valid ? (use_list ? (long long)a.flags[i] : i) : 0;
@@ -505,15 +508,28 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
         XT xr[DIM];
 #pragma unroll
         for (int l = 0; l < DIM; ++l) xr[l] = x[l];
-        for (int j = sl; j < K; j += G) {
-          const double d = ref_dist_regs<DIM, XT>(xr, cb + (long long)j * DIM);
-          if (d < best) {  // ascending j within the lane: first minimum kept
-            best = d;
+        int j = tl;
+        for (; j + T < K; j += 2 * T) {  // two codevectors in flight
+          const double d0 = ref_dist_regs<DIM, XT>(xr, cb + (long long)j * DIM);
+          const double d1 = ref_dist_regs<DIM, XT>(xr, cb + (long long)(j + T) * DIM);
+          if (d0 < best) {
+            best = d0;
+            bj = j;
+          }
+          if (d1 < best) {
+            best = d1;
+            bj = j + T;
+          }
+        }
+        if (j < K) {
+          const double d0 = ref_dist_regs<DIM, XT>(xr, cb + (long long)j * DIM);
+          if (d0 < best) {
+            best = d0;
             bj = j;
           }
         }
       } else {
-        for (int j = sl; j < K; j += G) {
+        for (int j = tl; j < K; j += T) {
           const double d = ref_dist(x, cb + (long long)j * dim, dim);
           if (d < best) {
             best = d;
@@ -522,7 +538,8 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
         }
       }
     }
-    for (int off = G >> 1; off > 0; off >>= 1) {
+    const int seg = T < 32 ? T : 32;
+    for (int off = seg >> 1; off > 0; off >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, off);
       const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
       if (ob < best || (ob == best && oj < bj)) {
@@ -530,7 +547,23 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
         bj = oj;
       }
     }
-    if (valid && sl == 0) a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
+    if (T > 32) {  // a row spans T/32 warps: combine them in order
+      const int w = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) {
+        s_best[w] = best;
+        s_bj[w] = bj;
+      }
+      __syncthreads();
+      if (tl == 0) {
+        for (int k = w + 1; k < w + T / 32; ++k)
+          if (s_best[k] < best || (s_best[k] == best && s_bj[k] < bj)) {
+            best = s_best[k];
+            bj = s_bj[k];
+          }
+      }
+      __syncthreads();
+    }
+    if (valid && tl == 0) a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
   }
 }
 
@@ -569,13 +602,39 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 // epilogue: exact winner distance, distortion tiles, fixed-point cell sums
 // ---------------------------------------------------------------------------
 
-enum Sink { kSinkWarp = 0, kSinkBlock = 1, kSinkGlobal = 2 };
-constexpr int kEpiSmem = 96 * 1024;
+// The epilogue runs one persistent block per SM over a contiguous,
+// tile-aligned row range.  Per row: the winner's exact FP64 distance (the
+// reference's arithmetic) -> dists, and a fixed-tree FP64 distortion partial
+// per 2048-row tile.  Cell sums are int64 fixed point (order-free, hence
+// deterministic for every grid shape and every GPU count):
+//  * small K: warp-private smem tables, rows aggregated per cell inside the
+//    warp (match_any), lanes = dims, plain adds;
+//  * otherwise: per 512-row sub-tile a counting sort by cell (native 32-bit
+//    smem atomics), then the thread owning each cell sums its segment into
+//    the block table with plain int64 adds -- no 64-bit atomics anywhere.
+//    Codebooks too large for one table are split into chunks (gridDim.y).
+// Each block writes its table to a partial slab; reduce_partials_kernel sums
+// the slabs into the exchange buffer.
+constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
+
+template <typename XT>
+__host__ __device__ inline long long epi_stage_bytes() {
+  return (long long)kEpiThreads * 16 * sizeof(XT) + 2LL * kEpiThreads * sizeof(int);
+}
+template <typename XT>
+__host__ __device__ inline long long epi_chunk_cells(int K, int dim) {
+  // per cell: dim int64 sums + uint32 count + uint32 hist + uint32 cursor
+  long long kc = (kEpiSmem - epi_stage_bytes<XT>() - 64) / ((long long)dim * 8 + 12);
+  return kc < K ? kc : K;
+}
+__host__ __device__ inline bool epi_warp_sink(int K, int dim) {
+  return (long long)K * (dim * 8 + 4) * (kEpiThreads / 32) <= 96 * 1024;
+}
 
 template <typename XT, int DIM>
-__global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, const XT* __restrict__ X,
-                                                              int want_dists, int want_sums,
-                                                              int zero_cells) {
+__global__ void __launch_bounds__(kEpiThreads, 1) epilogue_kernel(KernelArgs a, const XT* __restrict__ X,
+                                                                 int want_dists, int want_sums,
+                                                                 int zero_cells) {
   const DevState* st = a.st;
   if (st->done) return;
   const int K = zero_cells ? 1 : st->size;
@@ -583,75 +642,122 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
   const int metric = st->metric;
   const double* __restrict__ cb = a.cb[st->cur];
   const double scale = ldexp(1.0, st->fixed_shift);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kWarps = kEpiThreads / 32;
 
-  // Sink for the fixed-point sums, chosen by the CURRENT codebook size: warp
-  // private smem tables (small K: group-aggregated plain adds), one block
-  // table (smem atomics), or RED straight into the exchange buffer (large K:
-  // few collisions).  Integer adds commute, so every sink gives the same bits.
+  const bool warp_sink = epi_warp_sink(K, dim);
+  const long long kc = warp_sink ? K : epi_chunk_cells<XT>(K, dim);
+  const long long nchunks = (K + kc - 1) / kc;
+  const int chunk = blockIdx.y;
+  if (want_sums ? chunk >= nchunks : chunk > 0) return;
+  const long long c_lo = chunk * kc;
+  const long long c_hi = (c_lo + kc < K) ? c_lo + kc : K;
+  const int ncell = (int)(c_hi - c_lo);
+  const bool do_td = !zero_cells && chunk == 0;
+
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  long long* table = reinterpret_cast<long long*>(smem_raw);  // sums then counts
-  const long long twords = (long long)K * dim + K;
-  int sink = kSinkGlobal;
-  if (want_sums) {
-    if (twords * 8 * kWarps <= kEpiSmem)
-      sink = kSinkWarp;
-    else if (twords * 8 <= kEpiSmem)
-      sink = kSinkBlock;
-  }
   __shared__ double red[kWarps];
-  if (want_sums && sink != kSinkGlobal) {
-    const long long total = (sink == kSinkWarp) ? twords * kWarps : twords;
-    for (long long i = threadIdx.x; i < total; i += blockDim.x) table[i] = 0;
+  __shared__ int s_wsum[kWarps];
+  // warp sink: kWarps tables of [ncell*dim int64 | ncell uint32]
+  // block sink: stage XT[kEpiThreads][16] | cells int[kEpiThreads] | perm int[kEpiThreads]
+  //             | sums int64[ncell*dim] | counts u32[ncell] | hist u32[ncell] | cursor u32[ncell]
+  const long long wt_bytes = ((long long)ncell * dim * 8 + ncell * 4 + 15) / 16 * 16;
+  XT* stage = reinterpret_cast<XT*>(smem_raw);
+  int* s_cells = reinterpret_cast<int*>(smem_raw + (long long)kEpiThreads * 16 * sizeof(XT));
+  int* s_perm = s_cells + kEpiThreads;
+  long long* bsums = reinterpret_cast<long long*>(smem_raw + epi_stage_bytes<XT>());
+  unsigned* bcounts = reinterpret_cast<unsigned*>(bsums + (long long)ncell * dim);
+  unsigned* hist = bcounts + ncell;
+  unsigned* cursor = hist + ncell;
+  long long* wsums = reinterpret_cast<long long*>(smem_raw + warp * wt_bytes);
+  unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
+  if (want_sums) {
+    if (warp_sink) {
+      uint4* z = reinterpret_cast<uint4*>(smem_raw);
+      for (long long i = tid; i < wt_bytes * kWarps / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (long long i = tid; i < (long long)ncell * dim; i += blockDim.x) bsums[i] = 0;
+      for (int i = tid; i < ncell; i += blockDim.x) bcounts[i] = 0;
+    }
     __syncthreads();
   }
-  long long* my_table = (sink == kSinkWarp) ? table + warp * twords : table;
-  unsigned long long* gsums = reinterpret_cast<unsigned long long*>(a.ex.sums());
-  unsigned long long* gcounts = reinterpret_cast<unsigned long long*>(a.ex.counts());
 
   const long long n = a.n;
   const long long ntiles = (n + kTdTile - 1) / kTdTile;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const long long t_lo = ntiles * blockIdx.x / gridDim.x;
+  const long long t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
+  for (long long t = t_lo; t < t_hi; ++t) {
     const long long tbase = t * kTdTile;
     double tsum = 0.0;
     for (int r = 0; r < kTdTile / kEpiThreads; ++r) {
-      const long long row = tbase + (long long)r * kEpiThreads + threadIdx.x;
+      const long long row = tbase + (long long)r * kEpiThreads + tid;
       const bool valid = row < n;
-      int cell = 0;
+      const int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
+      const bool mine = want_sums && valid && cell >= c_lo && cell < c_hi;
+      const int lc = mine ? cell - (int)c_lo : -1;
+      const bool block_sums = want_sums && !warp_sink;
+      if (block_sums) {
+        // counting sort of this sub-tile by local cell
+        for (int i = tid; i < ncell; i += blockDim.x) hist[i] = 0;
+        s_cells[tid] = lc;
+        __syncthreads();
+        if (mine) atomicAdd(&hist[lc], 1u);
+        __syncthreads();
+        // exclusive scan hist -> cursor (each thread a contiguous run)
+        const int per = (ncell + kEpiThreads - 1) / kEpiThreads;
+        const int i0 = tid * per, i1 = min(ncell, i0 + per);
+        int run = 0;
+        for (int i = i0; i < i1; ++i) run += hist[i];
+        int incl = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += o;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        int wbase = 0;
+        for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
+        int pos = wbase + incl - run;
+        for (int i = i0; i < i1; ++i) {
+          cursor[i] = pos;
+          pos += hist[i];
+        }
+        __syncthreads();
+        if (mine) s_perm[atomicAdd(&cursor[lc], 1u)] = tid;
+        __syncthreads();
+      }
+      const XT* x = X + (valid ? row : 0) * dim;
+      const double* c = cb + (long long)(cell > 0 ? cell : 0) * dim;
       double d = 0.0;
-      if (valid) {
-        cell = zero_cells ? 0 : a.idx[row];
-        const XT* x = X + row * dim;
-        const double* c = cb + (long long)cell * dim;
-        const bool direct = want_sums && sink != kSinkWarp;
-        unsigned long long* dsum = (sink == kSinkBlock)
-                                       ? reinterpret_cast<unsigned long long*>(my_table) + (long long)cell * dim
-                                       : gsums + (long long)cell * dim;
-        if constexpr (DIM > 0) {
+      for (int c0 = 0; c0 < dim; c0 += 16) {
+        const int cw = dim - c0 < 16 ? dim - c0 : 16;
+        double xr[16];
+        if (valid) {
+          if constexpr (DIM > 0 && sizeof(XT) == 4) {
+            const float4* x4 = reinterpret_cast<const float4*>(x + c0);
 #pragma unroll
-          for (int c0 = 0; c0 < DIM; c0 += 16) {
-            double xr[16];
-            if constexpr (sizeof(XT) == 4) {
-              const float4* x4 = reinterpret_cast<const float4*>(x + c0);
-#pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                const float4 q = __ldg(x4 + v);
-                xr[4 * v] = q.x;
-                xr[4 * v + 1] = q.y;
-                xr[4 * v + 2] = q.z;
-                xr[4 * v + 3] = q.w;
-              }
-            } else {
-              const double2* x2 = reinterpret_cast<const double2*>(x + c0);
-#pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                const double2 q = __ldg(x2 + v);
-                xr[2 * v] = q.x;
-                xr[2 * v + 1] = q.y;
-              }
+            for (int v = 0; v < 4; ++v) {
+              const float4 q = __ldg(x4 + v);
+              xr[4 * v] = q.x;
+              xr[4 * v + 1] = q.y;
+              xr[4 * v + 2] = q.z;
+              xr[4 * v + 3] = q.w;
             }
-            if (!zero_cells) {
+          } else if constexpr (DIM > 0) {
+            const double2* x2 = reinterpret_cast<const double2*>(x + c0);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const double2 q = __ldg(x2 + v);
+              xr[2 * v] = q.x;
+              xr[2 * v + 1] = q.y;
+            }
+          } else {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) xr[l] = l < cw ? load_x(x, c0 + l) : 0.0;
+          }
+          if (do_td) {
+            if constexpr (DIM > 0) {
               double cr[16];
               const double2* c2 = reinterpret_cast<const double2*>(c + c0);
 #pragma unroll
@@ -665,41 +771,54 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
                 const double diff = __dsub_rn(xr[l], cr[l]);
                 d = __dadd_rn(d, __dmul_rn(diff, diff));
               }
-            }
-            if (direct) {
-#pragma unroll
-              for (int l = 0; l < 16; ++l)
-                atomicAdd(dsum + c0 + l, (unsigned long long)to_fixed(xr[l], scale));
+            } else {
+              for (int l = 0; l < cw; ++l) {
+                const double diff = __dsub_rn(xr[l], c[c0 + l]);
+                d = __dadd_rn(d, __dmul_rn(diff, diff));
+              }
             }
           }
-        } else {
-          if (!zero_cells) d = ref_dist(x, c, dim);
-          if (direct)
-            for (int l = 0; l < dim; ++l)
-              atomicAdd(dsum + l, (unsigned long long)to_fixed(load_x(x, l), scale));
         }
-        if (direct) {
-          if (sink == kSinkBlock)
-            atomicAdd(reinterpret_cast<unsigned long long*>(my_table + (long long)K * dim + cell), 1ull);
-          else
-            atomicAdd(gcounts + cell, 1ull);
-        }
-        if (!zero_cells) {
-          if (metric == kEuclidean) d = sqrt(d);
-          if (want_dists) a.dists[row] = d;
+        if (block_sums) {
+          // stage this 16-dim slice; then each thread sums the segments of
+          // the cells it owns (cell i -> thread i mod blockDim) in sorted order
+#pragma unroll
+          for (int l = 0; l < 16; ++l) stage[tid * 16 + l] = (XT)xr[l];
+          __syncthreads();
+          for (int i = tid; i < ncell; i += blockDim.x) {
+            const unsigned cnt = hist[i];
+            if (cnt == 0) continue;
+            const unsigned beg = cursor[i] - cnt;  // cursor ran to the segment end
+            long long acc[16];
+#pragma unroll
+            for (int l = 0; l < 16; ++l) acc[l] = 0;
+            for (unsigned m = beg; m < beg + cnt; ++m) {
+              const XT* xs = stage + s_perm[m] * 16;
+#pragma unroll
+              for (int l = 0; l < 16; ++l) acc[l] += to_fixed((double)xs[l], scale);
+            }
+            long long* dst = bsums + (long long)i * dim + c0;
+            for (int l = 0; l < cw; ++l) dst[l] += acc[l];
+            if (c0 == 0) bcounts[i] += cnt;
+          }
+          __syncthreads();
         }
       }
+      if (valid && do_td) {
+        if (metric == kEuclidean) d = sqrt(d);
+        if (want_dists) a.dists[row] = d;
+      }
       tsum = __dadd_rn(tsum, d);
-      if (want_sums && sink == kSinkWarp) {
+      if (want_sums && warp_sink) {
         // few cells: aggregate the warp's rows per cell (lanes = dims)
-        const unsigned active = __ballot_sync(0xffffffffu, valid);
-        const unsigned grp = __match_any_sync(0xffffffffu, valid ? cell : -1);
+        const unsigned active = __ballot_sync(0xffffffffu, mine);
+        const unsigned grp = __match_any_sync(0xffffffffu, lc);
         unsigned remaining = active;
         const long long wrow0 = tbase + (long long)r * kEpiThreads + warp * 32;
         while (remaining) {
           const int leader = __ffs(remaining) - 1;
           const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
-          const int cl = __shfl_sync(0xffffffffu, cell, leader);
+          const int cl = __shfl_sync(0xffffffffu, lc, leader);
           remaining &= ~members;
           for (int l0 = 0; l0 < dim; l0 += 32) {
             const int l = l0 + lane;
@@ -711,54 +830,110 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_kernel(KernelArgs a, con
                 m &= m - 1;
                 acc += to_fixed(load_x(X, (wrow0 + b) * dim + l), scale);
               }
-              my_table[(long long)cl * dim + l] += acc;
+              wsums[(long long)cl * dim + l] += acc;
             }
           }
-          if (lane == 0) my_table[(long long)K * dim + cl] += __popc(members);
+          if (lane == 0) wcounts[cl] += __popc(members);
           __syncwarp();
         }
       }
     }
-    if (!zero_cells) {
+    if (do_td) {
       // fixed tree: lanes (xor butterfly), then warps in order
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1)
         tsum = __dadd_rn(tsum, __shfl_xor_sync(0xffffffffu, tsum, off));
       if (lane == 0) red[warp] = tsum;
       __syncthreads();
-      if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, red[w]);
-        a.ex.td()[a.tile0 + t] = __double_as_longlong(s);
+      if (tid == 0) {
+        double sacc = 0.0;
+        for (int w = 0; w < kWarps; ++w) sacc = __dadd_rn(sacc, red[w]);
+        a.ex.td()[a.tile0 + t] = __double_as_longlong(sacc);
       }
       __syncthreads();
     }
   }
-  if (want_sums && sink != kSinkGlobal) {
+  if (want_sums) {
     __syncthreads();
-    // merge tables into the exchange buffer (int64: any order is exact)
-    for (long long i = threadIdx.x; i < twords; i += blockDim.x) {
-      long long v = 0;
-      if (sink == kSinkWarp)
-        for (int w = 0; w < kWarps; ++w) v += table[w * twords + i];
-      else
-        v = table[i];
-      if (v != 0) {
-        long long* dst = (i < (long long)K * dim) ? a.ex.sums() + i : a.ex.counts() + (i - (long long)K * dim);
-        atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)v);
+    // block partial slab [blockIdx.x][K*dim sums | K counts] (int64)
+    long long* slab = a.partials + (long long)blockIdx.x * ((long long)a.kmax * dim + a.kmax);
+    const long long words = (long long)ncell * dim;
+    if (warp_sink) {
+      for (long long i = tid; i < words; i += blockDim.x) {
+        long long v = 0;
+        for (int w = 0; w < kWarps; ++w)
+          v += reinterpret_cast<const long long*>(smem_raw + w * wt_bytes)[i];
+        slab[c_lo * dim + i] = v;
       }
+      for (int i = tid; i < ncell; i += blockDim.x) {
+        long long v = 0;
+        for (int w = 0; w < kWarps; ++w)
+          v += reinterpret_cast<const unsigned*>(smem_raw + w * wt_bytes + words * 8)[i];
+        slab[(long long)K * dim + c_lo + i] = v;
+      }
+    } else {
+      for (long long i = tid; i < words; i += blockDim.x) slab[c_lo * dim + i] = bsums[i];
+      for (int i = tid; i < ncell; i += blockDim.x) slab[(long long)K * dim + c_lo + i] = bcounts[i];
     }
+  }
+}
+
+// sum the per-block slabs into the exchange buffer: 32 words x 8 slab groups
+// per 256-thread block, int64 (any order is exact)
+__global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int nblocks, int zero_cells) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = zero_cells ? 1 : st->size;
+  const long long dim = a.dim;
+  const long long words = (long long)K * dim + K;
+  const long long stride = a.kmax * dim + a.kmax;
+  __shared__ long long part[8][32];
+  const int wl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  for (long long w0 = (long long)blockIdx.x * 32; w0 < words; w0 += (long long)gridDim.x * 32) {
+    const long long w = w0 + wl;
+    long long v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    if (w < words) {
+      int b = g;
+      for (; b + 24 < nblocks; b += 32) {
+        v0 += a.partials[(long long)b * stride + w];
+        v1 += a.partials[(long long)(b + 8) * stride + w];
+        v2 += a.partials[(long long)(b + 16) * stride + w];
+        v3 += a.partials[(long long)(b + 24) * stride + w];
+      }
+      for (; b < nblocks; b += 8) v0 += a.partials[(long long)b * stride + w];
+    }
+    part[g][wl] = v0 + v1 + v2 + v3;
+    __syncthreads();
+    if (g == 0 && w < words) {
+      long long v = 0;
+      for (int k = 0; k < 8; ++k) v += part[k][wl];
+      if (w < K * dim)
+        a.ex.sums()[w] = v;
+      else
+        a.ex.counts()[w - K * dim] = v;
+    }
+    __syncthreads();
   }
 }
 
 template <typename XT, int DIM>
 static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
                                   bool zero_cells, int blocks, cudaStream_t s) {
+  const long long kmax = zero_cells ? 1 : a.kmax;
+  const long long kc = epi_warp_sink((int)kmax, a.dim) ? kmax : epi_chunk_cells<XT>((int)kmax, a.dim);
+  const int chunks = want_sums ? (int)((kmax + kc - 1) / kc) : 1;
   const size_t smem = want_sums ? kEpiSmem : 0;
   cudaError_t e = cudaFuncSetAttribute(epilogue_kernel<XT, DIM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kEpiSmem);
   if (e != cudaSuccess) return e;
-  epilogue_kernel<XT, DIM><<<blocks, kEpiThreads, smem, s>>>(a, X, want_dists, want_sums, zero_cells);
+  epilogue_kernel<XT, DIM><<<dim3(blocks, chunks), kEpiThreads, smem, s>>>(a, X, want_dists, want_sums,
+                                                                         zero_cells);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !want_sums) return e;
+  const long long words = kmax * a.dim + kmax;
+  int rb = (int)((words + 31) / 32);
+  if (rb > 8192) rb = 8192;
+  reduce_partials_kernel<<<rb, 256, 0, s>>>(a, blocks, zero_cells ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -766,7 +941,7 @@ template <typename XT>
 static cudaError_t launch_epi_t(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
                                 bool zero_cells, int sms, cudaStream_t s) {
   const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
-  int blocks = (int)(ntiles < (long long)sms * 2 ? ntiles : (long long)sms * 2);
+  int blocks = (int)(ntiles < (long long)sms ? ntiles : (long long)sms);
   if (blocks < 1) blocks = 1;
   switch (a.dim) {
     case 16: return launch_epi_dim<XT, 16>(a, X, want_dists, want_sums, zero_cells, blocks, s);

@@ -11,7 +11,7 @@ namespace vqb {
 constexpr int kMaxHist = 8192;   // levels x max_iterations_per_level records
 constexpr int kMaxWarn = 64;     // one warning per level at most
 constexpr int kTdTile = 2048;    // rows per distortion partial (fixed, global)
-constexpr int kEpiThreads = 256; // epilogue block: 8 rows per thread per tile
+constexpr int kEpiThreads = 512; // epilogue block: 4 rows per thread per tile
 
 // metric codes (reference _kernels.py:14-15)
 constexpr int kSquared = 0;
@@ -99,6 +99,7 @@ struct KernelArgs {
   int* flags;
   double* dists;        // nullable
   Exchange ex;
+  long long* partials;  // per-block fixed-point slabs, sms x (kmax*dim + kmax)
   DevState* st;
 };
 
