@@ -345,7 +345,7 @@ def run_b200(args):
         cpu_rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=4.0)
         cores, model = _cpu_info()
         c = clocks.summary()
-        launches_per_step = 7 if sess_fast(sess) else 5
+        launches_per_step = 8 if sess_fast(sess) else 6
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

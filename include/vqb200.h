@@ -177,8 +177,8 @@ int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per
 
 /* Time `reps` device-resident Lloyd passes (assign + re-rank + update) at a
  * codebook (the bench's kernel-only step; each pass continues from the
- * previous update).  ms_segments[5] = average ms of [state reset + codebook
- * staging, assign, re-rank, epilogue, finalize]; flagged = rows re-ranked
+ * previous update).  ms_segments[5] = average ms of [state reset (the codebook
+ * staging happens in apply), assign, re-rank, epilogue, finalize+apply]; flagged = rows re-ranked
  * per pass. */
 int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
                         double* ms_segments, int64_t* flagged);

@@ -81,6 +81,7 @@ struct vqb_session {
   double* dists = nullptr;
   long long* ex = nullptr;
   long long* partials = nullptr;
+  double* ord = nullptr;
   long long ntiles_global = 0;
   DevState* st = nullptr;
   DevState* st_host = nullptr;  // pinned
@@ -112,6 +113,7 @@ struct vqb_session {
     a.ex.dim = dim;
     a.ex.ntiles = ntiles_global;
     a.partials = partials;
+    a.ord = ord;
     a.st = st;
     return a;
   }
@@ -124,6 +126,8 @@ struct vqb_session {
     cudaFree(nrm);
     cudaFree(ex);
     cudaFree(partials);
+    cudaFree(ord);
+    ord = nullptr;
     cb[0] = cb[1] = nullptr;
     w = nrm = nullptr;
     ex = nullptr;
@@ -136,6 +140,7 @@ struct vqb_session {
     CK(dalloc(&nrm, (size_t)(kpad + 64)));
     CK(dalloc(&ex, (size_t)(k * dim + k + ntiles_global)));
     CK(dalloc(&partials, (size_t)sms * (size_t)(k * dim + k)));
+    CK(dalloc(&ord, (size_t)(k * dim)));
     CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (k * dim + k + ntiles_global), stream));
     return VQB_OK;
   }
@@ -155,6 +160,7 @@ struct vqb_session {
     cudaFree(dists);
     cudaFree(ex);
     cudaFree(partials);
+    cudaFree(ord);
     cudaFree(st);
     cudaFree(scratch);
     if (st_host) cudaFreeHost(st_host);
@@ -381,12 +387,11 @@ int vqb_step_local(vqb_session* s) {
 int vqb_step_finalize(vqb_session* s) {
   KernelArgs a = s->args();
   if (s->pending_init) {
-    CK(launch_init_centroid(a, s->stream));
+    CK(launch_init_centroid(a, s->fast, s->stream));
     s->pending_init = false;
   } else {
-    CK(launch_finalize(a, s->stream));
+    CK(launch_finalize(a, s->fast, s->stream));
   }
-  if (s->fast) CK(launch_prep_codebook(a, s->stream));
   return VQB_OK;
 }
 
@@ -536,7 +541,7 @@ int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric,
   CK(launch_assign(a, s->fast, s->sms, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
   CK(launch_epilogue(a, true, false, false, s->sms, s->stream));
-  CK(launch_finalize(a, s->stream));
+  CK(launch_finalize(a, false, s->stream));
   std::vector<int> tmp;
   if (cells64 || idx32) {
     if (idx32) {
@@ -577,7 +582,7 @@ int vqb_update(vqb_session* s, const int64_t* cells, const double* old_codebook,
     CK(launch_ordered_update(a, s->stream));
   else
     CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
-  CK(launch_finalize(a, s->stream));
+  CK(launch_finalize(a, false, s->stream));
   std::vector<long long> hc((size_t)size);
   CK(cudaMemcpyAsync(new_codebook, s->cb[1], sizeof(double) * size * s->dim, cudaMemcpyDeviceToHost,
                      s->stream));
@@ -763,7 +768,7 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   CK(launch_assign(a, s->fast, s->sms, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
   CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
-  CK(launch_finalize(a, s->stream));
+  CK(launch_finalize(a, false, s->stream));
   CK(cudaMemcpyAsync(new_codebook, s->cb[1], sizeof(double) * size * dim, cudaMemcpyDeviceToHost,
                      s->stream));
   std::vector<int> tmp;
@@ -844,7 +849,7 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     CK(launch_assign(a, s->fast, s->sms, s->stream));
     if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
     CK(launch_epilogue(a, false, false, false, s->sms, s->stream));
-    CK(launch_finalize(a, s->stream));
+    CK(launch_finalize(a, false, s->stream));
     CK(cudaMemcpyAsync(idx_out + r0, s->idx, sizeof(int) * rows, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(tot_pinned + c, &s->st->total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   }
@@ -875,13 +880,15 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
   for (auto& e : ev) CK(cudaEventCreate(&e));
   double acc[5] = {0, 0, 0, 0, 0};
   KernelArgs a = s->args();
+  // staging of the first codebook (later passes are staged by apply_kernel,
+  // exactly as inside the training loop)
+  CK(launch_clear(a, s->stream));
+  if (s->fast) CK(launch_prep_codebook(a, s->stream));
   for (int r = 0; r < reps; ++r) {
     // keep iterating on the device: after each update the new codebook
     // becomes current (cur flips), exactly like consecutive Lloyd passes
     CK(cudaEventRecord(ev[0], s->stream));
     CK(launch_reset(s->st, kModeLloydStep, (int)size, 0, 0, 1, s->stream));
-    CK(launch_clear(a, s->stream));
-    if (s->fast) CK(launch_prep_codebook(a, s->stream));
     CK(cudaEventRecord(ev[1], s->stream));
     CK(launch_assign(a, s->fast, s->sms, s->stream));
     CK(cudaEventRecord(ev[2], s->stream));
@@ -889,7 +896,7 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
     CK(cudaEventRecord(ev[3], s->stream));
     CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
     CK(cudaEventRecord(ev[4], s->stream));
-    CK(launch_finalize(a, s->stream));
+    CK(launch_finalize(a, s->fast, s->stream));
     CK(cudaEventRecord(ev[5], s->stream));
     CK(cudaEventSynchronize(ev[5]));
     float m;

@@ -602,139 +602,69 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 // epilogue: exact winner distance, distortion tiles, fixed-point cell sums
 // ---------------------------------------------------------------------------
 
-// The epilogue runs one persistent block per SM over a contiguous,
-// tile-aligned row range.  Per row: the winner's exact FP64 distance (the
-// reference's arithmetic) -> dists, and a fixed-tree FP64 distortion partial
-// per 2048-row tile.  Cell sums are int64 fixed point (order-free, hence
-// deterministic for every grid shape and every GPU count):
+// The epilogue is two kernels.
+//
+// dist_td_kernel (thread per row, one block per 2048-row distortion tile,
+// high occupancy): the winner's exact FP64 distance in the reference's
+// arithmetic -> dists, and the tile's fixed-tree FP64 distortion partial.
+//
+// sums_kernel (one persistent 1024-thread block per SM over a contiguous row
+// range): int64 fixed-point cell sums + counts (integer adds commute, so the
+// result is deterministic for every grid shape and every GPU count):
 //  * small K: warp-private smem tables, rows aggregated per cell inside the
 //    warp (match_any), lanes = dims, plain adds;
-//  * otherwise: per 512-row sub-tile a counting sort by cell (native 32-bit
-//    smem atomics), then the thread owning each cell sums its segment into
-//    the block table with plain int64 adds -- no 64-bit atomics anywhere.
-//    Codebooks too large for one table are split into chunks (gridDim.y).
-// Each block writes its table to a partial slab; reduce_partials_kernel sums
-// the slabs into the exchange buffer.
+//  * otherwise: per 1024-row sub-tile a counting sort by cell (native 32-bit
+//    smem atomics), rows staged in smem (padded, conflict-free STS.128), then
+//    the thread owning each cell sums its segment into the block table with
+//    plain int64 adds -- no 64-bit atomics.  Codebooks whose table would not
+//    fit are split into chunks (gridDim.y).
+// Each block writes its table to a slab; reduce_partials_kernel sums them.
+constexpr int kSumThreads = 512;
+constexpr int kStageStride = 20;  // floats per staged row: 16 used, padded (bank-conflict free)
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
 
 template <typename XT>
-__host__ __device__ inline long long epi_stage_bytes() {
-  return (long long)kEpiThreads * 16 * sizeof(XT) + 2LL * kEpiThreads * sizeof(int);
+__host__ __device__ inline long long sums_stage_bytes() {
+  return (long long)kSumThreads * kStageStride * sizeof(XT) + 2LL * kSumThreads * sizeof(int);
 }
 template <typename XT>
-__host__ __device__ inline long long epi_chunk_cells(int K, int dim) {
+__host__ __device__ inline long long sums_chunk_cells(int K, int dim) {
   // per cell: dim int64 sums + uint32 count + uint32 hist + uint32 cursor
-  long long kc = (kEpiSmem - epi_stage_bytes<XT>() - 64) / ((long long)dim * 8 + 12);
+  long long kc = (kEpiSmem - sums_stage_bytes<XT>() - 64) / ((long long)dim * 8 + 12);
   return kc < K ? kc : K;
 }
-__host__ __device__ inline bool epi_warp_sink(int K, int dim) {
-  return (long long)K * (dim * 8 + 4) * (kEpiThreads / 32) <= 96 * 1024;
+__host__ __device__ inline bool sums_warp_sink(int K, int dim) {
+  return (long long)K * (dim * 8 + 4) * (kSumThreads / 32) <= 128 * 1024;
 }
 
 template <typename XT, int DIM>
-__global__ void __launch_bounds__(kEpiThreads, 1) epilogue_kernel(KernelArgs a, const XT* __restrict__ X,
-                                                                 int want_dists, int want_sums,
-                                                                 int zero_cells) {
+__global__ void __launch_bounds__(kEpiThreads, 2) dist_td_kernel(KernelArgs a, const XT* __restrict__ X,
+                                                             int want_dists) {
   const DevState* st = a.st;
   if (st->done) return;
-  const int K = zero_cells ? 1 : st->size;
   const int dim = DIM ? DIM : a.dim;
   const int metric = st->metric;
   const double* __restrict__ cb = a.cb[st->cur];
-  const double scale = ldexp(1.0, st->fixed_shift);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kWarps = kEpiThreads / 32;
-
-  const bool warp_sink = epi_warp_sink(K, dim);
-  const long long kc = warp_sink ? K : epi_chunk_cells<XT>(K, dim);
-  const long long nchunks = (K + kc - 1) / kc;
-  const int chunk = blockIdx.y;
-  if (want_sums ? chunk >= nchunks : chunk > 0) return;
-  const long long c_lo = chunk * kc;
-  const long long c_hi = (c_lo + kc < K) ? c_lo + kc : K;
-  const int ncell = (int)(c_hi - c_lo);
-  const bool do_td = !zero_cells && chunk == 0;
-
-  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[kWarps];
-  __shared__ int s_wsum[kWarps];
-  // warp sink: kWarps tables of [ncell*dim int64 | ncell uint32]
-  // block sink: stage XT[kEpiThreads][16] | cells int[kEpiThreads] | perm int[kEpiThreads]
-  //             | sums int64[ncell*dim] | counts u32[ncell] | hist u32[ncell] | cursor u32[ncell]
-  const long long wt_bytes = ((long long)ncell * dim * 8 + ncell * 4 + 15) / 16 * 16;
-  XT* stage = reinterpret_cast<XT*>(smem_raw);
-  int* s_cells = reinterpret_cast<int*>(smem_raw + (long long)kEpiThreads * 16 * sizeof(XT));
-  int* s_perm = s_cells + kEpiThreads;
-  long long* bsums = reinterpret_cast<long long*>(smem_raw + epi_stage_bytes<XT>());
-  unsigned* bcounts = reinterpret_cast<unsigned*>(bsums + (long long)ncell * dim);
-  unsigned* hist = bcounts + ncell;
-  unsigned* cursor = hist + ncell;
-  long long* wsums = reinterpret_cast<long long*>(smem_raw + warp * wt_bytes);
-  unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
-  if (want_sums) {
-    if (warp_sink) {
-      uint4* z = reinterpret_cast<uint4*>(smem_raw);
-      for (long long i = tid; i < wt_bytes * kWarps / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    } else {
-      for (long long i = tid; i < (long long)ncell * dim; i += blockDim.x) bsums[i] = 0;
-      for (int i = tid; i < ncell; i += blockDim.x) bcounts[i] = 0;
-    }
-    __syncthreads();
-  }
-
   const long long n = a.n;
-  const long long ntiles = (n + kTdTile - 1) / kTdTile;
-  const long long t_lo = ntiles * blockIdx.x / gridDim.x;
-  const long long t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
-  for (long long t = t_lo; t < t_hi; ++t) {
-    const long long tbase = t * kTdTile;
-    double tsum = 0.0;
-    for (int r = 0; r < kTdTile / kEpiThreads; ++r) {
-      const long long row = tbase + (long long)r * kEpiThreads + tid;
-      const bool valid = row < n;
-      const int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
-      const bool mine = want_sums && valid && cell >= c_lo && cell < c_hi;
-      const int lc = mine ? cell - (int)c_lo : -1;
-      const bool block_sums = want_sums && !warp_sink;
-      if (block_sums) {
-        // counting sort of this sub-tile by local cell
-        for (int i = tid; i < ncell; i += blockDim.x) hist[i] = 0;
-        s_cells[tid] = lc;
-        __syncthreads();
-        if (mine) atomicAdd(&hist[lc], 1u);
-        __syncthreads();
-        // exclusive scan hist -> cursor (each thread a contiguous run)
-        const int per = (ncell + kEpiThreads - 1) / kEpiThreads;
-        const int i0 = tid * per, i1 = min(ncell, i0 + per);
-        int run = 0;
-        for (int i = i0; i < i1; ++i) run += hist[i];
-        int incl = run;
+  const long long t = blockIdx.x;  // one distortion tile per block
+  const long long tbase = t * kTdTile;
+  double tsum = 0.0;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int o = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += o;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        int wbase = 0;
-        for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
-        int pos = wbase + incl - run;
-        for (int i = i0; i < i1; ++i) {
-          cursor[i] = pos;
-          pos += hist[i];
-        }
-        __syncthreads();
-        if (mine) s_perm[atomicAdd(&cursor[lc], 1u)] = tid;
-        __syncthreads();
-      }
-      const XT* x = X + (valid ? row : 0) * dim;
-      const double* c = cb + (long long)(cell > 0 ? cell : 0) * dim;
-      double d = 0.0;
-      for (int c0 = 0; c0 < dim; c0 += 16) {
-        const int cw = dim - c0 < 16 ? dim - c0 : 16;
-        double xr[16];
-        if (valid) {
-          if constexpr (DIM > 0 && sizeof(XT) == 4) {
+  for (int r = 0; r < kTdTile / kEpiThreads; ++r) {
+    const long long row = tbase + (long long)r * kEpiThreads + tid;
+    double d = 0.0;
+    if (row < n) {
+      const int cell = a.idx[row];
+      const XT* x = X + row * dim;
+      const double* c = cb + (long long)cell * dim;
+      if constexpr (DIM > 0) {
+#pragma unroll
+        for (int c0 = 0; c0 < DIM; c0 += 16) {
+          double xr[16], cr[16];
+          if constexpr (sizeof(XT) == 4) {
             const float4* x4 = reinterpret_cast<const float4*>(x + c0);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
@@ -744,7 +674,7 @@ __global__ void __launch_bounds__(kEpiThreads, 1) epilogue_kernel(KernelArgs a, 
               xr[4 * v + 2] = q.z;
               xr[4 * v + 3] = q.w;
             }
-          } else if constexpr (DIM > 0) {
+          } else {
             const double2* x2 = reinterpret_cast<const double2*>(x + c0);
 #pragma unroll
             for (int v = 0; v < 8; ++v) {
@@ -752,129 +682,272 @@ __global__ void __launch_bounds__(kEpiThreads, 1) epilogue_kernel(KernelArgs a, 
               xr[2 * v] = q.x;
               xr[2 * v + 1] = q.y;
             }
-          } else {
-#pragma unroll
-            for (int l = 0; l < 16; ++l) xr[l] = l < cw ? load_x(x, c0 + l) : 0.0;
           }
-          if (do_td) {
-            if constexpr (DIM > 0) {
-              double cr[16];
-              const double2* c2 = reinterpret_cast<const double2*>(c + c0);
+          const double2* c2 = reinterpret_cast<const double2*>(c + c0);
 #pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                const double2 q = __ldg(c2 + v);
-                cr[2 * v] = q.x;
-                cr[2 * v + 1] = q.y;
-              }
+          for (int v = 0; v < 8; ++v) {
+            const double2 q = __ldg(c2 + v);
+            cr[2 * v] = q.x;
+            cr[2 * v + 1] = q.y;
+          }
 #pragma unroll
-              for (int l = 0; l < 16; ++l) {
-                const double diff = __dsub_rn(xr[l], cr[l]);
-                d = __dadd_rn(d, __dmul_rn(diff, diff));
-              }
-            } else {
-              for (int l = 0; l < cw; ++l) {
-                const double diff = __dsub_rn(xr[l], c[c0 + l]);
-                d = __dadd_rn(d, __dmul_rn(diff, diff));
-              }
-            }
+          for (int l = 0; l < 16; ++l) {
+            const double diff = __dsub_rn(xr[l], cr[l]);
+            d = __dadd_rn(d, __dmul_rn(diff, diff));
           }
         }
-        if (block_sums) {
-          // stage this 16-dim slice; then each thread sums the segments of
-          // the cells it owns (cell i -> thread i mod blockDim) in sorted order
-#pragma unroll
-          for (int l = 0; l < 16; ++l) stage[tid * 16 + l] = (XT)xr[l];
-          __syncthreads();
-          for (int i = tid; i < ncell; i += blockDim.x) {
-            const unsigned cnt = hist[i];
-            if (cnt == 0) continue;
-            const unsigned beg = cursor[i] - cnt;  // cursor ran to the segment end
-            long long acc[16];
-#pragma unroll
-            for (int l = 0; l < 16; ++l) acc[l] = 0;
-            for (unsigned m = beg; m < beg + cnt; ++m) {
-              const XT* xs = stage + s_perm[m] * 16;
-#pragma unroll
-              for (int l = 0; l < 16; ++l) acc[l] += to_fixed((double)xs[l], scale);
-            }
-            long long* dst = bsums + (long long)i * dim + c0;
-            for (int l = 0; l < cw; ++l) dst[l] += acc[l];
-            if (c0 == 0) bcounts[i] += cnt;
-          }
-          __syncthreads();
-        }
+      } else {
+        d = ref_dist(x, c, dim);
       }
-      if (valid && do_td) {
-        if (metric == kEuclidean) d = sqrt(d);
-        if (want_dists) a.dists[row] = d;
-      }
-      tsum = __dadd_rn(tsum, d);
-      if (want_sums && warp_sink) {
-        // few cells: aggregate the warp's rows per cell (lanes = dims)
-        const unsigned active = __ballot_sync(0xffffffffu, mine);
-        const unsigned grp = __match_any_sync(0xffffffffu, lc);
-        unsigned remaining = active;
-        const long long wrow0 = tbase + (long long)r * kEpiThreads + warp * 32;
-        while (remaining) {
-          const int leader = __ffs(remaining) - 1;
-          const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
-          const int cl = __shfl_sync(0xffffffffu, lc, leader);
-          remaining &= ~members;
-          for (int l0 = 0; l0 < dim; l0 += 32) {
-            const int l = l0 + lane;
-            if (l < dim) {
-              long long acc = 0;
-              unsigned m = members;
-              while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                acc += to_fixed(load_x(X, (wrow0 + b) * dim + l), scale);
-              }
-              wsums[(long long)cl * dim + l] += acc;
+      if (metric == kEuclidean) d = sqrt(d);
+      if (want_dists) a.dists[row] = d;
+    }
+    tsum = __dadd_rn(tsum, d);
+  }
+  // fixed tree: lanes (xor butterfly), then warps in order
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tsum = __dadd_rn(tsum, __shfl_xor_sync(0xffffffffu, tsum, off));
+  if (lane == 0) red[warp] = tsum;
+  __syncthreads();
+  if (tid == 0) {
+    double sacc = 0.0;
+    for (int w = 0; w < kWarps; ++w) sacc = __dadd_rn(sacc, red[w]);
+    a.ex.td()[a.tile0 + t] = __double_as_longlong(sacc);
+  }
+}
+
+template <typename XT, int DIM>
+__device__ __forceinline__ void load_row16(const XT* __restrict__ X, long long row, int dim, int c0,
+                                           bool valid, XT (&xr)[16]) {
+  if (!valid) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) xr[l] = (XT)0;
+    return;
+  }
+  const XT* x = X + row * dim + c0;
+  if constexpr (DIM > 0 && sizeof(XT) == 4) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const float4 q = __ldg(x4 + v);
+      xr[4 * v] = q.x;
+      xr[4 * v + 1] = q.y;
+      xr[4 * v + 2] = q.z;
+      xr[4 * v + 3] = q.w;
+    }
+  } else if constexpr (DIM > 0) {
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double2 q = __ldg(x2 + v);
+      xr[2 * v] = q.x;
+      xr[2 * v + 1] = q.y;
+    }
+  } else {
+    for (int l = 0; l < 16; ++l) xr[l] = (c0 + l < dim) ? x[l] : (XT)0;
+  }
+}
+
+template <typename XT, int DIM>
+__global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, const XT* __restrict__ X,
+                                                             int zero_cells) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = zero_cells ? 1 : st->size;
+  const int dim = DIM ? DIM : a.dim;
+  const double scale = ldexp(1.0, st->fixed_shift);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kSumThreads / 32;
+
+  const bool warp_sink = sums_warp_sink(K, dim);
+  const long long kc = warp_sink ? K : sums_chunk_cells<XT>(K, dim);
+  const long long nchunks = (K + kc - 1) / kc;
+  const int chunk = blockIdx.y;
+  if (chunk >= nchunks) return;
+  const long long c_lo = chunk * kc;
+  const long long c_hi = (c_lo + kc < K) ? c_lo + kc : K;
+  const int ncell = (int)(c_hi - c_lo);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ int s_wsum[kWarps];
+  const long long wt_bytes = ((long long)ncell * dim * 8 + ncell * 4 + 15) / 16 * 16;
+  XT* stage = reinterpret_cast<XT*>(smem_raw);
+  int* s_perm = reinterpret_cast<int*>(smem_raw + (long long)kSumThreads * kStageStride * sizeof(XT));
+  long long* bsums = reinterpret_cast<long long*>(smem_raw + sums_stage_bytes<XT>());
+  unsigned* bcounts = reinterpret_cast<unsigned*>(bsums + (long long)ncell * dim);
+  unsigned* hist = bcounts + ncell;
+  unsigned* cursor = hist + ncell;
+  long long* wsums = reinterpret_cast<long long*>(smem_raw + warp * wt_bytes);
+  unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
+  if (warp_sink) {
+    uint4* z = reinterpret_cast<uint4*>(smem_raw);
+    for (long long i = tid; i < wt_bytes * kWarps / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+  } else {
+    for (long long i = tid; i < (long long)ncell * dim; i += blockDim.x) bsums[i] = 0;
+    for (int i = tid; i < ncell; i += blockDim.x) bcounts[i] = 0;
+  }
+  __syncthreads();
+
+  const long long n = a.n;
+  const long long lo = n * blockIdx.x / gridDim.x;
+  const long long hi = n * (blockIdx.x + 1) / gridDim.x;
+  const int nsub = (int)((hi - lo + kSumThreads - 1) / kSumThreads);
+  // software pipeline: the next sub-tile's cell and first 16 dims are loaded
+  // before this sub-tile's barriers
+  long long row = lo + tid;
+  bool valid = row < hi;
+  int cell_next = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
+  XT xn[16];
+  load_row16<XT, DIM>(X, row, dim, 0, valid, xn);
+  for (int sb = 0; sb < nsub; ++sb) {
+    const int cell = cell_next;
+    XT x0[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) x0[l] = xn[l];
+    const long long cur_row = row;
+    const bool cur_valid = valid;
+    row += kSumThreads;
+    valid = row < hi;
+    if (sb + 1 < nsub) {
+      cell_next = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
+      load_row16<XT, DIM>(X, row, dim, 0, valid, xn);
+    }
+    const bool mine = cur_valid && cell >= c_lo && cell < c_hi;
+    const int lc = mine ? cell - (int)c_lo : -1;
+    if (warp_sink) {
+      // few cells: aggregate the warp's rows per cell (lanes = dims)
+      const unsigned active = __ballot_sync(0xffffffffu, mine);
+      const unsigned grp = __match_any_sync(0xffffffffu, lc);
+      unsigned remaining = active;
+      const long long wrow0 = cur_row - lane;
+      while (remaining) {
+        const int leader = __ffs(remaining) - 1;
+        const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
+        const int cl = __shfl_sync(0xffffffffu, lc, leader);
+        remaining &= ~members;
+        for (int l0 = 0; l0 < dim; l0 += 32) {
+          const int l = l0 + lane;
+          if (l < dim) {
+            long long acc = 0;
+            unsigned m = members;
+            while (m) {
+              const int b = __ffs(m) - 1;
+              m &= m - 1;
+              acc += to_fixed(load_x(X, (wrow0 + b) * dim + l), scale);
             }
+            wsums[(long long)cl * dim + l] += acc;
           }
-          if (lane == 0) wcounts[cl] += __popc(members);
-          __syncwarp();
         }
+        if (lane == 0) wcounts[cl] += __popc(members);
+        __syncwarp();
+      }
+      continue;
+    }
+    // ---- counting sort of this sub-tile by local cell
+    for (int i = tid; i < ncell; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    if (mine) atomicAdd(&hist[lc], 1u);
+    __syncthreads();
+    {
+      const int per = (ncell + kSumThreads - 1) / kSumThreads;
+      const int i0 = tid * per, i1 = min(ncell, i0 + per);
+      int run = 0;
+      for (int i = i0; i < i1; ++i) run += hist[i];
+      int incl = run;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      int wbase = 0;
+      for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
+      int pos = wbase + incl - run;
+      for (int i = i0; i < i1; ++i) {
+        cursor[i] = pos;
+        pos += hist[i];
       }
     }
-    if (do_td) {
-      // fixed tree: lanes (xor butterfly), then warps in order
+    __syncthreads();
+    if (mine) s_perm[atomicAdd(&cursor[lc], 1u)] = tid;
+    for (int c0 = 0; c0 < dim; c0 += 16) {
+      const int cw = dim - c0 < 16 ? dim - c0 : 16;
+      XT xr[16];
+      if (c0 == 0) {
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-        tsum = __dadd_rn(tsum, __shfl_xor_sync(0xffffffffu, tsum, off));
-      if (lane == 0) red[warp] = tsum;
+        for (int l = 0; l < 16; ++l) xr[l] = x0[l];
+      } else {
+        load_row16<XT, DIM>(X, cur_row, dim, c0, mine, xr);
+      }
+      if (mine) {
+        if constexpr (sizeof(XT) == 4) {
+          float4* dst = reinterpret_cast<float4*>(stage + tid * kStageStride);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) dst[v] = make_float4(xr[4 * v], xr[4 * v + 1], xr[4 * v + 2], xr[4 * v + 3]);
+        } else {
+          double2* dst = reinterpret_cast<double2*>(stage + tid * kStageStride);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) dst[v] = make_double2(xr[2 * v], xr[2 * v + 1]);
+        }
+      }
       __syncthreads();
-      if (tid == 0) {
-        double sacc = 0.0;
-        for (int w = 0; w < kWarps; ++w) sacc = __dadd_rn(sacc, red[w]);
-        a.ex.td()[a.tile0 + t] = __double_as_longlong(sacc);
+      for (int i = tid; i < ncell; i += blockDim.x) {
+        const unsigned cnt = hist[i];
+        if (cnt == 0) continue;
+        const unsigned beg = cursor[i] - cnt;  // cursor ran to the segment end
+        long long acc[16];
+#pragma unroll
+        for (int l = 0; l < 16; ++l) acc[l] = 0;
+        for (unsigned m = beg; m < beg + cnt; ++m) {
+          const XT* xs = stage + s_perm[m] * kStageStride;
+          XT v[16];
+          if constexpr (sizeof(XT) == 4) {
+            const float4* s4 = reinterpret_cast<const float4*>(xs);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 t4 = s4[q];
+              v[4 * q] = t4.x;
+              v[4 * q + 1] = t4.y;
+              v[4 * q + 2] = t4.z;
+              v[4 * q + 3] = t4.w;
+            }
+          } else {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) v[l] = xs[l];
+          }
+#pragma unroll
+          for (int l = 0; l < 16; ++l) acc[l] += to_fixed((double)v[l], scale);
+        }
+        // table is [dim][ncell]: consecutive threads -> consecutive words
+        for (int l = 0; l < cw; ++l) bsums[(long long)(c0 + l) * ncell + i] += acc[l];
+        if (c0 == 0) bcounts[i] += cnt;
       }
       __syncthreads();
     }
   }
-  if (want_sums) {
-    __syncthreads();
-    // block partial slab [blockIdx.x][K*dim sums | K counts] (int64)
-    long long* slab = a.partials + (long long)blockIdx.x * ((long long)a.kmax * dim + a.kmax);
-    const long long words = (long long)ncell * dim;
-    if (warp_sink) {
-      for (long long i = tid; i < words; i += blockDim.x) {
-        long long v = 0;
-        for (int w = 0; w < kWarps; ++w)
-          v += reinterpret_cast<const long long*>(smem_raw + w * wt_bytes)[i];
-        slab[c_lo * dim + i] = v;
-      }
-      for (int i = tid; i < ncell; i += blockDim.x) {
-        long long v = 0;
-        for (int w = 0; w < kWarps; ++w)
-          v += reinterpret_cast<const unsigned*>(smem_raw + w * wt_bytes + words * 8)[i];
-        slab[(long long)K * dim + c_lo + i] = v;
-      }
-    } else {
-      for (long long i = tid; i < words; i += blockDim.x) slab[c_lo * dim + i] = bsums[i];
-      for (int i = tid; i < ncell; i += blockDim.x) slab[(long long)K * dim + c_lo + i] = bcounts[i];
+  __syncthreads();
+  // block slab [blockIdx.x][K*dim sums | K counts] (int64)
+  long long* slab = a.partials + (long long)blockIdx.x * ((long long)a.kmax * dim + a.kmax);
+  const long long words = (long long)ncell * dim;
+  if (warp_sink) {
+    for (long long i = tid; i < words; i += blockDim.x) {
+      long long v = 0;
+      for (int w = 0; w < kWarps; ++w) v += reinterpret_cast<const long long*>(smem_raw + w * wt_bytes)[i];
+      slab[c_lo * dim + i] = v;
     }
+    for (int i = tid; i < ncell; i += blockDim.x) {
+      long long v = 0;
+      for (int w = 0; w < kWarps; ++w)
+        v += reinterpret_cast<const unsigned*>(smem_raw + w * wt_bytes + words * 8)[i];
+      slab[(long long)K * dim + c_lo + i] = v;
+    }
+  } else {
+    for (long long i = tid; i < words; i += blockDim.x) {
+      const long long cl = i / dim, l = i % dim;
+      slab[c_lo * dim + i] = bsums[l * ncell + cl];
+    }
+    for (int i = tid; i < ncell; i += blockDim.x) slab[(long long)K * dim + c_lo + i] = bcounts[i];
   }
 }
 
@@ -918,18 +991,27 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int 
 
 template <typename XT, int DIM>
 static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
-                                  bool zero_cells, int blocks, cudaStream_t s) {
+                                  bool zero_cells, int sms, cudaStream_t s) {
+  cudaError_t e;
+  if (!zero_cells) {
+    const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
+    dist_td_kernel<XT, DIM><<<(unsigned)ntiles, kEpiThreads, 0, s>>>(a, X, want_dists ? 1 : 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (!want_sums) return cudaSuccess;
   const long long kmax = zero_cells ? 1 : a.kmax;
-  const long long kc = epi_warp_sink((int)kmax, a.dim) ? kmax : epi_chunk_cells<XT>((int)kmax, a.dim);
-  const int chunks = want_sums ? (int)((kmax + kc - 1) / kc) : 1;
-  const size_t smem = want_sums ? kEpiSmem : 0;
-  cudaError_t e = cudaFuncSetAttribute(epilogue_kernel<XT, DIM>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kEpiSmem);
+  const long long kc = sums_warp_sink((int)kmax, a.dim) ? kmax : sums_chunk_cells<XT>((int)kmax, a.dim);
+  const int chunks = (int)((kmax + kc - 1) / kc);
+  const long long rows_per_block = 4LL * kSumThreads;
+  int blocks = (int)((a.n + rows_per_block - 1) / rows_per_block);
+  if (blocks > sms) blocks = sms;
+  if (blocks < 1) blocks = 1;
+  e = cudaFuncSetAttribute(sums_kernel<XT, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEpiSmem);
   if (e != cudaSuccess) return e;
-  epilogue_kernel<XT, DIM><<<dim3(blocks, chunks), kEpiThreads, smem, s>>>(a, X, want_dists, want_sums,
-                                                                         zero_cells);
+  sums_kernel<XT, DIM><<<dim3(blocks, chunks), kSumThreads, kEpiSmem, s>>>(a, X, zero_cells ? 1 : 0);
   e = cudaGetLastError();
-  if (e != cudaSuccess || !want_sums) return e;
+  if (e != cudaSuccess) return e;
   const long long words = kmax * a.dim + kmax;
   int rb = (int)((words + 31) / 32);
   if (rb > 8192) rb = 8192;
@@ -940,14 +1022,11 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_di
 template <typename XT>
 static cudaError_t launch_epi_t(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
                                 bool zero_cells, int sms, cudaStream_t s) {
-  const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
-  int blocks = (int)(ntiles < (long long)sms ? ntiles : (long long)sms);
-  if (blocks < 1) blocks = 1;
   switch (a.dim) {
-    case 16: return launch_epi_dim<XT, 16>(a, X, want_dists, want_sums, zero_cells, blocks, s);
-    case 32: return launch_epi_dim<XT, 32>(a, X, want_dists, want_sums, zero_cells, blocks, s);
-    case 64: return launch_epi_dim<XT, 64>(a, X, want_dists, want_sums, zero_cells, blocks, s);
-    default: return launch_epi_dim<XT, 0>(a, X, want_dists, want_sums, zero_cells, blocks, s);
+    case 16: return launch_epi_dim<XT, 16>(a, X, want_dists, want_sums, zero_cells, sms, s);
+    case 32: return launch_epi_dim<XT, 32>(a, X, want_dists, want_sums, zero_cells, sms, s);
+    case 64: return launch_epi_dim<XT, 64>(a, X, want_dists, want_sums, zero_cells, sms, s);
+    default: return launch_epi_dim<XT, 0>(a, X, want_dists, want_sums, zero_cells, sms, s);
   }
 }
 
@@ -959,8 +1038,9 @@ cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums
 
 // ---------------------------------------------------------------------------
 // ordered update: the reference's own summation order (update_rows,
-// _kernels.py:47-58: members of cell i summed in ascending training index)
-// one thread per (cell, dim); writes the new codebook directly.
+// _kernels.py:47-58: members of cell i summed in ascending training index),
+// one thread per (cell, dim).  Writes the new centroids to the `ord` buffer;
+// apply_kernel picks them up.
 // ---------------------------------------------------------------------------
 
 template <typename XT>
@@ -970,7 +1050,6 @@ __global__ void ordered_update_kernel(KernelArgs a, const XT* __restrict__ X) {
   const int K = st->size;
   const int dim = a.dim;
   const double* old = a.cb[st->cur];
-  double* out = a.cb[st->cur ^ 1];
   const long long n = a.n;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)K * dim;
        t += (long long)gridDim.x * blockDim.x) {
@@ -983,7 +1062,7 @@ __global__ void ordered_update_kernel(KernelArgs a, const XT* __restrict__ X) {
         ++cnt;
       }
     }
-    out[t] = cnt > 0 ? __ddiv_rn(s, (double)cnt) : old[t];
+    a.ord[t] = cnt > 0 ? __ddiv_rn(s, (double)cnt) : old[t];
     if (l == 0) a.ex.counts()[k] = cnt;
   }
 }
@@ -1000,8 +1079,10 @@ cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// finalize: one block.  phase 0 = after the initial column-sum pass,
-// phase 1 = after an allocation pass.
+// finalize (one block): the pass's distortion, the convergence test
+// (core.py:342-356), level / guard logic (core.py:384-415) and history.  It
+// only DECIDES: the codebook work (centroids, split, FP32 staging) is done
+// by apply_kernel over all SMs.  phase 0 = after the initial column-sum pass.
 // ---------------------------------------------------------------------------
 
 __device__ void record_hist(DevState* st, int size, int it, double td, long long empty) {
@@ -1016,51 +1097,54 @@ __device__ void record_hist(DevState* st, int size, int it, double td, long long
   st->n_hist += 1;
 }
 
-__global__ void __launch_bounds__(1024) finalize_kernel(KernelArgs a, int phase) {
+// action bits for apply_kernel
+constexpr int kActUpdate = 1;
+constexpr int kActSplit = 2;
+
+__device__ __forceinline__ void set_action(DevState* st, int act) {
+  // the source codebook is the current one; the result goes to the other buffer
+  st->act = act;
+  st->act_src = st->cur;
+  st->act_k = st->size;
+  st->cur ^= 1;
+  if (act & kActSplit) {
+    st->size = 2 * st->size;
+    st->iteration = 1;
+    st->td_prev = INFINITY;
+  }
+}
+
+__global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) {
   DevState* st = a.st;
   if (st->done) return;
-  if (threadIdx.x == 0) st->flagged_total += st->flag_count;
-  __shared__ int s_action;  // 0 none, 1 update, 2 split-after(cur), 3 update+split, 4 done
+  __shared__ double red[8];
+  __shared__ long long s_empty[8];
   __shared__ double s_td;
-  __shared__ double red[32];
-  const int tid = threadIdx.x;
-  const int dim = a.dim;
-  const double inv_scale = ldexp(1.0, -st->fixed_shift);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    st->flagged_total += st->flag_count;
+    st->flag_count = 0;
+  }
 
   if (phase == 0) {
-    // global centroid: column sums / m (core.py:380 / parallel.py:273)
-    double* cb = a.cb[st->cur];
-    if (!st->ordered) {
-      for (int l = tid; l < dim; l += blockDim.x)
-        cb[l] = __ddiv_rn((double)a.ex.sums()[l] * inv_scale, (double)st->n_global);
-    }
-    __syncthreads();
+    // global centroid = column sums / m (core.py:380, parallel.py:273): an
+    // "update" of the size-1 codebook whose single cell holds every row,
+    // followed by the first split unless target_size == 1 (core.py:417-422)
     if (tid == 0) {
       st->t0_ns = globaltimer();
-      if (st->ordered) st->cur ^= 1;  // ordered_update wrote the centroid there
-    }
-    __syncthreads();
-    // split or final-assign setup happens below via the same split code
-    if (st->target <= 1) {
-      if (tid == 0) {
+      if (st->target <= 1) {
         st->mode = kModeFinalAssign;
-        st->size = 1;
+        set_action(st, kActUpdate);
+      } else {
+        set_action(st, kActUpdate | kActSplit);
       }
-      goto clear;
     }
-    if (tid == 0) s_action = 2;
-    __syncthreads();
-    goto apply;
+    return;
   }
 
-  if (st->mode == kModeUpdateOnly) {
-    if (tid == 0) s_action = 1;
-    __syncthreads();
-    goto update;
-  }
-  {
-    // ---- distortion of this pass
-    double td;
+  // ---- distortion of this pass (fixed tree over tiles; in-order if ordered)
+  const int K = st->size;
+  if (st->mode != kModeUpdateOnly) {
     if (st->ordered) {
       if (tid == 0) {
         double s = 0.0;  // _kernels.sum_inorder (_kernels.py:92-98)
@@ -1075,7 +1159,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(KernelArgs a, int phase)
         s = __dadd_rn(s, __longlong_as_double(a.ex.td()[i]));
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
-      if ((tid & 31) == 0) red[tid >> 5] = s;
+      if (lane == 0) red[warp] = s;
       __syncthreads();
       if (tid == 0) {
         double t2 = 0.0;
@@ -1083,147 +1167,182 @@ __global__ void __launch_bounds__(1024) finalize_kernel(KernelArgs a, int phase)
         s_td = t2;
       }
     }
-    __syncthreads();
-    td = s_td;
-    const int K = st->size;
-    if (tid == 0) {
-      st->passes += 1;
-      st->evals += a.n * (long long)K;
-      st->last_td = td;
-    }
-    if (st->mode == kModeFinalAssign || st->mode == kModeAssignOnly) {
-      if (tid == 0) {
-        st->total = td;
-        st->done = 1;
-      }
-      return;
-    }
-    if (st->mode == kModeLloydStep) {
-      if (tid == 0) {
-        st->total = td;
-        s_action = 1;
-      }
-      __syncthreads();
-      goto update;
-    }
-    // ---- convergence test (core.py:342-356) -- only tid 0 decides
-    if (tid == 0) {
-      const double p = st->td_prev;
-      bool conv;
-      if (isinf(p))
-        conv = false;
-      else if (p == 0.0)
-        conv = true;
-      else
-        conv = __ddiv_rn(__dsub_rn(p, td), p) <= st->eps;
-      s_action = conv ? 2 : 1;
-    }
-    __syncthreads();
-    if (s_action != 1) {
-      if (tid == 0) record_hist(st, K, st->iteration, td, 0);
-      __syncthreads();
-      goto apply;
-    }
   }
-
-update:
-  {
-    // centroid update (update_rows _kernels.py:59-66): sum / n, empty keeps old
-    const int K = st->size;
-    const double* old = a.cb[st->cur];
-    double* out = a.cb[st->cur ^ 1];
-    int empty = 0;
-    for (int k = tid; k < K; k += blockDim.x) {
-      const long long cnt = a.ex.counts()[k];
-      if (cnt == 0) ++empty;
-      if (!st->ordered) {
-        for (int l = 0; l < dim; ++l) {
-          const long long idx = (long long)k * dim + l;
-          out[idx] = cnt > 0 ? __ddiv_rn((double)a.ex.sums()[idx] * inv_scale, (double)cnt) : old[idx];
-        }
-      }
-    }
-    // empties: block reduction (integer, order-free)
+  // ---- empty cells (counts == 0) of this pass
+  long long e = 0;
+  for (int k = tid; k < K; k += blockDim.x) e += (a.ex.counts()[k] == 0);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) empty += __shfl_xor_sync(0xffffffffu, empty, off);
-    if ((tid & 31) == 0) red[tid >> 5] = (double)empty;
-    __syncthreads();
-    if (tid == 0) {
-      long long e = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) e += (long long)red[w];
-      st->last_empty = e;
-      st->cur ^= 1;
-      if (st->mode == kModeUpdateOnly || st->mode == kModeLloydStep) {
-        st->done = 1;
-        s_action = 0;
-      } else {
-        record_hist(st, K, st->iteration, st->last_td, e);
-        st->td_prev = st->last_td;
-        st->iteration += 1;
-        if (st->iteration > st->max_iter) {
-          // guard exhausted: warning, level ends with the UPDATED codebook
-          // (core.py:400-415); the total stays the pre-update TD.
-          if (st->n_warn < kMaxWarn) st->warn_sizes[st->n_warn] = K;
-          st->n_warn += 1;
-          s_action = 2;
-        } else {
-          s_action = 0;
-        }
-      }
-    }
-    __syncthreads();
-    if (st->mode == kModeUpdateOnly || st->mode == kModeLloydStep) return;
-  }
-
-apply:
-  if (s_action == 2) {
-    const int K = st->size;
-    if (K < st->target) {
-      // split (core.py:277-281): row i -> 2i (+delta), 2i+1 (-delta)
-      const double* src = a.cb[st->cur];
-      double* dst = a.cb[st->cur ^ 1];
-      const double delta = st->delta;
-      for (long long i = tid; i < (long long)K * dim; i += blockDim.x) {
-        const long long k = i / dim, l = i % dim;
-        dst[(2 * k) * dim + l] = __dadd_rn(src[i], delta);
-        dst[(2 * k + 1) * dim + l] = __dsub_rn(src[i], delta);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        st->cur ^= 1;
-        st->size = 2 * K;
-        st->iteration = 1;
-        st->td_prev = INFINITY;
-      }
-    } else {
-      if (tid == 0) {
-        st->total = st->last_td;
-        st->done = 1;
-      }
-    }
-  }
-
-clear:
+  for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+  if (lane == 0) s_empty[warp] = e;
   __syncthreads();
-  // zero the exchange buffer for the next pass
-  for (long long i = tid; i < a.ex.words(); i += blockDim.x) a.ex.base[i] = 0;
-  if (tid == 0) st->flag_count = 0;
+  if (tid != 0) return;
+  long long empties = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) empties += s_empty[w];
+  const double td = s_td;
+
+  if (st->mode == kModeUpdateOnly) {
+    st->last_empty = empties;
+    set_action(st, kActUpdate);
+    st->done = 1;
+    return;
+  }
+  st->passes += 1;
+  st->evals += a.n * (long long)K;
+  st->last_td = td;
+  if (st->mode == kModeFinalAssign || st->mode == kModeAssignOnly) {
+    st->total = td;
+    st->act = 0;
+    st->done = 1;
+    return;
+  }
+  if (st->mode == kModeLloydStep) {
+    st->total = td;
+    st->last_empty = empties;
+    set_action(st, kActUpdate);
+    st->done = 1;
+    return;
+  }
+  // ---- convergence test (core.py:342-356)
+  const double p = st->td_prev;
+  bool conv;
+  if (isinf(p))
+    conv = false;
+  else if (p == 0.0)
+    conv = true;
+  else
+    conv = __ddiv_rn(__dsub_rn(p, td), p) <= st->eps;
+  if (conv) {
+    // history rows of a converged pass carry empty_cells = 0 (core.py:395-397)
+    record_hist(st, K, st->iteration, td, 0);
+    if (K < st->target) {
+      set_action(st, kActSplit);
+    } else {
+      st->act = 0;
+      st->total = td;
+      st->done = 1;
+    }
+    return;
+  }
+  record_hist(st, K, st->iteration, td, empties);
+  st->td_prev = td;
+  st->iteration += 1;
+  if (st->iteration > st->max_iter) {
+    // guard exhausted: a warning, and the level ends with the UPDATED
+    // codebook while the total stays the pre-update TD (core.py:400-417)
+    if (st->n_warn < kMaxWarn) st->warn_sizes[st->n_warn] = K;
+    st->n_warn += 1;
+    if (K < st->target) {
+      set_action(st, kActUpdate | kActSplit);
+    } else {
+      set_action(st, kActUpdate);
+      st->total = td;
+      st->done = 1;
+    }
+  } else {
+    set_action(st, kActUpdate);
+  }
 }
 
-cudaError_t launch_finalize(const KernelArgs& a, cudaStream_t s) {
-  finalize_kernel<<<1, 1024, 0, s>>>(a, 1);
+// ---------------------------------------------------------------------------
+// apply: one thread per source codevector.  Update (update_rows,
+// _kernels.py:59-66: sum / n with the int64 fixed-point sum, empty cells keep
+// the old row), split (core.py:277-281: rows 2i = c + delta, 2i+1 = c - delta)
+// or both, into the other codebook buffer, plus the centred FP32 staging of
+// the new rows for the next candidate pass.  Idempotent (speculative passes
+// after `done` may repeat it harmlessly).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void stage_row(const KernelArgs& a, long long k, const double* row, int dim) {
+  double n = 0.0;
+  float* w = a.w + k * dim;
+  for (int l = 0; l < dim; ++l) {
+    const float c = (float)(row[l] - (double)a.mu[l]);
+    n += (double)c * (double)c;
+    w[l] = -2.0f * c;
+  }
+  a.nrm[k] = (float)n;
+}
+
+__global__ void __launch_bounds__(128) apply_kernel(KernelArgs a, int stage) {
+  const DevState* st = a.st;
+  const int act = st->act;
+  // zero the distortion tiles (other ranks' slots must be 0 before the next
+  // allreduce); finalize has consumed them
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.ex.ntiles;
+       i += (long long)gridDim.x * blockDim.x)
+    a.ex.td()[i] = 0;
+  if (act == 0) return;
+  const int K = st->act_k;
+  const int dim = a.dim;
+  const double* src = a.cb[st->act_src];
+  double* dst = a.cb[st->act_src ^ 1];
+  const double inv_scale = ldexp(1.0, -st->fixed_shift);
+  const double delta = st->delta;
+  const int ordered = st->ordered;
+  double newr[64], r2[64];
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < K;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long cnt = (act & kActUpdate) ? a.ex.counts()[k] : 0;
+    for (int c0 = 0; c0 < dim; c0 += 64) {
+      const int cw = dim - c0 < 64 ? dim - c0 : 64;
+      for (int l = 0; l < cw; ++l) {
+        const long long i = k * dim + c0 + l;
+        double v = src[i];
+        if ((act & kActUpdate) && cnt > 0)
+          v = ordered ? a.ord[i] : __ddiv_rn((double)a.ex.sums()[i] * inv_scale, (double)cnt);
+        newr[l] = v;
+      }
+      if (act & kActSplit) {
+        for (int l = 0; l < cw; ++l) {
+          r2[l] = __dsub_rn(newr[l], delta);
+          newr[l] = __dadd_rn(newr[l], delta);
+          dst[(2 * k) * dim + c0 + l] = newr[l];
+          dst[(2 * k + 1) * dim + c0 + l] = r2[l];
+        }
+      } else {
+        for (int l = 0; l < cw; ++l) dst[k * dim + c0 + l] = newr[l];
+      }
+    }
+    if (stage) {
+      if (act & kActSplit) {
+        stage_row(a, 2 * k, dst + (2 * k) * dim, dim);
+        stage_row(a, 2 * k + 1, dst + (2 * k + 1) * dim, dim);
+      } else {
+        stage_row(a, k, dst + k * dim, dim);
+      }
+    }
+  }
+}
+
+cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s) {
+  finalize_kernel<<<1, 256, 0, s>>>(a, 1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int blocks = (int)((a.kmax + 127) / 128);
+  if (blocks < 8) blocks = 8;
+  apply_kernel<<<blocks, 128, 0, s>>>(a, stage ? 1 : 0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_init_centroid(const KernelArgs& a, cudaStream_t s) {
-  finalize_kernel<<<1, 1024, 0, s>>>(a, 0);
+cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s) {
+  finalize_kernel<<<1, 256, 0, s>>>(a, 0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  apply_kernel<<<8, 128, 0, s>>>(a, stage ? 1 : 0);
   return cudaGetLastError();
 }
 
+// staging padding (rows >= K never win) and a clean exchange buffer
 __global__ void clear_kernel(KernelArgs a) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.ex.words();
        i += (long long)gridDim.x * blockDim.x)
     a.ex.base[i] = 0;
+  const long long kpad = (a.kmax + 3) / 4 * 4;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < kpad;
+       k += (long long)gridDim.x * blockDim.x) {
+    a.nrm[k] = INFINITY;
+    for (int l = 0; l < a.dim; ++l) a.w[k * a.dim + l] = 0.0f;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.st->flag_count = 0;
 }
 

@@ -11,7 +11,7 @@ namespace vqb {
 constexpr int kMaxHist = 8192;   // levels x max_iterations_per_level records
 constexpr int kMaxWarn = 64;     // one warning per level at most
 constexpr int kTdTile = 2048;    // rows per distortion partial (fixed, global)
-constexpr int kEpiThreads = 512; // epilogue block: 4 rows per thread per tile
+constexpr int kEpiThreads = 1024; // dist/TD block: 2 rows per thread per 2048-row tile
 
 // metric codes (reference _kernels.py:14-15)
 constexpr int kSquared = 0;
@@ -63,6 +63,9 @@ struct DevState {
   int passes;          // allocation passes executed
   long long flagged_total;  // rows re-ranked over the whole run (diagnostic)
   long long evals;     // sum over passes of rows * size (this shard)
+  int act;             // apply_kernel action bits (update 1, split 2)
+  int act_src;         // buffer holding the source codebook of the action
+  int act_k;           // source codebook size
   unsigned long long t0_ns;  // %globaltimer at the initial centroid
   HistRec hist[kMaxHist];
 };
@@ -100,6 +103,7 @@ struct KernelArgs {
   double* dists;        // nullable
   Exchange ex;
   long long* partials;  // per-block fixed-point slabs, sms x (kmax*dim + kmax)
+  double* ord;          // reference-order centroids (ordered mode), kmax x dim
   DevState* st;
 };
 
@@ -110,8 +114,8 @@ cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s);
 cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums, bool zero_cells,
                             int sms, cudaStream_t s);
 cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s);
-cudaError_t launch_finalize(const KernelArgs& a, cudaStream_t s);
-cudaError_t launch_init_centroid(const KernelArgs& a, cudaStream_t s);
+cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s);
+cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s);
 cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s);
 cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
                           unsigned long long* out_bits, int sms, cudaStream_t s);
