@@ -489,6 +489,100 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
   const int K = st->size;
   const int dim = DIM ? DIM : a.dim;
   const double* __restrict__ cb = a.cb[st->cur];
+  if constexpr (DIM > 0) {
+    if (K > 32) {
+      // large K: a batch of 8 rows per block shares every codevector load;
+      // thread t scans j = t, t + 256, ... for all 8 rows
+      constexpr int B = 8;
+      __shared__ XT xs[B][DIM];
+      __shared__ double s_b[8][B];
+      __shared__ int s_j[8][B];
+      __shared__ long long s_row[B];
+      const long long count = use_list ? (long long)st->flag_count : a.n;
+      for (long long base = (long long)blockIdx.x * B; base < count; base += (long long)gridDim.x * B) {
+        if (threadIdx.x < B) {
+          const long long i = base + threadIdx.x;
+          s_row[threadIdx.x] = i < count ? (use_list ? (long long)a.flags[i] : i) : -1;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < B * DIM; e += blockDim.x) {
+          const long long r = s_row[e / DIM];
+          xs[e / DIM][e % DIM] = r >= 0 ? X[r * DIM + e % DIM] : (XT)0;
+        }
+        __syncthreads();
+        double best[B];
+        int bj[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          best[b] = INFINITY;
+          bj[b] = 0x7fffffff;
+        }
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
+          const double* c = cb + (long long)j * DIM;
+          double d[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) d[b] = 0.0;
+#pragma unroll
+          for (int c0 = 0; c0 < DIM; c0 += 16) {
+            double cr[16];
+            const double2* c2 = reinterpret_cast<const double2*>(c + c0);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const double2 q = __ldg(c2 + v);
+              cr[2 * v] = q.x;
+              cr[2 * v + 1] = q.y;
+            }
+            // the reference's arithmetic, ascending c (_kernels.py:25-29)
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+#pragma unroll
+              for (int l = 0; l < 16; ++l) {
+                const double diff = __dsub_rn((double)xs[b][c0 + l], cr[l]);
+                d[b] = __dadd_rn(d[b], __dmul_rn(diff, diff));
+              }
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+            if (d[b] < best[b]) {  // ascending j per thread: first minimum kept
+              best[b] = d[b];
+              bj[b] = j;
+            }
+        }
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best[b], off);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj[b], off);
+            if (ob < best[b] || (ob == best[b] && oj < bj[b])) {
+              best[b] = ob;
+              bj[b] = oj;
+            }
+          }
+          if (lane == 0) {
+            s_b[w][b] = best[b];
+            s_j[w][b] = bj[b];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < B && s_row[threadIdx.x] >= 0) {
+          const int b = threadIdx.x;
+          double bb = s_b[0][b];
+          int jj = s_j[0][b];
+          for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+            if (s_b[k][b] < bb || (s_b[k][b] == bb && s_j[k][b] < jj)) {
+              bb = s_b[k][b];
+              jj = s_j[k][b];
+            }
+          a.idx[s_row[b]] = (bb < INFINITY) ? jj : 0;  // nothing < inf -> index 0
+        }
+        __syncthreads();
+      }
+      return;
+    }
+  }
   int T = 1;
   while (T < K && T < (int)blockDim.x) T <<= 1;
   const int rpb = blockDim.x / T;
@@ -602,105 +696,115 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 // epilogue: exact winner distance, distortion tiles, fixed-point cell sums
 // ---------------------------------------------------------------------------
 
-// The epilogue is two kernels.
+// The epilogue:
 //
-// dist_td_kernel (thread per row, one block per 2048-row distortion tile,
-// high occupancy): the winner's exact FP64 distance in the reference's
-// arithmetic -> dists, and the tile's fixed-tree FP64 distortion partial.
+// dist_td_kernel (one block per 2048-row tile): each row's exact FP64
+// distance to its final winner and the tile's fixed-tree distortion partial
+// (sum_inorder's role, _kernels.py:92-98, in a fixed order that does not
+// depend on the grid or on the number of GPUs).
 //
-// sums_kernel (one persistent 1024-thread block per SM over a contiguous row
-// range): int64 fixed-point cell sums + counts (integer adds commute, so the
-// result is deterministic for every grid shape and every GPU count):
+// sums_kernel (one persistent block per SM over a contiguous row range,
+// thread per row): int64 fixed-point cell sums + counts.  Integer adds
+// commute, so the result is deterministic for every grid shape and GPU count.
 //  * small K: warp-private smem tables, rows aggregated per cell inside the
 //    warp (match_any), lanes = dims, plain adds;
-//  * otherwise: per 1024-row sub-tile a counting sort by cell (native 32-bit
-//    smem atomics), rows staged in smem (padded, conflict-free STS.128), then
-//    the thread owning each cell sums its segment into the block table with
-//    plain int64 adds -- no 64-bit atomics.  Codebooks whose table would not
-//    fit are split into chunks (gridDim.y).
+//  * otherwise: a block table [dim][cell] accumulated with NATIVE 32-bit smem
+//    atomics -- an exact int64 add is atomicAdd on the low word (the returned
+//    old value gives the carry) plus atomicAdd on the high word.  Codebooks
+//    whose table would not fit are split into chunks (gridDim.y).
 // Each block writes its table to a slab; reduce_partials_kernel sums them.
 constexpr int kSumThreads = 512;
-constexpr int kStageStride = 20;  // floats per staged row: 16 used, padded (bank-conflict free)
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
 
-template <typename XT>
-__host__ __device__ inline long long sums_stage_bytes() {
-  return (long long)kSumThreads * kStageStride * sizeof(XT) + 2LL * kSumThreads * sizeof(int);
-}
-template <typename XT>
 __host__ __device__ inline long long sums_chunk_cells(int K, int dim) {
-  // per cell: dim int64 sums + uint32 count + uint32 hist + uint32 cursor
-  long long kc = (kEpiSmem - sums_stage_bytes<XT>() - 64) / ((long long)dim * 8 + 12);
+  // per cell: dim x (u32 lo + i32 hi) + u32 count
+  long long kc = (kEpiSmem - 64) / ((long long)dim * 8 + 4);
   return kc < K ? kc : K;
 }
 __host__ __device__ inline bool sums_warp_sink(int K, int dim) {
   return (long long)K * (dim * 8 + 4) * (kSumThreads / 32) <= 128 * 1024;
 }
 
+// exact int64 accumulation from two native 32-bit shared atomics
+__device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, long long t) {
+  const unsigned lo = (unsigned)(unsigned long long)t;
+  int hi = (int)(t >> 32);
+  const unsigned old = atomicAdd(lo_word, lo);
+  if (old + lo < old) hi += 1;  // carry out of the low word
+  if (hi) atomicAdd(hi_word, hi);
+}
+
 template <typename XT, int DIM>
-__global__ void __launch_bounds__(kEpiThreads, 2) dist_td_kernel(KernelArgs a, const XT* __restrict__ X,
-                                                             int want_dists) {
+__device__ __forceinline__ double winner_dist(const XT* __restrict__ x, const double* __restrict__ c,
+                                              int dim) {
+  double d = 0.0;
+  if constexpr (DIM > 0) {
+#pragma unroll
+    for (int c0 = 0; c0 < DIM; c0 += 16) {
+      double xr[16], cr[16];
+      if constexpr (sizeof(XT) == 4) {
+        const float4* x4 = reinterpret_cast<const float4*>(x + c0);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float4 q = __ldg(x4 + v);
+          xr[4 * v] = q.x;
+          xr[4 * v + 1] = q.y;
+          xr[4 * v + 2] = q.z;
+          xr[4 * v + 3] = q.w;
+        }
+      } else {
+        const double2* x2 = reinterpret_cast<const double2*>(x + c0);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const double2 q = __ldg(x2 + v);
+          xr[2 * v] = q.x;
+          xr[2 * v + 1] = q.y;
+        }
+      }
+      const double2* c2 = reinterpret_cast<const double2*>(c + c0);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double2 q = __ldg(c2 + v);
+        cr[2 * v] = q.x;
+        cr[2 * v + 1] = q.y;
+      }
+#pragma unroll
+      for (int l = 0; l < 16; ++l) {
+        const double diff = __dsub_rn(xr[l], cr[l]);
+        d = __dadd_rn(d, __dmul_rn(diff, diff));
+      }
+    }
+  } else {
+    d = ref_dist(x, c, dim);
+  }
+  return d;
+}
+
+// One block per 2048-row tile: the final winner's distance in the
+// reference's FP64 arithmetic (_kernels.py:25-34) -> dists, and the tile's
+// fixed-tree distortion partial (sum_inorder's role, in an order independent
+// of the grid and of the number of GPUs).
+template <typename XT, int DIM>
+__global__ void __launch_bounds__(256, 4) dist_td_kernel(KernelArgs a, const XT* __restrict__ X) {
   const DevState* st = a.st;
   if (st->done) return;
+  __shared__ double red[8];
   const int dim = DIM ? DIM : a.dim;
   const int metric = st->metric;
   const double* __restrict__ cb = a.cb[st->cur];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int kWarps = kEpiThreads / 32;
-  __shared__ double red[kWarps];
+  const long long t = blockIdx.x;
   const long long n = a.n;
-  const long long t = blockIdx.x;  // one distortion tile per block
-  const long long tbase = t * kTdTile;
   double tsum = 0.0;
-#pragma unroll
-  for (int r = 0; r < kTdTile / kEpiThreads; ++r) {
-    const long long row = tbase + (long long)r * kEpiThreads + tid;
+#pragma unroll 2
+  for (int r = 0; r < kTdTile / 256; ++r) {
+    const long long row = t * kTdTile + (long long)r * 256 + tid;
     double d = 0.0;
     if (row < n) {
       const int cell = a.idx[row];
-      const XT* x = X + row * dim;
-      const double* c = cb + (long long)cell * dim;
-      if constexpr (DIM > 0) {
-#pragma unroll
-        for (int c0 = 0; c0 < DIM; c0 += 16) {
-          double xr[16], cr[16];
-          if constexpr (sizeof(XT) == 4) {
-            const float4* x4 = reinterpret_cast<const float4*>(x + c0);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const float4 q = __ldg(x4 + v);
-              xr[4 * v] = q.x;
-              xr[4 * v + 1] = q.y;
-              xr[4 * v + 2] = q.z;
-              xr[4 * v + 3] = q.w;
-            }
-          } else {
-            const double2* x2 = reinterpret_cast<const double2*>(x + c0);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              const double2 q = __ldg(x2 + v);
-              xr[2 * v] = q.x;
-              xr[2 * v + 1] = q.y;
-            }
-          }
-          const double2* c2 = reinterpret_cast<const double2*>(c + c0);
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const double2 q = __ldg(c2 + v);
-            cr[2 * v] = q.x;
-            cr[2 * v + 1] = q.y;
-          }
-#pragma unroll
-          for (int l = 0; l < 16; ++l) {
-            const double diff = __dsub_rn(xr[l], cr[l]);
-            d = __dadd_rn(d, __dmul_rn(diff, diff));
-          }
-        }
-      } else {
-        d = ref_dist(x, c, dim);
-      }
+      d = winner_dist<XT, DIM>(X + row * dim, cb + (long long)cell * dim, dim);
       if (metric == kEuclidean) d = sqrt(d);
-      if (want_dists) a.dists[row] = d;
+      a.dists[row] = d;
     }
     tsum = __dadd_rn(tsum, d);
   }
@@ -711,40 +815,8 @@ __global__ void __launch_bounds__(kEpiThreads, 2) dist_td_kernel(KernelArgs a, c
   __syncthreads();
   if (tid == 0) {
     double sacc = 0.0;
-    for (int w = 0; w < kWarps; ++w) sacc = __dadd_rn(sacc, red[w]);
+    for (int w = 0; w < 8; ++w) sacc = __dadd_rn(sacc, red[w]);
     a.ex.td()[a.tile0 + t] = __double_as_longlong(sacc);
-  }
-}
-
-template <typename XT, int DIM>
-__device__ __forceinline__ void load_row16(const XT* __restrict__ X, long long row, int dim, int c0,
-                                           bool valid, XT (&xr)[16]) {
-  if (!valid) {
-#pragma unroll
-    for (int l = 0; l < 16; ++l) xr[l] = (XT)0;
-    return;
-  }
-  const XT* x = X + row * dim + c0;
-  if constexpr (DIM > 0 && sizeof(XT) == 4) {
-    const float4* x4 = reinterpret_cast<const float4*>(x);
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const float4 q = __ldg(x4 + v);
-      xr[4 * v] = q.x;
-      xr[4 * v + 1] = q.y;
-      xr[4 * v + 2] = q.z;
-      xr[4 * v + 3] = q.w;
-    }
-  } else if constexpr (DIM > 0) {
-    const double2* x2 = reinterpret_cast<const double2*>(x);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const double2 q = __ldg(x2 + v);
-      xr[2 * v] = q.x;
-      xr[2 * v + 1] = q.y;
-    }
-  } else {
-    for (int l = 0; l < 16; ++l) xr[l] = (c0 + l < dim) ? x[l] : (XT)0;
   }
 }
 
@@ -760,7 +832,7 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   constexpr int kWarps = kSumThreads / 32;
 
   const bool warp_sink = sums_warp_sink(K, dim);
-  const long long kc = warp_sink ? K : sums_chunk_cells<XT>(K, dim);
+  const long long kc = warp_sink ? K : sums_chunk_cells(K, dim);
   const long long nchunks = (K + kc - 1) / kc;
   const int chunk = blockIdx.y;
   if (chunk >= nchunks) return;
@@ -769,57 +841,36 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const int ncell = (int)(c_hi - c_lo);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ int s_wsum[kWarps];
+  // warp sink: kWarps tables [ncell*dim int64 | ncell u32]
+  // block sink: lo u32 [dim][ncell] | hi i32 [dim][ncell] | counts u32 [ncell]
   const long long wt_bytes = ((long long)ncell * dim * 8 + ncell * 4 + 15) / 16 * 16;
-  XT* stage = reinterpret_cast<XT*>(smem_raw);
-  int* s_perm = reinterpret_cast<int*>(smem_raw + (long long)kSumThreads * kStageStride * sizeof(XT));
-  long long* bsums = reinterpret_cast<long long*>(smem_raw + sums_stage_bytes<XT>());
-  unsigned* bcounts = reinterpret_cast<unsigned*>(bsums + (long long)ncell * dim);
-  unsigned* hist = bcounts + ncell;
-  unsigned* cursor = hist + ncell;
   long long* wsums = reinterpret_cast<long long*>(smem_raw + warp * wt_bytes);
   unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
-  if (warp_sink) {
+  unsigned* blo = reinterpret_cast<unsigned*>(smem_raw);
+  int* bhi = reinterpret_cast<int*>(blo + (long long)ncell * dim);
+  unsigned* bcounts = reinterpret_cast<unsigned*>(bhi + (long long)ncell * dim);
+  {
+    const long long zbytes = warp_sink ? wt_bytes * kWarps : (long long)ncell * dim * 8 + ncell * 4;
     uint4* z = reinterpret_cast<uint4*>(smem_raw);
-    for (long long i = tid; i < wt_bytes * kWarps / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-  } else {
-    for (long long i = tid; i < (long long)ncell * dim; i += blockDim.x) bsums[i] = 0;
-    for (int i = tid; i < ncell; i += blockDim.x) bcounts[i] = 0;
+    for (long long i = tid; i < (zbytes + 15) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
 
   const long long n = a.n;
   const long long lo = n * blockIdx.x / gridDim.x;
   const long long hi = n * (blockIdx.x + 1) / gridDim.x;
-  const int nsub = (int)((hi - lo + kSumThreads - 1) / kSumThreads);
-  // software pipeline: the next sub-tile's cell and first 16 dims are loaded
-  // before this sub-tile's barriers
-  long long row = lo + tid;
-  bool valid = row < hi;
-  int cell_next = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
-  XT xn[16];
-  load_row16<XT, DIM>(X, row, dim, 0, valid, xn);
-  for (int sb = 0; sb < nsub; ++sb) {
-    const int cell = cell_next;
-    XT x0[16];
-#pragma unroll
-    for (int l = 0; l < 16; ++l) x0[l] = xn[l];
-    const long long cur_row = row;
-    const bool cur_valid = valid;
-    row += kSumThreads;
-    valid = row < hi;
-    if (sb + 1 < nsub) {
-      cell_next = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
-      load_row16<XT, DIM>(X, row, dim, 0, valid, xn);
-    }
-    const bool mine = cur_valid && cell >= c_lo && cell < c_hi;
+  for (long long base = lo; base < hi; base += kSumThreads) {
+    const long long row = base + tid;
+    const bool valid = row < hi;
+    const int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
+    const bool mine = valid && cell >= c_lo && cell < c_hi;
     const int lc = mine ? cell - (int)c_lo : -1;
     if (warp_sink) {
       // few cells: aggregate the warp's rows per cell (lanes = dims)
       const unsigned active = __ballot_sync(0xffffffffu, mine);
       const unsigned grp = __match_any_sync(0xffffffffu, lc);
       unsigned remaining = active;
-      const long long wrow0 = cur_row - lane;
+      const long long wrow0 = row - lane;
       while (remaining) {
         const int leader = __ffs(remaining) - 1;
         const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
@@ -843,88 +894,41 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
       }
       continue;
     }
-    // ---- counting sort of this sub-tile by local cell
-    for (int i = tid; i < ncell; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    if (mine) atomicAdd(&hist[lc], 1u);
-    __syncthreads();
-    {
-      const int per = (ncell + kSumThreads - 1) / kSumThreads;
-      const int i0 = tid * per, i1 = min(ncell, i0 + per);
-      int run = 0;
-      for (int i = i0; i < i1; ++i) run += hist[i];
-      int incl = run;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += o;
-      }
-      if (lane == 31) s_wsum[warp] = incl;
-      __syncthreads();
-      int wbase = 0;
-      for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
-      int pos = wbase + incl - run;
-      for (int i = i0; i < i1; ++i) {
-        cursor[i] = pos;
-        pos += hist[i];
-      }
-    }
-    __syncthreads();
-    if (mine) s_perm[atomicAdd(&cursor[lc], 1u)] = tid;
+    if (!mine) continue;
+    const XT* x = X + row * dim;
     for (int c0 = 0; c0 < dim; c0 += 16) {
       const int cw = dim - c0 < 16 ? dim - c0 : 16;
       XT xr[16];
-      if (c0 == 0) {
+      if constexpr (DIM > 0 && sizeof(XT) == 4) {
+        const float4* x4 = reinterpret_cast<const float4*>(x + c0);
 #pragma unroll
-        for (int l = 0; l < 16; ++l) xr[l] = x0[l];
+        for (int v = 0; v < 4; ++v) {
+          const float4 q = __ldg(x4 + v);
+          xr[4 * v] = q.x;
+          xr[4 * v + 1] = q.y;
+          xr[4 * v + 2] = q.z;
+          xr[4 * v + 3] = q.w;
+        }
+      } else if constexpr (DIM > 0) {
+        const double2* x2 = reinterpret_cast<const double2*>(x + c0);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const double2 q = __ldg(x2 + v);
+          xr[2 * v] = q.x;
+          xr[2 * v + 1] = q.y;
+        }
       } else {
-        load_row16<XT, DIM>(X, cur_row, dim, c0, mine, xr);
+        for (int l = 0; l < 16; ++l) xr[l] = l < cw ? x[c0 + l] : (XT)0;
       }
-      if (mine) {
-        if constexpr (sizeof(XT) == 4) {
-          float4* dst = reinterpret_cast<float4*>(stage + tid * kStageStride);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) dst[v] = make_float4(xr[4 * v], xr[4 * v + 1], xr[4 * v + 2], xr[4 * v + 3]);
-        } else {
-          double2* dst = reinterpret_cast<double2*>(stage + tid * kStageStride);
-#pragma unroll
-          for (int v = 0; v < 8; ++v) dst[v] = make_double2(xr[2 * v], xr[2 * v + 1]);
+      for (int l = 0; l < 16; ++l) {
+        if (l < cw) {
+          const long long w = (long long)(c0 + l) * ncell + lc;  // [dim][cell]: spread banks
+          smem_add_i64(blo + w, bhi + w, to_fixed((double)xr[l], scale));
         }
       }
-      __syncthreads();
-      for (int i = tid; i < ncell; i += blockDim.x) {
-        const unsigned cnt = hist[i];
-        if (cnt == 0) continue;
-        const unsigned beg = cursor[i] - cnt;  // cursor ran to the segment end
-        long long acc[16];
-#pragma unroll
-        for (int l = 0; l < 16; ++l) acc[l] = 0;
-        for (unsigned m = beg; m < beg + cnt; ++m) {
-          const XT* xs = stage + s_perm[m] * kStageStride;
-          XT v[16];
-          if constexpr (sizeof(XT) == 4) {
-            const float4* s4 = reinterpret_cast<const float4*>(xs);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 t4 = s4[q];
-              v[4 * q] = t4.x;
-              v[4 * q + 1] = t4.y;
-              v[4 * q + 2] = t4.z;
-              v[4 * q + 3] = t4.w;
-            }
-          } else {
-#pragma unroll
-            for (int l = 0; l < 16; ++l) v[l] = xs[l];
-          }
-#pragma unroll
-          for (int l = 0; l < 16; ++l) acc[l] += to_fixed((double)v[l], scale);
-        }
-        // table is [dim][ncell]: consecutive threads -> consecutive words
-        for (int l = 0; l < cw; ++l) bsums[(long long)(c0 + l) * ncell + i] += acc[l];
-        if (c0 == 0) bcounts[i] += cnt;
-      }
-      __syncthreads();
     }
+    atomicAdd(bcounts + lc, 1u);
   }
   __syncthreads();
   // block slab [blockIdx.x][K*dim sums | K counts] (int64)
@@ -945,7 +949,8 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   } else {
     for (long long i = tid; i < words; i += blockDim.x) {
       const long long cl = i / dim, l = i % dim;
-      slab[c_lo * dim + i] = bsums[l * ncell + cl];
+      const long long w = l * ncell + cl;
+      slab[c_lo * dim + i] = (long long)(((unsigned long long)(unsigned)bhi[w] << 32) + blo[w]);
     }
     for (int i = tid; i < ncell; i += blockDim.x) slab[(long long)K * dim + c_lo + i] = bcounts[i];
   }
@@ -990,18 +995,18 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int 
 }
 
 template <typename XT, int DIM>
-static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
+static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td, bool want_sums,
                                   bool zero_cells, int sms, cudaStream_t s) {
   cudaError_t e;
-  if (!zero_cells) {
+  if (want_td && !zero_cells) {
     const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
-    dist_td_kernel<XT, DIM><<<(unsigned)ntiles, kEpiThreads, 0, s>>>(a, X, want_dists ? 1 : 0);
+    dist_td_kernel<XT, DIM><<<(unsigned)ntiles, 256, 0, s>>>(a, X);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (!want_sums) return cudaSuccess;
   const long long kmax = zero_cells ? 1 : a.kmax;
-  const long long kc = sums_warp_sink((int)kmax, a.dim) ? kmax : sums_chunk_cells<XT>((int)kmax, a.dim);
+  const long long kc = sums_warp_sink((int)kmax, a.dim) ? kmax : sums_chunk_cells((int)kmax, a.dim);
   const int chunks = (int)((kmax + kc - 1) / kc);
   const long long rows_per_block = 4LL * kSumThreads;
   int blocks = (int)((a.n + rows_per_block - 1) / rows_per_block);
