@@ -289,6 +289,12 @@ def run_b200(args):
     traffic = _load_traffic()
 
     result = None
+    if getattr(args, "profile_steps", False):
+        clocks.__exit__(None, None, None)
+        if rank == 0:
+            print(json.dumps({"profile_steps": args.steps, "ms_per_step": ms_step,
+                              "segments_ms": seg}), flush=True)
+        return 0
     if rank == 0:
         # ---- e2e: the same iteration through the C ABI with host buffers
         xp = torch.from_numpy(x).pin_memory().numpy()
@@ -395,6 +401,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--profile-steps", action="store_true",
+                    help="only the warm-up + timed steps (for ncu launch lists)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

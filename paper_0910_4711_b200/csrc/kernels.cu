@@ -724,6 +724,7 @@ __host__ __device__ inline long long sums_chunk_cells(int K, int dim) {
 __host__ __device__ inline bool sums_warp_sink(int K, int dim) {
   return (long long)K * (dim * 8 + 4) * (kSumThreads / 32) <= 128 * 1024;
 }
+constexpr int kWStageStride = 20;  // staged row stride (elements), padded against bank conflicts
 
 // exact int64 accumulation from two native 32-bit shared atomics
 __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, long long t) {
@@ -821,6 +822,38 @@ __global__ void __launch_bounds__(256, 4) dist_td_kernel(KernelArgs a, const XT*
 }
 
 template <typename XT, int DIM>
+__device__ __forceinline__ void load_row16(const XT* __restrict__ X, long long row, int dim, int c0,
+                                           bool valid, XT (&xr)[16]) {
+  if (!valid) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) xr[l] = (XT)0;
+    return;
+  }
+  const XT* x = X + row * dim + c0;
+  if constexpr (DIM > 0 && sizeof(XT) == 4) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const float4 q = __ldg(x4 + v);
+      xr[4 * v] = q.x;
+      xr[4 * v + 1] = q.y;
+      xr[4 * v + 2] = q.z;
+      xr[4 * v + 3] = q.w;
+    }
+  } else if constexpr (DIM > 0) {
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double2 q = __ldg(x2 + v);
+      xr[2 * v] = q.x;
+      xr[2 * v + 1] = q.y;
+    }
+  } else {
+    for (int l = 0; l < 16; ++l) xr[l] = (c0 + l < dim) ? x[l] : (XT)0;
+  }
+}
+
+template <typename XT, int DIM>
 __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, const XT* __restrict__ X,
                                                              int zero_cells) {
   const DevState* st = a.st;
@@ -846,6 +879,7 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const long long wt_bytes = ((long long)ncell * dim * 8 + ncell * 4 + 15) / 16 * 16;
   long long* wsums = reinterpret_cast<long long*>(smem_raw + warp * wt_bytes);
   unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
+  XT* wstage = reinterpret_cast<XT*>(smem_raw + wt_bytes * kWarps);  // [warps][32][kWStageStride]
   unsigned* blo = reinterpret_cast<unsigned*>(smem_raw);
   int* bhi = reinterpret_cast<int*>(blo + (long long)ncell * dim);
   unsigned* bcounts = reinterpret_cast<unsigned*>(bhi + (long long)ncell * dim);
@@ -866,30 +900,36 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
     const bool mine = valid && cell >= c_lo && cell < c_hi;
     const int lc = mine ? cell - (int)c_lo : -1;
     if (warp_sink) {
-      // few cells: aggregate the warp's rows per cell (lanes = dims)
+      // few cells: aggregate the warp's rows per cell.  The warp's 32 rows
+      // are staged 16 dims at a time in its smem slice (coalesced loads,
+      // padded rows), then lanes = dims sum each cell group.
       const unsigned active = __ballot_sync(0xffffffffu, mine);
       const unsigned grp = __match_any_sync(0xffffffffu, lc);
-      unsigned remaining = active;
-      const long long wrow0 = row - lane;
-      while (remaining) {
-        const int leader = __ffs(remaining) - 1;
-        const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
-        const int cl = __shfl_sync(0xffffffffu, lc, leader);
-        remaining &= ~members;
-        for (int l0 = 0; l0 < dim; l0 += 32) {
-          const int l = l0 + lane;
-          if (l < dim) {
+      XT* xs = wstage + warp * 32 * kWStageStride;
+      for (int c0 = 0; c0 < dim; c0 += 16) {
+        XT xr[16];
+        load_row16<XT, DIM>(X, row, dim, c0, mine, xr);
+#pragma unroll
+        for (int l = 0; l < 16; ++l) xs[lane * kWStageStride + l] = xr[l];
+        __syncwarp();
+        unsigned remaining = active;
+        while (remaining) {
+          const int leader = __ffs(remaining) - 1;
+          const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
+          const int cl = __shfl_sync(0xffffffffu, lc, leader);
+          remaining &= ~members;
+          if (lane < 16 && c0 + lane < dim) {
             long long acc = 0;
             unsigned m = members;
             while (m) {
               const int b = __ffs(m) - 1;
               m &= m - 1;
-              acc += to_fixed(load_x(X, (wrow0 + b) * dim + l), scale);
+              acc += to_fixed((double)xs[b * kWStageStride + lane], scale);
             }
-            wsums[(long long)cl * dim + l] += acc;
+            wsums[(long long)cl * dim + c0 + lane] += acc;
           }
+          if (lane == 0 && c0 == 0) wcounts[cl] += __popc(members);
         }
-        if (lane == 0) wcounts[cl] += __popc(members);
         __syncwarp();
       }
       continue;
