@@ -176,6 +176,61 @@ __global__ void __launch_bounds__(256) dist_const_kernel(float* out, const float
   if (s == 123.456f || si == -7) out[0] = s + si;
 }
 
+
+// FFMA2 and scalar FFMA interleaved (independent chains): does the scalar
+// FFMA co-issue on the fmalite half while FFMA2 occupies fmaheavy?
+template <int CHAINS>
+__global__ void __launch_bounds__(256) ffma2_mix_kernel(float* out, int iters, float a, float b) {
+  unsigned long long acc[CHAINS];
+  float sc[CHAINS];
+  float2 av = make_float2(a, a), bv = make_float2(b, b);
+  unsigned long long ab = *reinterpret_cast<unsigned long long*>(&av);
+  unsigned long long bb = *reinterpret_cast<unsigned long long*>(&bv);
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    float2 v = make_float2(threadIdx.x * 1e-7f + c, c * 0.5f);
+    acc[c] = *reinterpret_cast<unsigned long long*>(&v);
+    sc[c] = threadIdx.x * 3e-7f + c;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) {
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(acc[c]) : "l"(ab), "l"(bb));
+        sc[c] = fmaf(sc[c], a, b);
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    float2 v = *reinterpret_cast<float2*>(&acc[c]);
+    s += v.x + v.y + sc[c];
+  }
+  if (s == 123.456f) out[0] = s;
+}
+
+// ALU-pipe rate: FMNMX chains (top-2 bookkeeping is FMNMX/FSETP/SEL)
+template <int CHAINS>
+__global__ void __launch_bounds__(256) fmnmx_kernel(float* out, int iters, float a) {
+  float acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-7f + c;
+  for (int it = 0; it < iters; ++it) {
+    const float t = a + it;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) acc[c] = fminf(acc[c], (k & 1) ? -t : t);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 123.456f) out[0] = s;
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -183,7 +238,8 @@ using namespace vqb;
 // Returns achieved lane-ops/s (FMA counted once) for pipe `which`:
 // 0 = FFMA, 1 = FFMA2 (2 lane-ops per instruction), 2 = 16xFFMA + top-2 mix
 // (counts the 16 FFMA only), 3 = DADD, 4 = 3-register FFMA, 5 = evals/s of a
-// constant-memory-codebook distance loop.  `seconds` gets the kernel time.
+// constant-memory-codebook distance loop, 6 = FFMA2 + FFMA interleaved (FMA
+// lane-ops), 7 = FMNMX (ALU pipe).  `seconds` gets the kernel time.
 extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
                                    double* seconds) {
   int dev = 0, sms = 0;
@@ -226,6 +282,14 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         break;
       case 4:
         ffma3r_kernel<8><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
+        break;
+      case 6:
+        ffma2_mix_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.999f, 1e-3f);
+        lane_ops = 3.0 * blocks * threads * iters * 16 * 8;
+        break;
+      case 7:
+        fmnmx_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.5f);
         lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
         break;
       default:  // 5: evals/s of the constant-codebook distance loop (K=512, R=4)
