@@ -391,6 +391,138 @@ def run_b200(args):
     return 0
 
 
+def _workload_golden(name):
+    path = os.path.join(ROOT, "tests", "golden",
+                        f"{name}_{'encode' if name == 'cfg5' else 'design'}.npz")
+    return np.load(path) if os.path.exists(path) else None
+
+
+def run_workload(args):
+    """One BASELINE config end to end on one GPU (parity-checked against the
+    reference's committed outputs where they exist):
+      cfg1/cfg3/cfg4  full codebook design (device-resident wall time and
+                      through lbg_train with host buffers) + one Lloyd
+                      iteration at the final codebook;
+      cfg5            encode of 2^26 queries (device-resident allocation pass,
+                      and through encode() from host memory)."""
+    import torch
+
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200 import _lib, synthetic
+    from paper_0910_4711_b200.core import _Session
+
+    name = args.workload
+    L = _lib.lib()
+    spec = synthetic.WORKLOADS[name]
+    g = _workload_golden(name)
+    clocks = ClockSampler(0).__enter__()
+    out = {"impl": "b200", "n_gpus": 1, "data": "synthetic", "steps": args.steps,
+           "warmup": args.warmup, "scaling": "weak", "vs_baseline": None}
+    if name == "cfg5":
+        cb32, q = synthetic.make_encode_case()
+        cb = cb32.astype(np.float64)
+        n, K = q.shape[0], cb.shape[0]
+        sess = _Session(q, None)
+        ms, total, fl = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _lib.check(L.vqb_bench_assign(sess.handle, _lib.ptr(cb), K, max(1, args.warmup),
+                                      ctypes.byref(ms), ctypes.byref(total), ctypes.byref(fl)))
+        _lib.check(L.vqb_bench_assign(sess.handle, _lib.ptr(cb), K, args.steps,
+                                      ctypes.byref(ms), ctypes.byref(total), ctypes.byref(fl)))
+        dev_ms = ms.value
+        idx = sess.assign_u32(cb)
+        sess.close()
+        del sess
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        stream = vq.encode(q, vq.Codebook(cb))
+        e2e_s = time.perf_counter() - t0
+        import hashlib
+        parity = None
+        if g is not None:
+            parity = {
+                "indices_sha256_match": hashlib.sha256(idx.tobytes()).hexdigest()
+                == g["idx_sha256"].item().decode(),
+                "encode_api_sha256_match": hashlib.sha256(stream.indices.tobytes()).hexdigest()
+                == g["idx_sha256"].item().decode(),
+                "total_rel_err": abs(total.value - float(g["total"])) / float(g["total"]),
+                "reference_encode_s": float(g["seconds"]),
+                "reference_workers": int(g["workers"]),
+            }
+        out.update({
+            "metric": "G vector·codeword distance evals/s (encode pass)",
+            "value": n * K / (dev_ms * 1e-3) / 1e9, "unit": "G evals/s",
+            "ms_per_step": dev_ms, "higher_is_better": True, "dtype": "f32+f64",
+            "config": {"workload": f"{name}: encode N=2^26 L=16 K=1024 (fixed seeded codebook)",
+                       "rows": n, "codebook": K, "dim": 16},
+            "rerank_rows_per_step": int(fl.value),
+            "e2e": {"value": n * K / e2e_s / 1e9, "unit": "G evals/s", "seconds": e2e_s,
+                    "h2d_bytes_per_step": int(q.nbytes + cb.nbytes),
+                    "d2h_bytes_per_step": int(n * 4)},
+            "parity": parity,
+        })
+    else:
+        x = synthetic.make_training(name)
+        n, dim = x.shape
+        conf = vq.LbgConfig(target_size=spec.target_size, epsilon=spec.epsilon, delta=spec.delta)
+        sess = _Session(x, None)
+        for _ in range(max(1, args.warmup if name != "cfg4" else 1)):
+            dcb, hist, warns, total, _d, summ = sess.train(conf)
+        reps = max(1, args.steps if name != "cfg4" else min(args.steps, 2))
+        walls = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            dcb, hist, warns, total, _d, summ = sess.train(conf)
+            walls.append(time.perf_counter() - t0)
+        wall = min(walls)
+        cbf = np.ascontiguousarray(g["cb"]) if g is not None else np.ascontiguousarray(dcb)
+        segs = (ctypes.c_double * 5)()
+        flagged = ctypes.c_int64()
+        _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cbf), cbf.shape[0], 3, segs,
+                                         ctypes.byref(flagged)))
+        _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cbf), cbf.shape[0], args.steps, segs,
+                                         ctypes.byref(flagged)))
+        it_ms = sum(segs)
+        t0 = time.perf_counter()
+        cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)
+        e2e_s = time.perf_counter() - t0
+        parity = None
+        if g is not None:
+            gh = g["hist"]
+            parity = {
+                "reference_passes": int(gh.shape[0]),
+                "schedule_matches_reference": bool(
+                    len(hist) == gh.shape[0] and all(
+                        (h.codebook_size, h.iteration, h.empty_cells) ==
+                        (int(r[0]), int(r[1]), int(r[3])) for h, r in zip(hist, gh))),
+                "total_rel_err": abs(total - float(g["total"])) / float(g["total"]),
+                "codebook_max_rel_err": float(np.max(np.abs(dcb - g["cb"]) /
+                                                     np.maximum(np.abs(g["cb"]), 1e-300))),
+                "codebook_bit_identical": bool(dcb.tobytes() == g["cb"].tobytes()),
+                "reference_wall_s": float(g["seconds"]),
+                "reference_workers": int(g["workers"]),
+            }
+        out.update({
+            "metric": "codebook design wall-time (s)", "value": wall, "unit": "s",
+            "ms_per_step": wall * 1e3, "higher_is_better": False, "dtype": "f32+f64",
+            "config": {"workload": f"{name}: {spec.name} N={n} L={dim} K 1->{spec.target_size}, "
+                                   f"delta={spec.delta}, eps={spec.epsilon}",
+                       "rows": n, "dim": dim, "target_size": spec.target_size},
+            "passes": int(summ.passes), "evals": int(summ.evals),
+            "design_g_evals_per_s": summ.evals / wall / 1e9,
+            "flagged_rows": int(summ.flagged_rows),
+            "final_iteration": {"ms": it_ms, "g_evals_per_s": n * cbf.shape[0] / (it_ms * 1e-3) / 1e9,
+                                "segments_ms": list(segs), "rerank_rows": int(flagged.value)},
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(x.nbytes),
+                    "d2h_bytes_per_step": int(dcb.nbytes)},
+            "parity": parity,
+        })
+    clocks.__exit__(None, None, None)
+    c = clocks.summary()
+    out["clocks"] = {k: c[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def sess_fast(sess) -> bool:
     return sess.dim in (16, 32, 64)
 
@@ -401,11 +533,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg2 (default) is the headline line; the others print one line each")
     ap.add_argument("--profile-steps", action="store_true",
                     help="only the warm-up + timed steps (for ncu launch lists)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload != "cfg2":
+        return run_workload(args)
     return run_b200(args)
 
 

@@ -183,6 +183,12 @@ int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per
 int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
                         double* ms_segments, int64_t* flagged);
 
+/* Time `reps` device-resident allocation passes (assign + re-rank + exact
+ * distances + distortion) at a fixed codebook: ms_out = average ms per pass,
+ * total_out = that pass's distortion, flagged = rows re-ranked per pass. */
+int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int reps,
+                     double* ms_out, double* total_out, int64_t* flagged);
+
 #ifdef __cplusplus
 }
 #endif

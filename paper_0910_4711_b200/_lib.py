@@ -98,6 +98,7 @@ def lib():
             "vqb_lloyd_step_f32": ([_P, _I64, _I64, _P, _I64, _I32, _P, _P, _P, _P], _I32),
             "vqb_pipe_microbench": ([_I32, _I32, _I32, _P, _P], _I32),
             "vqb_bench_iteration": ([_P, _P, _I64, _I32, _P, _P], _I32),
+            "vqb_bench_assign": ([_P, _P, _I64, _I32, _P, _P, _P], _I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -913,4 +913,44 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
   return VQB_OK;
 }
 
+// Time `reps` device-resident allocation passes (assign_cells / encode over
+// the session's rows: candidate pass + re-rank + exact distances + tree-order
+// distortion) at a fixed codebook.  ms_out = average per pass (CUDA events on
+// the session stream); total_out = the last pass's distortion.
+int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int reps, double* ms_out,
+                     double* total_out, int64_t* flagged) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  if (reps < 1) return fail(VQB_USAGE, "reps must be >= 1");
+  CK(cudaSetDevice(s->device));
+  int rc = upload_codebook(s, codebook, size);
+  if (rc) return rc;
+  rc = set_state(s, kModeAssignOnly, size, 0, 0);
+  if (rc) return rc;
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  if (s->fast) CK(launch_prep_codebook(a, s->stream));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s->stream));
+  for (int r = 0; r < reps; ++r) {
+    CK(launch_reset(s->st, kModeAssignOnly, (int)size, 0, 0, 1, s->stream));
+    CK(launch_assign(a, s->fast, s->sms, s->stream));
+    if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+    CK(launch_epilogue(a, true, false, false, s->sms, s->stream));
+    CK(launch_finalize(a, false, s->stream));
+  }
+  CK(cudaEventRecord(e1, s->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(cudaMemcpy(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost));
+  *ms_out = ms / reps;
+  if (total_out) *total_out = s->st_host->total;
+  if (flagged) *flagged = s->st_host->flagged_total / reps;
+  return VQB_OK;
+}
+
 }  // extern "C"
