@@ -151,18 +151,23 @@ class DeviceShard:
         return cb[: int(summ.final_size)], history, warnings, float(summ.total), dists
 
 
-def run_sharded(backend, config, batch: int = 4):
+def run_sharded(backend, config, batch: int = 4, collective: bool = True):
     """Drive the pass loop on every rank.  Collectives: one MAX allreduce of
     |x| (common fixed-point scale), then per pass one SUM allreduce of the
     packed int64 exchange buffer.  Ranks stay in lockstep because every rank
-    derives `done` from identical combined bits."""
+    derives `done` from identical combined bits.  ``collective=False`` runs
+    the same loop on one rank without any collective."""
     import torch.distributed as dist
 
+    def all_reduce(t, op):
+        if collective:
+            dist.all_reduce(t, op=op)
+
     gmax = backend.tensor([backend.maxabs()])
-    dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+    all_reduce(gmax, dist.ReduceOp.MAX)
     backend.begin(config, float(gmax.item()))
     ex = backend.exchange()
-    dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+    all_reduce(ex, dist.ReduceOp.SUM)
     backend.finalize()
     levels = max(1, int(math.log2(config.target_size)))
     limit = (levels + 1) * (config.max_iterations_per_level + 1) + 2 * batch
@@ -170,7 +175,7 @@ def run_sharded(backend, config, batch: int = 4):
     while True:
         for _ in range(batch):
             backend.local()
-            dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+            all_reduce(ex, dist.ReduceOp.SUM)
             backend.finalize()
         passes += batch
         if backend.poll():
@@ -210,6 +215,21 @@ def sharded_lbg_train(ts, config, backend_factory=None):
 
     rank, world = dist.get_rank(), dist.get_world_size()
     plan = ShardPlan(ts.m, world)
+    if plan.tiles < world:
+        # fewer 2048-row tiles than ranks: some shard would be empty.  Every
+        # rank designs the whole (small) set on its own device instead -- the
+        # result is the same bits everywhere, no collective needed.
+        plan = ShardPlan(ts.m, 1)
+        world, rank = 1, 0
+        from .core import _session_of
+
+        if backend_factory is None:
+            cb, history, warnings, total, dists, _summ = _session_of(ts).train(config)
+            per_worker = [_inorder(dists[a:b])
+                          for a, b in partition_training(ts.m, config.workers).ranges]
+            return Codebook(cb), DistortionStats(per_worker=per_worker, total=total,
+                                                 history=history, warnings=warnings,
+                                                 vector_count=ts.m)
     lo, hi = plan.bounds(rank)
     x32 = ts.__dict__.get("_x32")
     rows = (x32 if x32 is not None else ts.vectors)[lo:hi]
@@ -220,8 +240,12 @@ def sharded_lbg_train(ts, config, backend_factory=None):
     else:
         backend = backend_factory(rows, lo, ts.m)
         gdev = None
-    cb, history, warnings, total, dists = run_sharded(backend, config)
-    all_dists = gather_rows(dists, plan, gdev)
+    if plan.world == 1:  # replica fallback above: no collective
+        cb, history, warnings, total, dists = run_sharded(backend, config, collective=False)
+        all_dists = dists
+    else:
+        cb, history, warnings, total, dists = run_sharded(backend, config)
+        all_dists = gather_rows(dists, plan, gdev)
     per_worker = [_inorder(all_dists[a:b]) for a, b in partition_training(ts.m, config.workers).ranges]
     stats = DistortionStats(per_worker=per_worker, total=total, history=history,
                             warnings=warnings, vector_count=ts.m)

@@ -1,0 +1,286 @@
+"""Multi-GPU host logic on CPU: world_size-2 gloo runs of the sharded design
+driver (paper_0910_4711_b200/distributed.py: ShardPlan, run_sharded,
+gather_rows, sharded_lbg_train).
+
+The GPU backend (DeviceShard over libvqb200.so) is replaced by
+``EmulatedShard``, a numpy restatement of the device pass protocol
+(kernels.cu: epilogue -> packed int64 exchange buffer [K*L fixed-point sums |
+K counts | distortion tile partials], finalize_kernel / apply_kernel state
+machine) with the oracle doing the allocation.  The collectives are the real
+torch.distributed calls over gloo, so what is tested is exactly the rank
+protocol: one MAX allreduce for the fixed-point scale, one SUM allreduce of
+the exchange buffer per pass, lockstep termination, the row all-gather for
+per_worker -- and that the result is bit-identical for world sizes 1 and 2
+and matches the reference's design (oracle) pass for pass.
+"""
+
+import math
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TILE = 2048
+
+
+def _fixed_shift(n_global: int, maxabs: float) -> int:
+    """api.cu fixed_shift_for: int64 sums of n rows of |x| < 2^e_x cannot overflow."""
+    e_n = 0
+    while (1 << e_n) < n_global and e_n < 62:
+        e_n += 1
+    e_x = math.frexp(maxabs)[1] if maxabs > 0 else 0
+    return max(-1000, min(1000, 62 - e_n - e_x - 1))
+
+
+class EmulatedShard:
+    """numpy stand-in for distributed.DeviceShard (same method surface)."""
+
+    def __init__(self, rows: np.ndarray, row_offset: int, n_global: int):
+        import torch
+
+        self.torch = torch
+        self.x = np.ascontiguousarray(rows, dtype=np.float64)
+        self.x32 = rows if rows.dtype == np.float32 else None
+        self.n, self.dim = self.x.shape
+        self.row_offset = row_offset
+        self.n_global = n_global
+        assert row_offset % TILE == 0
+        self.ntiles = -(-n_global // TILE)
+
+    # -- backend surface used by run_sharded ------------------------------
+    def maxabs(self) -> float:
+        return float(np.max(np.abs(self.x))) if self.x.size else 0.0
+
+    def tensor(self, values):
+        return self.torch.tensor(values, dtype=self.torch.float64)
+
+    def begin(self, config, global_maxabs: float) -> None:
+        self.cfg = config
+        self.kmax = config.target_size
+        self.shift = _fixed_shift(self.n_global, global_maxabs)
+        self.scale = 2.0 ** self.shift
+        self.ex = self.torch.zeros(self.kmax * self.dim + self.kmax + self.ntiles, dtype=self.torch.int64)
+        self.cb = np.zeros((self.kmax, self.dim))
+        self.size, self.iteration, self.td_prev = 1, 1, math.inf
+        self.done, self.mode_final = False, False
+        self.hist, self.warn, self.total = [], [], 0.0
+        self.pending_init = True
+        self.dists = np.zeros(self.n)
+        # initial column-sum pass: every row in cell 0 (epilogue with zero_cells)
+        self._write_sums(np.zeros(self.n, dtype=np.int64), 1)
+
+    def exchange(self):
+        return self.ex
+
+    def _fixed(self, v: np.ndarray) -> np.ndarray:
+        return np.rint(v * self.scale).astype(np.int64)  # __double2ll_rn(v * 2^shift)
+
+    def _write_sums(self, cells: np.ndarray, k: int) -> None:
+        e = self.ex.numpy()
+        kd = self.kmax * self.dim
+        sums = np.zeros((k, self.dim), dtype=np.int64)
+        np.add.at(sums, cells, self._fixed(self.x))
+        e[: k * self.dim] = sums.reshape(-1)
+        e[kd: kd + k] = np.bincount(cells, minlength=k)
+
+    def local(self) -> None:
+        if self.done:
+            return
+        k = self.size
+        metric = oracle.EUCLIDEAN if self.cfg.distortion_metric == "euclidean" else 0
+        cells, dists = oracle.assign_all(self.x, self.cb[:k], metric)
+        self.dists = dists
+        e = self.ex.numpy()
+        base = self.kmax * self.dim + self.kmax
+        t0 = self.row_offset // TILE
+        for t in range(-(-self.n // TILE)):
+            s = 0.0
+            for v in dists[t * TILE:(t + 1) * TILE]:
+                s += v
+            e[base + t0 + t] = np.float64(s).view(np.int64)
+        self._write_sums(cells, k)
+
+    def _set_action(self, update: bool, split: bool) -> None:
+        e = self.ex.numpy()
+        kd = self.kmax * self.dim
+        k = self.size
+        src = self.cb[:k].copy()
+        if update:
+            counts = e[kd: kd + k]
+            sums = e[: k * self.dim].reshape(k, self.dim).astype(np.float64) * (2.0 ** -self.shift)
+            nz = counts > 0
+            src[nz] = sums[nz] / counts[nz, None]
+        if split:
+            out = np.empty((2 * k, self.dim))
+            out[0::2] = src + self.cfg.delta
+            out[1::2] = src - self.cfg.delta
+            self.cb[: 2 * k] = out
+            self.size, self.iteration, self.td_prev = 2 * k, 1, math.inf
+        else:
+            self.cb[:k] = src
+
+    def finalize(self) -> None:
+        e = self.ex.numpy()
+        base = self.kmax * self.dim + self.kmax
+        if self.done:
+            return
+        if self.pending_init:
+            self.pending_init = False
+            if self.cfg.target_size <= 1:
+                self.mode_final = True
+                self._set_action(True, False)
+            else:
+                self._set_action(True, True)
+            e[base:] = 0
+            return
+        k = self.size
+        td = 0.0
+        for t in range(self.ntiles):
+            td += float(e[base + t: base + t + 1].view(np.float64)[0])
+        e[base:] = 0
+        kd = self.kmax * self.dim
+        empties = int(np.count_nonzero(e[kd: kd + k] == 0))
+        if self.mode_final:
+            self.total, self.done = td, True
+            return
+        p = self.td_prev
+        conv = False if math.isinf(p) else (True if p == 0.0 else (p - td) / p <= self.cfg.epsilon)
+        if conv:
+            self.hist.append((k, self.iteration, td, 0))
+            if k < self.cfg.target_size:
+                self._set_action(False, True)
+            else:
+                self.total, self.done = td, True
+            return
+        self.hist.append((k, self.iteration, td, empties))
+        self.td_prev = td
+        self.iteration += 1
+        if self.iteration > self.cfg.max_iterations_per_level:
+            self.warn.append(k)
+            if k < self.cfg.target_size:
+                self._set_action(True, True)
+            else:
+                self._set_action(True, False)
+                self.total, self.done = td, True
+        else:
+            self._set_action(True, False)
+
+    def poll(self) -> bool:
+        return self.done
+
+    def result(self):
+        from paper_0910_4711_b200.core import LevelIteration, _max_iter_warning
+
+        history = [LevelIteration(s, i, td, e) for s, i, td, e in self.hist]
+        warnings = [_max_iter_warning(s, self.cfg.max_iterations_per_level) for s in self.warn]
+        return self.cb[: self.size].copy(), history, warnings, self.total, self.dists
+
+
+# ---------------------------------------------------------------------------
+# worker processes
+# ---------------------------------------------------------------------------
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _case(name):
+    rng = np.random.default_rng(11)
+    if name == "gmm":
+        means = rng.uniform(0, 255, (12, 4)).astype(np.float32)
+        lab = rng.integers(0, 12, 5000)
+        x = (means[lab] + rng.standard_normal((5000, 4)).astype(np.float32) * 6).astype(np.float32)
+        cfg = dict(target_size=16, epsilon=1e-3, delta=0.01, workers=3)
+    elif name == "tiny":  # fewer 2048-row tiles than ranks: replica fallback
+        x = rng.random((300, 2))
+        cfg = dict(target_size=4, epsilon=1e-3, delta=0.01, workers=5)
+    else:  # guard exhaustion + euclidean, float64 input
+        x = rng.random((4500, 3))
+        cfg = dict(target_size=8, epsilon=0.0, delta=0.05, max_iterations_per_level=3,
+                   distortion_metric="euclidean", workers=2)
+    return x, cfg
+
+
+def _worker(rank, world, port, name, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    for p in (ROOT, os.path.join(ROOT, "oracle")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    import torch.distributed as dist
+
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200 import distributed
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, cfg = _case(name)
+        ts = vq.TrainingSet(x)
+        cb, stats = distributed.sharded_lbg_train(ts, vq.LbgConfig(**cfg),
+                                                  backend_factory=EmulatedShard)
+        if rank == 0:
+            np.savez(out_path, cb=cb.codevectors,
+                     hist=np.array([(h.codebook_size, h.iteration, h.td, h.empty_cells)
+                                    for h in stats.history]),
+                     total=stats.total, per_worker=np.array(stats.per_worker),
+                     nwarn=len(stats.warnings))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, name, tmp_path):
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / f"{name}_w{world}.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), name, out), nprocs=world,
+                       join=True, start_method="spawn")
+    return np.load(out)
+
+
+# ---------------------------------------------------------------------------
+# tests
+# ---------------------------------------------------------------------------
+
+def test_shard_plan_tile_aligned_and_covering():
+    from paper_0910_4711_b200.distributed import ShardPlan
+
+    for n, world in [(5000, 2), (1 << 20, 8), (2049, 4), (100, 3), ((1 << 24) + 7, 8)]:
+        plan = ShardPlan(n, world)
+        cursor = 0
+        for r in range(world):
+            lo, hi = plan.bounds(r)
+            assert lo == cursor and hi >= lo
+            assert lo % TILE == 0 or lo == hi == n  # empty trailing shards only when tiles < world
+            cursor = hi
+        assert cursor == n
+        tiles = [-(-(hi - lo) // TILE) for lo, hi in (plan.bounds(r) for r in range(world))]
+        assert max(tiles) - min(tiles) <= 1
+
+
+@pytest.mark.parametrize("name", ["gmm", "guard_euclidean", "tiny"])
+def test_sharded_design_world2_matches_world1_and_reference(name, tmp_path):
+    r1 = _run(1, name, tmp_path)
+    r2 = _run(2, name, tmp_path)
+    # world-size invariance: bit-identical codebook, history, total, per_worker
+    for key in ("cb", "hist", "total", "per_worker", "nwarn"):
+        assert r1[key].tobytes() == r2[key].tobytes(), key
+    # and the reference's design (oracle), pass for pass
+    x, cfg = _case(name)
+    ref = oracle.lbg_train(np.asarray(x, dtype=np.float64), cfg["target_size"],
+                           epsilon=cfg["epsilon"], delta=cfg["delta"], workers=cfg["workers"],
+                           max_iterations_per_level=cfg.get("max_iterations_per_level", 100),
+                           metric=cfg.get("distortion_metric", "squared_euclidean"))
+    want = np.array(ref.history, dtype=np.float64)
+    got = r2["hist"]
+    assert got.shape == want.shape
+    assert np.array_equal(got[:, [0, 1, 3]], want[:, [0, 1, 3]])
+    np.testing.assert_allclose(got[:, 2], want[:, 2], rtol=1e-12)
+    np.testing.assert_allclose(r2["cb"], ref.codebook, rtol=1e-12, atol=1e-12)
+    assert int(r2["nwarn"]) == len(ref.warnings)
+    np.testing.assert_allclose(r2["per_worker"], ref.per_worker, rtol=1e-12)

@@ -165,12 +165,46 @@ def test_cfg2_full_design_vs_reference():
     _design_check("cfg2", g, synthetic.make_training("cfg2"))
 
 
-def test_teacher_forced_counts_cfg1():
+def test_cfg3_full_design_vs_reference():
+    """L=64 image blocks (BASELINE configs[2]): 8-bit pixels, so the whole
+    design is bit-identical to the reference's."""
+    from paper_0910_4711_b200 import synthetic
+    g = _golden("cfg3_design")
+    cb, _ = _design_check("cfg3", g, synthetic.make_training("cfg3"))
+    assert cb.codevectors.tobytes() == g["cb"].tobytes()
+
+
+def test_cfg4_full_design_vs_reference():
+    """N=2^24, K=4096 (BASELINE configs[3]) on one device."""
+    from paper_0910_4711_b200 import synthetic
+    g = _golden("cfg4_design")
+    _design_check("cfg4", g, synthetic.make_training("cfg4"))
+
+
+def test_cfg5_encode_vs_reference():
+    """2^26 queries against the fixed K=1024 codebook (BASELINE configs[4]):
+    indices bit-identical to the reference's encode, distortion to 1e-12."""
+    from paper_0910_4711_b200 import synthetic
+    g = _golden("cfg5_encode")
+    cb, q = synthetic.make_encode_case()
+    assert hashlib.sha256(q.tobytes()).hexdigest() == g["q_sha256"].item().decode()
+    stream = vq.encode(q, vq.Codebook(cb.astype(np.float64)))
+    assert stream.indices.dtype == np.uint32
+    assert np.array_equal(stream.indices[:65536], g["head"])
+    assert np.array_equal(np.bincount(stream.indices, minlength=1024), g["bincount"])
+    assert hashlib.sha256(stream.indices.tobytes()).hexdigest() == g["idx_sha256"].item().decode()
+    del stream
+    _, total = vq.assign_cells(q, vq.Codebook(cb.astype(np.float64)))
+    assert abs(total - float(g["total"])) <= 1e-12 * float(g["total"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
+def test_teacher_forced_counts(cfg):
     """Every recorded codebook of the reference run, fed to the device, gives
     the reference's cell counts exactly."""
     from paper_0910_4711_b200 import synthetic
-    g = _golden("cfg1_design")
-    x = synthetic.make_training("cfg1")
+    g = _golden(f"{cfg}_design")
+    x = synthetic.make_training(cfg)
     ts = vq.TrainingSet(x)
     counts = g["pass_counts"]
     offs = np.cumsum([0] + [int(s) for s in g["hist"][:, 0]])
@@ -184,6 +218,10 @@ def test_teacher_forced_counts_cfg1():
         assert np.array_equal(got, counts[offs[p]:offs[p + 1]]), p
         checked += 1
     assert checked > 10
+    # the reference's final codebook too (its last pass converged on it)
+    table, _ = vq.assign_cells(ts, vq.Codebook(g["cb"]))
+    assert np.array_equal(np.bincount(table.cells, minlength=g["cb"].shape[0]),
+                          counts[offs[-2]:offs[-1]])
 
 
 # ---------------------------------------------------------------------------
@@ -227,3 +265,51 @@ def test_determinism_repeat_runs():
     cb2, s2 = vq.lbg_train(vq.TrainingSet(x.copy()), cfg)
     assert cb1.codevectors.tobytes() == cb2.codevectors.tobytes()
     assert s1.td_history() == s2.td_history()
+
+
+# ---------------------------------------------------------------------------
+# kernel surface (drop-in for vqkit._kernels) against the reference's outputs
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(len(cases.assign_cases())))
+def test_kernel_surface_assign_range(golden_small, i):
+    from paper_0910_4711_b200 import kernels
+    case = cases.assign_cases()[i]
+    m = case["x"].shape[0]
+    cells = np.full(m, -7, dtype=np.int64)
+    dists = np.full(m, -1.0)
+    lo, hi = m // 3, m
+    kernels.assign_range(case["x"], case["cb"], 0, lo, case["metric"], cells, dists)
+    kernels.assign_range(case["x"], case["cb"], lo, hi, case["metric"], cells, dists)
+    assert np.array_equal(cells, golden_small[f"assign{i}_cells"])
+    assert dists.tobytes() == golden_small[f"assign{i}_dists"].tobytes()
+    assert kernels.sum_inorder(dists) == float(golden_small[f"assign{i}_total"])
+
+
+@pytest.mark.parametrize("i", range(len(cases.update_cases())))
+def test_kernel_surface_update_rows_round_robin(golden_small, i):
+    """update_rows over a (worker, stride) decomposition, as parallel_update
+    drives it (parallel.py:144-154), equals the reference's single-worker run."""
+    from paper_0910_4711_b200 import kernels
+    case = cases.update_cases()[i]
+    cb = case["cb"]
+    out = np.full_like(cb, np.nan)
+    counts = np.full(cb.shape[0], -1, dtype=np.int64)
+    for w in range(3):
+        kernels.update_rows(case["x"], case["cells"], cb, w, 3, out, counts)
+    assert np.array_equal(counts, golden_small[f"update{i}_counts"])
+    want = golden_small[f"update{i}_cb"]
+    if i == 5:
+        np.testing.assert_allclose(out, want, rtol=1e-13, atol=1e-13)
+    else:
+        assert out.tobytes() == want.tobytes()
+
+
+def test_kernel_surface_small_helpers():
+    from paper_0910_4711_b200 import kernels
+    rng = np.random.default_rng(3)
+    x = rng.normal(size=(1000, 5))
+    assert kernels.column_sums(x).tobytes() == oracle.column_sums(x).tobytes()
+    assert kernels.sum_inorder(x[:, 0]) == oracle.sum_inorder(x[:, 0])
+    assert kernels.pair_distance(x[0], x[1], 1) == oracle.pair_distance(x[0], x[1], 1)
+    assert kernels.pair_distance(x[0], x[1], 0) == oracle.pair_distance(x[0], x[1], 0)
