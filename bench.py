@@ -337,6 +337,7 @@ def run_b200(args):
                 "wall_s": design_s, "e2e_wall_s": design_e2e_s, "passes": int(summ.passes),
                 "evals": int(summ.evals), "g_evals_per_s": summ.evals / design_s / 1e9,
                 "flagged_rows": int(summ.flagged_rows),
+                "flagged_full_scan_rows": int(summ.flagged_full),
                 "reference_passes": int(ghist.shape[0]),
                 "schedule_matches_reference": bool(
                     len(hist) == ghist.shape[0] and all(
@@ -510,6 +511,7 @@ def run_workload(args):
             "passes": int(summ.passes), "evals": int(summ.evals),
             "design_g_evals_per_s": summ.evals / wall / 1e9,
             "flagged_rows": int(summ.flagged_rows),
+            "flagged_full_scan_rows": int(summ.flagged_full),
             "final_iteration": {"ms": it_ms, "g_evals_per_s": n * cbf.shape[0] / (it_ms * 1e-3) / 1e9,
                                 "segments_ms": list(segs), "rerank_rows": int(flagged.value)},
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(x.nbytes),

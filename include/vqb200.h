@@ -122,6 +122,7 @@ typedef struct {
   int64_t final_size;
   int32_t fast_path;     /* 1: FP32 candidate + FP64 re-rank; 0: exact FP64 scan */
   int32_t ordered;
+  int64_t flagged_full;  /* of flagged_rows, those whose shortlist overflowed (full FP64 scan) */
 } vqb_train_summary;
 
 /* Full LBG design on the device (lbg_train / parallel_lbg_train).  Outputs:

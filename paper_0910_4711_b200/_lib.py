@@ -57,6 +57,7 @@ class TrainSummary(ctypes.Structure):
         ("final_size", ctypes.c_int64),
         ("fast_path", ctypes.c_int32),
         ("ordered", ctypes.c_int32),
+        ("flagged_full", ctypes.c_int64),
     ]
 
 

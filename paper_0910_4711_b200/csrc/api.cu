@@ -78,6 +78,8 @@ struct vqb_session {
   float* nrm = nullptr;
   int* idx = nullptr;
   int* flags = nullptr;
+  float* flag_thr = nullptr;
+  int* flags2 = nullptr;
   double* dists = nullptr;
   long long* ex = nullptr;
   long long* partials = nullptr;
@@ -107,6 +109,8 @@ struct vqb_session {
     a.kmax = kmax;
     a.idx = idx;
     a.flags = flags;
+    a.flag_thr = flag_thr;
+    a.flags2 = flags2;
     a.dists = dists;
     a.ex.base = ex;
     a.ex.kmax = kmax;
@@ -157,6 +161,8 @@ struct vqb_session {
     cudaFree(nrm);
     cudaFree(idx);
     cudaFree(flags);
+    cudaFree(flag_thr);
+    cudaFree(flags2);
     cudaFree(dists);
     cudaFree(ex);
     cudaFree(partials);
@@ -251,6 +257,8 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
   CK(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
   CK(dalloc(&s->idx, (size_t)rows + 32));
   CK(dalloc(&s->flags, (size_t)rows + 32));
+  CK(dalloc(&s->flag_thr, (size_t)rows + 32));
+  CK(dalloc(&s->flags2, (size_t)rows + 32));
   CK(dalloc(&s->dists, (size_t)rows + 32));
   CK(dalloc(&s->st, 1));
   CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
@@ -441,6 +449,7 @@ int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* h
     summary->n_warn = h->n_warn;
     summary->passes = h->passes;
     summary->flagged_rows = h->flagged_total;
+    summary->flagged_full = h->flagged2_total;
     summary->evals = h->evals;
     summary->final_size = size;
     summary->fast_path = s->fast ? 1 : 0;
@@ -717,6 +726,8 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
   CK(dalloc(&s->x32, (size_t)(n * dim + 16)));
   CK(dalloc(&s->idx, (size_t)n + 32));
   CK(dalloc(&s->flags, (size_t)n + 32));
+  CK(dalloc(&s->flag_thr, (size_t)n + 32));
+  CK(dalloc(&s->flags2, (size_t)n + 32));
   CK(dalloc(&s->dists, (size_t)n + 32));
   CK(dalloc(&s->st, 1));
   CK(dalloc(&s->scratch, 64));
@@ -809,6 +820,8 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     CK(dalloc(&s->x32, (size_t)(chunk * dim + 16)));
     CK(dalloc(&s->idx, (size_t)chunk + 32));
     CK(dalloc(&s->flags, (size_t)chunk + 32));
+    CK(dalloc(&s->flag_thr, (size_t)chunk + 32));
+    CK(dalloc(&s->flags2, (size_t)chunk + 32));
     CK(dalloc(&s->dists, (size_t)chunk + 32));
     CK(dalloc(&s->st, 1));
     CK(dalloc(&s->scratch, 64));

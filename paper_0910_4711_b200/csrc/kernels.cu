@@ -331,6 +331,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
   for (int r = 0; r < R; ++r) {
     long long row = row0 + tid + (long long)r * NT;
     bool ok = false;
+    float thr = NAN;
     if (valid[r]) {
       const float yn = sqrtf(q[r]);
       const float d2 = fmaxf(m2[r] + q[r], 0.f);
@@ -338,6 +339,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
       const float S = 2.02f * yn + sd;
       const float E = (float)(L + 3) * u * S * S + 2.5f * u * sd * S + 1e-14f * S * S;
       ok = (m2[r] - m1[r]) > 3.0f * E;
+      thr = m1[r] + 3.0f * E;  // shortlist band (shortlist_kernel)
       a.idx[row] = i1[r];
     }
     const bool flag = valid[r] && !ok;
@@ -347,7 +349,11 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
       const int leader = __ffs(mask) - 1;
       if (lane == leader) base = atomicAdd(&a.st->flag_count, __popc(mask));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (flag) a.flags[base + __popc(mask & ((1u << lane) - 1u))] = (int)row;
+      if (flag) {
+        const int pos = base + __popc(mask & ((1u << lane) - 1u));
+        a.flags[pos] = (int)row;
+        a.flag_thr[pos] = thr;
+      }
     }
   }
 }
@@ -480,6 +486,7 @@ __device__ __forceinline__ double ref_dist_regs(const XT (&xr)[DIM], const doubl
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT* __restrict__ X,
                                                          int use_list) {
+  // use_list: 0 every row, 1 the assign_fast queue, 2 the shortlist overflow queue
   // T threads per row (T = pow2 >= K, capped at the block): K=2 packs 128
   // rows per block, K >= 256 gives one block per row.  Each thread scans
   // j = t, t+T, ... (ascending) with the reference's strict <, then a
@@ -498,11 +505,13 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
       __shared__ double s_b[8][B];
       __shared__ int s_j[8][B];
       __shared__ long long s_row[B];
-      const long long count = use_list ? (long long)st->flag_count : a.n;
+      const int* list = use_list == 2 ? a.flags2 : a.flags;
+      const long long count = use_list == 2 ? (long long)st->flag2_count
+                              : use_list ? (long long)st->flag_count : a.n;
       for (long long base = (long long)blockIdx.x * B; base < count; base += (long long)gridDim.x * B) {
         if (threadIdx.x < B) {
           const long long i = base + threadIdx.x;
-          s_row[threadIdx.x] = i < count ? (use_list ? (long long)a.flags[i] : i) : -1;
+          s_row[threadIdx.x] = i < count ? (use_list ? (long long)list[i] : i) : -1;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < B * DIM; e += blockDim.x) {
@@ -589,11 +598,13 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
   const int sub = threadIdx.x / T, tl = threadIdx.x % T;
   __shared__ double s_best[8];
   __shared__ int s_bj[8];
-  const long long count = use_list ? (long long)st->flag_count : a.n;
+  const int* list = use_list == 2 ? a.flags2 : a.flags;
+  const long long count = use_list == 2 ? (long long)st->flag2_count
+                          : use_list ? (long long)st->flag_count : a.n;
   for (long long base = (long long)blockIdx.x * rpb; base < count; base += (long long)gridDim.x * rpb) {
     const long long i = base + sub;
     const bool valid = i < count;
-    const long long row = valid ? (use_list ? (long long)a.flags[i] : i) : 0;
+    const long long row = valid ? (use_list ? (long long)list[i] : i) : 0;
     double best = INFINITY;
     int bj = 0x7fffffff;
     if (valid) {
@@ -674,7 +685,241 @@ static cudaError_t launch_exact_t(const KernelArgs& a, const XT* X, int use_list
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// shortlist: the queued rows' exact winner from a band of candidates.
+//
+// A row is queued when its FP32 top-2 gap is within the certified error
+// 3E.  The reference's winner j* then satisfies v_j* <= m1 + 3E in the same
+// FP32 expanded form (any evaluation order: E bounds every order of the
+// length-L FMA chain, and 3E >= 2E + 2x the FP64 reference's own rounding),
+// so rescanning the codebook in FP32 and keeping every j with v_j <= m1 + 3E
+// yields a shortlist that contains j* and every index tied with it.  Only
+// the shortlist is evaluated in the reference's FP64 arithmetic (ascending j,
+// strict <: lowest index on ties).  A row whose band holds more than kShort
+// candidates (or a non-finite threshold) goes to the full FP64 scan.
+// Costs ~L FFMA per codevector instead of 3L FP64 ops.
+// ---------------------------------------------------------------------------
+
+template <typename XT, int DIM>
+__device__ __forceinline__ double winner_dist(const XT* __restrict__ x, const double* __restrict__ c,
+                                              int dim);
+
+template <int L>
+struct ShortCfg {
+  static constexpr int NT = 256;
+  static constexpr int TK = L == 16 ? 1024 : (L == 32 ? 512 : 256);  // 64 KB FP32 tile
+  static constexpr size_t kSmem = (size_t)TK * L * 4 + (size_t)TK * 4;
+};
+constexpr int kShort = 8;
+
+template <int L>
+__global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
+  using C = ShortCfg<L>;
+  constexpr int NT = C::NT, TK = C::TK;
+  const DevState* st = a.st;
+  if (st->done) return;
+  const long long count = st->flag_count;
+  if (count == 0) return;
+  const int K = st->size;
+  const double* __restrict__ cb = a.cb[st->cur];
+  if (count < (long long)gridDim.x * NT) {
+    // Few queued rows (e.g. a converged codebook): one warp per row, lanes
+    // stride the codebook (j = lane, lane + 32, ...) so the rows' work
+    // spreads over every SM; candidates are gathered by ballot in
+    // ascending j, then evaluated one per lane in FP64.
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (NT / 32);
+    for (long long i = blockIdx.x * (long long)(NT / 32) + (threadIdx.x >> 5); i < count; i += warps) {
+      const long long row = a.flags[i];
+      const float thr = a.flag_thr[i];
+      float y[L];
+      const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L);
+#pragma unroll
+      for (int v = 0; v < L / 4; ++v) {
+        const float4 t = __ldg(src + v);
+        y[4 * v + 0] = __fsub_rn(t.x, a.mu[4 * v + 0]);
+        y[4 * v + 1] = __fsub_rn(t.y, a.mu[4 * v + 1]);
+        y[4 * v + 2] = __fsub_rn(t.z, a.mu[4 * v + 2]);
+        y[4 * v + 3] = __fsub_rn(t.w, a.mu[4 * v + 3]);
+      }
+      int nc = 0;
+      int mine = -1;  // lane c holds the c-th candidate (ascending j)
+      for (int jb = 0; jb < K; jb += 32) {
+        const int j = jb + lane;
+        bool in = false;
+        if (j < K) {
+          const float4* wj = reinterpret_cast<const float4*>(a.w + (long long)j * L);
+          float v0 = __ldg(a.nrm + j), v1 = 0.f;
+#pragma unroll
+          for (int c = 0; c < L / 4; ++c) {
+            const float4 w4 = __ldg(wj + c);
+            if (c & 1) {
+              v1 = fmaf(w4.x, y[4 * c + 0], v1);
+              v1 = fmaf(w4.y, y[4 * c + 1], v1);
+              v1 = fmaf(w4.z, y[4 * c + 2], v1);
+              v1 = fmaf(w4.w, y[4 * c + 3], v1);
+            } else {
+              v0 = fmaf(w4.x, y[4 * c + 0], v0);
+              v0 = fmaf(w4.y, y[4 * c + 1], v0);
+              v0 = fmaf(w4.z, y[4 * c + 2], v0);
+              v0 = fmaf(w4.w, y[4 * c + 3], v0);
+            }
+          }
+          in = (v0 + v1) <= thr;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        // lane c picks the c-th candidate overall (ascending j)
+        const int before = nc;
+        nc += __popc(m);
+        if (lane >= before && lane < nc && lane < 32) {
+          // position of the (lane - before)-th set bit of m
+          unsigned mm = m;
+          for (int k = 0; k < lane - before; ++k) mm &= mm - 1;
+          mine = jb + __ffs(mm) - 1;
+        }
+      }
+      if (nc == 0 || nc > kShort || !(thr < INFINITY)) {
+        if (lane == 0) {
+          const int pos = atomicAdd(&a.st->flag2_count, 1);
+          a.flags2[pos] = (int)row;
+        }
+        continue;
+      }
+      double d = INFINITY;
+      int dj = 0x7fffffff;
+      if (mine >= 0) {
+        d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)mine * L, L);
+        dj = mine;
+        if (!(d < INFINITY)) {  // NaN / inf never wins a strict < (index 0 if nothing does)
+          d = INFINITY;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, d, off);
+        const int oj = __shfl_xor_sync(0xffffffffu, dj, off);
+        if (od < d || (od == d && oj < dj)) {
+          d = od;
+          dj = oj;
+        }
+      }
+      if (lane == 0) a.idx[row] = (d < INFINITY) ? dj : 0;
+    }
+    return;
+  }
+  if ((long long)blockIdx.x * NT >= count) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sW = reinterpret_cast<float*>(smem_raw);
+  float* sN = sW + TK * L;
+  const int ntiles = (K + TK - 1) / TK;
+  for (long long base = (long long)blockIdx.x * NT; base < count; base += (long long)gridDim.x * NT) {
+    const long long i = base + threadIdx.x;
+    const bool valid = i < count;
+    const long long row = valid ? (long long)a.flags[i] : 0;
+    const float thr = valid ? a.flag_thr[i] : -INFINITY;
+    float y[L];
+    {
+      const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L);
+#pragma unroll
+      for (int v = 0; v < L / 4; ++v) {
+        const float4 t = __ldg(src + v);
+        y[4 * v + 0] = __fsub_rn(t.x, a.mu[4 * v + 0]);
+        y[4 * v + 1] = __fsub_rn(t.y, a.mu[4 * v + 1]);
+        y[4 * v + 2] = __fsub_rn(t.z, a.mu[4 * v + 2]);
+        y[4 * v + 3] = __fsub_rn(t.w, a.mu[4 * v + 3]);
+      }
+    }
+    int list[kShort];
+    int nc = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int jbase = t * TK;
+      const int cnt = min(TK, K - jbase);
+      if (ntiles > 1 || base == (long long)blockIdx.x * NT) {
+        __syncthreads();
+        const float4* gW = reinterpret_cast<const float4*>(a.w + (long long)jbase * L);
+        float4* dW = reinterpret_cast<float4*>(sW);
+        for (int e = threadIdx.x; e < cnt * L / 4; e += NT) dW[e] = __ldg(gW + e);
+        for (int e = threadIdx.x; e < cnt; e += NT) sN[e] = __ldg(a.nrm + jbase + e);
+        __syncthreads();
+      }
+      if (!valid) continue;
+#pragma unroll 2
+      for (int j = 0; j < cnt; ++j) {
+        const float4* wj = reinterpret_cast<const float4*>(sW + j * L);
+        float v0 = sN[j], v1 = 0.f;  // two chains
+#pragma unroll
+        for (int c = 0; c < L / 4; ++c) {
+          const float4 w4 = wj[c];
+          if (c & 1) {
+            v1 = fmaf(w4.x, y[4 * c + 0], v1);
+            v1 = fmaf(w4.y, y[4 * c + 1], v1);
+            v1 = fmaf(w4.z, y[4 * c + 2], v1);
+            v1 = fmaf(w4.w, y[4 * c + 3], v1);
+          } else {
+            v0 = fmaf(w4.x, y[4 * c + 0], v0);
+            v0 = fmaf(w4.y, y[4 * c + 1], v0);
+            v0 = fmaf(w4.z, y[4 * c + 2], v0);
+            v0 = fmaf(w4.w, y[4 * c + 3], v0);
+          }
+        }
+        if (v0 + v1 <= thr) {
+          if (nc < kShort) list[nc] = jbase + j;
+          ++nc;
+        }
+      }
+    }
+    if (!valid) continue;
+    if (nc == 0 || nc > kShort) {
+      const int pos = atomicAdd(&a.st->flag2_count, 1);
+      a.flags2[pos] = (int)row;
+      continue;
+    }
+    double best = INFINITY;
+    int bj = 0;  // nothing < inf -> index 0 (_kernels.py:23-32)
+    for (int c = 0; c < nc; ++c) {
+      const int j = list[c];
+      const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)j * L, L);
+      if (d < best) {
+        best = d;
+        bj = j;
+      }
+    }
+    a.idx[row] = bj;
+  }
+}
+
+bool shortlist_enabled() {
+  // VQB_RERANK=full selects the full FP64 scan of every queued row (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VQB_RERANK");
+    v = (e && strcmp(e, "full") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int L>
+static cudaError_t launch_shortlist_L(const KernelArgs& a, int sms, cudaStream_t s) {
+  using C = ShortCfg<L>;
+  cudaError_t e = cudaFuncSetAttribute(shortlist_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::kSmem);
+  if (e != cudaSuccess) return e;
+  shortlist_kernel<L><<<sms * 2, C::NT, C::kSmem, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
+  if (a.x32 && shortlist_enabled()) {
+    cudaError_t e;
+    switch (a.dim) {
+      case 16: e = launch_shortlist_L<16>(a, sms, s); break;
+      case 32: e = launch_shortlist_L<32>(a, sms, s); break;
+      case 64: e = launch_shortlist_L<64>(a, sms, s); break;
+      default: e = cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    return launch_exact_t<float>(a, a.x32, 2, sms, s);
+  }
   if (a.x32) return launch_exact_t<float>(a, a.x32, 1, sms, s);
   return launch_exact_t<double>(a, a.x64, 1, sms, s);
 }
@@ -1168,7 +1413,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     st->flagged_total += st->flag_count;
+    st->flagged2_total += st->flag2_count;
     st->flag_count = 0;
+    st->flag2_count = 0;
   }
 
   if (phase == 0) {
@@ -1388,7 +1635,10 @@ __global__ void clear_kernel(KernelArgs a) {
     a.nrm[k] = INFINITY;
     for (int l = 0; l < a.dim; ++l) a.w[k * a.dim + l] = 0.0f;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.st->flag_count = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.st->flag_count = 0;
+    a.st->flag2_count = 0;
+  }
 }
 
 cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s) {
@@ -1449,6 +1699,7 @@ __global__ void reset_kernel(DevState* st, int mode, int size, int metric, int o
   st->done = 0;
   if (!keep_cur) st->cur = 0;
   st->flag_count = 0;
+  st->flag2_count = 0;
   st->iteration = 1;
   st->td_prev = INFINITY;
   if (!keep_cur) {
@@ -1457,6 +1708,7 @@ __global__ void reset_kernel(DevState* st, int mode, int size, int metric, int o
     st->passes = 0;
     st->evals = 0;
     st->flagged_total = 0;
+    st->flagged2_total = 0;
   }
 }
 

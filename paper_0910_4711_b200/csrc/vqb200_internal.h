@@ -58,10 +58,12 @@ struct DevState {
   int n_hist;
   int n_warn;
   int warn_sizes[kMaxWarn];
-  int flag_count;      // rows queued for the FP64 re-rank this pass
+  int flag_count;      // rows queued for the re-rank this pass (assign_fast -> shortlist)
+  int flag2_count;     // rows whose shortlist overflowed -> full FP64 scan
   unsigned int cmax_bits;  // float bits of max_j ||c~_j|| (centred FP32 codebook)
   int passes;          // allocation passes executed
   long long flagged_total;  // rows re-ranked over the whole run (diagnostic)
+  long long flagged2_total; // of which needed the full FP64 scan
   long long evals;     // sum over passes of rows * size (this shard)
   int act;             // apply_kernel action bits (update 1, split 2)
   int act_src;         // buffer holding the source codebook of the action
@@ -100,6 +102,8 @@ struct KernelArgs {
   // per-row outputs
   int* idx;
   int* flags;
+  float* flag_thr;      // per queued row: band threshold m1 + 3E (FP32 expanded form)
+  int* flags2;          // shortlist overflow rows
   double* dists;        // nullable
   Exchange ex;
   long long* partials;  // per-block fixed-point slabs, sms x (kmax*dim + kmax)
@@ -111,6 +115,7 @@ struct KernelArgs {
 cudaError_t launch_prep_codebook(const KernelArgs& a, cudaStream_t s);
 cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s);
 cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s);
+bool shortlist_enabled();
 cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums, bool zero_cells,
                             int sms, cudaStream_t s);
 cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s);

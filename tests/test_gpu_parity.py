@@ -134,7 +134,12 @@ def test_trace_kat_exact():
     assert stats.mean == 0.25
 
 
-def _design_check(cfg_name, g, x, rtol_td=1e-12):
+def _design_check(cfg_name, g, x, rtol_td=None):
+    # The reference sums TD left to right, the device in a fixed tile tree:
+    # both are within n*u of the exact sum (u = 2^-53), so they agree to
+    # ~2nu -- far inside the north star's 1e-4.
+    if rtol_td is None:
+        rtol_td = max(1e-12, 2.0 * x.shape[0] * 2.0 ** -53)
     from paper_0910_4711_b200 import synthetic
     spec = synthetic.WORKLOADS[cfg_name]
     assert hashlib.sha256(x.tobytes()).hexdigest() == g["x_sha256"].item().decode()
