@@ -304,8 +304,10 @@ def run_b200(args):
         empty = ctypes.c_int64()
 
         def e2e_step():
+            # the step's result is the new codebook + distortion (what the
+            # next Lloyd pass consumes); the cell table stays on the device
             _lib.check(L.vqb_lloyd_step_f32(_lib.ptr(xp), n, 16, _lib.ptr(cb), K, local_rank,
-                                            _lib.ptr(new_cb), _lib.ptr(cells), ctypes.byref(td),
+                                            _lib.ptr(new_cb), None, ctypes.byref(td),
                                             ctypes.byref(empty)))
 
         for _ in range(max(1, args.warmup)):
@@ -374,9 +376,11 @@ def run_b200(args):
                          "algorithmic": "3L = 48 flops per vector-codeword eval, N*K evals/launch",
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
                          "algorithmic_bytes": n * 16 * 4 + n * 4},
-            "e2e": {"value": evals / e2e_s / 1e9, "unit": UNIT,
+            "e2e": {"value": evals / e2e_s / 1e9, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+                    "api": "vqb_lloyd_step_f32 (C ABI), X from pinned host memory",
                     "h2d_bytes_per_step": n * 16 * 4 + K * 16 * 8,
-                    "d2h_bytes_per_step": n * 8 + K * 16 * 8},
+                    "d2h_bytes_per_step": K * 16 * 8 + 8,
+                    "result": "new codebook + distortion"},
             "cpu_baseline": {"value": cpu_rate, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"{rows} leading rows x K=1024, assign+TD+update "
                                        f"(oracle/ C+OpenMP, reference arithmetic), min of 3",

@@ -190,6 +190,16 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
 int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int reps,
                      double* ms_out, double* total_out, int64_t* flagged);
 
+/* Tensor-core candidate-pass probe (tests): raw fp32 accumulators of rows
+ * [0,128) of the session against `codebook` (size a multiple of 256),
+ * dump[128][size]; scales[5] = {ey, ew, kn, tc_on, tc_bad}. */
+int vqb_debug_tc_tile(vqb_session* s, const double* codebook, int64_t size, float* dump,
+                      int32_t* scales);
+
+/* Host->device copy-engine bandwidth probe: mode 0 staged/pinned upload,
+ * 1 plain cudaMemcpy, 2 cudaHostRegister + upload (register cost included). */
+int vqb_bench_upload(const void* src, int64_t bytes, int mode, double* seconds);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,8 @@ def lib():
             "vqb_pipe_microbench": ([_I32, _I32, _I32, _P, _P], _I32),
             "vqb_bench_iteration": ([_P, _P, _I64, _I32, _P, _P], _I32),
             "vqb_bench_assign": ([_P, _P, _I64, _I32, _P, _P, _P], _I32),
+            "vqb_bench_upload": ([_P, _I64, _I32, _P], _I32),
+            "vqb_debug_tc_tile": ([_P, _P, _I64, _P, _P], _I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

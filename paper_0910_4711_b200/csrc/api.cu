@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -13,6 +14,7 @@
 #include <vector>
 
 #include "../../include/vqb200.h"
+#include "transfer.h"
 #include "vqb200_internal.h"
 
 using namespace vqb;
@@ -65,12 +67,15 @@ struct vqb_session {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D pieces (transfer.cpp), overlapped with kernels
   bool own_stream = false;
   long long n = 0, dim = 0, row_offset = 0, n_global = 0;
   float* x32 = nullptr;
   double* x64 = nullptr;
   float* mu = nullptr;
+  std::vector<float> mu_host;  // host copy of the centring vector
   double maxabs = -1.0;
+  unsigned short* tcb = nullptr;  // fp16 operand image of the codebook (assign_tc)
   // run buffers
   long long kmax = 0;
   double* cb[2] = {nullptr, nullptr};
@@ -99,12 +104,15 @@ struct vqb_session {
     a.x32 = x32;
     a.x64 = x64;
     a.n = n;
+    a.r0 = 0;
+    a.r1 = n;
     a.dim = (int)dim;
     a.tile0 = row_offset / kTdTile;
     a.mu = mu;
     a.cb[0] = cb[0];
     a.cb[1] = cb[1];
     a.w = w;
+    a.tcb = tcb;
     a.nrm = nrm;
     a.kmax = kmax;
     a.idx = idx;
@@ -131,7 +139,9 @@ struct vqb_session {
     cudaFree(ex);
     cudaFree(partials);
     cudaFree(ord);
+    cudaFree(tcb);
     ord = nullptr;
+    tcb = nullptr;
     cb[0] = cb[1] = nullptr;
     w = nrm = nullptr;
     ex = nullptr;
@@ -145,6 +155,8 @@ struct vqb_session {
     CK(dalloc(&ex, (size_t)(k * dim + k + ntiles_global)));
     CK(dalloc(&partials, (size_t)sms * (size_t)(k * dim + k)));
     CK(dalloc(&ord, (size_t)(k * dim)));
+    if (fast_dim_supported((int)dim))
+      CK(dalloc(&tcb, (size_t)(((k + kTcChunk - 1) / kTcChunk) * tc_chunk_elems((int)dim))));
     CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (k * dim + k + ntiles_global), stream));
     return VQB_OK;
   }
@@ -167,6 +179,7 @@ struct vqb_session {
     cudaFree(ex);
     cudaFree(partials);
     cudaFree(ord);
+    cudaFree(tcb);
     cudaFree(st);
     cudaFree(scratch);
     if (st_host) cudaFreeHost(st_host);
@@ -174,6 +187,14 @@ struct vqb_session {
     for (auto& e : ev_batch)
       if (e) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+  }
+
+  int make_streams() {
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    own_stream = true;
+    return VQB_OK;
   }
 };
 
@@ -217,8 +238,7 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
   std::unique_ptr<vqb_session> s(new vqb_session());
   s->device = device;
   CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  s->own_stream = true;
+  if (int rc = s->make_streams()) return rc;
   s->n = rows;
   s->dim = dim;
   s->row_offset = row_offset;
@@ -228,10 +248,10 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
   CK(dalloc(&s->scratch, 64));
   if (x32) {
     CK(dalloc(&s->x32, count + 16));
-    CK(cudaMemcpyAsync(s->x32, x32, count * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+    CK(upload(s->x32, x32, count * sizeof(float), 16u << 20, s->copy_stream, s->stream));
   } else {
     CK(dalloc(&s->x64, count + 8));
-    CK(cudaMemcpyAsync(s->x64, x64, count * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CK(upload(s->x64, x64, count * sizeof(double), 16u << 20, s->copy_stream, s->stream));
     // float64 rows that are exactly float32 take the FP32 candidate path
     float* tmp = nullptr;
     CK(dalloc(&tmp, count + 16));
@@ -291,6 +311,7 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
       mu[(size_t)l] = std::isfinite(acc) ? (float)(acc / (double)m) : 0.f;
     }
     CK(cudaMemcpy(s->mu, mu.data(), dim * sizeof(float), cudaMemcpyHostToDevice));
+    s->mu_host = mu;
   }
   s->fast = s->x32 != nullptr && fast_dim_supported((int)dim) && s->maxabs < 1099511627776.0;
   *out = s.release();
@@ -345,6 +366,61 @@ static bool choose_ordered(const vqb_session* s, int requested, long long kmax) 
          (double)s->n * (double)kmax * (double)s->dim <= 2.7e8;
 }
 
+static bool tc_enabled() {
+  // VQB_TC=0 (or VQB_ASSIGN=ffma) keeps every pass on the FP32 FFMA kernel
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VQB_TC");
+    const char* f = getenv("VQB_ASSIGN");
+    v = ((e && strcmp(e, "0") == 0) || (f && strcmp(f, "ffma") == 0)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// max over a codebook of |c - mu| (the staged operand's magnitude)
+static double codebook_span(const vqb_session* s, const double* codebook, long long size) {
+  double mx = 0.0;
+  for (long long k = 0; k < size; ++k)
+    for (long long l = 0; l < s->dim; ++l) {
+      const double v = std::fabs(codebook[k * s->dim + l] - (double)s->mu_host[(size_t)l]);
+      mx = v > mx ? v : mx;
+    }
+  return mx;
+}
+
+// Power-of-two scales for the fp16 hi/lo operand split of assign_tc: |y~|
+// scaled to <= 2^10 (my bounds |x - mu|), |w| = 2|c~| to <= 2^10 (mw bounds
+// |w|), and the norm column to <= 2^14 with a power-of-two A column 2^kn.
+// Values outside the assumed bounds are caught on the device (rows are
+// re-ranked, codebooks send the pass to the FP32 kernel), never mis-scored.
+static void tc_configure(const vqb_session* s, DevState* h, double my, double mw) {
+  h->tc_on = 0;
+  h->tc_bad = 0;
+  if (!s->tcb || !s->fast || !tc_enabled()) return;
+  if (!(my > 0) || !(mw > 0) || !std::isfinite(my) || !std::isfinite(mw)) return;
+  const int ey = 10 - (int)std::ceil(std::log2(my));
+  const int ew = 10 - (int)std::ceil(std::log2(mw));
+  if (ey + ew > 90 || ey + ew < -90) return;
+  const double nmax = (double)s->dim * (mw / 2) * (mw / 2);
+  const int kn = std::max(0, (int)std::ceil(std::log2(std::ldexp(nmax, ey + ew))) - 14);
+  if (kn > 15) return;
+  h->tc_ey = ey;
+  h->tc_ew = ew;
+  h->tc_kn = kn;
+  h->tc_kmin = kTcChunk;
+  h->tc_kmax = (int)std::min<long long>(tc_max_size((int)s->dim), s->kmax);
+  h->tc_on = h->tc_kmax >= h->tc_kmin ? 1 : 0;
+}
+
+static double data_span(const vqb_session* s, const double* codebook, long long size) {
+  // |x - mu| bound: exact from the session's max |x| when known, else the
+  // codebook's span (rows beyond it are flagged on the device)
+  double mu_max = 0.0;
+  for (float v : s->mu_host) mu_max = std::max(mu_max, (double)std::fabs(v));
+  if (s->maxabs > 0 && std::isfinite(s->maxabs)) return s->maxabs + mu_max;
+  return codebook ? std::max(codebook_span(s, codebook, size), 1e-30) : 0.0;
+}
+
 int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
   int rc = check_config(cfg);
   if (rc) return rc;
@@ -364,6 +440,11 @@ int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
   h->eps = cfg->epsilon;
   h->delta = cfg->delta;
   h->n_global = s->n_global;
+  {
+    // centroids stay in the data's convex hull; a split adds delta per level
+    const double my = data_span(s, nullptr, 0);
+    tc_configure(s, h, my, 2.0 * (my + 16.0 * cfg->delta));
+  }
   h->mode = kModeTrain;
   h->ordered = s->ordered ? 1 : 0;
   h->size = 1;
@@ -513,7 +594,8 @@ static int upload_codebook(vqb_session* s, const double* codebook, long long siz
   return VQB_OK;
 }
 
-static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered) {
+static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered,
+                     const double* codebook = nullptr) {
   DevState* h = s->st_host;
   // configuration fields are written by the reset kernel + this header copy
   std::memset(h, 0, offsetof(DevState, hist));
@@ -527,6 +609,7 @@ static int set_state(vqb_session* s, int mode, long long size, int metric, int o
   h->size = (int)size;
   h->iteration = 1;
   h->td_prev = INFINITY;
+  if (codebook) tc_configure(s, h, data_span(s, codebook, size), 2.0 * codebook_span(s, codebook, size));
   CK(cudaMemcpyAsync(s->st, h, offsetof(DevState, hist), cudaMemcpyHostToDevice, s->stream));
   return VQB_OK;
 }
@@ -542,7 +625,7 @@ int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric,
   // in-order distortion (sum_inorder) when it is cheap: assign_cells returns
   // the chunk total accumulated in input order (core.py:315-316)
   const int ordered_td = (s->n == s->n_global && s->n <= (1LL << 20)) ? 1 : 0;
-  rc = set_state(s, kModeAssignOnly, size, metric, ordered_td);
+  rc = set_state(s, kModeAssignOnly, size, metric, ordered_td, codebook);
   if (rc) return rc;
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
@@ -718,8 +801,7 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
   CK(cudaSetDevice(device));
   s->device = device;
   CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  s->own_stream = true;
+  if (int rc = s->make_streams()) return rc;
   s->n = s->n_global = n;
   s->dim = dim;
   s->ntiles_global = (n + kTdTile - 1) / kTdTile;
@@ -733,6 +815,7 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
   CK(dalloc(&s->scratch, 64));
   CK(dalloc(&s->mu, (size_t)dim + 4));
   CK(cudaMemset(s->mu, 0, sizeof(float) * dim));
+  s->mu_host.assign((size_t)dim, 0.f);
   CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
   CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
   s->fast = fast_dim_supported((int)dim);
@@ -744,16 +827,41 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
   return VQB_OK;
 }
 
-int refresh_maxabs(vqb_session* s) {
-  unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
-  CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
-  CK(launch_maxabs(s->x32, nullptr, s->n * s->dim, mb, s->sms, s->stream));
-  unsigned long long bits = 0;
-  CK(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  std::memcpy(&s->maxabs, &bits, sizeof(double));
-  if (!(s->maxabs <= 1.7976931348623157e308)) s->maxabs = INFINITY;
-  s->fast = fast_dim_supported((int)s->dim) && s->maxabs < 1099511627776.0;
+// centre of the FP32 staging: the codebook's column mean (any centre is
+// exact after the re-rank; a central one keeps the certified band tight)
+int set_centre_from_codebook(vqb_session* s, const double* codebook, long long size) {
+  std::vector<float> mu((size_t)s->dim, 0.f);
+  for (long long l = 0; l < s->dim; ++l) {
+    double acc = 0;
+    for (long long k = 0; k < size; ++k) acc += codebook[k * s->dim + l];
+    mu[(size_t)l] = std::isfinite(acc) ? (float)(acc / (double)size) : 0.f;
+  }
+  CK(cudaMemcpy(s->mu, mu.data(), sizeof(float) * s->dim, cudaMemcpyHostToDevice));
+  s->mu_host = mu;
+  return VQB_OK;
+}
+
+// Enqueue the H2D of `rows` host rows into s->x32 in pieces, each piece's
+// max |x| and FP32 candidate pass launched as soon as it lands (the copy of
+// piece i+1 overlaps the distance pass of piece i).  For dims without a fast
+// path the exact scan runs after the last piece.
+int stream_rows_and_assign(vqb_session* s, const float* x, long long rows, unsigned long long* maxabs_bits) {
+  KernelArgs a = s->args();
+  const size_t row_bytes = sizeof(float) * (size_t)s->dim;
+  const size_t piece = std::max<size_t>(row_bytes, ((size_t)8 << 20) / row_bytes * row_bytes);
+  CK(cudaMemsetAsync(maxabs_bits, 0, sizeof(unsigned long long), s->stream));
+  CK(upload(s->x32, x, row_bytes * rows, piece, s->copy_stream, s->stream,
+            [&](size_t off, size_t len) -> cudaError_t {
+              const long long r0 = (long long)(off / row_bytes), r1 = (long long)((off + len) / row_bytes);
+              cudaError_t e = launch_maxabs(s->x32 + r0 * s->dim, nullptr, (r1 - r0) * s->dim, maxabs_bits,
+                                            s->sms, s->stream);
+              if (e != cudaSuccess || !s->fast) return e;
+              KernelArgs c = a;
+              c.r0 = r0;
+              c.r1 = r1;
+              return launch_assign(c, true, s->sms, s->stream);
+            }));
+  if (!s->fast) CK(launch_assign(a, false, s->sms, s->stream));
   return VQB_OK;
 }
 }  // namespace
@@ -761,36 +869,39 @@ int refresh_maxabs(vqb_session* s) {
 int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* codebook,
                        int64_t size, int device, double* new_codebook, int64_t* cells_out,
                        double* td, int64_t* n_empty) {
+  if (n < 1 || dim < 1 || size < 1) return fail(VQB_USAGE, "Lloyd step needs non-empty rows and codebook");
   std::lock_guard<std::mutex> lock(g_cache_mu);
   vqb_session* s = nullptr;
   int rc = cached_session(n, dim, device, &s);
   if (rc) return rc;
   CK(cudaSetDevice(device));
-  CK(cudaMemcpyAsync(s->x32, x, sizeof(float) * n * dim, cudaMemcpyHostToDevice, s->stream));
-  rc = refresh_maxabs(s);
+  s->fast = fast_dim_supported((int)dim);
+  rc = set_centre_from_codebook(s, codebook, size);
   if (rc) return rc;
   rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
-  rc = set_state(s, kModeLloydStep, size, 0, 0);
+  rc = set_state(s, kModeLloydStep, size, 0, 0, codebook);
   if (rc) return rc;
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
   if (s->fast) CK(launch_prep_codebook(a, s->stream));
-  CK(launch_assign(a, s->fast, s->sms, s->stream));
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
+  rc = stream_rows_and_assign(s, x, n, mb);
+  if (rc) return rc;
+  CK(launch_set_shift(s->st, mb, s->n_global, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
-  CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
+  CK(launch_epilogue(a, true, true, false, s->sms, s->stream));  // distortion + cell sums
   CK(launch_finalize(a, false, s->stream));
   CK(cudaMemcpyAsync(new_codebook, s->cb[1], sizeof(double) * size * dim, cudaMemcpyDeviceToHost,
                      s->stream));
-  std::vector<int> tmp;
-  if (cells_out) {
-    tmp.resize((size_t)n);
-    CK(cudaMemcpyAsync(tmp.data(), s->idx, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream));
-  }
   CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  if (cells_out) {
+    long long* wide = reinterpret_cast<long long*>(s->dists);  // dists are consumed by now
+    CK(launch_widen_idx(s->idx, wide, n, s->sms, s->stream));
+    CK(download(cells_out, wide, sizeof(long long) * n, s->stream));
+  }
   CK(cudaStreamSynchronize(s->stream));
-  if (cells_out)
-    for (long long i = 0; i < n; ++i) cells_out[i] = tmp[(size_t)i];
+  if (s->st_host->nonfinite) return fail(VQB_USAGE, "training vectors contain non-finite values");
   if (td) *td = s->st_host->total;
   if (n_empty) *n_empty = s->st_host->last_empty;
   return VQB_OK;
@@ -802,9 +913,12 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     if (total) *total = 0.0;
     return VQB_OK;
   }
+  if (n < 0 || dim < 1 || size < 1) return fail(VQB_USAGE, "encode needs a non-empty codebook");
   CK(cudaSetDevice(device));
-  // Two slots, each a session over a chunk of rows; slot i%2 runs chunk i:
-  // H2D of chunk i+1 overlaps the kernels of chunk i.
+  // Two slots, each a session over a chunk of rows; slot c%2 runs chunk c.
+  // The H2D of chunk c (in pieces, each piece's candidate pass launched as
+  // it lands) overlaps the tail kernels of chunk c-1; chunk c-1's indices
+  // are drained while chunk c computes.
   const long long chunk = std::min<long long>(n, 1LL << 22);
   std::unique_ptr<vqb_session> slot[2];
   for (int i = 0; i < 2; ++i) {
@@ -812,8 +926,7 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     vqb_session* s = slot[i].get();
     s->device = device;
     CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
-    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    s->own_stream = true;
+    if (int rc = s->make_streams()) return rc;
     s->n = s->n_global = chunk;
     s->dim = dim;
     s->ntiles_global = (chunk + kTdTile - 1) / kTdTile;
@@ -828,44 +941,47 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     CK(dalloc(&s->mu, (size_t)dim + 4));
     CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
     CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
-    // centre at the codebook mean (any centre is exact after the re-rank)
-    std::vector<float> mu((size_t)dim, 0.f);
-    for (long long l = 0; l < dim; ++l) {
-      double acc = 0;
-      for (long long k = 0; k < size; ++k) acc += codebook[k * dim + l];
-      mu[(size_t)l] = std::isfinite(acc) ? (float)(acc / (double)size) : 0.f;
-    }
-    CK(cudaMemcpy(s->mu, mu.data(), sizeof(float) * dim, cudaMemcpyHostToDevice));
     s->maxabs = 0;
     s->fast = fast_dim_supported((int)dim);
-    int rc = upload_codebook(s, codebook, size);
+    int rc = set_centre_from_codebook(s, codebook, size);
+    if (rc) return rc;
+    rc = upload_codebook(s, codebook, size);
     if (rc) return rc;
   }
   const long long nchunks = (n + chunk - 1) / chunk;
-  std::vector<double> totals((size_t)nchunks, 0.0);
-  std::vector<std::vector<double>> tot_host(2);
   double* tot_pinned = nullptr;
   CK(cudaMallocHost(reinterpret_cast<void**>(&tot_pinned), sizeof(double) * nchunks));
   std::unique_ptr<double, decltype(&cudaFreeHost)> gp(tot_pinned, &cudaFreeHost);
+  auto drain = [&](long long c) -> int {
+    vqb_session* s = slot[c & 1].get();
+    const long long r0 = c * chunk;
+    const long long rows = std::min(chunk, n - r0);
+    CK(download(idx_out + r0, s->idx, sizeof(int) * rows, s->stream));
+    return VQB_OK;
+  };
   for (long long c = 0; c < nchunks; ++c) {
     vqb_session* s = slot[c & 1].get();
     const long long r0 = c * chunk;
     const long long rows = std::min(chunk, n - r0);
     s->n = rows;  // last chunk may be short; tiles beyond it stay zero
-    CK(cudaMemcpyAsync(s->x32, x + r0 * dim, sizeof(float) * rows * dim, cudaMemcpyHostToDevice,
-                       s->stream));
-    // fixed-point scale unused (no sums); state reset on the device
     KernelArgs a = s->args();
     CK(launch_reset(s->st, kModeAssignOnly, (int)size, 0, 0, 0, s->stream));
     CK(launch_clear(a, s->stream));
     if (s->fast) CK(launch_prep_codebook(a, s->stream));
-    CK(launch_assign(a, s->fast, s->sms, s->stream));
+    unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
+    int rc = stream_rows_and_assign(s, x + r0 * dim, rows, mb);
+    if (rc) return rc;
     if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
-    CK(launch_epilogue(a, false, false, false, s->sms, s->stream));
+    CK(launch_epilogue(a, total != nullptr, false, false, s->sms, s->stream));
     CK(launch_finalize(a, false, s->stream));
-    CK(cudaMemcpyAsync(idx_out + r0, s->idx, sizeof(int) * rows, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(tot_pinned + c, &s->st->total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    if (c > 0) {
+      rc = drain(c - 1);
+      if (rc) return rc;
+    }
   }
+  int rc = drain(nchunks - 1);
+  if (rc) return rc;
   CK(cudaStreamSynchronize(slot[0]->stream));
   CK(cudaStreamSynchronize(slot[1]->stream));
   if (total) {
@@ -886,7 +1002,7 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
-  rc = set_state(s, kModeLloydStep, size, 0, 0);
+  rc = set_state(s, kModeLloydStep, size, 0, 0, codebook);
   if (rc) return rc;
   // segments: [prep+clear, assign, rerank, epilogue, finalize]
   cudaEvent_t ev[6];
@@ -907,7 +1023,7 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
     CK(cudaEventRecord(ev[2], s->stream));
     if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
     CK(cudaEventRecord(ev[3], s->stream));
-    CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
+    CK(launch_epilogue(a, true, true, false, s->sms, s->stream));  // distortion + cell sums
     CK(cudaEventRecord(ev[4], s->stream));
     CK(launch_finalize(a, s->fast, s->stream));
     CK(cudaEventRecord(ev[5], s->stream));
@@ -937,7 +1053,7 @@ int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int r
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
-  rc = set_state(s, kModeAssignOnly, size, 0, 0);
+  rc = set_state(s, kModeAssignOnly, size, 0, 0, codebook);
   if (rc) return rc;
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
@@ -963,6 +1079,68 @@ int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int r
   *ms_out = ms / reps;
   if (total_out) *total_out = s->st_host->total;
   if (flagged) *flagged = s->st_host->flagged_total / reps;
+  return VQB_OK;
+}
+
+// Tensor-core probe (tests): raw accumulators D = 2^(ey+ew) v of rows
+// [0, 128) against a codebook of `size` (a multiple of 256 that fits the smem
+// image) -> dump[128][size]; scales = {ey, ew, kn, tc_on, tc_bad}.
+int vqb_debug_tc_tile(vqb_session* s, const double* codebook, int64_t size, float* dump,
+                      int32_t* scales) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  if (size % kTcChunk != 0 || size > tc_max_size((int)s->dim))
+    return fail(VQB_USAGE, "probe needs a codebook size that is a multiple of %d and <= %d", kTcChunk,
+                tc_max_size((int)s->dim));
+  CK(cudaSetDevice(s->device));
+  int rc = upload_codebook(s, codebook, size);
+  if (rc) return rc;
+  rc = set_state(s, kModeAssignOnly, size, 0, 0, codebook);
+  if (rc) return rc;
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  CK(launch_prep_codebook(a, s->stream));
+  float* d = nullptr;
+  CK(dalloc(&d, (size_t)(kTcRows * size)));
+  std::unique_ptr<float, decltype(&cudaFree)> g(d, &cudaFree);
+  CK(cudaMemsetAsync(d, 0xff, sizeof(float) * kTcRows * size, s->stream));
+  CK(launch_tc_probe(a, d, s->stream));
+  CK(cudaMemcpyAsync(dump, d, sizeof(float) * kTcRows * size, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  scales[0] = s->st_host->tc_ey;
+  scales[1] = s->st_host->tc_ew;
+  scales[2] = s->st_host->tc_kn;
+  scales[3] = s->st_host->tc_on;
+  scales[4] = s->st_host->tc_bad;
+  return VQB_OK;
+}
+
+// Host->device bandwidth of the copy engine: mode 0 = transfer.cpp upload
+// (pinned straight / pageable staged), 1 = one plain cudaMemcpy, 2 =
+// cudaHostRegister + upload + unregister (the register cost included).
+int vqb_bench_upload(const void* src, int64_t bytes, int mode, double* seconds) {
+  void* d = nullptr;
+  CK(cudaMalloc(&d, (size_t)bytes));
+  std::unique_ptr<void, decltype(&cudaFree)> g(d, &cudaFree);
+  cudaStream_t cs, ks;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking));
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t e = cudaSuccess;
+  if (mode == 1) {
+    e = cudaMemcpy(d, src, (size_t)bytes, cudaMemcpyHostToDevice);
+  } else {
+    if (mode == 2) e = cudaHostRegister(const_cast<void*>(src), (size_t)bytes, cudaHostRegisterDefault);
+    if (e == cudaSuccess) e = upload(d, src, (size_t)bytes, 16u << 20, cs, ks);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ks);
+    if (mode == 2) cudaHostUnregister(const_cast<void*>(src));
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  cudaStreamDestroy(cs);
+  cudaStreamDestroy(ks);
+  CK(e);
+  *seconds = std::chrono::duration<double>(t1 - t0).count();
   return VQB_OK;
 }
 

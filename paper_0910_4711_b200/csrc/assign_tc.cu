@@ -1,0 +1,360 @@
+// Tensor-core candidate pass for the nearest-codevector search (sm_100a,
+// tcgen05 + TMEM).  Reference: _kernels.assign_range (_kernels.py:18-36).
+//
+// The distance pass is GEMM-shaped: for a tile of 128 rows and a chunk of
+// 256 codewords, v_ij = ||c~_j||^2 - 2 y~_i . c~_j is one M=128 x N=256 MMA
+// with K = L.  FP32-level accuracy comes from an fp16 hi/lo split of both
+// operands (y = yh + yl, w = wh + wl; the yl.wl term is below 2^-44) and the
+// norm folded in as an extra K-step (a constant column 2^kn times nh + nl):
+//
+//   D = yh.wh + yh.wl + yl.wh + 2^kn (nh + nl) = 2^(ey+ew) v      (fp32, TMEM)
+//
+// so the epilogue only does the top-2 bookkeeping (5 ALU ops per value) on
+// values read straight from TMEM.  The certification band is the FP32 one
+// widened for the split (4 x 2^-22) and for tensor-core accumulation (2 x
+// 2^-22 of the magnitude sum per MMA instruction; tools/tc_probe.py measures
+// <= 0.5 x 2^-22 per MMA against a float64 emulation of the same operands);
+// rows that do not certify go to the same shortlist / FP64 re-rank as the
+// FP32 pass, so a certified index is the reference's index.
+//
+// CTA = 1 MMA-issuer warp + 8 epilogue warps, persistent over 128-row tiles.
+// The codebook's operand image (staged by apply_kernel / prep_codebook in the
+// exact smem layout) is bulk-copied into smem once; the row tile's operands
+// are converted by the epilogue warps into a double-buffered smem tile;
+// accumulators are double-buffered in TMEM (2 x 256 columns), so the MMAs of
+// chunk c+1 overlap the epilogue of chunk c, and the conversion of tile i+1
+// overlaps the MMAs of tile i.
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "ptx.h"
+#include "vqb200_internal.h"
+
+namespace vqb {
+
+template <int L>
+struct TcCfg {
+  static constexpr int kEpiWarps = 8;
+  static constexpr int kThreads = 32 * (1 + kEpiWarps);
+  static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
+  static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
+  static constexpr size_t kMisc = 4096;
+  static constexpr size_t kSmemCap = 227 * 1024;
+  static constexpr int kMaxChunks = (int)((kSmemCap - 2 * kABytes - kMisc) / kChunkBytes);
+};
+
+int tc_max_size(int dim) {
+  switch (dim) {
+    case 16: return TcCfg<16>::kMaxChunks * kTcChunk;
+    case 32: return TcCfg<32>::kMaxChunks * kTcChunk;
+    case 64: return TcCfg<64>::kMaxChunks * kTcChunk;
+    default: return 0;
+  }
+}
+
+// misc smem: barriers | tmem slot | merge area [2][128][3]
+struct TcMisc {
+  uint64_t b_full;
+  uint64_t a_full[2];
+  uint64_t a_empty[2];
+  uint64_t d_full[2];
+  uint64_t d_empty[2];
+  uint32_t tmem;
+  uint32_t pad;
+  float merge[2][kTcRows][3];
+};
+static_assert(sizeof(TcMisc) <= 4096, "misc smem");
+
+template <int L, bool DUMP>
+__global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(KernelArgs a, float* dump) {
+  using C = TcCfg<L>;
+  DevState* st = a.st;
+  if (st->done) return;
+  const int K = st->size;
+  if (!DUMP && !tc_handles(st, K)) return;
+  const int nch = K / kTcChunk;
+  const long long nrows = a.r1 - a.r0;
+  const long long ntiles = (nrows + kTcRows - 1) / kTcRows;
+  const long long my_tiles =
+      DUMP ? 1 : ((long long)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  if (my_tiles <= 0) return;
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sB = smem;
+  unsigned char* sA = smem + (size_t)nch * C::kChunkBytes;
+  TcMisc* m = reinterpret_cast<TcMisc*>(sA + 2 * C::kABytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&m->b_full, 1);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&m->a_full[i], kTcRows);
+        mbar_init(&m->a_empty[i], 1);
+        mbar_init(&m->d_full[i], 1);
+        mbar_init(&m->d_empty[i], 32 * C::kEpiWarps);
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc(&m->tmem, 512);
+  }
+  // the norm term's constant A columns (0 and 1 = 2^kn) in both row buffers
+  {
+    const unsigned short one = __half_as_ushort(__float2half_rn(ldexpf(1.0f, st->tc_kn)));
+    for (int e = threadIdx.x; e < 2 * kTcRows * 16; e += blockDim.x) {
+      const int b = e / (kTcRows * 16), r = (e / 16) % kTcRows, c = e % 16;
+      unsigned short* ones = reinterpret_cast<unsigned short*>(sA + b * C::kABytes) + 2 * kTcRows * L;
+      ones[tc_off(r, c, 16)] = c < 2 ? one : (unsigned short)0;
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = m->tmem;
+
+  if (warp == 0) {
+    // ===== MMA issuer (one thread) =====
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&m->b_full, (uint32_t)(nch * C::kChunkBytes));
+      for (int c = 0; c < nch; ++c)
+        bulk_g2s(sB + c * C::kChunkBytes,
+                 reinterpret_cast<const unsigned char*>(a.tcb) + (size_t)c * C::kChunkBytes,
+                 (uint32_t)C::kChunkBytes, &m->b_full);
+      mbar_wait(&m->b_full, 0);
+      tc_fence_after();
+      // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N=256, M=128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcChunk >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+      constexpr uint32_t kSboL = L * 16, kSbo16 = 16 * 16;
+      const uint32_t sBa = smem_u32(sB), sAa = smem_u32(sA);
+      long long g = 0;
+      for (long long i = 0; i < my_tiles; ++i) {
+        const int b = (int)(i & 1);
+        mbar_wait(&m->a_full[b], (uint32_t)((i >> 1) & 1));
+        tc_fence_after();
+        const uint32_t aYh = sAa + b * (uint32_t)C::kABytes;
+        const uint32_t aYl = aYh + kTcRows * L * 2;
+        const uint32_t aOne = aYh + 2 * kTcRows * L * 2;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = (int)(g & 1);
+          mbar_wait(&m->d_empty[s], (uint32_t)(((g >> 1) & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(s * kTcChunk);
+          const uint32_t bWh = sBa + c * (uint32_t)C::kChunkBytes;
+          const uint32_t bWl = bWh + kTcChunk * L * 2;
+          const uint32_t bN = bWh + 2 * kTcChunk * L * 2;
+#pragma unroll
+          for (int k = 0; k < L / 16; ++k) {
+            const uint64_t dyh = umma_desc(aYh + k * 256, 128, kSboL);
+            const uint64_t dyl = umma_desc(aYl + k * 256, 128, kSboL);
+            const uint64_t dwh = umma_desc(bWh + k * 256, 128, kSboL);
+            const uint64_t dwl = umma_desc(bWl + k * 256, 128, kSboL);
+            mma_f16_ss(d, dyh, dwh, idesc, k > 0 ? 1u : 0u);
+            mma_f16_ss(d, dyh, dwl, idesc, 1u);
+            mma_f16_ss(d, dyl, dwh, idesc, 1u);
+          }
+          mma_f16_ss(d, umma_desc(aOne, 128, kSbo16), umma_desc(bN, 128, kSbo16), idesc, 1u);
+          mma_commit(&m->d_full[s]);
+        }
+        mma_commit(&m->a_empty[b]);
+      }
+    }
+  } else {
+    // ===== epilogue warps: row conversion + top-2 over TMEM =====
+    const int e = warp - 1;
+    const int h = e >> 2;       // column half of every 256-column chunk
+    const int qd = warp & 3;    // TMEM lane quarter this warp may access
+    const int r = qd * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
+    const float sy = ldexpf(1.0f, st->tc_ey);
+
+    // h == 0 threads own row r: convert it into A buffer b, return ||y~||^2
+    auto convert = [&](long long i, int b, float& q, bool& bad) {
+      const long long t = (long long)blockIdx.x + i * gridDim.x;
+      const long long row = a.r0 + t * kTcRows + r;
+      const bool valid = row < a.r1;
+      unsigned short* yh = reinterpret_cast<unsigned short*>(sA + b * C::kABytes);
+      unsigned short* yl = yh + kTcRows * L;
+      float qq = 0.f;
+      bool bb = false;
+#pragma unroll
+      for (int c8 = 0; c8 < L / 8; ++c8) {
+        float xv[8];
+        if (valid) {
+          const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
+          const float4 p0 = __ldg(src), p1 = __ldg(src + 1);
+          xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
+          xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) xv[k] = 0.f;
+        }
+        unsigned short hs[8], ls[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float yv = valid ? __fsub_rn(xv[k], a.mu[c8 * 8 + k]) : 0.f;
+          qq = fmaf(yv, yv, qq);
+          const float v = yv * sy;
+          bb |= !(fabsf(v) <= 60000.0f);
+          const __half hi = __float2half_rn(v);
+          const __half lo = __float2half_rn(v - __half2float(hi));
+          hs[k] = __half_as_ushort(hi);
+          ls[k] = __half_as_ushort(lo);
+        }
+        uint4 ph, pl;
+        ph.x = hs[0] | ((uint32_t)hs[1] << 16); ph.y = hs[2] | ((uint32_t)hs[3] << 16);
+        ph.z = hs[4] | ((uint32_t)hs[5] << 16); ph.w = hs[6] | ((uint32_t)hs[7] << 16);
+        pl.x = ls[0] | ((uint32_t)ls[1] << 16); pl.y = ls[2] | ((uint32_t)ls[3] << 16);
+        pl.z = ls[4] | ((uint32_t)ls[5] << 16); pl.w = ls[6] | ((uint32_t)ls[7] << 16);
+        *reinterpret_cast<uint4*>(yh + tc_off(r, c8 * 8, L)) = ph;
+        *reinterpret_cast<uint4*>(yl + tc_off(r, c8 * 8, L)) = pl;
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&m->a_full[b]);
+      q = qq;
+      bad = bb;
+    };
+
+    float qcur = 0.f, qnext = 0.f;
+    bool badcur = false, badnext = false;
+    if (h == 0) convert(0, 0, qcur, badcur);
+    long long g = 0;
+    for (long long i = 0; i < my_tiles; ++i) {
+      const int b = (int)(i & 1);
+      float m1 = INFINITY, m2 = INFINITY;
+      int i1 = 0;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int s = (int)(g & 1);
+        mbar_wait(&m->d_full[s], (uint32_t)((g >> 1) & 1));
+        tc_fence_after();
+#pragma unroll 1
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float v[32];
+          const int col = s * kTcChunk + h * 128 + q4 * 32;
+          tmem_ld32(trow + (uint32_t)col, v);
+          tmem_wait_ld();
+          const int jb = c * kTcChunk + h * 128 + q4 * 32;
+          if constexpr (DUMP) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) dump[(long long)r * K + jb + t] = v[t];
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const float x = v[t];
+              const float n2 = fminf(m2, fmaxf(m1, x));
+              const bool p = x < m1;
+              m1 = fminf(m1, x);
+              i1 = p ? jb + t : i1;
+              m2 = n2;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&m->d_empty[s]);
+        if (c == 0 && h == 0 && i + 1 < my_tiles) {
+          // convert the next tile while this tile's remaining MMAs run
+          const int nb = (int)((i + 1) & 1);
+          const long long use = (i + 1) >> 1;
+          mbar_wait(&m->a_empty[nb], (uint32_t)((use & 1) ^ 1));
+          convert(i + 1, nb, qnext, badnext);
+        }
+      }
+      if constexpr (!DUMP) {
+        float* mg = &m->merge[b][0][0];
+        if (h == 1) {
+          mg[r * 3 + 0] = m1;
+          mg[r * 3 + 1] = m2;
+          mg[r * 3 + 2] = __int_as_float(i1);
+        }
+        named_bar(1, 32 * C::kEpiWarps);
+        if (h == 0) {
+          const float om1 = mg[r * 3 + 0], om2 = mg[r * 3 + 1];
+          const int oi1 = __float_as_int(mg[r * 3 + 2]);
+          m2 = fminf(fmaxf(m1, om1), fminf(m2, om2));
+          if (om1 < m1) {
+            m1 = om1;
+            i1 = oi1;
+          }
+          // certification (see the header comment and assign_chunk in kernels.cu)
+          const long long t = (long long)blockIdx.x + i * gridDim.x;
+          const long long row = a.r0 + t * kTcRows + r;
+          const bool valid = row < a.r1;
+          bool flag = false;
+          float thr = NAN;
+          if (valid) {
+            const float inv = ldexpf(1.0f, -(st->tc_ey + st->tc_ew));
+            const float m1v = m1 * inv, m2v = m2 * inv;
+            const float u = 5.9604645e-8f, u22 = 2.3841858e-7f;
+            const float yn = sqrtf(qcur);
+            const float sd = sqrtf(fmaxf(m2v + qcur, 0.f)) * 1.01f + 1.0f;
+            const float S = 2.02f * yn + sd;
+            // accumulation: each of the 3L/16 + 1 MMAs may lose 2 x 2^-22 of the
+            // magnitude sum (measured: <= 0.25 of that, tools/tc_probe.py);
+            // split: 4 x 2^-22; the rest as in the FP32 pass
+            const float E = (float)(2 * (3 * L / 16 + 1) + 4) * u22 * S * S + 2.5f * u * sd * S + 1e-14f * S * S +
+                            sqrtf((float)L) * S * u *
+                                (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
+            flag = badcur || !((m2v - m1v) > 3.0f * E);
+            thr = m1v + 3.0f * E;
+            a.idx[row] = i1;
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, flag);
+          if (mask) {
+            int base = 0;
+            const int leader = __ffs(mask) - 1;
+            if (lane == leader) base = atomicAdd(&st->flag_count, __popc(mask));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (flag) {
+              const int pos = base + __popc(mask & ((1u << lane) - 1u));
+              a.flags[pos] = (int)row;
+              a.flag_thr[pos] = thr;
+            }
+          }
+          qcur = qnext;
+          badcur = badnext;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int L, bool DUMP>
+static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaStream_t s) {
+  using C = TcCfg<L>;
+  const int nch = (int)std::min<long long>(C::kMaxChunks, a.kmax / kTcChunk);
+  if (nch < 1 || !a.tcb) return cudaSuccess;
+  const size_t smem = (size_t)nch * C::kChunkBytes + 2 * C::kABytes + C::kMisc;
+  cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, DUMP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  assign_tc_kernel<L, DUMP><<<grid, C::kThreads, smem, s>>>(a, dump);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s) {
+  switch (a.dim) {
+    case 16: return launch_tc_L<16, false>(a, sms, nullptr, s);
+    case 32: return launch_tc_L<32, false>(a, sms, nullptr, s);
+    case 64: return launch_tc_L<64, false>(a, sms, nullptr, s);
+    default: return cudaSuccess;
+  }
+}
+
+cudaError_t launch_tc_probe(const KernelArgs& a, float* dump, cudaStream_t s) {
+  switch (a.dim) {
+    case 16: return launch_tc_L<16, true>(a, 1, dump, s);
+    case 32: return launch_tc_L<32, true>(a, 1, dump, s);
+    case 64: return launch_tc_L<64, true>(a, 1, dump, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace vqb

@@ -22,58 +22,10 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "ptx.h"
 #include "vqb200_internal.h"
 
 namespace vqb {
-
-// ---------------------------------------------------------------------------
-// small helpers
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 // packed f32x2 (sm_100 FFMA2): two rows' accumulators in one 64-bit register
 // pair; the codebook value is a scalar broadcast operand (R.F32 in SASS).
@@ -134,6 +86,7 @@ __global__ void prep_codebook_kernel(KernelArgs a) {
         w[l] = -2.0f * c;
       }
       a.nrm[k] = (float)n;
+      stage_tc_row(a, k, w, n);
     } else {
       for (int l = 0; l < dim; ++l) w[l] = 0.0f;
       a.nrm[k] = INFINITY;  // padding never wins
@@ -365,15 +318,16 @@ __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelAr
   const DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
+  if (a.tcb && tc_handles(st, K)) return;  // assign_tc runs this pass
   const int ntiles = (K + TK - 1) / TK;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
   __shared__ __align__(8) uint64_t bars[2];
 
-  // contiguous, balanced row range for this block
-  const long long n = a.n;
-  const long long lo = n * blockIdx.x / gridDim.x;
-  const long long hi = n * (blockIdx.x + 1) / gridDim.x;
+  // contiguous, balanced row range for this block (within [r0, r1))
+  const long long n = a.r1 - a.r0;
+  const long long lo = a.r0 + n * blockIdx.x / gridDim.x;
+  const long long hi = a.r0 + n * (blockIdx.x + 1) / gridDim.x;
   const long long rows = hi - lo;
   const long long per_chunk = (long long)NT * R;
   const long long full = rows / per_chunk;
@@ -926,12 +880,17 @@ cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
 
 cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s) {
   if (fast) {
+    // both candidate kernels are enqueued; each reads the device-side codebook
+    // size and exactly one of them runs (assign_tc for tc_kmin <= K <= tc_kmax)
+    cudaError_t e;
     switch (a.dim) {
-      case 16: return launch_fast_L<16>(a, sms, s);
-      case 32: return launch_fast_L<32>(a, sms, s);
-      case 64: return launch_fast_L<64>(a, sms, s);
+      case 16: e = launch_fast_L<16>(a, sms, s); break;
+      case 32: e = launch_fast_L<32>(a, sms, s); break;
+      case 64: e = launch_fast_L<64>(a, sms, s); break;
       default: return cudaErrorInvalidValue;
     }
+    if (e != cudaSuccess || !a.tcb) return e;
+    return launch_assign_tc(a, sms, s);
   }
   if (a.x32) return launch_exact_t<float>(a, a.x32, 0, sms, s);
   return launch_exact_t<double>(a, a.x64, 0, sms, s);
@@ -1412,6 +1371,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) 
   __shared__ double s_td;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
+    st->tc_bad = 0;  // apply_kernel re-stages the operand image
     st->flagged_total += st->flag_count;
     st->flagged2_total += st->flag2_count;
     st->flag_count = 0;
@@ -1553,6 +1513,7 @@ __device__ __forceinline__ void stage_row(const KernelArgs& a, long long k, cons
     w[l] = -2.0f * c;
   }
   a.nrm[k] = (float)n;
+  stage_tc_row(a, k, w, n);
 }
 
 __global__ void __launch_bounds__(128) apply_kernel(KernelArgs a, int stage) {
@@ -1675,6 +1636,37 @@ cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
     maxabs_kernel<float><<<sms * 4, 256, 0, s>>>(x32, count, out_bits);
   else
     maxabs_kernel<double><<<sms * 4, 256, 0, s>>>(x64, count, out_bits);
+  return cudaGetLastError();
+}
+
+// fixed-point scale from a device-side max |x| (api.cu fixed_shift_for, on
+// the device so the host-buffer Lloyd step needs no host round trip)
+__global__ void set_shift_kernel(DevState* st, const unsigned long long* maxabs_bits, long long n_global) {
+  const double m = __longlong_as_double((long long)*maxabs_bits);
+  int e_n = 0;
+  while ((1LL << e_n) < n_global && e_n < 62) ++e_n;
+  int e_x = 0;
+  if (m > 0 && m <= DBL_MAX) frexp(m, &e_x);
+  int sft = 62 - e_n - e_x - 1;
+  sft = sft > 1000 ? 1000 : (sft < -1000 ? -1000 : sft);
+  st->fixed_shift = sft;
+  st->nonfinite = !(m <= DBL_MAX);
+}
+
+cudaError_t launch_set_shift(DevState* st, const unsigned long long* maxabs_bits, long long n_global,
+                             cudaStream_t s) {
+  set_shift_kernel<<<1, 1, 0, s>>>(st, maxabs_bits, n_global);
+  return cudaGetLastError();
+}
+
+__global__ void widen_idx_kernel(const int* idx, long long* out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = idx[i];
+}
+
+cudaError_t launch_widen_idx(const int* idx, long long* out, long long n, int sms, cudaStream_t s) {
+  widen_idx_kernel<<<sms * 4, 256, 0, s>>>(idx, out, n);
   return cudaGetLastError();
 }
 

@@ -2,6 +2,7 @@
 // native training loop (api.cu).  Not part of the public ABI: that is
 // include/vqb200.h.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -62,6 +63,13 @@ struct DevState {
   int flag2_count;     // rows whose shortlist overflowed -> full FP64 scan
   unsigned int cmax_bits;  // float bits of max_j ||c~_j|| (centred FP32 codebook)
   int passes;          // allocation passes executed
+  int nonfinite;       // set_shift saw a non-finite |x| (host-buffer Lloyd step)
+  // tensor-core candidate pass (assign_tc.cu): power-of-two scales of the
+  // fp16 hi/lo operand split, chosen on the host from |x| / codebook bounds
+  int tc_on;           // 1: the TC pass may run when tc_kmin <= size <= tc_kmax
+  int tc_kmin, tc_kmax;
+  int tc_ey, tc_ew, tc_kn;
+  int tc_bad;          // staging saw an fp16-unrepresentable codebook value
   long long flagged_total;  // rows re-ranked over the whole run (diagnostic)
   long long flagged2_total; // of which needed the full FP64 scan
   long long evals;     // sum over passes of rows * size (this shard)
@@ -91,12 +99,14 @@ struct KernelArgs {
   const float* x32;
   const double* x64;
   long long n;          // local rows
+  long long r0, r1;     // row range of the candidate pass (a chunk of [0, n))
   int dim;
   long long tile0;      // global index of this shard's first TD tile
   const float* mu;      // centring vector (FP32, dim)
   // codebooks
   double* cb[2];        // FP64 master, double buffered, kmax x dim
   float* w;             // -2 * c~ (FP32), kpad x dim
+  unsigned short* tcb;  // fp16 hi/lo operand image of the codebook for the TC pass (nullable)
   float* nrm;           // ||c~||^2 (FP32), kpad
   long long kmax;
   // per-row outputs
@@ -124,6 +134,9 @@ cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s
 cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s);
 cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
                           unsigned long long* out_bits, int sms, cudaStream_t s);
+cudaError_t launch_set_shift(DevState* st, const unsigned long long* maxabs_bits, long long n_global,
+                             cudaStream_t s);
+cudaError_t launch_widen_idx(const int* idx, long long* out, long long n, int sms, cudaStream_t s);
 cudaError_t launch_sum_inorder(const double* v, long long n, double* out, cudaStream_t s);
 cudaError_t launch_reset(DevState* st, int mode, int size, int metric, int ordered, int keep_cur,
                          cudaStream_t s);
@@ -135,5 +148,56 @@ cudaError_t launch_column_sums_ordered(const double* x64, const float* x32, long
 cudaError_t launch_pair_distance(const double* a, const double* b, int dim, int metric, double* out,
                                  cudaStream_t s);
 bool fast_dim_supported(int dim);
+
+// tensor-core candidate pass (assign_tc.cu)
+constexpr int kTcChunk = 256;  // codewords per MMA N
+constexpr int kTcRows = 128;   // rows per tile (MMA M)
+__host__ __device__ inline long long tc_chunk_elems(int dim) { return (long long)kTcChunk * (2 * dim + 16); }
+int tc_max_size(int dim);      // largest codebook whose operand image fits in smem
+// does assign_tc (rather than assign_fast) run the candidate pass at size K?
+__host__ __device__ __forceinline__ bool tc_handles(const DevState* st, int K) {
+  return st->tc_on && !st->tc_bad && K >= st->tc_kmin && K <= st->tc_kmax && K % kTcChunk == 0;
+}
+cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_tc_probe(const KernelArgs& a, float* dump, cudaStream_t s);
+
+// element offset of (row, col) in a K-major, no-swizzle UMMA operand tile with
+// kt columns: 8-row x 16-byte core matrices, K-adjacent core matrices 128 B
+// apart (LBO), 8-row groups kt*16 B apart (SBO)
+__host__ __device__ __forceinline__ long long tc_off(int row, int col, int kt) {
+  return (long long)(row >> 3) * (kt * 8) + (col >> 3) * 64 + (row & 7) * 8 + (col & 7);
+}
+
+// fp16 hi/lo image of staged codevector k (w = -2 c~ in FP32, nrm = ||c~||^2
+// in FP64): chunk k/256 = [wh 256 x L | wl 256 x L | wn 256 x 16], where
+// wh + wl = w * 2^ew and 2^kn (nh + nl) = nrm * 2^(ey + ew).  Values fp16
+// cannot hold set tc_bad, which sends the pass to the FP32 kernel.
+__device__ __forceinline__ void stage_tc_row(const KernelArgs& a, long long k, const float* w, double nrm) {
+  if (!a.tcb) return;
+  DevState* st = a.st;
+  const int L = a.dim;
+  unsigned short* img = a.tcb + (k / kTcChunk) * tc_chunk_elems(L);
+  const int r = (int)(k % kTcChunk);
+  unsigned short* wh = img;
+  unsigned short* wl = img + (long long)kTcChunk * L;
+  unsigned short* wn = img + 2LL * kTcChunk * L;
+  const float sw = ldexpf(1.0f, st->tc_ew);
+  bool bad = false;
+  for (int l = 0; l < L; ++l) {
+    const float v = w[l] * sw;
+    const __half h = __float2half_rn(v);
+    const __half lo = __float2half_rn(v - __half2float(h));
+    bad |= !(fabsf(v) <= 60000.0f);
+    wh[tc_off(r, l, L)] = __half_as_ushort(h);
+    wl[tc_off(r, l, L)] = __half_as_ushort(lo);
+  }
+  const double nv = ldexp(nrm, st->tc_ey + st->tc_ew - st->tc_kn);
+  const __half nh = __double2half(nv);
+  const __half nl = __double2half(nv - (double)__half2float(nh));
+  bad |= !(fabs(nv) <= 60000.0);
+  for (int c = 0; c < 16; ++c)
+    wn[tc_off(r, c, 16)] = c == 0 ? __half_as_ushort(nh) : (c == 1 ? __half_as_ushort(nl) : 0);
+  if (bad) st->tc_bad = 1;
+}
 
 }  // namespace vqb

@@ -318,3 +318,91 @@ def test_kernel_surface_small_helpers():
     assert kernels.sum_inorder(x[:, 0]) == oracle.sum_inorder(x[:, 0])
     assert kernels.pair_distance(x[0], x[1], 1) == oracle.pair_distance(x[0], x[1], 1)
     assert kernels.pair_distance(x[0], x[1], 0) == oracle.pair_distance(x[0], x[1], 0)
+
+
+# ---------------------------------------------------------------------------
+# host-buffer entry points (transfer engine: pinned and pageable sources)
+# ---------------------------------------------------------------------------
+
+def _pinned_copy(a):
+    torch = pytest.importorskip("torch")
+    t = torch.from_numpy(a).pin_memory()
+    return t, t.numpy()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_lloyd_step_f32_host_buffers(pinned):
+    import ctypes
+    from paper_0910_4711_b200 import _lib, synthetic
+    g = _golden("cfg2_design")
+    x = synthetic.make_training("cfg2", n=(1 << 18) + 777)
+    keep = None
+    if pinned:
+        keep, x = _pinned_copy(x)
+    last = max(int(k[4:-3]) for k in g.files if k.startswith("pass") and k.endswith("_cb"))
+    cb = np.ascontiguousarray(g[f"pass{last}_cb"])  # a K=64 codebook of the reference's run
+    k = cb.shape[0]
+    new = np.empty_like(cb)
+    cells = np.empty(x.shape[0], dtype=np.int64)
+    td, empty = ctypes.c_double(), ctypes.c_int64()
+    _lib.check(_lib.lib().vqb_lloyd_step_f32(_lib.ptr(x), x.shape[0], 16, _lib.ptr(cb), k, 0,
+                                             _lib.ptr(new), _lib.ptr(cells), ctypes.byref(td),
+                                             ctypes.byref(empty)))
+    x64 = x.astype(np.float64)
+    want_cells, dists = oracle.assign_all(x64, cb, workers=8)
+    assert np.array_equal(cells, want_cells)
+    want_cb, counts = oracle.update_all(x64, want_cells, cb, workers=8)
+    np.testing.assert_allclose(new, want_cb, rtol=1e-13, atol=0)
+    assert empty.value == int(np.count_nonzero(counts == 0))
+    assert abs(td.value - oracle.sum_inorder(dists)) <= 1e-12 * td.value
+    del keep
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_encode_f32_host_buffers_and_total(pinned):
+    import ctypes
+    from paper_0910_4711_b200 import _lib, synthetic
+    cb32, q = synthetic.make_encode_case(n=(1 << 22) * 2 + 4097)  # 3 pipeline chunks
+    keep = None
+    if pinned:
+        keep, q = _pinned_copy(q)
+    cb = cb32.astype(np.float64)
+    idx = np.empty(q.shape[0], dtype=np.uint32)
+    total = ctypes.c_double()
+    _lib.check(_lib.lib().vqb_encode_f32(_lib.ptr(q), q.shape[0], 16, _lib.ptr(cb), cb.shape[0], 0,
+                                         _lib.ptr(idx), ctypes.byref(total)))
+    for sl in (slice(0, 100000), slice((1 << 22) - 5000, (1 << 22) + 5000),
+               slice(q.shape[0] - 60000, q.shape[0])):
+        cells, _ = oracle.assign_all(q[sl].astype(np.float64), cb, workers=8)
+        assert np.array_equal(idx[sl], cells.astype(np.uint32))
+    _, want_total = vq.assign_cells(q, vq.Codebook(cb))
+    assert abs(total.value - want_total) <= 1e-10 * want_total
+    del keep
+
+
+# ---------------------------------------------------------------------------
+# tensor-core candidate pass: raw accumulators vs a float64 emulation
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dim,k", [(16, 1024), (32, 256), (64, 512)])
+def test_tc_accumulators_vs_float64_emulation(dim, k):
+    """The tcgen05 MMA chain (fp16 hi/lo operands, fp32 TMEM accumulation)
+    against the exact value of the same operands: the error stays inside the
+    certification band's accumulation term (2 x 2^-22 of the magnitude sum
+    per MMA), with a 2x margin."""
+    import tc_emulation as te
+    from paper_0910_4711_b200 import _lib
+    from paper_0910_4711_b200.core import _Session
+    rng = np.random.default_rng(dim + k)
+    x = rng.normal(100, 40, (1000, dim)).astype(np.float32)
+    cb = rng.normal(100, 40, (k, dim))
+    s = _Session(x, None)
+    dump = np.empty((128, k), dtype=np.float32)
+    sc = np.zeros(5, dtype=np.int32)
+    _lib.check(_lib.lib().vqb_debug_tc_tile(s.handle, _lib.ptr(cb), k, _lib.ptr(dump), _lib.ptr(sc)))
+    assert sc[3] == 1 and sc[4] == 0  # TC pass configured, codebook representable
+    d, mag, v = te.expected_accumulators(x[:128], te.session_mu(x), cb, int(sc[0]), int(sc[1]), int(sc[2]))
+    rel = np.abs(dump.astype(np.float64) - d) / mag
+    n_mma = 3 * dim // 16 + 1
+    assert rel.max() <= 0.5 * 2 * n_mma * 2.0 ** -22, rel.max()
+    assert np.array_equal(np.argmin(dump, 1), np.argmin(v, 1))
