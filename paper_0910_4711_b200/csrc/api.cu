@@ -845,8 +845,8 @@ int set_centre_from_codebook(vqb_session* s, const double* codebook, long long s
 // max |x| and FP32 candidate pass launched as soon as it lands (the copy of
 // piece i+1 overlaps the distance pass of piece i).  For dims without a fast
 // path the exact scan runs after the last piece.
-int stream_rows_and_assign(vqb_session* s, const float* x, long long rows, unsigned long long* maxabs_bits) {
-  KernelArgs a = s->args();
+int stream_rows_and_assign(vqb_session* s, const KernelArgs& a, const float* x, long long rows,
+                           unsigned long long* maxabs_bits) {
   const size_t row_bytes = sizeof(float) * (size_t)s->dim;
   const size_t piece = std::max<size_t>(row_bytes, ((size_t)8 << 20) / row_bytes * row_bytes);
   CK(cudaMemsetAsync(maxabs_bits, 0, sizeof(unsigned long long), s->stream));
@@ -886,7 +886,7 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   CK(launch_clear(a, s->stream));
   if (s->fast) CK(launch_prep_codebook(a, s->stream));
   unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
-  rc = stream_rows_and_assign(s, x, n, mb);
+  rc = stream_rows_and_assign(s, a, x, n, mb);
   if (rc) return rc;
   CK(launch_set_shift(s->st, mb, s->n_global, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
@@ -965,11 +965,12 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     const long long rows = std::min(chunk, n - r0);
     s->n = rows;  // last chunk may be short; tiles beyond it stay zero
     KernelArgs a = s->args();
+    if (!total) a.dists = nullptr;  // indices only: no per-row distances
     CK(launch_reset(s->st, kModeAssignOnly, (int)size, 0, 0, 0, s->stream));
     CK(launch_clear(a, s->stream));
     if (s->fast) CK(launch_prep_codebook(a, s->stream));
     unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
-    int rc = stream_rows_and_assign(s, x + r0 * dim, rows, mb);
+    int rc = stream_rows_and_assign(s, a, x + r0 * dim, rows, mb);
     if (rc) return rc;
     if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
     CK(launch_epilogue(a, total != nullptr, false, false, s->sms, s->stream));

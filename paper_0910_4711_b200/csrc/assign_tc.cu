@@ -29,6 +29,7 @@
 #include <cstdint>
 
 #include "ptx.h"
+#include "refarith.cuh"
 #include "vqb200_internal.h"
 
 namespace vqb {
@@ -39,7 +40,7 @@ struct TcCfg {
   static constexpr int kThreads = 32 * (1 + kEpiWarps);
   static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
   static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
-  static constexpr size_t kMisc = 4096;
+  static constexpr size_t kMisc = 8192;
   static constexpr size_t kSmemCap = 227 * 1024;
   static constexpr int kMaxChunks = (int)((kSmemCap - 2 * kABytes - kMisc) / kChunkBytes);
 };
@@ -53,7 +54,7 @@ int tc_max_size(int dim) {
   }
 }
 
-// misc smem: barriers | tmem slot | merge area [2][128][3]
+// misc smem: barriers | tmem slot | merge area (per row-buffer parity)
 struct TcMisc {
   uint64_t b_full;
   uint64_t a_full[2];
@@ -62,22 +63,35 @@ struct TcMisc {
   uint64_t d_empty[2];
   uint32_t tmem;
   uint32_t pad;
-  float merge[2][kTcRows][3];
+  union {
+    float top2[2][kTcRows][3];                      // h == 1 half's (m1, m2, i1)
+    unsigned short cand[2][kTcRows][1 + kTcShort];  // h == 1 half's shortlist
+  } merge;
 };
-static_assert(sizeof(TcMisc) <= 4096, "misc smem");
+static_assert(sizeof(TcMisc) <= 8192, "misc smem");
 
-template <int L, bool DUMP>
+enum { kTcTop2 = 0, kTcShortlist = 1, kTcDump = 2 };
+
+// MODE kTcTop2: candidate pass over rows [r0, r1) -> idx + certified band /
+//   re-rank queue (flags, flag_thr).
+// MODE kTcShortlist: the queued rows again (gathered from flags): every j
+//   with v_j <= thr (the same TC arithmetic, so the band argument of
+//   shortlist_kernel holds with the TC error), FP64 on <= 8 candidates,
+//   overflow -> flags2.  ~2 ALU ops per value instead of 5.
+// MODE kTcDump: tile 0's raw accumulators -> dump (tests).
+template <int L, int MODE>
 __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(KernelArgs a, float* dump) {
   using C = TcCfg<L>;
   DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
-  if (!DUMP && !tc_handles(st, K)) return;
+  if (MODE != kTcDump && !tc_handles(st, K)) return;
   const int nch = K / kTcChunk;
-  const long long nrows = a.r1 - a.r0;
-  const long long ntiles = (nrows + kTcRows - 1) / kTcRows;
-  const long long my_tiles =
-      DUMP ? 1 : ((long long)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  const long long nitems = MODE == kTcShortlist ? (long long)st->flag_count : a.r1 - a.r0;
+  const long long ntiles = (nitems + kTcRows - 1) / kTcRows;
+  const long long my_tiles = MODE == kTcDump
+                                 ? 1
+                                 : ((long long)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   if (my_tiles <= 0) return;
 
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -162,19 +176,29 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
       }
     }
   } else {
-    // ===== epilogue warps: row conversion + top-2 over TMEM =====
+    // ===== epilogue warps: row conversion + per-value work over TMEM =====
     const int e = warp - 1;
     const int h = e >> 2;       // column half of every 256-column chunk
     const int qd = warp & 3;    // TMEM lane quarter this warp may access
     const int r = qd * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
     const float sy = ldexpf(1.0f, st->tc_ey);
+    const float dscale = ldexpf(1.0f, st->tc_ey + st->tc_ew);
+
+    // row of (local tile i, tile row r); valid = inside the range / queue
+    auto row_of = [&](long long i, long long& entry, bool& valid) -> long long {
+      const long long t = (long long)blockIdx.x + i * gridDim.x;
+      entry = t * kTcRows + r;
+      valid = entry < nitems;
+      if (MODE == kTcShortlist) return valid ? (long long)a.flags[entry] : 0;
+      return a.r0 + entry;
+    };
 
     // h == 0 threads own row r: convert it into A buffer b, return ||y~||^2
     auto convert = [&](long long i, int b, float& q, bool& bad) {
-      const long long t = (long long)blockIdx.x + i * gridDim.x;
-      const long long row = a.r0 + t * kTcRows + r;
-      const bool valid = row < a.r1;
+      long long entry;
+      bool valid;
+      const long long row = row_of(i, entry, valid);
       unsigned short* yh = reinterpret_cast<unsigned short*>(sA + b * C::kABytes);
       unsigned short* yl = yh + kTcRows * L;
       float qq = 0.f;
@@ -223,8 +247,16 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
     long long g = 0;
     for (long long i = 0; i < my_tiles; ++i) {
       const int b = (int)(i & 1);
+      // top-2 state (kTcTop2) / shortlist state (kTcShortlist)
       float m1 = INFINITY, m2 = INFINITY;
       int i1 = 0;
+      int nc = 0;
+      int cand[kTcShort];
+      float thr_d = -INFINITY;
+      long long entry;
+      bool valid;
+      const long long row = row_of(i, entry, valid);
+      if (MODE == kTcShortlist && valid) thr_d = a.flag_thr[entry] * dscale;  // NaN stays NaN -> overflow
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = (int)(g & 1);
         mbar_wait(&m->d_full[s], (uint32_t)((g >> 1) & 1));
@@ -236,9 +268,17 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           tmem_ld32(trow + (uint32_t)col, v);
           tmem_wait_ld();
           const int jb = c * kTcChunk + h * 128 + q4 * 32;
-          if constexpr (DUMP) {
+          if constexpr (MODE == kTcDump) {
 #pragma unroll
             for (int t = 0; t < 32; ++t) dump[(long long)r * K + jb + t] = v[t];
+          } else if constexpr (MODE == kTcShortlist) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              if (v[t] <= thr_d) {
+                if (nc < kTcShort) cand[nc] = jb + t;
+                ++nc;
+              }
+            }
           } else {
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
@@ -261,8 +301,8 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           convert(i + 1, nb, qnext, badnext);
         }
       }
-      if constexpr (!DUMP) {
-        float* mg = &m->merge[b][0][0];
+      if constexpr (MODE == kTcTop2) {
+        float* mg = &m->merge.top2[b][0][0];
         if (h == 1) {
           mg[r * 3 + 0] = m1;
           mg[r * 3 + 1] = m2;
@@ -278,13 +318,10 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
             i1 = oi1;
           }
           // certification (see the header comment and assign_chunk in kernels.cu)
-          const long long t = (long long)blockIdx.x + i * gridDim.x;
-          const long long row = a.r0 + t * kTcRows + r;
-          const bool valid = row < a.r1;
           bool flag = false;
           float thr = NAN;
           if (valid) {
-            const float inv = ldexpf(1.0f, -(st->tc_ey + st->tc_ew));
+            const float inv = 1.0f / dscale;
             const float m1v = m1 * inv, m2v = m2 * inv;
             const float u = 5.9604645e-8f, u22 = 2.3841858e-7f;
             const float yn = sqrtf(qcur);
@@ -299,6 +336,12 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
             flag = badcur || !((m2v - m1v) > 3.0f * E);
             thr = m1v + 3.0f * E;
             a.idx[row] = i1;
+            if (!flag && a.dists) {
+              // exact FP64 distance to the certified winner (_kernels.py:25-34);
+              // the row is L2-resident from its conversion one tile ago
+              const double d = winner_dist<float, L>(a.x32 + row * L, a.cb[st->cur] + (long long)i1 * L, L);
+              a.dists[row] = st->metric == kEuclidean ? sqrt(d) : d;
+            }
           }
           const unsigned mask = __ballot_sync(0xffffffffu, flag);
           if (mask) {
@@ -312,9 +355,41 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
               a.flag_thr[pos] = thr;
             }
           }
-          qcur = qnext;
-          badcur = badnext;
         }
+      } else if constexpr (MODE == kTcShortlist) {
+        unsigned short* mg = &m->merge.cand[b][r][0];
+        if (h == 1) {
+          mg[0] = (unsigned short)min(nc, kTcShort + 1);
+          for (int k = 0; k < kTcShort; ++k) mg[1 + k] = k < nc ? (unsigned short)cand[k] : 0;
+        }
+        named_bar(1, 32 * C::kEpiWarps);
+        if (h == 0 && valid) {
+          const int onc = mg[0];
+          if (nc + onc == 0 || nc + onc > kTcShort || badcur) {
+            const int pos = atomicAdd(&st->flag2_count, 1);
+            a.flags2[pos] = (int)row;
+          } else {
+            // FP64 in the reference's arithmetic; lexicographic (d, j) so the
+            // two halves' candidate order does not matter (_kernels.py:23-32)
+            const double* __restrict__ cb = a.cb[st->cur];
+            double best = INFINITY;
+            int bj = 0x7fffffff;
+            for (int k = 0; k < nc + onc; ++k) {
+              const int j = k < nc ? cand[k] : (int)mg[1 + k - nc];
+              const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)j * L, L);
+              if (d < best || (d == best && j < bj)) {
+                best = d;
+                bj = j;
+              }
+            }
+            a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
+            if (a.dists) a.dists[row] = st->metric == kEuclidean ? sqrt(best) : best;
+          }
+        }
+      }
+      if (h == 0) {
+        qcur = qnext;
+        badcur = badnext;
       }
     }
   }
@@ -326,33 +401,42 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   }
 }
 
-template <int L, bool DUMP>
+template <int L, int MODE>
 static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaStream_t s) {
   using C = TcCfg<L>;
   const int nch = (int)std::min<long long>(C::kMaxChunks, a.kmax / kTcChunk);
   if (nch < 1 || !a.tcb) return cudaSuccess;
   const size_t smem = (size_t)nch * C::kChunkBytes + 2 * C::kABytes + C::kMisc;
-  cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, DUMP>,
+  cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  assign_tc_kernel<L, DUMP><<<grid, C::kThreads, smem, s>>>(a, dump);
+  assign_tc_kernel<L, MODE><<<grid, C::kThreads, smem, s>>>(a, dump);
   return cudaGetLastError();
 }
 
 cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s) {
   switch (a.dim) {
-    case 16: return launch_tc_L<16, false>(a, sms, nullptr, s);
-    case 32: return launch_tc_L<32, false>(a, sms, nullptr, s);
-    case 64: return launch_tc_L<64, false>(a, sms, nullptr, s);
+    case 16: return launch_tc_L<16, kTcTop2>(a, sms, nullptr, s);
+    case 32: return launch_tc_L<32, kTcTop2>(a, sms, nullptr, s);
+    case 64: return launch_tc_L<64, kTcTop2>(a, sms, nullptr, s);
+    default: return cudaSuccess;
+  }
+}
+
+cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s) {
+  switch (a.dim) {
+    case 16: return launch_tc_L<16, kTcShortlist>(a, sms, nullptr, s);
+    case 32: return launch_tc_L<32, kTcShortlist>(a, sms, nullptr, s);
+    case 64: return launch_tc_L<64, kTcShortlist>(a, sms, nullptr, s);
     default: return cudaSuccess;
   }
 }
 
 cudaError_t launch_tc_probe(const KernelArgs& a, float* dump, cudaStream_t s) {
   switch (a.dim) {
-    case 16: return launch_tc_L<16, true>(a, 1, dump, s);
-    case 32: return launch_tc_L<32, true>(a, 1, dump, s);
-    case 64: return launch_tc_L<64, true>(a, 1, dump, s);
+    case 16: return launch_tc_L<16, kTcDump>(a, 1, dump, s);
+    case 32: return launch_tc_L<32, kTcDump>(a, 1, dump, s);
+    case 64: return launch_tc_L<64, kTcDump>(a, 1, dump, s);
     default: return cudaErrorInvalidValue;
   }
 }

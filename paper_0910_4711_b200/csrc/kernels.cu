@@ -23,6 +23,7 @@
 #include <cstring>
 
 #include "ptx.h"
+#include "refarith.cuh"
 #include "vqb200_internal.h"
 
 namespace vqb {
@@ -44,20 +45,11 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
   return d;
 }
 
-__device__ __forceinline__ double load_x(const float* x, long long i) { return (double)x[i]; }
-__device__ __forceinline__ double load_x(const double* x, long long i) { return x[i]; }
-
-// Squared distance in the reference's arithmetic (_kernels.py:25-29): for c
-// ascending, diff = x - c; d = d + diff*diff, every op rounded separately
-// (the _rn intrinsics forbid FMA contraction).
-template <typename XT>
-__device__ __forceinline__ double ref_dist(const XT* x, const double* c, int dim) {
-  double d = 0.0;
-  for (int l = 0; l < dim; ++l) {
-    double diff = __dsub_rn(load_x(x, l), c[l]);
-    d = __dadd_rn(d, __dmul_rn(diff, diff));
-  }
-  return d;
+// the row's exact distance to its winner (reference arithmetic; sqrt under
+// euclidean, _kernels.py:33-34) -- every assignment path stores it, so the
+// distortion pass only reads dists
+__device__ __forceinline__ void store_dist(const KernelArgs& a, long long row, double d) {
+  if (a.dists) a.dists[row] = a.st->metric == kEuclidean ? sqrt(d) : d;
 }
 
 __device__ __forceinline__ long long to_fixed(double v, double scale) {
@@ -294,6 +286,8 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
       ok = (m2[r] - m1[r]) > 3.0f * E;
       thr = m1[r] + 3.0f * E;  // shortlist band (shortlist_kernel)
       a.idx[row] = i1[r];
+      if (ok && a.dists)
+        store_dist(a, row, winner_dist<float, L>(a.x32 + row * L, a.cb[a.st->cur] + (long long)i1[r] * L, L));
     }
     const bool flag = valid[r] && !ok;
     const unsigned mask = __ballot_sync(0xffffffffu, flag);
@@ -540,6 +534,7 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
               jj = s_j[k][b];
             }
           a.idx[s_row[b]] = (bb < INFINITY) ? jj : 0;  // nothing < inf -> index 0
+          store_dist(a, s_row[b], bb);
         }
         __syncthreads();
       }
@@ -622,7 +617,10 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
       }
       __syncthreads();
     }
-    if (valid && tl == 0) a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
+    if (valid && tl == 0) {
+      a.idx[row] = (best < INFINITY) ? bj : 0;  // nothing < inf -> index 0
+      store_dist(a, row, best);
+    }
   }
 }
 
@@ -654,10 +652,6 @@ static cudaError_t launch_exact_t(const KernelArgs& a, const XT* X, int use_list
 // Costs ~L FFMA per codevector instead of 3L FP64 ops.
 // ---------------------------------------------------------------------------
 
-template <typename XT, int DIM>
-__device__ __forceinline__ double winner_dist(const XT* __restrict__ x, const double* __restrict__ c,
-                                              int dim);
-
 template <int L>
 struct ShortCfg {
   static constexpr int NT = 256;
@@ -675,6 +669,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
   const long long count = st->flag_count;
   if (count == 0) return;
   const int K = st->size;
+  if (a.tcb && tc_handles(st, K)) return;  // the TC shortlist (assign_tc.cu) runs this pass
   const double* __restrict__ cb = a.cb[st->cur];
   if (count < (long long)gridDim.x * NT) {
     // Few queued rows (e.g. a converged codebook): one warp per row, lanes
@@ -757,7 +752,10 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
           dj = oj;
         }
       }
-      if (lane == 0) a.idx[row] = (d < INFINITY) ? dj : 0;
+      if (lane == 0) {
+        a.idx[row] = (d < INFINITY) ? dj : 0;
+        store_dist(a, row, d);
+      }
     }
     return;
   }
@@ -839,6 +837,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
       }
     }
     a.idx[row] = bj;
+    store_dist(a, row, best);
   }
 }
 
@@ -864,7 +863,8 @@ static cudaError_t launch_shortlist_L(const KernelArgs& a, int sms, cudaStream_t
 
 cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
   if (a.x32 && shortlist_enabled()) {
-    cudaError_t e;
+    cudaError_t e = a.tcb ? launch_shortlist_tc(a, sms, s) : cudaSuccess;
+    if (e != cudaSuccess) return e;
     switch (a.dim) {
       case 16: e = launch_shortlist_L<16>(a, sms, s); break;
       case 32: e = launch_shortlist_L<32>(a, sms, s); break;
@@ -920,13 +920,28 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 constexpr int kSumThreads = 512;
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
 
-__host__ __device__ inline long long sums_chunk_cells(int K, int dim) {
-  // per cell: dim x (u32 lo + i32 hi) + u32 count
-  long long kc = (kEpiSmem - 64) / ((long long)dim * 8 + 4);
-  return kc < K ? kc : K;
-}
 __host__ __device__ inline bool sums_warp_sink(int K, int dim) {
   return (long long)K * (dim * 8 + 4) * (kSumThreads / 32) <= 128 * 1024;
+}
+// Block-table split when K x L does not fit one table: first split the
+// dimensions (each piece still reads every row once in total), then the
+// cells (each cell piece re-reads X).  blockIdx.y = cell piece * ndc + dim piece.
+struct SumsPlan {
+  int dc, ndc;
+  long long kc, nkc;
+};
+__host__ __device__ inline SumsPlan sums_plan(int K, int dim) {
+  SumsPlan p;
+  p.dc = dim;
+  p.kc = K;
+  if (!sums_warp_sink(K, dim)) {
+    while (p.dc > 8 && (long long)K * (p.dc * 8 + 4) > kEpiSmem - 64) p.dc = (p.dc / 2 + 7) / 8 * 8;
+    const long long kc = (kEpiSmem - 64) / ((long long)p.dc * 8 + 4);
+    p.kc = kc < K ? kc : K;
+  }
+  p.ndc = (dim + p.dc - 1) / p.dc;
+  p.nkc = (K + p.kc - 1) / p.kc;
+  return p;
 }
 constexpr int kWStageStride = 20;  // staged row stride (elements), padded against bank conflicts
 
@@ -939,50 +954,35 @@ __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, lo
   if (hi) atomicAdd(hi_word, hi);
 }
 
-template <typename XT, int DIM>
-__device__ __forceinline__ double winner_dist(const XT* __restrict__ x, const double* __restrict__ c,
-                                              int dim) {
-  double d = 0.0;
-  if constexpr (DIM > 0) {
+// One block per 2048-row tile: the tile's distortion partial from the
+// stored per-row distances, in a fixed order (thread t sums rows t, t+256,
+// ... of the tile, then a lane butterfly, then the 8 warps in order) that
+// does not depend on the grid or on the number of GPUs -- sum_inorder's role
+// (_kernels.py:92-98).
+__global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a) {
+  const DevState* st = a.st;
+  if (st->done) return;
+  __shared__ double red[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long t = blockIdx.x;
+  double v[kTdTile / 256];
 #pragma unroll
-    for (int c0 = 0; c0 < DIM; c0 += 16) {
-      double xr[16], cr[16];
-      if constexpr (sizeof(XT) == 4) {
-        const float4* x4 = reinterpret_cast<const float4*>(x + c0);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float4 q = __ldg(x4 + v);
-          xr[4 * v] = q.x;
-          xr[4 * v + 1] = q.y;
-          xr[4 * v + 2] = q.z;
-          xr[4 * v + 3] = q.w;
-        }
-      } else {
-        const double2* x2 = reinterpret_cast<const double2*>(x + c0);
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const double2 q = __ldg(x2 + v);
-          xr[2 * v] = q.x;
-          xr[2 * v + 1] = q.y;
-        }
-      }
-      const double2* c2 = reinterpret_cast<const double2*>(c + c0);
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const double2 q = __ldg(c2 + v);
-        cr[2 * v] = q.x;
-        cr[2 * v + 1] = q.y;
-      }
-#pragma unroll
-      for (int l = 0; l < 16; ++l) {
-        const double diff = __dsub_rn(xr[l], cr[l]);
-        d = __dadd_rn(d, __dmul_rn(diff, diff));
-      }
-    }
-  } else {
-    d = ref_dist(x, c, dim);
+  for (int r = 0; r < kTdTile / 256; ++r) {
+    const long long row = t * kTdTile + (long long)r * 256 + tid;
+    v[r] = row < a.n ? a.dists[row] : 0.0;
   }
-  return d;
+  double s = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTdTile / 256; ++r) s = __dadd_rn(s, v[r]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double acc = 0.0;
+    for (int w = 0; w < 8; ++w) acc = __dadd_rn(acc, red[w]);
+    a.ex.td()[a.tile0 + t] = __double_as_longlong(acc);
+  }
 }
 
 // One block per 2048-row tile: the final winner's distance in the
@@ -1069,13 +1069,17 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   constexpr int kWarps = kSumThreads / 32;
 
   const bool warp_sink = sums_warp_sink(K, dim);
-  const long long kc = warp_sink ? K : sums_chunk_cells(K, dim);
-  const long long nchunks = (K + kc - 1) / kc;
+  const SumsPlan plan = sums_plan(K, dim);
   const int chunk = blockIdx.y;
-  if (chunk >= nchunks) return;
-  const long long c_lo = chunk * kc;
-  const long long c_hi = (c_lo + kc < K) ? c_lo + kc : K;
+  const long long cy = chunk / plan.ndc;
+  const int dy = chunk % plan.ndc;
+  if (cy >= plan.nkc) return;
+  const long long c_lo = cy * plan.kc;
+  const long long c_hi = (c_lo + plan.kc < K) ? c_lo + plan.kc : K;
   const int ncell = (int)(c_hi - c_lo);
+  const int d_lo = dy * plan.dc;
+  const int d_hi = d_lo + plan.dc < dim ? d_lo + plan.dc : dim;
+  const int ndim = d_hi - d_lo;  // == dim on the warp-sink path
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // warp sink: kWarps tables [ncell*dim int64 | ncell u32]
@@ -1085,10 +1089,10 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
   XT* wstage = reinterpret_cast<XT*>(smem_raw + wt_bytes * kWarps);  // [warps][32][kWStageStride]
   unsigned* blo = reinterpret_cast<unsigned*>(smem_raw);
-  int* bhi = reinterpret_cast<int*>(blo + (long long)ncell * dim);
-  unsigned* bcounts = reinterpret_cast<unsigned*>(bhi + (long long)ncell * dim);
+  int* bhi = reinterpret_cast<int*>(blo + (long long)ncell * ndim);
+  unsigned* bcounts = reinterpret_cast<unsigned*>(bhi + (long long)ncell * ndim);
   {
-    const long long zbytes = warp_sink ? wt_bytes * kWarps : (long long)ncell * dim * 8 + ncell * 4;
+    const long long zbytes = warp_sink ? wt_bytes * kWarps : (long long)ncell * ndim * 8 + ncell * 4;
     uint4* z = reinterpret_cast<uint4*>(smem_raw);
     for (long long i = tid; i < (zbytes + 15) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
@@ -1140,8 +1144,8 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
     }
     if (!mine) continue;
     const XT* x = X + row * dim;
-    for (int c0 = 0; c0 < dim; c0 += 16) {
-      const int cw = dim - c0 < 16 ? dim - c0 : 16;
+    for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
+      const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
       XT xr[16];
       if constexpr (DIM > 0 && sizeof(XT) == 4) {
         const float4* x4 = reinterpret_cast<const float4*>(x + c0);
@@ -1167,12 +1171,12 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
 #pragma unroll
       for (int l = 0; l < 16; ++l) {
         if (l < cw) {
-          const long long w = (long long)(c0 + l) * ncell + lc;  // [dim][cell]: spread banks
+          const long long w = (long long)(c0 + l - d_lo) * ncell + lc;  // [dim][cell]: spread banks
           smem_add_i64(blo + w, bhi + w, to_fixed((double)xr[l], scale));
         }
       }
     }
-    atomicAdd(bcounts + lc, 1u);
+    if (dy == 0) atomicAdd(bcounts + lc, 1u);
   }
   __syncthreads();
   // block slab [blockIdx.x][K*dim sums | K counts] (int64)
@@ -1191,12 +1195,13 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
       slab[(long long)K * dim + c_lo + i] = v;
     }
   } else {
-    for (long long i = tid; i < words; i += blockDim.x) {
-      const long long cl = i / dim, l = i % dim;
+    for (long long i = tid; i < (long long)ncell * ndim; i += blockDim.x) {
+      const long long cl = i / ndim, l = i % ndim;
       const long long w = l * ncell + cl;
-      slab[c_lo * dim + i] = (long long)(((unsigned long long)(unsigned)bhi[w] << 32) + blo[w]);
+      slab[(c_lo + cl) * dim + d_lo + l] = (long long)(((unsigned long long)(unsigned)bhi[w] << 32) + blo[w]);
     }
-    for (int i = tid; i < ncell; i += blockDim.x) slab[(long long)K * dim + c_lo + i] = bcounts[i];
+    if (dy == 0)
+      for (int i = tid; i < ncell; i += blockDim.x) slab[(long long)K * dim + c_lo + i] = bcounts[i];
   }
 }
 
@@ -1243,15 +1248,16 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
                                   bool zero_cells, int sms, cudaStream_t s) {
   cudaError_t e;
   if (want_td && !zero_cells) {
+    // every assignment path stored the rows' exact distances (store_dist)
     const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
-    dist_td_kernel<XT, DIM><<<(unsigned)ntiles, 256, 0, s>>>(a, X);
+    td_tiles_kernel<<<(unsigned)ntiles, 256, 0, s>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (!want_sums) return cudaSuccess;
   const long long kmax = zero_cells ? 1 : a.kmax;
-  const long long kc = sums_warp_sink((int)kmax, a.dim) ? kmax : sums_chunk_cells((int)kmax, a.dim);
-  const int chunks = (int)((kmax + kc - 1) / kc);
+  const SumsPlan plan = sums_plan((int)kmax, a.dim);
+  const int chunks = (int)(plan.nkc * plan.ndc);
   const long long rows_per_block = 4LL * kSumThreads;
   int blocks = (int)((a.n + rows_per_block - 1) / rows_per_block);
   if (blocks > sms) blocks = sms;
@@ -1271,6 +1277,7 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
 template <typename XT>
 static cudaError_t launch_epi_t(const KernelArgs& a, const XT* X, bool want_dists, bool want_sums,
                                 bool zero_cells, int sms, cudaStream_t s) {
+
   switch (a.dim) {
     case 16: return launch_epi_dim<XT, 16>(a, X, want_dists, want_sums, zero_cells, sms, s);
     case 32: return launch_epi_dim<XT, 32>(a, X, want_dists, want_sums, zero_cells, sms, s);

@@ -231,6 +231,42 @@ __global__ void __launch_bounds__(256) fmnmx_kernel(float* out, int iters, float
   if (s == 123.456f) out[0] = s;
 }
 
+
+// ALU-pipe probes for the top-2 epilogue: FMNMX (two register operands),
+// integer VIMNMX, and the two interleaved (do they share one pipe?)
+template <int CHAINS, int MODE>
+__global__ void __launch_bounds__(256) minmax_kernel(float* out, const float* in, int iters) {
+  float fa[CHAINS], fb[CHAINS];
+  int ia[CHAINS], ib[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    fa[c] = in[(threadIdx.x + c) & 255];
+    fb[c] = in[(threadIdx.x * 3 + c) & 255];
+    ia[c] = __float_as_int(fa[c]) ^ c;
+    ib[c] = __float_as_int(fb[c]) + c;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) {
+        if (MODE == 0 || MODE == 2) {
+          asm volatile("min.f32 %0, %0, %1;" : "+f"(fa[c]) : "f"(fb[c]));
+          asm volatile("max.f32 %0, %0, %1;" : "+f"(fb[c]) : "f"(fa[c]));
+        }
+        if (MODE == 1 || MODE == 2) {
+          asm volatile("min.s32 %0, %0, %1;" : "+r"(ia[c]) : "r"(ib[c]));
+          asm volatile("max.s32 %0, %0, %1;" : "+r"(ib[c]) : "r"(ia[c]));
+        }
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += fa[c] + fb[c] + (float)(ia[c] + ib[c]);
+  if (s == 123.456f) out[0] = s;
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -292,6 +328,16 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         fmnmx_kernel<8><<<blocks, threads>>>((float*)buf, iters, 0.5f);
         lane_ops = 1.0 * blocks * threads * iters * 16 * 8;
         break;
+      case 8:
+      case 9:
+      case 10: {
+        const int mode = which - 8;
+        if (mode == 0) minmax_kernel<8, 0><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        if (mode == 1) minmax_kernel<8, 1><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        if (mode == 2) minmax_kernel<8, 2><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        lane_ops = (mode == 2 ? 4.0 : 2.0) * blocks * threads * iters * 8 * 8;
+        break;
+      }
       default:  // 5: evals/s of the constant-codebook distance loop (K=512, R=4)
         dist_const_kernel<4><<<blocks, threads>>>((float*)buf, (const float*)inbuf, 512, iters / 100 + 1);
         lane_ops = 1.0 * blocks * threads * 4 * 512 * (iters / 100 + 1);

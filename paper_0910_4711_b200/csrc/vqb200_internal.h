@@ -152,6 +152,7 @@ bool fast_dim_supported(int dim);
 // tensor-core candidate pass (assign_tc.cu)
 constexpr int kTcChunk = 256;  // codewords per MMA N
 constexpr int kTcRows = 128;   // rows per tile (MMA M)
+constexpr int kTcShort = 8;    // shortlist candidates per row before the full FP64 scan
 __host__ __device__ inline long long tc_chunk_elems(int dim) { return (long long)kTcChunk * (2 * dim + 16); }
 int tc_max_size(int dim);      // largest codebook whose operand image fits in smem
 // does assign_tc (rather than assign_fast) run the candidate pass at size K?
@@ -159,6 +160,7 @@ __host__ __device__ __forceinline__ bool tc_handles(const DevState* st, int K) {
   return st->tc_on && !st->tc_bad && K >= st->tc_kmin && K <= st->tc_kmax && K % kTcChunk == 0;
 }
 cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s);
 cudaError_t launch_tc_probe(const KernelArgs& a, float* dump, cudaStream_t s);
 
 // element offset of (row, col) in a K-major, no-swizzle UMMA operand tile with
