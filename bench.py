@@ -12,8 +12,10 @@ N * K.  L2 is flushed (256 MiB write) between timed steps.
 Keys beyond the base contract:
   e2e          same iteration through the C ABI with HOST buffers
                (vqb_lloyd_step_f32: H2D of X + codebook, D2H of cells + codebook)
-  roofline     dominant kernel (assign_fast<16>): algorithmic 3L flops per
-               eval / its CUDA-event time, against the measured FFMA peak
+  roofline     dominant kernel (assign_tc<16>): algorithmic 3L flops per
+               eval / its CUDA-event time, against the measured tensor peak,
+               with the ALU-pipe ceiling of its argmin epilogue and the
+               FP32 FFMA peak (the north star's denominator) beside it
   cpu_baseline oracle/ (C + OpenMP restatement of the reference kernels) on a
                bounded row sample of the same iteration, all host cores
   design       one full cfg2 design (1 -> 1024, 244 passes in the reference):
@@ -154,6 +156,43 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    except (OSError, ValueError):
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks):
+    """Roofline of the dominant kernel, assign_tc<16> (tcgen05 kind::f16 MMA
+    chain into TMEM + top-2 epilogue).  achieved = ALGORITHMIC flops (3L = 48
+    per vector-codeword eval) per launch / its CUDA-event time.
+    The tensor pipe is not what binds it: the argmin epilogue is ~3.5 ALU-pipe
+    ops per value (FMNMX x2, FSETP, half an FMNMX3), and the ALU pipe retires
+    16 lanes/clk/SMSP for two-register operands (profiles/r01_microbench.json
+    fmnmx_2reg), so `limiter` reports that ceiling too."""
+    peaks, src = _measured_peaks()
+    tensor_peak = float(peaks.get("bf16_tflops", 1590.0))
+    mhz = (clocks.summary().get("sm_mhz") if clocks else None) or 1965.0
+    alu_ceiling = 148 * 4 * 16 / 3.5 * mhz * 1e6  # evals/s
+    evals_per_s = evals / (assign_ms * 1e-3)
+    return {
+        "bound": "tensor", "kernel": "assign_tc<16>",
+        "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s", "frac": achieved / tensor_peak,
+        "peak_source": f"{src} bf16_tflops (dense burst; kind::f16 runs at the bf16 rate)",
+        "algorithmic": "3L = 48 flops per vector-codeword eval, N*K evals per launch",
+        "issued_mma_tflops": evals * 2 * (3 * 16 + 16) / (assign_ms * 1e-3) / 1e12,
+        "traffic": traffic.get("bytes_per_launch") if traffic else None,
+        "algorithmic_bytes": n * 16 * 4 + n * 4,
+        "limiter": {"pipe": "ALU (top-2 over TMEM values)", "alu_ops_per_eval": 3.5,
+                    "ceiling_g_evals_per_s": alu_ceiling / 1e9,
+                    "frac": evals_per_s / alu_ceiling},
+        "vs_fp32_ffma_peak": {"peak_tflops": ffma_peak_tflops, "frac": achieved / ffma_peak_tflops,
+                              "peak_source": "measured FFMA microbenchmark (vqb_pipe_microbench)"},
+    }
+
+
 def _load_traffic():
     path = os.path.join(ROOT, "profiles", "assign_traffic.json")
     try:
@@ -229,6 +268,8 @@ def run_b200(args):
         rng = np.random.default_rng(1000 + rank)
         x = synthetic.gaussian_mixture(rng, 1 << 20, 16, 1024, 2.0, 20.0)
     n = x.shape[0]
+    xp_t = torch.from_numpy(x).pin_memory() if rank == 0 else None  # e2e input, pinned early
+    xp = xp_t.numpy() if xp_t is not None else None
     sess = _Session(x, None, device=local_rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
 
@@ -297,7 +338,8 @@ def run_b200(args):
         return 0
     if rank == 0:
         # ---- e2e: the same iteration through the C ABI with host buffers
-        xp = torch.from_numpy(x).pin_memory().numpy()
+        # (xp was pinned at start-up: on these VMs the DMA from freshly pinned
+        # pages runs at ~half rate for about a second, tools/e2e_probe3.py)
         new_cb = np.empty_like(cb)
         cells = np.empty(n, dtype=np.int64)
         td = ctypes.c_double()
@@ -371,14 +413,7 @@ def run_b200(args):
             "segments_ms": {"stage": seg[0], "assign": seg[1], "rerank": seg[2],
                             "epilogue": seg[3], "finalize": seg[4]},
             "rerank_rows_per_step": int(flagged.value),
-            "roofline": {"bound": "fp32_ffma", "kernel": "assign_fast<16>",
-                         "achieved": achieved, "peak": ffma_peak_tflops, "unit": "TFLOP/s",
-                         "frac": achieved / ffma_peak_tflops,
-                         "peak_source": "measured FFMA microbenchmark (vqb_pipe_microbench), "
-                                        "2 FLOP per FMA; nominal 148x128x2x1.965 GHz = 74.45",
-                         "algorithmic": "3L = 48 flops per vector-codeword eval, N*K evals/launch",
-                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
-                         "algorithmic_bytes": n * 16 * 4 + n * 4},
+            "roofline": _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks),
             "e2e": {"value": evals / e2e_s / 1e9, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                     "api": "vqb_lloyd_step_f32 (C ABI), X from pinned host memory",
                     "h2d_bytes_per_step": n * 16 * 4 + K * 16 * 8,
@@ -423,11 +458,11 @@ def run_workload(args):
     L = _lib.lib()
     spec = synthetic.WORKLOADS[name]
     g = _workload_golden(name)
-    clocks = ClockSampler(0).__enter__()
     out = {"impl": "b200", "n_gpus": 1, "data": "synthetic", "steps": args.steps,
            "warmup": args.warmup, "scaling": "weak", "vs_baseline": None}
     if name == "cfg5":
         cb32, q = synthetic.make_encode_case()
+        clocks = ClockSampler(0).__enter__()  # sampled from here on: GPU work only
         cb = cb32.astype(np.float64)
         n, K = q.shape[0], cb.shape[0]
         sess = _Session(q, None)
@@ -473,6 +508,7 @@ def run_workload(args):
         })
     else:
         x = synthetic.make_training(name)
+        clocks = ClockSampler(0).__enter__()  # sampled from here on: GPU work only
         n, dim = x.shape
         conf = vq.LbgConfig(target_size=spec.target_size, epsilon=spec.epsilon, delta=spec.delta)
         sess = _Session(x, None)

@@ -98,6 +98,41 @@ struct vqb_session {
   bool ordered = false;
   bool pending_init = false;
   cudaEvent_t ev_batch[2] = {nullptr, nullptr};
+  // pinned host arena for small per-call transfers (codebooks, centre) so
+  // they never take the synchronous pageable-copy path; reset per call
+  char* pin = nullptr;
+  size_t pin_cap = 0, pin_off = 0;
+  std::vector<cudaEvent_t> piece_ev;  // H2D piece completions (host-buffer paths)
+  // captured batch of training passes (vqb_train); rebuilt when buffers or the
+  // pass shape (fast / ordered) change
+  cudaGraphExec_t graph = nullptr;
+  long long graph_kmax = -1;
+  int graph_key = -1;
+  int batch_graph(int batch);
+  void drop_graph() {
+    if (graph) cudaGraphExecDestroy(graph);
+    graph = nullptr;
+    graph_kmax = -1;
+    graph_key = -1;
+  }
+
+  char* pin_alloc(size_t bytes) {
+    bytes = (bytes + 255) / 256 * 256;
+    if (pin_off + bytes > pin_cap) return nullptr;
+    char* p = pin + pin_off;
+    pin_off += bytes;
+    return p;
+  }
+  int pin_reserve(size_t bytes) {
+    if (bytes <= pin_cap) return VQB_OK;
+    if (stream) cudaStreamSynchronize(stream);
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    pin_cap = 0;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&pin), bytes));
+    pin_cap = bytes;
+    return VQB_OK;
+  }
 
   KernelArgs args() const {
     KernelArgs a{};
@@ -132,6 +167,7 @@ struct vqb_session {
 
   int ensure(long long k) {
     if (k <= kmax && cb[0]) return VQB_OK;
+    drop_graph();
     cudaFree(cb[0]);
     cudaFree(cb[1]);
     cudaFree(w);
@@ -186,6 +222,9 @@ struct vqb_session {
     if (done_host) cudaFreeHost(done_host);
     for (auto& e : ev_batch)
       if (e) cudaEventDestroy(e);
+    for (auto& e : piece_ev) cudaEventDestroy(e);
+    if (pin) cudaFreeHost(pin);
+    drop_graph();
     if (own_stream && stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
   }
@@ -484,6 +523,37 @@ int vqb_step_finalize(vqb_session* s) {
   return VQB_OK;
 }
 
+int vqb_session::batch_graph(int batch) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("VQB_GRAPH");
+    enabled = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  if (!enabled || !own_stream) return VQB_OK;  // a caller's stream: plain launches
+  const int key = (fast ? 1 : 0) | (ordered ? 2 : 0) | (batch << 2);
+  if (graph && graph_kmax == kmax && graph_key == key) return VQB_OK;
+  drop_graph();
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+  int rc = VQB_OK;
+  for (int i = 0; i < batch && rc == VQB_OK; ++i) {
+    rc = vqb_step_local(this);
+    if (rc == VQB_OK) rc = vqb_step_finalize(this);
+  }
+  cudaError_t e = cudaStreamEndCapture(stream, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CK(e);
+  e = cudaGraphInstantiate(&graph, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  graph_kmax = kmax;
+  graph_key = key;
+  return VQB_OK;
+}
+
 int vqb_step_exchange(vqb_session* s, int64_t** device_words, int64_t* count) {
   *device_words = reinterpret_cast<int64_t*>(s->ex);
   *count = s->kmax * s->dim + s->kmax + s->ntiles_global;
@@ -558,12 +628,22 @@ int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
   int b = 0;
   const long long max_passes = (long long)(std::log2((double)cfg->target_size) + 1) *
                                    (cfg->max_iterations_per_level + 1) + 8;
+  // One batch of passes is captured once into a CUDA graph (every kernel reads
+  // its size / mode from the device state, so the same graph serves every
+  // level) and relaunched per batch: one host call instead of ~12 launches
+  // per pass, which is what bounds the small-codebook levels.
+  rc = s->batch_graph(batch);
+  if (rc) return rc;
   while (true) {
-    for (int i = 0; i < batch; ++i) {
-      rc = vqb_step_local(s);
-      if (rc) return rc;
-      rc = vqb_step_finalize(s);
-      if (rc) return rc;
+    if (s->graph) {
+      CK(cudaGraphLaunch(s->graph, s->stream));
+    } else {
+      for (int i = 0; i < batch; ++i) {
+        rc = vqb_step_local(s);
+        if (rc) return rc;
+        rc = vqb_step_finalize(s);
+        if (rc) return rc;
+      }
     }
     issued += batch;
     CK(cudaMemcpyAsync(&s->done_host[b], &s->st->done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
@@ -589,8 +669,14 @@ int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
 static int upload_codebook(vqb_session* s, const double* codebook, long long size) {
   int rc = s->ensure(size);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(s->cb[0], codebook, sizeof(double) * size * s->dim, cudaMemcpyHostToDevice,
-                     s->stream));
+  const size_t bytes = sizeof(double) * size * s->dim;
+  char* p = s->pin_alloc(bytes);
+  if (p) {  // through the pinned arena: an asynchronous DMA, no pageable staging
+    std::memcpy(p, codebook, bytes);
+    CK(cudaMemcpyAsync(s->cb[0], p, bytes, cudaMemcpyHostToDevice, s->stream));
+  } else {
+    CK(cudaMemcpyAsync(s->cb[0], codebook, bytes, cudaMemcpyHostToDevice, s->stream));
+  }
   return VQB_OK;
 }
 
@@ -830,13 +916,19 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
 // centre of the FP32 staging: the codebook's column mean (any centre is
 // exact after the re-rank; a central one keeps the certified band tight)
 int set_centre_from_codebook(vqb_session* s, const double* codebook, long long size) {
+  std::vector<double> acc((size_t)s->dim, 0.0);
+  for (long long k = 0; k < size; ++k)
+    for (long long l = 0; l < s->dim; ++l) acc[(size_t)l] += codebook[k * s->dim + l];
   std::vector<float> mu((size_t)s->dim, 0.f);
-  for (long long l = 0; l < s->dim; ++l) {
-    double acc = 0;
-    for (long long k = 0; k < size; ++k) acc += codebook[k * s->dim + l];
-    mu[(size_t)l] = std::isfinite(acc) ? (float)(acc / (double)size) : 0.f;
+  for (long long l = 0; l < s->dim; ++l)
+    mu[(size_t)l] = std::isfinite(acc[(size_t)l]) ? (float)(acc[(size_t)l] / (double)size) : 0.f;
+  char* p = s->pin_alloc(sizeof(float) * s->dim);
+  if (p) {
+    std::memcpy(p, mu.data(), sizeof(float) * s->dim);
+    CK(cudaMemcpyAsync(s->mu, p, sizeof(float) * s->dim, cudaMemcpyHostToDevice, s->stream));
+  } else {
+    CK(cudaMemcpy(s->mu, mu.data(), sizeof(float) * s->dim, cudaMemcpyHostToDevice));
   }
-  CK(cudaMemcpy(s->mu, mu.data(), sizeof(float) * s->dim, cudaMemcpyHostToDevice));
   s->mu_host = mu;
   return VQB_OK;
 }
@@ -866,6 +958,43 @@ int stream_rows_and_assign(vqb_session* s, const KernelArgs& a, const float* x, 
 }
 }  // namespace
 
+namespace {
+// VQB_TRACE=1: host timestamps + device event times of the host-buffer paths
+struct Trace {
+  bool on = false;
+  std::chrono::steady_clock::time_point t0;
+  std::vector<std::pair<const char*, double>> host;
+  std::vector<std::pair<const char*, cudaEvent_t>> dev;
+  cudaStream_t s = nullptr;
+  explicit Trace(cudaStream_t st) : s(st) {
+    const char* e = getenv("VQB_TRACE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, bool device = true) {
+    if (!on) return;
+    host.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count()});
+    if (device) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      dev.push_back({what, e});
+    }
+  }
+  ~Trace() {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    for (auto& h : host) fprintf(stderr, "[trace] host %-18s %8.3f ms\n", h.first, h.second);
+    for (size_t i = 1; i < dev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, dev[0].second, dev[i].second);
+      fprintf(stderr, "[trace] dev  %-18s %8.3f ms\n", dev[i].first, ms);
+    }
+    for (auto& d : dev) cudaEventDestroy(d.second);
+  }
+};
+}  // namespace
+
 int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* codebook,
                        int64_t size, int device, double* new_codebook, int64_t* cells_out,
                        double* td, int64_t* n_empty) {
@@ -876,24 +1005,79 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   if (rc) return rc;
   CK(cudaSetDevice(device));
   s->fast = fast_dim_supported((int)dim);
+  rc = s->ensure(size);
+  if (rc) return rc;
+  rc = s->pin_reserve(2 * sizeof(double) * size * dim + 4096);
+  if (rc) return rc;
+  s->pin_off = 0;
+  Trace tr(s->stream);
+  tr.mark("start");
+  const size_t row_bytes = sizeof(float) * (size_t)dim;
+  const size_t piece = std::max<size_t>(row_bytes, ((size_t)8 << 20) / row_bytes * row_bytes);
+  const bool pinned_x = host_is_pinned(x);
+  if (tr.on) fprintf(stderr, "[trace] pinned=%d\n", pinned_x ? 1 : 0);
+  // the small uploads (centre, codebook, state) go first: they share the
+  // H2D copy engine with the rows and would otherwise queue behind 64 MB
   rc = set_centre_from_codebook(s, codebook, size);
   if (rc) return rc;
   rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
   rc = set_state(s, kModeLloydStep, size, 0, 0, codebook);
   if (rc) return rc;
+  size_t npieces = 0;
+  if (pinned_x) {
+    // the DMA of every piece starts now; the host work below overlaps it
+    npieces = (row_bytes * n + piece - 1) / piece;
+    while (s->piece_ev.size() < npieces) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->piece_ev.push_back(e);
+    }
+    CK(cudaEventRecord(s->piece_ev[0], s->stream));  // earlier readers of x32 are done
+    CK(cudaStreamWaitEvent(s->copy_stream, s->piece_ev[0], 0));
+    for (size_t i = 0; i < npieces; ++i) {
+      const size_t off = i * piece, len = std::min(piece, row_bytes * n - off);
+      CK(cudaMemcpyAsync(reinterpret_cast<char*>(s->x32) + off, reinterpret_cast<const char*>(x) + off, len,
+                         cudaMemcpyHostToDevice, s->copy_stream));
+      CK(cudaEventRecord(s->piece_ev[i], s->copy_stream));
+    }
+  }
+  tr.mark("copies_enqueued", false);
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
   if (s->fast) CK(launch_prep_codebook(a, s->stream));
+  tr.mark("prepped");
   unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
-  rc = stream_rows_and_assign(s, a, x, n, mb);
-  if (rc) return rc;
+  if (pinned_x) {
+    CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
+    for (size_t i = 0; i < npieces; ++i) {
+      const long long r0 = (long long)(i * piece / row_bytes);
+      const long long r1 = std::min<long long>(n, (long long)((i + 1) * piece / row_bytes));
+      CK(cudaStreamWaitEvent(s->stream, s->piece_ev[i], 0));
+      CK(launch_maxabs(s->x32 + r0 * dim, nullptr, (r1 - r0) * dim, mb, s->sms, s->stream));
+      if (s->fast) {
+        KernelArgs c = a;
+        c.r0 = r0;
+        c.r1 = r1;
+        CK(launch_assign(c, true, s->sms, s->stream));
+      }
+    }
+    if (!s->fast) CK(launch_assign(a, false, s->sms, s->stream));
+  } else {
+    rc = stream_rows_and_assign(s, a, x, n, mb);
+    if (rc) return rc;
+  }
+  tr.mark("assigned");
   CK(launch_set_shift(s->st, mb, s->n_global, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
+  tr.mark("reranked");
   CK(launch_epilogue(a, true, true, false, s->sms, s->stream));  // distortion + cell sums
+  tr.mark("epilogue");
   CK(launch_finalize(a, false, s->stream));
-  CK(cudaMemcpyAsync(new_codebook, s->cb[1], sizeof(double) * size * dim, cudaMemcpyDeviceToHost,
-                     s->stream));
+  tr.mark("finalized");
+  char* cb_pin = s->pin_alloc(sizeof(double) * size * dim);
+  CK(cudaMemcpyAsync(cb_pin ? cb_pin : reinterpret_cast<char*>(new_codebook), s->cb[1],
+                     sizeof(double) * size * dim, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
   if (cells_out) {
     long long* wide = reinterpret_cast<long long*>(s->dists);  // dists are consumed by now
@@ -901,6 +1085,8 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
     CK(download(cells_out, wide, sizeof(long long) * n, s->stream));
   }
   CK(cudaStreamSynchronize(s->stream));
+  tr.mark("synced", false);
+  if (cb_pin) std::memcpy(new_codebook, cb_pin, sizeof(double) * size * dim);
   if (s->st_host->nonfinite) return fail(VQB_USAGE, "training vectors contain non-finite values");
   if (td) *td = s->st_host->total;
   if (n_empty) *n_empty = s->st_host->last_empty;
