@@ -37,19 +37,22 @@ namespace vqb {
 template <int L>
 struct TcCfg {
   static constexpr int kEpiWarps = 8;
-  static constexpr int kThreads = 32 * (1 + kEpiWarps);
+  // warp 0 issues MMAs, warps 1..8 run the epilogue, warp 9 streams codebook
+  // chunks when the codebook does not fit in shared memory
+  static constexpr int kThreads = 32 * (2 + kEpiWarps);
   static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
   static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
   static constexpr size_t kMisc = 8192;
   static constexpr size_t kSmemCap = 227 * 1024;
   static constexpr int kMaxChunks = (int)((kSmemCap - 2 * kABytes - kMisc) / kChunkBytes);
+  static constexpr int kStages = kMaxChunks >= 4 ? 4 : kMaxChunks;  // streaming ring
 };
 
 int tc_max_size(int dim) {
+  // resident codebooks up to kMaxChunks x 256; larger ones stream through the
+  // ring (the shortlist merge stores candidates as 16-bit indices)
   switch (dim) {
-    case 16: return TcCfg<16>::kMaxChunks * kTcChunk;
-    case 32: return TcCfg<32>::kMaxChunks * kTcChunk;
-    case 64: return TcCfg<64>::kMaxChunks * kTcChunk;
+    case 16: case 32: case 64: return 65536;
     default: return 0;
   }
 }
@@ -57,6 +60,8 @@ int tc_max_size(int dim) {
 // misc smem: barriers | tmem slot | merge area (per row-buffer parity)
 struct TcMisc {
   uint64_t b_full;
+  uint64_t bs_full[4];   // streaming ring: chunk landed
+  uint64_t bs_empty[4];  // streaming ring: MMAs reading the stage completed
   uint64_t a_full[2];
   uint64_t a_empty[2];
   uint64_t d_full[2];
@@ -80,7 +85,8 @@ enum { kTcTop2 = 0, kTcShortlist = 1, kTcDump = 2 };
 //   overflow -> flags2.  ~2 ALU ops per value instead of 5.
 // MODE kTcDump: tile 0's raw accumulators -> dump (tests).
 template <int L, int MODE>
-__global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(KernelArgs a, float* dump) {
+__global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(KernelArgs a, float* dump,
+                                                                          int b_cap) {
   using C = TcCfg<L>;
   DevState* st = a.st;
   if (st->done) return;
@@ -94,15 +100,22 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
                                  : ((long long)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   if (my_tiles <= 0) return;
 
+  // resident: the whole operand image sits in smem for the kernel; streaming:
+  // chunks cycle through kStages slots, reloaded for every row tile
+  const bool resident = nch <= b_cap;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sB = smem;
-  unsigned char* sA = smem + (size_t)nch * C::kChunkBytes;
+  unsigned char* sA = smem + (size_t)b_cap * C::kChunkBytes;
   TcMisc* m = reinterpret_cast<TcMisc*>(sA + 2 * C::kABytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
     if (lane == 0) {
       mbar_init(&m->b_full, 1);
+      for (int i = 0; i < C::kStages; ++i) {
+        mbar_init(&m->bs_full[i], 1);
+        mbar_init(&m->bs_empty[i], 1);
+      }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&m->a_full[i], kTcRows);
         mbar_init(&m->a_empty[i], 1);
@@ -132,13 +145,15 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   if (warp == 0) {
     // ===== MMA issuer (one thread) =====
     if (lane == 0) {
-      mbar_arrive_expect_tx(&m->b_full, (uint32_t)(nch * C::kChunkBytes));
-      for (int c = 0; c < nch; ++c)
-        bulk_g2s(sB + c * C::kChunkBytes,
-                 reinterpret_cast<const unsigned char*>(a.tcb) + (size_t)c * C::kChunkBytes,
-                 (uint32_t)C::kChunkBytes, &m->b_full);
-      mbar_wait(&m->b_full, 0);
-      tc_fence_after();
+      if (resident) {
+        mbar_arrive_expect_tx(&m->b_full, (uint32_t)(nch * C::kChunkBytes));
+        for (int c = 0; c < nch; ++c)
+          bulk_g2s(sB + c * C::kChunkBytes,
+                   reinterpret_cast<const unsigned char*>(a.tcb) + (size_t)c * C::kChunkBytes,
+                   (uint32_t)C::kChunkBytes, &m->b_full);
+        mbar_wait(&m->b_full, 0);
+        tc_fence_after();
+      }
       // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N=256, M=128
       const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcChunk >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
       constexpr uint32_t kSboL = L * 16, kSbo16 = 16 * 16;
@@ -153,10 +168,15 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         const uint32_t aOne = aYh + 2 * kTcRows * L * 2;
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = (int)(g & 1);
+          int stage = c;
+          if (!resident) {
+            stage = (int)(g % C::kStages);
+            mbar_wait(&m->bs_full[stage], (uint32_t)((g / C::kStages) & 1));
+          }
           mbar_wait(&m->d_empty[s], (uint32_t)(((g >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(s * kTcChunk);
-          const uint32_t bWh = sBa + c * (uint32_t)C::kChunkBytes;
+          const uint32_t bWh = sBa + stage * (uint32_t)C::kChunkBytes;
           const uint32_t bWl = bWh + kTcChunk * L * 2;
           const uint32_t bN = bWh + 2 * kTcChunk * L * 2;
 #pragma unroll
@@ -171,8 +191,24 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           }
           mma_f16_ss(d, umma_desc(aOne, 128, kSbo16), umma_desc(bN, 128, kSbo16), idesc, 1u);
           mma_commit(&m->d_full[s]);
+          if (!resident) mma_commit(&m->bs_empty[stage]);
         }
         mma_commit(&m->a_empty[b]);
+      }
+    }
+  } else if (warp == 1 + C::kEpiWarps) {
+    // ===== codebook streamer (streaming mode only) =====
+    if (!resident && lane == 0) {
+      long long g = 0;
+      for (long long i = 0; i < my_tiles; ++i) {
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int stage = (int)(g % C::kStages);
+          mbar_wait(&m->bs_empty[stage], (uint32_t)(((g / C::kStages) & 1) ^ 1));
+          mbar_arrive_expect_tx(&m->bs_full[stage], (uint32_t)C::kChunkBytes);
+          bulk_g2s(sB + stage * C::kChunkBytes,
+                   reinterpret_cast<const unsigned char*>(a.tcb) + (size_t)c * C::kChunkBytes,
+                   (uint32_t)C::kChunkBytes, &m->bs_full[stage]);
+        }
       }
     }
   } else {
@@ -404,13 +440,15 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
 template <int L, int MODE>
 static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaStream_t s) {
   using C = TcCfg<L>;
-  const int nch = (int)std::min<long long>(C::kMaxChunks, a.kmax / kTcChunk);
-  if (nch < 1 || !a.tcb) return cudaSuccess;
-  const size_t smem = (size_t)nch * C::kChunkBytes + 2 * C::kABytes + C::kMisc;
+  const long long kchunks = a.kmax / kTcChunk;
+  if (kchunks < 1 || !a.tcb) return cudaSuccess;
+  // B region: the whole image when it fits (resident), else the ring
+  const int b_cap = (int)(kchunks <= C::kMaxChunks ? kchunks : C::kMaxChunks);
+  const size_t smem = (size_t)std::max(b_cap, C::kStages) * C::kChunkBytes + 2 * C::kABytes + C::kMisc;
   cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  assign_tc_kernel<L, MODE><<<grid, C::kThreads, smem, s>>>(a, dump);
+  assign_tc_kernel<L, MODE><<<grid, C::kThreads, smem, s>>>(a, dump, b_cap);
   return cudaGetLastError();
 }
 
