@@ -36,7 +36,12 @@ namespace vqb {
 
 template <int L>
 struct TcCfg {
-  static constexpr int kEpiWarps = 8;
+  // epilogue warps: kParts per TMEM lane quarter, each scanning 256 / kParts
+  // columns of every chunk (more warps hide the argmin chains' latency; L=16
+  // has the registers for 16)
+  static constexpr int kEpiWarps = L == 16 ? 16 : 8;
+  static constexpr int kParts = kEpiWarps / 4;
+  static constexpr int kSpan = kTcChunk / kParts;
   // warp 0 issues MMAs, warps 1..8 run the epilogue, warp 9 streams codebook
   // chunks when the codebook does not fit in shared memory
   static constexpr int kThreads = 32 * (2 + kEpiWarps);
@@ -69,8 +74,8 @@ struct TcMisc {
   uint32_t tmem;
   uint32_t pad;
   union {
-    float top2[2][kTcRows][3];                      // h == 1 half's (m1, m2, i1)
-    unsigned short cand[2][kTcRows][1 + kTcShort];  // h == 1 half's shortlist
+    float top2[3][kTcRows][3];                      // parts 1..3: (m1, m2, i1)
+    unsigned short cand[3][kTcRows][1 + kTcShort];  // parts 1..3: shortlist
   } merge;
 };
 static_assert(sizeof(TcMisc) <= 8192, "misc smem");
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   } else {
     // ===== epilogue warps: row conversion + per-value work over TMEM =====
     const int e = warp - 1;
-    const int h = e >> 2;       // column half of every 256-column chunk
+    const int h = e >> 2;       // column part of every 256-column chunk (0: owns the row)
     const int qd = warp & 3;    // TMEM lane quarter this warp may access
     const int r = qd * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
@@ -282,7 +287,6 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
     if (h == 0) convert(0, 0, qcur, badcur);
     long long g = 0;
     for (long long i = 0; i < my_tiles; ++i) {
-      const int b = (int)(i & 1);
       // top-2 state (kTcTop2) / shortlist state (kTcShortlist)
       float m1 = INFINITY, m2 = INFINITY;
       int i1 = 0;
@@ -298,12 +302,12 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         mbar_wait(&m->d_full[s], (uint32_t)((g >> 1) & 1));
         tc_fence_after();
 #pragma unroll 1
-        for (int q4 = 0; q4 < 4; ++q4) {
+        for (int q4 = 0; q4 < C::kSpan / 32; ++q4) {
           float v[32];
-          const int col = s * kTcChunk + h * 128 + q4 * 32;
+          const int col = s * kTcChunk + h * C::kSpan + q4 * 32;
           tmem_ld32(trow + (uint32_t)col, v);
           tmem_wait_ld();
-          const int jb = c * kTcChunk + h * 128 + q4 * 32;
+          const int jb = c * kTcChunk + h * C::kSpan + q4 * 32;
           if constexpr (MODE == kTcDump) {
 #pragma unroll
             for (int t = 0; t < 32; ++t) dump[(long long)r * K + jb + t] = v[t];
@@ -338,21 +342,28 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         }
       }
       if constexpr (MODE == kTcTop2) {
-        float* mg = &m->merge.top2[b][0][0];
-        if (h == 1) {
-          mg[r * 3 + 0] = m1;
-          mg[r * 3 + 1] = m2;
-          mg[r * 3 + 2] = __int_as_float(i1);
+        if (h > 0) {
+          float* mg = &m->merge.top2[h - 1][r][0];
+          mg[0] = m1;
+          mg[1] = m2;
+          mg[2] = __int_as_float(i1);
         }
         named_bar(1, 32 * C::kEpiWarps);
         if (h == 0) {
-          const float om1 = mg[r * 3 + 0], om2 = mg[r * 3 + 1];
-          const int oi1 = __float_as_int(mg[r * 3 + 2]);
-          m2 = fminf(fmaxf(m1, om1), fminf(m2, om2));
-          if (om1 < m1) {
-            m1 = om1;
-            i1 = oi1;
+#pragma unroll
+          for (int p = 1; p < C::kParts; ++p) {
+            const float* mg = &m->merge.top2[p - 1][r][0];
+            const float om1 = mg[0], om2 = mg[1];
+            const int oi1 = __float_as_int(mg[2]);
+            m2 = fminf(fmaxf(m1, om1), fminf(m2, om2));
+            if (om1 < m1) {
+              m1 = om1;
+              i1 = oi1;
+            }
           }
+        }
+        named_bar(2, 32 * C::kEpiWarps);  // the merge area is free for the next tile
+        if (h == 0) {
           // certification (see the header comment and assign_chunk in kernels.cu)
           bool flag = false;
           float thr = NAN;
@@ -393,14 +404,26 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           }
         }
       } else if constexpr (MODE == kTcShortlist) {
-        unsigned short* mg = &m->merge.cand[b][r][0];
-        if (h == 1) {
+        if (h > 0) {
+          unsigned short* mg = &m->merge.cand[h - 1][r][0];
           mg[0] = (unsigned short)min(nc, kTcShort + 1);
           for (int k = 0; k < kTcShort; ++k) mg[1 + k] = k < nc ? (unsigned short)cand[k] : 0;
         }
         named_bar(1, 32 * C::kEpiWarps);
+        int onc = 0;
         if (h == 0 && valid) {
-          const int onc = mg[0];
+          // gather the other parts' candidates behind this part's own
+#pragma unroll
+          for (int p = 1; p < C::kParts; ++p) {
+            const unsigned short* mg = &m->merge.cand[p - 1][r][0];
+            const int pn = mg[0];
+            for (int k = 0; k < pn && k < kTcShort; ++k)
+              if (nc + onc + k < kTcShort) cand[nc + onc + k] = mg[1 + k];
+            onc += pn;
+          }
+        }
+        named_bar(2, 32 * C::kEpiWarps);  // the merge area is free for the next tile
+        if (h == 0 && valid) {
           if (nc + onc == 0 || nc + onc > kTcShort || badcur) {
             const int pos = atomicAdd(&st->flag2_count, 1);
             a.flags2[pos] = (int)row;
@@ -411,7 +434,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
             double best = INFINITY;
             int bj = 0x7fffffff;
             for (int k = 0; k < nc + onc; ++k) {
-              const int j = k < nc ? cand[k] : (int)mg[1 + k - nc];
+              const int j = cand[k];
               const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)j * L, L);
               if (d < best || (d == best && j < bj)) {
                 best = d;
