@@ -99,6 +99,9 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   if (MODE != kTcDump && !tc_handles(st, K)) return;
   const int nch = K / kTcChunk;
   const long long nitems = MODE == kTcShortlist ? (long long)st->flag_count : a.r1 - a.r0;
+  // a short queue is rescanned faster by shortlist_kernel's warp-per-row mode
+  // (valid for TC-flagged rows: its FP32 error is below the TC band's)
+  if (MODE == kTcShortlist && nitems < kTcShortlistMin) return;
   const long long ntiles = (nitems + kTcRows - 1) / kTcRows;
   const long long my_tiles = MODE == kTcDump
                                  ? 1

@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
   const long long count = st->flag_count;
   if (count == 0) return;
   const int K = st->size;
-  if (a.tcb && tc_handles(st, K)) return;  // the TC shortlist (assign_tc.cu) runs this pass
+  if (a.tcb && tc_handles(st, K) && count >= kTcShortlistMin) return;  // the TC shortlist runs
   const double* __restrict__ cb = a.cb[st->cur];
   if (count < (long long)gridDim.x * NT) {
     // Few queued rows (e.g. a converged codebook): one warp per row, lanes
@@ -1511,19 +1511,60 @@ __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) 
 // after `done` may repeat it harmlessly).
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void stage_row(const KernelArgs& a, long long k, const double* row, int dim) {
-  double n = 0.0;
-  float* w = a.w + k * dim;
-  for (int l = 0; l < dim; ++l) {
+// Warp-cooperative staging of destination row k (lane l holds dimension l,
+// l + 32, ...): FP32 w = -2 c~ and ||c~||^2 for the FP32 pass, the fp16 hi/lo
+// operand image for the TC pass (stage_tc_row's layout).
+__device__ __forceinline__ void stage_row_warp(const KernelArgs& a, long long k, const double* row, int dim,
+                                               int lane) {
+  double part = 0.0;
+  float wv[2] = {0.f, 0.f};
+  for (int l = lane, t = 0; l < dim; l += 32, ++t) {
     const float c = (float)(row[l] - (double)a.mu[l]);
-    n += (double)c * (double)c;
-    w[l] = -2.0f * c;
+    part += (double)c * (double)c;
+    const float w = -2.0f * c;
+    a.w[k * dim + l] = w;
+    if (t < 2) wv[t] = w;
   }
-  a.nrm[k] = (float)n;
-  stage_tc_row(a, k, w, n);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  if (lane == 0) a.nrm[k] = (float)part;
+  if (!a.tcb || dim > 64 || (dim % 16) != 0) return;
+  DevState* st = a.st;
+  unsigned short* img = a.tcb + (k / kTcChunk) * tc_chunk_elems(dim);
+  const int r = (int)(k % kTcChunk);
+  unsigned short* wh = img;
+  unsigned short* wl = img + (long long)kTcChunk * dim;
+  unsigned short* wn = img + 2LL * kTcChunk * dim;
+  const float sw = ldexpf(1.0f, st->tc_ew);
+  bool bad = false;
+  for (int l = lane, t = 0; l < dim; l += 32, ++t) {
+    const float v = wv[t] * sw;
+    const __half h = __float2half_rn(v);
+    const __half lo = __float2half_rn(v - __half2float(h));
+    bad |= !(fabsf(v) <= 60000.0f);
+    wh[tc_off(r, l, dim)] = __half_as_ushort(h);
+    wl[tc_off(r, l, dim)] = __half_as_ushort(lo);
+  }
+  if (lane < 16) {
+    unsigned short val = 0;
+    if (lane < 2) {
+      const double nv = ldexp(part, st->tc_ey + st->tc_ew - st->tc_kn);
+      const __half nh = __double2half(nv);
+      bad |= lane == 0 && !(fabs(nv) <= 60000.0);
+      val = lane == 0 ? __half_as_ushort(nh) : __half_as_ushort(__double2half(nv - (double)__half2float(nh)));
+    }
+    wn[tc_off(r, lane, 16)] = val;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) st->tc_bad = 1;
 }
 
-__global__ void __launch_bounds__(128) apply_kernel(KernelArgs a, int stage) {
+// apply: one warp per source codevector, lanes over dimensions.  Update
+// (update_rows, _kernels.py:59-66: sum / n with the int64 fixed-point sum,
+// empty cells keep the old row), split (core.py:277-281: rows 2i = c + delta,
+// 2i+1 = c - delta) or both, into the other codebook buffer, then the staging
+// of the new rows for the next candidate pass.  Idempotent (speculative
+// passes after `done` may repeat it harmlessly).
+__global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
   const DevState* st = a.st;
   const int act = st->act;
   // zero the distortion tiles (other ranks' slots must be 0 before the next
@@ -1539,36 +1580,29 @@ __global__ void __launch_bounds__(128) apply_kernel(KernelArgs a, int stage) {
   const double inv_scale = ldexp(1.0, -st->fixed_shift);
   const double delta = st->delta;
   const int ordered = st->ordered;
-  double newr[64], r2[64];
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < K;
-       k += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += warps) {
     const long long cnt = (act & kActUpdate) ? a.ex.counts()[k] : 0;
-    for (int c0 = 0; c0 < dim; c0 += 64) {
-      const int cw = dim - c0 < 64 ? dim - c0 : 64;
-      for (int l = 0; l < cw; ++l) {
-        const long long i = k * dim + c0 + l;
-        double v = src[i];
-        if ((act & kActUpdate) && cnt > 0)
-          v = ordered ? a.ord[i] : __ddiv_rn((double)a.ex.sums()[i] * inv_scale, (double)cnt);
-        newr[l] = v;
-      }
+    for (int l = lane; l < dim; l += 32) {
+      const long long i = k * dim + l;
+      double v = src[i];
+      if ((act & kActUpdate) && cnt > 0)
+        v = ordered ? a.ord[i] : __ddiv_rn((double)a.ex.sums()[i] * inv_scale, (double)cnt);
       if (act & kActSplit) {
-        for (int l = 0; l < cw; ++l) {
-          r2[l] = __dsub_rn(newr[l], delta);
-          newr[l] = __dadd_rn(newr[l], delta);
-          dst[(2 * k) * dim + c0 + l] = newr[l];
-          dst[(2 * k + 1) * dim + c0 + l] = r2[l];
-        }
+        dst[(2 * k) * dim + l] = __dadd_rn(v, delta);
+        dst[(2 * k + 1) * dim + l] = __dsub_rn(v, delta);
       } else {
-        for (int l = 0; l < cw; ++l) dst[k * dim + c0 + l] = newr[l];
+        dst[k * dim + l] = v;
       }
     }
     if (stage) {
+      __syncwarp();
       if (act & kActSplit) {
-        stage_row(a, 2 * k, dst + (2 * k) * dim, dim);
-        stage_row(a, 2 * k + 1, dst + (2 * k + 1) * dim, dim);
+        stage_row_warp(a, 2 * k, dst + (2 * k) * dim, dim, lane);
+        stage_row_warp(a, 2 * k + 1, dst + (2 * k + 1) * dim, dim, lane);
       } else {
-        stage_row(a, k, dst + k * dim, dim);
+        stage_row_warp(a, k, dst + k * dim, dim, lane);
       }
     }
   }
@@ -1578,9 +1612,9 @@ cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s) {
   finalize_kernel<<<1, 256, 0, s>>>(a, 1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  int blocks = (int)((a.kmax + 127) / 128);
+  int blocks = (int)((a.kmax + 7) / 8);  // one warp per codevector
   if (blocks < 8) blocks = 8;
-  apply_kernel<<<blocks, 128, 0, s>>>(a, stage ? 1 : 0);
+  apply_kernel<<<blocks, 256, 0, s>>>(a, stage ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -1588,7 +1622,7 @@ cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s
   finalize_kernel<<<1, 256, 0, s>>>(a, 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  apply_kernel<<<8, 128, 0, s>>>(a, stage ? 1 : 0);
+  apply_kernel<<<8, 256, 0, s>>>(a, stage ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -153,6 +153,7 @@ bool fast_dim_supported(int dim);
 constexpr int kTcChunk = 256;  // codewords per MMA N
 constexpr int kTcRows = 128;   // rows per tile (MMA M)
 constexpr int kTcShort = 8;    // shortlist candidates per row before the full FP64 scan
+constexpr int kTcShortlistMin = 0;  // queued rows below which the FP32 shortlist rescans (TC-flagged rows: either works)
 __host__ __device__ inline long long tc_chunk_elems(int dim) { return (long long)kTcChunk * (2 * dim + 16); }
 int tc_max_size(int dim);      // largest codebook whose operand image fits in smem
 // does assign_tc (rather than assign_fast) run the candidate pass at size K?
