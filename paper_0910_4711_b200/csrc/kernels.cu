@@ -1101,7 +1101,49 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const long long n = a.n;
   const long long lo = n * blockIdx.x / gridDim.x;
   const long long hi = n * (blockIdx.x + 1) / gridDim.x;
-  for (long long base = lo; base < hi; base += kSumThreads) {
+  if (!warp_sink) {
+    // Block tables.  Two rows per thread per step, and every load of both
+    // (cells and coordinates) issued before the first atomic: the rows'
+    // HBM/L2 latency overlaps instead of chaining per row.
+    constexpr int R = 2;
+    for (long long base = lo; base < hi; base += (long long)kSumThreads * R) {
+      long long rr[R];
+      bool ok[R];
+      int lc[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        rr[k] = base + tid + (long long)k * kSumThreads;
+        ok[k] = rr[k] < hi;
+      }
+      int cell[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) cell[k] = ok[k] ? (zero_cells ? 0 : a.idx[rr[k]]) : -1;
+      for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
+        const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
+        XT xr[R][16];
+#pragma unroll
+        for (int k = 0; k < R; ++k) load_row16<XT, DIM>(X, rr[k], dim, c0, ok[k], xr[k]);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          lc[k] = (ok[k] && cell[k] >= c_lo && cell[k] < c_hi) ? cell[k] - (int)c_lo : -1;
+          if (lc[k] < 0) continue;
+#pragma unroll
+          for (int l = 0; l < 16; ++l) {
+            if (l < cw) {
+              const long long w = (long long)(c0 + l - d_lo) * ncell + lc[k];  // [dim][cell]: spread banks
+              smem_add_i64(blo + w, bhi + w, to_fixed((double)xr[k][l], scale));
+            }
+          }
+        }
+      }
+      if (dy == 0) {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (ok[k] && cell[k] >= c_lo && cell[k] < c_hi) atomicAdd(bcounts + (cell[k] - (int)c_lo), 1u);
+      }
+    }
+  }
+  for (long long base = lo; base < hi && warp_sink; base += kSumThreads) {
     const long long row = base + tid;
     const bool valid = row < hi;
     const int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;

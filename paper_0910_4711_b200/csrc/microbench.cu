@@ -267,6 +267,34 @@ __global__ void __launch_bounds__(256) minmax_kernel(float* out, const float* in
   if (s == 123.456f) out[0] = s;
 }
 
+
+// shared-memory atomics for the cell tables: non-returning adds (RED) vs
+// returning adds whose result feeds a dependent add (the 64-bit carry idiom)
+template <int MODE>
+__global__ void __launch_bounds__(512) smem_atomic_kernel(float* out, int iters) {
+  __shared__ unsigned tab[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  unsigned h = threadIdx.x * 2654435761u + blockIdx.x;
+  unsigned acc = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      h = h * 1664525u + 1013904223u;
+      const unsigned a = (h >> 8) & 8191u;
+      if (MODE == 0) {
+        atomicAdd(&tab[a], 1u);
+      } else {
+        const unsigned old = atomicAdd(&tab[a], 3u);
+        if (old + 3u < old) atomicAdd(&tab[(a + 1) & 8191u], 1u);
+        acc += old;
+      }
+    }
+  }
+  __syncthreads();
+  if (tab[threadIdx.x] == 0xdeadbeef || acc == 7u) out[0] = 1.f;
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -338,6 +366,12 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         lane_ops = (mode == 2 ? 4.0 : 2.0) * blocks * threads * iters * 8 * 8;
         break;
       }
+      case 11:
+      case 12:
+        if (which == 11) smem_atomic_kernel<0><<<sms, 512>>>((float*)buf, iters);
+        else smem_atomic_kernel<1><<<sms, 512>>>((float*)buf, iters);
+        lane_ops = 1.0 * sms * 512 * iters * 16;
+        break;
       default:  // 5: evals/s of the constant-codebook distance loop (K=512, R=4)
         dist_const_kernel<4><<<blocks, threads>>>((float*)buf, (const float*)inbuf, 512, iters / 100 + 1);
         lane_ops = 1.0 * blocks * threads * 4 * 512 * (iters / 100 + 1);
