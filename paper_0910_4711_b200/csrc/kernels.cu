@@ -1118,6 +1118,23 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
       int cell[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) cell[k] = ok[k] ? (zero_cells ? 0 : a.idx[rr[k]]) : -1;
+      // runs of equal cells among a warp's consecutive rows (image blocks of
+      // a smooth region) are summed in registers first -- a segmented scan
+      // -- so one atomic per run and dimension hits the table instead of one
+      // per row (same-address atomics serialise)
+      bool seg[R];
+      int hd[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        lc[k] = (ok[k] && cell[k] >= c_lo && cell[k] < c_hi) ? cell[k] - (int)c_lo : -1;
+        const int prev = __shfl_up_sync(0xffffffffu, lc[k], 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != lc[k]);
+        seg[k] = heads != 0xffffffffu;
+        const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+        hd[k] = 31 - __clz(heads & upto);  // my run's head lane
+        // lanes that are not their run's tail skip the atomics below
+        if (seg[k] && !(lane == 31 || ((heads & ~upto) & (1u << (lane + 1))))) lc[k] = -2;
+      }
       for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
         const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
         XT xr[R][16];
@@ -1125,7 +1142,23 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
         for (int k = 0; k < R; ++k) load_row16<XT, DIM>(X, rr[k], dim, c0, ok[k], xr[k]);
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          lc[k] = (ok[k] && cell[k] >= c_lo && cell[k] < c_hi) ? cell[k] - (int)c_lo : -1;
+          if (seg[k]) {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) {
+              if (l >= cw) continue;
+              long long v = ok[k] ? to_fixed((double)xr[k][l], scale) : 0;
+#pragma unroll
+              for (int off = 1; off < 32; off <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane - off >= hd[k]) v += t;
+              }
+              if (lc[k] >= 0) {
+                const long long w = (long long)(c0 + l - d_lo) * ncell + lc[k];
+                smem_add_i64(blo + w, bhi + w, v);
+              }
+            }
+            continue;
+          }
           if (lc[k] < 0) continue;
 #pragma unroll
           for (int l = 0; l < 16; ++l) {
@@ -1138,8 +1171,8 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
       }
       if (dy == 0) {
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-          if (ok[k] && cell[k] >= c_lo && cell[k] < c_hi) atomicAdd(bcounts + (cell[k] - (int)c_lo), 1u);
+        for (int k = 0; k < R; ++k)  // run tails count their whole run
+          if (lc[k] >= 0) atomicAdd(bcounts + lc[k], seg[k] ? (unsigned)(lane - hd[k] + 1) : 1u);
       }
     }
   }
@@ -1184,41 +1217,6 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
       }
       continue;
     }
-    if (!mine) continue;
-    const XT* x = X + row * dim;
-    for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
-      const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
-      XT xr[16];
-      if constexpr (DIM > 0 && sizeof(XT) == 4) {
-        const float4* x4 = reinterpret_cast<const float4*>(x + c0);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float4 q = __ldg(x4 + v);
-          xr[4 * v] = q.x;
-          xr[4 * v + 1] = q.y;
-          xr[4 * v + 2] = q.z;
-          xr[4 * v + 3] = q.w;
-        }
-      } else if constexpr (DIM > 0) {
-        const double2* x2 = reinterpret_cast<const double2*>(x + c0);
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const double2 q = __ldg(x2 + v);
-          xr[2 * v] = q.x;
-          xr[2 * v + 1] = q.y;
-        }
-      } else {
-        for (int l = 0; l < 16; ++l) xr[l] = l < cw ? x[c0 + l] : (XT)0;
-      }
-#pragma unroll
-      for (int l = 0; l < 16; ++l) {
-        if (l < cw) {
-          const long long w = (long long)(c0 + l - d_lo) * ncell + lc;  // [dim][cell]: spread banks
-          smem_add_i64(blo + w, bhi + w, to_fixed((double)xr[l], scale));
-        }
-      }
-    }
-    if (dy == 0) atomicAdd(bcounts + lc, 1u);
   }
   __syncthreads();
   // block slab [blockIdx.x][K*dim sums | K counts] (int64)
