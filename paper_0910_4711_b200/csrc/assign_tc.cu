@@ -42,12 +42,13 @@ struct TcCfg {
   static constexpr int kEpiWarps = L == 16 ? 16 : 8;
   static constexpr int kParts = kEpiWarps / 4;
   static constexpr int kSpan = kTcChunk / kParts;
-  // warp 0 issues MMAs, warps 1..8 run the epilogue, warp 9 streams codebook
-  // chunks when the codebook does not fit in shared memory
-  static constexpr int kThreads = 32 * (2 + kEpiWarps);
+  // warp 0 issues MMAs, warps 1..kEpiWarps run the epilogue, the next warp
+  // streams codebook chunks when the codebook does not fit in shared memory,
+  // the last warp converts row tiles into the A operand buffers
+  static constexpr int kThreads = 32 * (3 + kEpiWarps);
   static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
   static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
-  static constexpr size_t kMisc = 8192;
+  static constexpr size_t kMisc = 10240;
   static constexpr size_t kSmemCap = 227 * 1024;
   static constexpr int kMaxChunks = (int)((kSmemCap - 2 * kABytes - kMisc) / kChunkBytes);
   static constexpr int kStages = kMaxChunks >= 4 ? 4 : kMaxChunks;  // streaming ring
@@ -73,12 +74,18 @@ struct TcMisc {
   uint64_t d_empty[2];
   uint32_t tmem;
   uint32_t pad;
+  uint64_t q_full[4];      // converter -> epilogue: qrow[i & 3] written
+  float qrow[4][kTcRows];  // ||y~||^2 per row of tile i (slot i & 3; -1: row out of fp16 range)
   union {
-    float top2[3][kTcRows][3];                      // parts 1..3: (m1, m2, i1)
-    unsigned short cand[3][kTcRows][1 + kTcShort];  // parts 1..3: shortlist
+    float top2[3][kTcRows][3];  // parts 1..3: (m1, m2, i1)
+    struct {
+      unsigned char count[4][kTcRows];  // every part's shortlist size (saturated)
+      double best[4][kTcRows];   // every part's best FP64 distance ...
+      int bestj[4][kTcRows];     // ... and its index
+    } sl;
   } merge;
 };
-static_assert(sizeof(TcMisc) <= 8192, "misc smem");
+static_assert(sizeof(TcMisc) <= 10240, "misc smem");
 
 enum { kTcTop2 = 0, kTcShortlist = 1, kTcDump = 2 };
 
@@ -111,6 +118,9 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   // resident: the whole operand image sits in smem for the kernel; streaming:
   // chunks cycle through kStages slots, reloaded for every row tile
   const bool resident = nch <= b_cap;
+  // row conversion: the converter warp, joined by the streamer warp when the
+  // codebook is resident (the streamer has nothing to stream then)
+  const int conv_warps = resident ? 2 : 1;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sB = smem;
   unsigned char* sA = smem + (size_t)b_cap * C::kChunkBytes;
@@ -124,8 +134,9 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         mbar_init(&m->bs_full[i], 1);
         mbar_init(&m->bs_empty[i], 1);
       }
+      for (int i = 0; i < 4; ++i) mbar_init(&m->q_full[i], 32 * conv_warps);
       for (int i = 0; i < 2; ++i) {
-        mbar_init(&m->a_full[i], kTcRows);
+        mbar_init(&m->a_full[i], 32 * conv_warps);
         mbar_init(&m->a_empty[i], 1);
         mbar_init(&m->d_full[i], 1);
         mbar_init(&m->d_empty[i], 32 * C::kEpiWarps);
@@ -204,6 +215,60 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         mma_commit(&m->a_empty[b]);
       }
     }
+  } else if (warp == 2 + C::kEpiWarps || (resident && warp == 1 + C::kEpiWarps)) {
+    // ===== row converter(s): tile i's rows -> fp16 hi/lo A buffer (i & 1) =====
+    const float sy = ldexpf(1.0f, st->tc_ey);
+    const int cid = warp == 2 + C::kEpiWarps ? 0 : 1;
+    for (long long i = 0; i < my_tiles; ++i) {
+      const int b = (int)(i & 1);
+      mbar_wait(&m->a_empty[b], (uint32_t)(((i >> 1) & 1) ^ 1));  // tile i-2's MMAs are done
+      unsigned short* yh = reinterpret_cast<unsigned short*>(sA + b * C::kABytes);
+      unsigned short* yl = yh + kTcRows * L;
+      const long long t = (long long)blockIdx.x + i * gridDim.x;
+      for (int r = cid * 32 + lane; r < kTcRows; r += 32 * conv_warps) {
+        const long long entry = t * kTcRows + r;
+        const bool valid = entry < nitems;
+        const long long row = MODE == kTcShortlist ? (valid ? (long long)a.flags[entry] : 0) : a.r0 + entry;
+        float qq = 0.f;
+        bool bb = false;
+#pragma unroll
+        for (int c8 = 0; c8 < L / 8; ++c8) {
+          float xv[8];
+          if (valid) {
+            const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
+            const float4 p0 = __ldg(src), p1 = __ldg(src + 1);
+            xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
+            xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) xv[k] = 0.f;
+          }
+          unsigned short hs[8], ls[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float yv = valid ? __fsub_rn(xv[k], a.mu[c8 * 8 + k]) : 0.f;
+            qq = fmaf(yv, yv, qq);
+            const float v = yv * sy;
+            bb |= !(fabsf(v) <= 60000.0f);
+            const __half hi = __float2half_rn(v);
+            const __half lo = __float2half_rn(v - __half2float(hi));
+            hs[k] = __half_as_ushort(hi);
+            ls[k] = __half_as_ushort(lo);
+          }
+          uint4 ph, pl;
+          ph.x = hs[0] | ((uint32_t)hs[1] << 16); ph.y = hs[2] | ((uint32_t)hs[3] << 16);
+          ph.z = hs[4] | ((uint32_t)hs[5] << 16); ph.w = hs[6] | ((uint32_t)hs[7] << 16);
+          pl.x = ls[0] | ((uint32_t)ls[1] << 16); pl.y = ls[2] | ((uint32_t)ls[3] << 16);
+          pl.z = ls[4] | ((uint32_t)ls[5] << 16); pl.w = ls[6] | ((uint32_t)ls[7] << 16);
+          *reinterpret_cast<uint4*>(yh + tc_off(r, c8 * 8, L)) = ph;
+          *reinterpret_cast<uint4*>(yl + tc_off(r, c8 * 8, L)) = pl;
+        }
+        m->qrow[i & 3][r] = bb ? -1.0f : qq;
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&m->a_full[b]);
+      mbar_arrive(&m->q_full[i & 3]);
+    }
   } else if (warp == 1 + C::kEpiWarps) {
     // ===== codebook streamer (streaming mode only) =====
     if (!resident && lane == 0) {
@@ -238,56 +303,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
       return a.r0 + entry;
     };
 
-    // h == 0 threads own row r: convert it into A buffer b, return ||y~||^2
-    auto convert = [&](long long i, int b, float& q, bool& bad) {
-      long long entry;
-      bool valid;
-      const long long row = row_of(i, entry, valid);
-      unsigned short* yh = reinterpret_cast<unsigned short*>(sA + b * C::kABytes);
-      unsigned short* yl = yh + kTcRows * L;
-      float qq = 0.f;
-      bool bb = false;
-#pragma unroll
-      for (int c8 = 0; c8 < L / 8; ++c8) {
-        float xv[8];
-        if (valid) {
-          const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
-          const float4 p0 = __ldg(src), p1 = __ldg(src + 1);
-          xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
-          xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) xv[k] = 0.f;
-        }
-        unsigned short hs[8], ls[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float yv = valid ? __fsub_rn(xv[k], a.mu[c8 * 8 + k]) : 0.f;
-          qq = fmaf(yv, yv, qq);
-          const float v = yv * sy;
-          bb |= !(fabsf(v) <= 60000.0f);
-          const __half hi = __float2half_rn(v);
-          const __half lo = __float2half_rn(v - __half2float(hi));
-          hs[k] = __half_as_ushort(hi);
-          ls[k] = __half_as_ushort(lo);
-        }
-        uint4 ph, pl;
-        ph.x = hs[0] | ((uint32_t)hs[1] << 16); ph.y = hs[2] | ((uint32_t)hs[3] << 16);
-        ph.z = hs[4] | ((uint32_t)hs[5] << 16); ph.w = hs[6] | ((uint32_t)hs[7] << 16);
-        pl.x = ls[0] | ((uint32_t)ls[1] << 16); pl.y = ls[2] | ((uint32_t)ls[3] << 16);
-        pl.z = ls[4] | ((uint32_t)ls[5] << 16); pl.w = ls[6] | ((uint32_t)ls[7] << 16);
-        *reinterpret_cast<uint4*>(yh + tc_off(r, c8 * 8, L)) = ph;
-        *reinterpret_cast<uint4*>(yl + tc_off(r, c8 * 8, L)) = pl;
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&m->a_full[b]);
-      q = qq;
-      bad = bb;
-    };
 
-    float qcur = 0.f, qnext = 0.f;
-    bool badcur = false, badnext = false;
-    if (h == 0) convert(0, 0, qcur, badcur);
     long long g = 0;
     for (long long i = 0; i < my_tiles; ++i) {
       // top-2 state (kTcTop2) / shortlist state (kTcShortlist)
@@ -336,13 +352,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         }
         tc_fence_before();
         mbar_arrive(&m->d_empty[s]);
-        if (c == 0 && h == 0 && i + 1 < my_tiles) {
-          // convert the next tile while this tile's remaining MMAs run
-          const int nb = (int)((i + 1) & 1);
-          const long long use = (i + 1) >> 1;
-          mbar_wait(&m->a_empty[nb], (uint32_t)((use & 1) ^ 1));
-          convert(i + 1, nb, qnext, badnext);
-        }
+
       }
       if constexpr (MODE == kTcTop2) {
         if (h > 0) {
@@ -352,7 +362,12 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           mg[2] = __int_as_float(i1);
         }
         named_bar(1, 32 * C::kEpiWarps);
+        float qcur = 0.f;
+        bool badcur = false;
         if (h == 0) {
+          mbar_wait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1));
+          qcur = m->qrow[i & 3][r];
+          badcur = qcur < 0.f;
 #pragma unroll
           for (int p = 1; p < C::kParts; ++p) {
             const float* mg = &m->merge.top2[p - 1][r][0];
@@ -374,7 +389,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
             const float inv = 1.0f / dscale;
             const float m1v = m1 * inv, m2v = m2 * inv;
             const float u = 5.9604645e-8f, u22 = 2.3841858e-7f;
-            const float yn = sqrtf(qcur);
+            const float yn = sqrtf(fmaxf(qcur, 0.f));
             const float sd = sqrtf(fmaxf(m2v + qcur, 0.f)) * 1.01f + 1.0f;
             const float S = 2.02f * yn + sd;
             // accumulation: each of the 3L/16 + 1 MMAs may lose 2 x 2^-22 of the
@@ -407,38 +422,41 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           }
         }
       } else if constexpr (MODE == kTcShortlist) {
-        if (h > 0) {
-          unsigned short* mg = &m->merge.cand[h - 1][r][0];
-          mg[0] = (unsigned short)min(nc, kTcShort + 1);
-          for (int k = 0; k < kTcShort; ++k) mg[1 + k] = k < nc ? (unsigned short)cand[k] : 0;
-        }
+        // every part evaluates its own candidates in FP64; part 0 decides
+        // overflow from the total and merges the parts' lexicographic minima
+        m->merge.sl.count[h][r] = (unsigned char)min(nc, 255);
         named_bar(1, 32 * C::kEpiWarps);
-        int onc = 0;
-        if (h == 0 && valid) {
-          // gather the other parts' candidates behind this part's own
+        int total = 0;
 #pragma unroll
-          for (int p = 1; p < C::kParts; ++p) {
-            const unsigned short* mg = &m->merge.cand[p - 1][r][0];
-            const int pn = mg[0];
-            for (int k = 0; k < pn && k < kTcShort; ++k)
-              if (nc + onc + k < kTcShort) cand[nc + onc + k] = mg[1 + k];
-            onc += pn;
+        for (int p = 0; p < C::kParts; ++p) total += m->merge.sl.count[p][r];
+        mbar_wait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1));
+        const bool bad = m->qrow[i & 3][r] < 0.f;
+        const bool over = total == 0 || total > kTcShort || bad;
+        double best = INFINITY;
+        int bj = 0x7fffffff;
+        if (valid && !over) {
+          // the reference's arithmetic (_kernels.py:25-29); (d, j) order
+          const double* __restrict__ cb = a.cb[st->cur];
+          for (int k = 0; k < nc; ++k) {
+            const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)cand[k] * L, L);
+            if (d < best || (d == best && cand[k] < bj)) {
+              best = d;
+              bj = cand[k];
+            }
           }
         }
-        named_bar(2, 32 * C::kEpiWarps);  // the merge area is free for the next tile
+        m->merge.sl.best[h][r] = best;
+        m->merge.sl.bestj[h][r] = bj;
+        named_bar(2, 32 * C::kEpiWarps);
         if (h == 0 && valid) {
-          if (nc + onc == 0 || nc + onc > kTcShort || badcur) {
+          if (over) {
             const int pos = atomicAdd(&st->flag2_count, 1);
             a.flags2[pos] = (int)row;
           } else {
-            // FP64 in the reference's arithmetic; lexicographic (d, j) so the
-            // two halves' candidate order does not matter (_kernels.py:23-32)
-            const double* __restrict__ cb = a.cb[st->cur];
-            double best = INFINITY;
-            int bj = 0x7fffffff;
-            for (int k = 0; k < nc + onc; ++k) {
-              const int j = cand[k];
-              const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)j * L, L);
+#pragma unroll
+            for (int p = 1; p < C::kParts; ++p) {
+              const double d = m->merge.sl.best[p][r];
+              const int j = m->merge.sl.bestj[p][r];
               if (d < best || (d == best && j < bj)) {
                 best = d;
                 bj = j;
@@ -448,10 +466,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
             if (a.dists) a.dists[row] = st->metric == kEuclidean ? sqrt(best) : best;
           }
         }
-      }
-      if (h == 0) {
-        qcur = qnext;
-        badcur = badnext;
+        named_bar(3, 32 * C::kEpiWarps);  // the merge area is free for the next tile
       }
     }
   }
