@@ -399,7 +399,10 @@ def run_b200(args):
         cpu_rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=4.0)
         cores, model = _cpu_info()
         c = clocks.summary()
-        launches_per_step = 8 if sess_fast(sess) else 6
+        # per step (vqb_bench_iteration): reset, assign_fast + assign_tc (one
+        # of them exits at once), TC shortlist + FP32 shortlist + exact re-rank,
+        # td_tiles + sums + reduce_partials, finalize + apply
+        launches_per_step = 11 if sess_fast(sess) else 8
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

@@ -446,7 +446,7 @@ static void tc_configure(const vqb_session* s, DevState* h, double my, double mw
   h->tc_ey = ey;
   h->tc_ew = ew;
   h->tc_kn = kn;
-  h->tc_kmin = kTcChunk;
+  h->tc_kmin = 64;
   h->tc_kmax = (int)std::min<long long>(tc_max_size((int)s->dim), s->kmax);
   h->tc_on = h->tc_kmax >= h->tc_kmin ? 1 : 0;
 }

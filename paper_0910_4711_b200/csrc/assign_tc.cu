@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   if (st->done) return;
   const int K = st->size;
   if (MODE != kTcDump && !tc_handles(st, K)) return;
-  const int nch = K / kTcChunk;
+  const int ncols = K < kTcChunk ? K : kTcChunk;  // MMA N (64 / 128 for small codebooks)
+  const int nch = (K + kTcChunk - 1) / kTcChunk;
   const long long nitems = MODE == kTcShortlist ? (long long)st->flag_count : a.r1 - a.r0;
   // a short queue is rescanned faster by shortlist_kernel's warp-per-row mode
   // (valid for TC-flagged rows: its FP32 error is below the TC band's)
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         tc_fence_after();
       }
       // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N=256, M=128
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcChunk >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(ncols >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
       constexpr uint32_t kSboL = L * 16, kSbo16 = 16 * 16;
       const uint32_t sBa = smem_u32(sB), sAa = smem_u32(sA);
       long long g = 0;
@@ -320,20 +321,31 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         const int s = (int)(g & 1);
         mbar_wait(&m->d_full[s], (uint32_t)((g >> 1) & 1));
         tc_fence_after();
+        const int span = ncols / C::kParts;  // this part's columns of the chunk
 #pragma unroll 1
-        for (int q4 = 0; q4 < C::kSpan / 32; ++q4) {
+        for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
           float v[32];
-          const int col = s * kTcChunk + h * C::kSpan + q4 * 32;
-          tmem_ld32(trow + (uint32_t)col, v);
+          const int col = s * kTcChunk + h * span + q4 * 32;
+          if (span >= 32) {
+            tmem_ld32(trow + (uint32_t)col, v);
+          } else {
+            float v16[16];
+            tmem_ld16(trow + (uint32_t)col, v16);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] = v16[t];
+#pragma unroll
+            for (int t = 16; t < 32; ++t) v[t] = INFINITY;  // never a candidate
+          }
           tmem_wait_ld();
-          const int jb = c * kTcChunk + h * C::kSpan + q4 * 32;
+          const int jb = c * kTcChunk + h * span + q4 * 32;
           if constexpr (MODE == kTcDump) {
 #pragma unroll
-            for (int t = 0; t < 32; ++t) dump[(long long)r * K + jb + t] = v[t];
+            for (int t = 0; t < 32; ++t)
+              if (t < span) dump[(long long)r * K + jb + t] = v[t];
           } else if constexpr (MODE == kTcShortlist) {
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
-              if (v[t] <= thr_d) {
+              if (v[t] <= thr_d && jb + t < K) {
                 if (nc < kTcShort) cand[nc] = jb + t;
                 ++nc;
               }
@@ -481,7 +493,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
 template <int L, int MODE>
 static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaStream_t s) {
   using C = TcCfg<L>;
-  const long long kchunks = a.kmax / kTcChunk;
+  const long long kchunks = (a.kmax + kTcChunk - 1) / kTcChunk;
   if (kchunks < 1 || !a.tcb) return cudaSuccess;
   // B region: the whole image when it fits (resident), else the ring
   const int b_cap = (int)(kchunks <= C::kMaxChunks ? kchunks : C::kMaxChunks);

@@ -921,7 +921,10 @@ constexpr int kSumThreads = 512;
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
 
 __host__ __device__ inline bool sums_warp_sink(int K, int dim) {
-  return (long long)K * (dim * 8 + 4) * (kSumThreads / 32) <= 128 * 1024;
+  // 2 half-warp tables per warp + the 32-row staging slices (double rows)
+  const long long tables = ((long long)K * dim * 8 + K * 4 + 15) / 16 * 16 * 2 * (kSumThreads / 32);
+  const long long stage = (long long)(kSumThreads / 32) * 32 * 20 * 8;
+  return tables + stage <= kEpiSmem;
 }
 // Block-table split when K x L does not fit one table: first split the
 // dimensions (each piece still reads every row once in total), then the
@@ -1082,17 +1085,15 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const int ndim = d_hi - d_lo;  // == dim on the warp-sink path
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // warp sink: kWarps tables [ncell*dim int64 | ncell u32]
+  // warp sink: 2 x kWarps half-warp tables [ncell*dim int64 | ncell u32]
   // block sink: lo u32 [dim][ncell] | hi i32 [dim][ncell] | counts u32 [ncell]
   const long long wt_bytes = ((long long)ncell * dim * 8 + ncell * 4 + 15) / 16 * 16;
-  long long* wsums = reinterpret_cast<long long*>(smem_raw + warp * wt_bytes);
-  unsigned* wcounts = reinterpret_cast<unsigned*>(smem_raw + warp * wt_bytes + (long long)ncell * dim * 8);
-  XT* wstage = reinterpret_cast<XT*>(smem_raw + wt_bytes * kWarps);  // [warps][32][kWStageStride]
+  XT* wstage = reinterpret_cast<XT*>(smem_raw + wt_bytes * 2 * kWarps);  // [warps][32][kWStageStride]
   unsigned* blo = reinterpret_cast<unsigned*>(smem_raw);
   int* bhi = reinterpret_cast<int*>(blo + (long long)ncell * ndim);
   unsigned* bcounts = reinterpret_cast<unsigned*>(bhi + (long long)ncell * ndim);
   {
-    const long long zbytes = warp_sink ? wt_bytes * kWarps : (long long)ncell * ndim * 8 + ncell * 4;
+    const long long zbytes = warp_sink ? wt_bytes * 2 * kWarps : (long long)ncell * ndim * 8 + ncell * 4;
     uint4* z = reinterpret_cast<uint4*>(smem_raw);
     for (long long i = tid; i < (zbytes + 15) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
@@ -1176,46 +1177,38 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
       }
     }
   }
-  for (long long base = lo; base < hi && warp_sink; base += kSumThreads) {
-    const long long row = base + tid;
-    const bool valid = row < hi;
-    const int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
-    const bool mine = valid && cell >= c_lo && cell < c_hi;
-    const int lc = mine ? cell - (int)c_lo : -1;
-    if (warp_sink) {
-      // few cells: aggregate the warp's rows per cell.  The warp's 32 rows
-      // are staged 16 dims at a time in its smem slice (coalesced loads,
-      // padded rows), then lanes = dims sum each cell group.
-      const unsigned active = __ballot_sync(0xffffffffu, mine);
-      const unsigned grp = __match_any_sync(0xffffffffu, lc);
-      XT* xs = wstage + warp * 32 * kWStageStride;
+  if (warp_sink) {
+    // Few cells: a private table per half-warp, lanes = dimensions, plain
+    // (non-atomic) read-modify-writes.  A warp loads 32 consecutive rows
+    // (lanes = rows, coalesced), stages them 16 dimensions at a time, then
+    // walks them two at a time: lanes 0-15 take the even row, 16-31 the odd.
+    const int half = lane >> 4, hl = lane & 15;
+    long long* tab = reinterpret_cast<long long*>(smem_raw + (2 * warp + half) * wt_bytes);
+    unsigned* tcount = reinterpret_cast<unsigned*>(smem_raw + (2 * warp + half) * wt_bytes +
+                                                   (long long)ncell * dim * 8);
+    XT* xs = wstage + warp * 32 * kWStageStride;
+    for (long long base = lo + (long long)warp * 32; base < hi; base += (long long)kWarps * 32) {
+      const long long row = base + lane;
+      const bool valid = row < hi;
+      const int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
+      const int lc = (valid && cell >= c_lo && cell < c_hi) ? cell - (int)c_lo : -1;
       for (int c0 = 0; c0 < dim; c0 += 16) {
         XT xr[16];
-        load_row16<XT, DIM>(X, row, dim, c0, mine, xr);
+        load_row16<XT, DIM>(X, row, dim, c0, lc >= 0, xr);
 #pragma unroll
         for (int l = 0; l < 16; ++l) xs[lane * kWStageStride + l] = xr[l];
         __syncwarp();
-        unsigned remaining = active;
-        while (remaining) {
-          const int leader = __ffs(remaining) - 1;
-          const unsigned members = __shfl_sync(0xffffffffu, grp, leader);
-          const int cl = __shfl_sync(0xffffffffu, lc, leader);
-          remaining &= ~members;
-          if (lane < 16 && c0 + lane < dim) {
-            long long acc = 0;
-            unsigned m = members;
-            while (m) {
-              const int b = __ffs(m) - 1;
-              m &= m - 1;
-              acc += to_fixed((double)xs[b * kWStageStride + lane], scale);
-            }
-            wsums[(long long)cl * dim + c0 + lane] += acc;
+#pragma unroll 4
+        for (int p = 0; p < 16; ++p) {
+          const int rr = 2 * p + half;
+          const int cl = __shfl_sync(0xffffffffu, lc, rr);
+          if (cl >= 0) {
+            if (c0 + hl < dim) tab[(long long)cl * dim + c0 + hl] += to_fixed((double)xs[rr * kWStageStride + hl], scale);
+            if (c0 == 0 && hl == 0) tcount[cl] += 1;
           }
-          if (lane == 0 && c0 == 0) wcounts[cl] += __popc(members);
         }
         __syncwarp();
       }
-      continue;
     }
   }
   __syncthreads();
@@ -1225,12 +1218,12 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   if (warp_sink) {
     for (long long i = tid; i < words; i += blockDim.x) {
       long long v = 0;
-      for (int w = 0; w < kWarps; ++w) v += reinterpret_cast<const long long*>(smem_raw + w * wt_bytes)[i];
+      for (int w = 0; w < 2 * kWarps; ++w) v += reinterpret_cast<const long long*>(smem_raw + w * wt_bytes)[i];
       slab[c_lo * dim + i] = v;
     }
     for (int i = tid; i < ncell; i += blockDim.x) {
       long long v = 0;
-      for (int w = 0; w < kWarps; ++w)
+      for (int w = 0; w < 2 * kWarps; ++w)
         v += reinterpret_cast<const unsigned*>(smem_raw + w * wt_bytes + words * 8)[i];
       slab[(long long)K * dim + c_lo + i] = v;
     }

@@ -295,6 +295,31 @@ __global__ void __launch_bounds__(512) smem_atomic_kernel(float* out, int iters)
   if (tab[threadIdx.x] == 0xdeadbeef || acc == 7u) out[0] = 1.f;
 }
 
+
+// HBM read patterns of the epilogue passes over X [N][16] f32 (64 MiB):
+// MODE 0: one row per thread (4 x float4 per lane, rows 64 B apart),
+// MODE 1: fully coalesced float4 stream (consecutive lanes, consecutive 16 B)
+template <int MODE>
+__global__ void __launch_bounds__(256) xread_kernel(const float4* __restrict__ x, long long rows, float* out) {
+  float acc = 0.f;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (MODE == 0) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += stride) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const float4 q = __ldg(x + r * 4 + v);
+        acc += q.x + q.y + q.z + q.w;
+      }
+    }
+  } else {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows * 4; i += stride) {
+      const float4 q = __ldg(x + i);
+      acc += q.x + q.y + q.z + q.w;
+    }
+  }
+  if (acc == 123.456f) out[0] = acc;
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -372,6 +397,19 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         else smem_atomic_kernel<1><<<sms, 512>>>((float*)buf, iters);
         lane_ops = 1.0 * sms * 512 * iters * 16;
         break;
+      case 13:
+      case 14: {
+        static float4* xb = nullptr;
+        const long long rows = 1LL << 20;
+        if (!xb) {
+          cudaMalloc(&xb, rows * 64);
+          cudaMemset(xb, 0, rows * 64);
+        }
+        if (which == 13) xread_kernel<0><<<sms * 8, 256>>>(xb, rows, (float*)buf);
+        else xread_kernel<1><<<sms * 8, 256>>>(xb, rows, (float*)buf);
+        lane_ops = (double)rows * 64;  // bytes
+        break;
+      }
       default:  // 5: evals/s of the constant-codebook distance loop (K=512, R=4)
         dist_const_kernel<4><<<blocks, threads>>>((float*)buf, (const float*)inbuf, 512, iters / 100 + 1);
         lane_ops = 1.0 * blocks * threads * 4 * 512 * (iters / 100 + 1);

@@ -158,7 +158,9 @@ __host__ __device__ inline long long tc_chunk_elems(int dim) { return (long long
 int tc_max_size(int dim);      // largest codebook whose operand image fits in smem
 // does assign_tc (rather than assign_fast) run the candidate pass at size K?
 __host__ __device__ __forceinline__ bool tc_handles(const DevState* st, int K) {
-  return st->tc_on && !st->tc_bad && K >= st->tc_kmin && K <= st->tc_kmax && K % kTcChunk == 0;
+  // one chunk of N = K columns (K = 64, 128) or whole 256-column chunks
+  return st->tc_on && !st->tc_bad && K >= st->tc_kmin && K <= st->tc_kmax &&
+         (K % kTcChunk == 0 || K == 64 || K == 128);
 }
 cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s);
 cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s);

@@ -62,7 +62,8 @@ def test_assign_float32_input_uses_fast_path_and_matches():
     assert np.array_equal(table.cells, cells)
 
 
-@pytest.mark.parametrize("dim,k", [(16, 2), (16, 4096), (32, 300), (64, 512), (64, 1)])
+@pytest.mark.parametrize("dim,k", [(16, 2), (16, 64), (16, 128), (16, 4096), (32, 300), (32, 128),
+                                   (64, 64), (64, 512), (64, 1)])
 def test_assign_shapes_vs_oracle(dim, k):
     rng = np.random.default_rng(dim * 1000 + k)
     x = rng.integers(0, 256, (20000, dim)).astype(np.float32)
