@@ -1,0 +1,82 @@
+"""The sharded design on real hardware: two ranks (gloo, one process each)
+drive DeviceShard sessions on the box's GPU through run_sharded -- the same
+vqb_step_* loop and packed int64 exchange the NCCL path uses on an 8-GPU
+node.  The collectives are host-mediated (gloo copies the device buffers),
+so no kernel of one rank ever waits on the other.  The result must be the
+single-device design, bit for bit, and the reference's schedule."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _data():
+    sys.path.insert(0, ROOT)
+    from paper_0910_4711_b200 import synthetic
+
+    return synthetic.make_training("cfg2", n=(1 << 16) + 3000)  # ragged last shard
+
+
+def _worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    for p in (ROOT, os.path.join(ROOT, "oracle")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    import torch
+    import torch.distributed as dist
+
+    import paper_0910_4711_b200 as vq
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = _data()
+        cb, stats = vq.parallel_lbg_train(vq.TrainingSet(x),
+                                          vq.LbgConfig(target_size=256, epsilon=1e-3, delta=0.01,
+                                                       workers=3))
+        if rank == 0:
+            np.savez(out_path, cb=cb.codevectors,
+                     hist=np.array([(h.codebook_size, h.iteration, h.td, h.empty_cells)
+                                    for h in stats.history]),
+                     total=stats.total, per_worker=np.array(stats.per_worker))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_design_matches_single_device(tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+    import paper_0910_4711_b200 as vq
+
+    out = str(tmp_path / "w2.npz")
+    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    r2 = np.load(out)
+    x = _data()
+    cfg = vq.LbgConfig(target_size=256, epsilon=1e-3, delta=0.01, workers=3)
+    cb1, st1 = vq.parallel_lbg_train(vq.TrainingSet(x), cfg)
+    h1 = np.array([(h.codebook_size, h.iteration, h.td, h.empty_cells) for h in st1.history])
+    # world-size invariance: identical bits
+    assert r2["cb"].tobytes() == cb1.codevectors.tobytes()
+    assert r2["hist"].tobytes() == h1.tobytes()
+    assert float(r2["total"]) == st1.total
+    np.testing.assert_array_equal(r2["per_worker"], np.array(st1.per_worker))
+    # and the reference's pass schedule
+    ref = oracle.lbg_train(x.astype(np.float64), 256, epsilon=1e-3, delta=0.01, workers=3)
+    want = np.array(ref.history, dtype=np.float64)
+    assert np.array_equal(h1[:, [0, 1, 3]], want[:, [0, 1, 3]])
+    np.testing.assert_allclose(cb1.codevectors, ref.codebook, rtol=1e-12, atol=1e-12)
