@@ -49,8 +49,14 @@ struct TcCfg {
   static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
   static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
   static constexpr size_t kMisc = 10240;
+  // contiguous row tiles arrive by one bulk copy into this stage (L <= 32);
+  // the converter then reads shared memory instead of 64 B per lane from HBM
+  // (double-buffered at L = 16, where it costs no resident codebook chunk)
+  static constexpr int kXsStages = L == 16 ? 2 : 1;
+  static constexpr size_t kXsTile = (size_t)kTcRows * L * 4;
+  static constexpr size_t kXsBytes = L <= 32 ? kXsStages * kXsTile : 0;
   static constexpr size_t kSmemCap = 227 * 1024;
-  static constexpr int kMaxChunks = (int)((kSmemCap - 2 * kABytes - kMisc) / kChunkBytes);
+  static constexpr int kMaxChunks = (int)((kSmemCap - 2 * kABytes - kXsBytes - kMisc) / kChunkBytes);
   static constexpr int kStages = kMaxChunks >= 4 ? 4 : kMaxChunks;  // streaming ring
 };
 
@@ -75,9 +81,12 @@ struct TcMisc {
   uint32_t tmem;
   uint32_t pad;
   uint64_t q_full[4];      // converter -> epilogue: qrow[i & 3] written
+  uint64_t xs_full[2];     // row tile landed in X stage i % kXsStages
   float qrow[4][kTcRows];  // ||y~||^2 per row of tile i (slot i & 3; -1: row out of fp16 range)
   union {
-    float top2[3][kTcRows][3];  // parts 1..3: (m1, m2, i1)
+    struct {
+      float part[3][kTcRows][3];  // parts 1..3: (m1, count, i1)
+    } top2;
     struct {
       unsigned char count[4][kTcRows];  // every part's shortlist size (saturated)
       double best[4][kTcRows];   // every part's best FP64 distance ...
@@ -86,6 +95,26 @@ struct TcMisc {
   } merge;
 };
 static_assert(sizeof(TcMisc) <= 10240, "misc smem");
+
+// Certification band E (unscaled distance units) for a row with minimum
+// m1v = ||c||^2 - 2 y.c and q = ||y||^2: fp16 split (4 x 2^-22) and
+// tensor-core accumulation (2 x 2^-22 of the magnitude sum per MMA; measured
+// <= 0.25 of that, tools/tc_probe.py) of S = 2.02|y| + sd, the FP32 terms,
+// and the operands' fp16 quantisation (eyw = sqrt(L) u (2^-ey + 2^-ew)).  sd
+// bounds sqrt(distance) of every value inside the band (m1 + 3E, one
+// fixed-point step).
+template <int L>
+__device__ __forceinline__ float tc_band(float m1v, float q, float yn, float eyw) {
+  constexpr float u = 5.9604645e-8f;
+  constexpr float cacc = (float)(2 * (3 * L / 16 + 1) + 4) * 2.3841858e-7f + 1e-14f;
+  const float d1 = fmaxf(m1v + fmaxf(q, 0.f), 0.f);
+  auto poly = [&](float sd) {
+    const float S = fmaf(2.02f, yn, sd);
+    return fmaf(fmaf(cacc, S, 2.5f * u * sd), S, eyw * S);
+  };
+  const float e0 = poly(fmaf(sqrtf(d1), 1.01f, 1.0f));
+  return poly(fmaf(sqrtf(fmaf(4.0f, e0, d1)), 1.01f, 1.0f));
+}
 
 enum { kTcTop2 = 0, kTcShortlist = 1, kTcDump = 2 };
 
@@ -125,7 +154,8 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sB = smem;
   unsigned char* sA = smem + (size_t)b_cap * C::kChunkBytes;
-  TcMisc* m = reinterpret_cast<TcMisc*>(sA + 2 * C::kABytes);
+  float* sX = reinterpret_cast<float*>(sA + 2 * C::kABytes);
+  TcMisc* m = reinterpret_cast<TcMisc*>(sA + 2 * C::kABytes + C::kXsBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
@@ -136,6 +166,7 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         mbar_init(&m->bs_empty[i], 1);
       }
       for (int i = 0; i < 4; ++i) mbar_init(&m->q_full[i], 32 * conv_warps);
+      for (int i = 0; i < 2; ++i) mbar_init(&m->xs_full[i], 1);
       for (int i = 0; i < 2; ++i) {
         mbar_init(&m->a_full[i], 32 * conv_warps);
         mbar_init(&m->a_empty[i], 1);
@@ -220,9 +251,23 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
     // ===== row converter(s): tile i's rows -> fp16 hi/lo A buffer (i & 1) =====
     const float sy = ldexpf(1.0f, st->tc_ey);
     const int cid = warp == 2 + C::kEpiWarps ? 0 : 1;
+    constexpr bool kUseXs = MODE != kTcShortlist && C::kXsBytes > 0;
+    constexpr int kXs = C::kXsStages;
+    auto issue_xs = [&](long long i) {  // bulk copy of tile i's contiguous rows
+      const long long t = (long long)blockIdx.x + i * gridDim.x;
+      const long long rows = min((long long)kTcRows, nitems - t * kTcRows);
+      const uint32_t bytes = (uint32_t)(rows * L * 4);
+      const int xb = (int)(i % kXs);
+      mbar_arrive_expect_tx(&m->xs_full[xb], bytes);
+      bulk_g2s(sX + xb * (kTcRows * L), a.x32 + (a.r0 + t * kTcRows) * L, bytes, &m->xs_full[xb]);
+    };
+    if (kUseXs && cid == 0 && lane == 0)
+      for (int j = 0; j < kXs && j < my_tiles; ++j) issue_xs(j);
     for (long long i = 0; i < my_tiles; ++i) {
       const int b = (int)(i & 1);
       mbar_wait(&m->a_empty[b], (uint32_t)(((i >> 1) & 1) ^ 1));  // tile i-2's MMAs are done
+      const float* xs = sX + (int)(i % kXs) * (kTcRows * L);
+      if (kUseXs) mbar_wait(&m->xs_full[i % kXs], (uint32_t)((i / kXs) & 1));
       unsigned short* yh = reinterpret_cast<unsigned short*>(sA + b * C::kABytes);
       unsigned short* yl = yh + kTcRows * L;
       const long long t = (long long)blockIdx.x + i * gridDim.x;
@@ -236,8 +281,9 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         for (int c8 = 0; c8 < L / 8; ++c8) {
           float xv[8];
           if (valid) {
-            const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
-            const float4 p0 = __ldg(src), p1 = __ldg(src + 1);
+            const float4* src = kUseXs ? reinterpret_cast<const float4*>(xs + r * L + c8 * 8)
+                                       : reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
+            const float4 p0 = kUseXs ? src[0] : __ldg(src), p1 = kUseXs ? src[1] : __ldg(src + 1);
             xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
             xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
           } else {
@@ -265,6 +311,11 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           *reinterpret_cast<uint4*>(yl + tc_off(r, c8 * 8, L)) = pl;
         }
         m->qrow[i & 3][r] = bb ? -1.0f : qq;
+      }
+      if (kUseXs) {
+        // every converter lane is done with the stage: fetch the next tile
+        if (conv_warps > 1) named_bar(4, 32 * conv_warps); else __syncwarp();
+        if (cid == 0 && lane == 0 && i + kXs < my_tiles) issue_xs(i + kXs);
       }
       fence_proxy_async_smem();
       mbar_arrive(&m->a_full[b]);
@@ -305,11 +356,16 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
     };
 
 
+    const float inv = 1.0f / dscale;
+    const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
+
     long long g = 0;
     for (long long i = 0; i < my_tiles; ++i) {
-      // top-2 state (kTcTop2) / shortlist state (kTcShortlist)
-      float m1 = INFINITY, m2 = INFINITY;
-      int i1 = 0;
+      // kTcTop2: running minimum m1, the number of values inside the band
+      // above it (cnt) and the index of the last one (i1); kTcShortlist:
+      // candidate list
+      float m1 = INFINITY;
+      int i1 = 0, cnt = 0;
       int nc = 0;
       int cand[kTcShort];
       float thr_d = -INFINITY;
@@ -317,14 +373,19 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
       bool valid;
       const long long row = row_of(i, entry, valid);
       if (MODE == kTcShortlist && valid) thr_d = a.flag_thr[entry] * dscale;  // NaN stays NaN -> overflow
+      float qcur = 0.f, yn = 0.f;
+      if constexpr (MODE == kTcTop2) {
+        mbar_wait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1));
+        qcur = m->qrow[i & 3][r];
+        yn = sqrtf(fmaxf(qcur, 0.f));
+      }
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = (int)(g & 1);
         mbar_wait(&m->d_full[s], (uint32_t)((g >> 1) & 1));
         tc_fence_after();
         const int span = ncols / C::kParts;  // this part's columns of the chunk
-#pragma unroll 1
-        for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
-          float v[32];
+        // 32 accumulator columns of this part (padded with +inf below 32)
+        auto load = [&](int q4, float (&v)[32]) {
           const int col = s * kTcChunk + h * span + q4 * 32;
           if (span >= 32) {
             tmem_ld32(trow + (uint32_t)col, v);
@@ -337,58 +398,92 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
             for (int t = 16; t < 32; ++t) v[t] = INFINITY;  // never a candidate
           }
           tmem_wait_ld();
-          const int jb = c * kTcChunk + h * span + q4 * 32;
-          if constexpr (MODE == kTcDump) {
+        };
+        if constexpr (MODE == kTcTop2) {
+          // two reads of the chunk: its minimum (3-input FMNMX, 0.5 op per
+          // value), then one compare per value against the band above the
+          // running minimum (count + index packed in one predicated add)
+          float cm = INFINITY;
+#pragma unroll 1
+          for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
+            float v[32];
+            load(q4, v);
 #pragma unroll
-            for (int t = 0; t < 32; ++t)
-              if (t < span) dump[(long long)r * K + jb + t] = v[t];
-          } else if constexpr (MODE == kTcShortlist) {
+            for (int t = 0; t < 32; t += 2) cm = fminf(cm, fminf(v[t], v[t + 1]));
+          }
+          const float mnew = fminf(m1, cm);
+          const float thr = fmaf(3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw), dscale, mnew);
+          // a new minimum far below the old one: every earlier value is >= the
+          // old minimum > thr, so the count restarts (otherwise it is kept,
+          // which can only over-count)
+          if (cm < m1 && m1 > thr) cnt = 0;
+          m1 = mnew;
+#pragma unroll 1
+          for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
+            float v[32];
+            load(q4, v);
+            unsigned acc2[2] = {0u, 0u};  // two chains
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              if (v[t] <= thr_d && jb + t < K) {
-                if (nc < kTcShort) cand[nc] = jb + t;
-                ++nc;
-              }
+            for (int t = 0; t < 32; ++t)  // FSETP + predicated IADD
+              asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
+                  : "+r"(acc2[t & 1])
+                  : "f"(v[t]), "f"(thr), "r"(0x10000u + (unsigned)t));
+            const unsigned acc = acc2[0] + acc2[1];
+            if (acc) {
+              cnt += (int)(acc >> 16);
+              i1 = c * kTcChunk + h * span + q4 * 32 + (int)(acc & 0xffffu);  // exact when alone
             }
-          } else {
+          }
+        } else {
+#pragma unroll 1
+          for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
+            float v[32];
+            load(q4, v);
+            const int jb = c * kTcChunk + h * span + q4 * 32;
+            if constexpr (MODE == kTcDump) {
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              const float x = v[t];
-              const float n2 = fminf(m2, fmaxf(m1, x));
-              const bool p = x < m1;
-              m1 = fminf(m1, x);
-              i1 = p ? jb + t : i1;
-              m2 = n2;
+              for (int t = 0; t < 32; ++t)
+                if (t < span) dump[(long long)r * K + jb + t] = v[t];
+            } else {
+#pragma unroll
+              for (int t = 0; t < 32; ++t) {
+                if (v[t] <= thr_d && jb + t < K) {
+                  if (nc < kTcShort) cand[nc] = jb + t;
+                  ++nc;
+                }
+              }
             }
           }
         }
         tc_fence_before();
         mbar_arrive(&m->d_empty[s]);
-
       }
       if constexpr (MODE == kTcTop2) {
         if (h > 0) {
-          float* mg = &m->merge.top2[h - 1][r][0];
+          float* mg = &m->merge.top2.part[h - 1][r][0];
           mg[0] = m1;
-          mg[1] = m2;
+          mg[1] = __int_as_float(cnt);
           mg[2] = __int_as_float(i1);
         }
         named_bar(1, 32 * C::kEpiWarps);
-        float qcur = 0.f;
-        bool badcur = false;
+        const bool badcur = qcur < 0.f;
+        float E = 0.f, M1 = m1;
+        int total = 0;
         if (h == 0) {
-          mbar_wait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1));
-          qcur = m->qrow[i & 3][r];
-          badcur = qcur < 0.f;
+          // merge the parts: the band above the row's minimum; a part whose
+          // minimum lies above it has nothing inside
+#pragma unroll
+          for (int p = 1; p < C::kParts; ++p) M1 = fminf(M1, m->merge.top2.part[p - 1][r][0]);
+          E = tc_band<L>(M1 * inv, qcur, yn, eyw);
+          const float thr_s = fmaf(3.0f * E, dscale, M1);
+          if (m1 <= thr_s) total = cnt;
 #pragma unroll
           for (int p = 1; p < C::kParts; ++p) {
-            const float* mg = &m->merge.top2[p - 1][r][0];
-            const float om1 = mg[0], om2 = mg[1];
-            const int oi1 = __float_as_int(mg[2]);
-            m2 = fminf(fmaxf(m1, om1), fminf(m2, om2));
-            if (om1 < m1) {
-              m1 = om1;
-              i1 = oi1;
+            const float* mg = &m->merge.top2.part[p - 1][r][0];
+            const int pc = __float_as_int(mg[1]);
+            if (mg[0] <= thr_s && pc > 0) {
+              total += pc;
+              i1 = __float_as_int(mg[2]);
             }
           }
         }
@@ -398,20 +493,9 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
           bool flag = false;
           float thr = NAN;
           if (valid) {
-            const float inv = 1.0f / dscale;
-            const float m1v = m1 * inv, m2v = m2 * inv;
-            const float u = 5.9604645e-8f, u22 = 2.3841858e-7f;
-            const float yn = sqrtf(fmaxf(qcur, 0.f));
-            const float sd = sqrtf(fmaxf(m2v + qcur, 0.f)) * 1.01f + 1.0f;
-            const float S = 2.02f * yn + sd;
-            // accumulation: each of the 3L/16 + 1 MMAs may lose 2 x 2^-22 of the
-            // magnitude sum (measured: <= 0.25 of that, tools/tc_probe.py);
-            // split: 4 x 2^-22; the rest as in the FP32 pass
-            const float E = (float)(2 * (3 * L / 16 + 1) + 4) * u22 * S * S + 2.5f * u * sd * S + 1e-14f * S * S +
-                            sqrtf((float)L) * S * u *
-                                (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
-            flag = badcur || !((m2v - m1v) > 3.0f * E);
-            thr = m1v + 3.0f * E;
+            // certified iff the minimum is the only value within 3E of it
+            flag = badcur || total != 1;
+            thr = M1 * inv + 3.0f * E;
             a.idx[row] = i1;
             if (!flag && a.dists) {
               // exact FP64 distance to the certified winner (_kernels.py:25-34);
@@ -497,7 +581,8 @@ static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaS
   if (kchunks < 1 || !a.tcb) return cudaSuccess;
   // B region: the whole image when it fits (resident), else the ring
   const int b_cap = (int)(kchunks <= C::kMaxChunks ? kchunks : C::kMaxChunks);
-  const size_t smem = (size_t)std::max(b_cap, C::kStages) * C::kChunkBytes + 2 * C::kABytes + C::kMisc;
+  const size_t smem =
+      (size_t)std::max(b_cap, C::kStages) * C::kChunkBytes + 2 * C::kABytes + C::kXsBytes + C::kMisc;
   cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
