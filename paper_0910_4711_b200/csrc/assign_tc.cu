@@ -45,10 +45,17 @@ struct TcCfg {
   // warp 0 issues MMAs, warps 1..kEpiWarps run the epilogue, the next warp
   // streams codebook chunks when the codebook does not fit in shared memory,
   // the last warp converts row tiles into the A operand buffers
-  static constexpr int kThreads = 32 * (3 + kEpiWarps);
+  // and (L <= 32, kTcTop2) 4 certification warps, one per 32-row quarter,
+  // finish each tile's rows off the epilogue's critical path; at L = 64 the
+  // MMAs bind, registers are scarcer, and epilogue part 0 certifies
+  static constexpr bool kCertWarps = L <= 32;
+  static constexpr int kCertWarp0 = 3 + kEpiWarps;
+  static constexpr int threads(int mode) {
+    return 32 * (mode == 0 && kCertWarps ? 7 + kEpiWarps : 3 + kEpiWarps);
+  }
   static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
   static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
-  static constexpr size_t kMisc = 10240;
+  static constexpr size_t kMisc = kParts == 4 ? 16384 : 10240;
   // contiguous row tiles arrive by one bulk copy into this stage (L <= 32);
   // the converter then reads shared memory instead of 64 B per lane from HBM
   // (double-buffered at L = 16, where it costs no resident codebook chunk)
@@ -69,7 +76,8 @@ int tc_max_size(int dim) {
   }
 }
 
-// misc smem: barriers | tmem slot | merge area (per row-buffer parity)
+// misc smem: barriers | tmem slot | merge areas
+template <int P>
 struct TcMisc {
   uint64_t b_full;
   uint64_t bs_full[4];   // streaming ring: chunk landed
@@ -78,15 +86,20 @@ struct TcMisc {
   uint64_t a_empty[2];
   uint64_t d_full[2];
   uint64_t d_empty[2];
+  uint64_t res_full[2];   // epilogue -> certification: tile results in res[i & 1]
+  uint64_t res_empty[2];  // certification has read res[i & 1]
   uint32_t tmem;
   uint32_t pad;
   uint64_t q_full[4];      // converter -> epilogue: qrow[i & 3] written
   uint64_t xs_full[2];     // row tile landed in X stage i % kXsStages
   float qrow[4][kTcRows];  // ||y~||^2 per row of tile i (slot i & 3; -1: row out of fp16 range)
   union {
-    struct {
-      float part[3][kTcRows][3];  // parts 1..3: (m1, count, i1)
-    } top2;
+    struct {               // kTcTop2: every part's (minimum, band count, index) per row
+      float m1[P][kTcRows];
+      int cnt[P][kTcRows];
+      int i1[P][kTcRows];
+      float q[kTcRows];
+    } res[2];
     struct {
       unsigned char count[4][kTcRows];  // every part's shortlist size (saturated)
       double best[4][kTcRows];   // every part's best FP64 distance ...
@@ -94,7 +107,6 @@ struct TcMisc {
     } sl;
   } merge;
 };
-static_assert(sizeof(TcMisc) <= 10240, "misc smem");
 
 // Certification band E (unscaled distance units) for a row with minimum
 // m1v = ||c||^2 - 2 y.c and q = ||y||^2: fp16 split (4 x 2^-22) and
@@ -126,7 +138,7 @@ enum { kTcTop2 = 0, kTcShortlist = 1, kTcDump = 2 };
 //   overflow -> flags2.  ~2 ALU ops per value instead of 5.
 // MODE kTcDump: tile 0's raw accumulators -> dump (tests).
 template <int L, int MODE>
-__global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(KernelArgs a, float* dump,
+__global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(KernelArgs a, float* dump,
                                                                           int b_cap) {
   using C = TcCfg<L>;
   DevState* st = a.st;
@@ -155,7 +167,9 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   unsigned char* sB = smem;
   unsigned char* sA = smem + (size_t)b_cap * C::kChunkBytes;
   float* sX = reinterpret_cast<float*>(sA + 2 * C::kABytes);
-  TcMisc* m = reinterpret_cast<TcMisc*>(sA + 2 * C::kABytes + C::kXsBytes);
+  using Misc = TcMisc<C::kParts>;
+  static_assert(sizeof(Misc) <= C::kMisc, "misc smem");
+  Misc* m = reinterpret_cast<Misc*>(sA + 2 * C::kABytes + C::kXsBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
@@ -172,6 +186,8 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         mbar_init(&m->a_empty[i], 1);
         mbar_init(&m->d_full[i], 1);
         mbar_init(&m->d_empty[i], 32 * C::kEpiWarps);
+        mbar_init(&m->res_full[i], 32 * C::kEpiWarps);
+        mbar_init(&m->res_empty[i], 32 * 4);
       }
       mbar_fence_init();
     }
@@ -192,6 +208,73 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = m->tmem;
+
+  // certification of tile i's row r from the parts' results in res[i & 1]
+  // (kTcTop2; run by a certification warp, or by epilogue part 0 at L = 64)
+  auto certify = [&](long long i, int r) {
+    const float dscale = ldexpf(1.0f, st->tc_ey + st->tc_ew);
+    const float inv = 1.0f / dscale;
+    const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
+    const int rb = (int)(i & 1);
+    mbar_wait(&m->res_full[rb], (uint32_t)((i >> 1) & 1));
+    float pm[C::kParts];
+    int pc[C::kParts], pi[C::kParts];
+#pragma unroll
+    for (int p = 0; p < C::kParts; ++p) {
+      pm[p] = m->merge.res[rb].m1[p][r];
+      pc[p] = m->merge.res[rb].cnt[p][r];
+      pi[p] = m->merge.res[rb].i1[p][r];
+    }
+    const float qcur = m->merge.res[rb].q[r];
+    mbar_arrive(&m->res_empty[rb]);
+    const long long t = (long long)blockIdx.x + i * gridDim.x;
+    const long long entry = t * kTcRows + r;
+    const bool valid = entry < nitems;
+    const long long row = a.r0 + entry;
+    // merge the parts: the band above the row's minimum; a part whose
+    // minimum lies above it has nothing inside
+    float M1 = pm[0];
+#pragma unroll
+    for (int p = 1; p < C::kParts; ++p) M1 = fminf(M1, pm[p]);
+    const float E = tc_band<L>(M1 * inv, qcur, sqrtf(fmaxf(qcur, 0.f)), eyw);
+    const float thr_s = fmaf(3.0f * E, dscale, M1);
+    int total = 0, i1 = 0;
+#pragma unroll
+    for (int p = 0; p < C::kParts; ++p) {
+      if (pm[p] <= thr_s && pc[p] > 0) {
+        total += pc[p];
+        i1 = pi[p];
+      }
+    }
+    // certified iff the minimum is the only value within 3E of it (see the
+    // header comment and assign_chunk in kernels.cu)
+    bool flag = false;
+    float thr = NAN;
+    if (valid) {
+      flag = qcur < 0.f || total != 1;
+      thr = M1 * inv + 3.0f * E;
+      a.idx[row] = i1;
+      if (!flag && a.dists) {
+        // exact FP64 distance to the certified winner (_kernels.py:25-34);
+        // the row is L2-resident from its conversion
+        const double d = winner_dist<float, L>(a.x32 + row * L, a.cb[st->cur] + (long long)i1 * L, L);
+        a.dists[row] = st->metric == kEuclidean ? sqrt(d) : d;
+      }
+    }
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    if (mask) {
+      int base = 0;
+      const int leader = __ffs(mask) - 1;
+      if (lane == leader) base = atomicAdd(&st->flag_count, __popc(mask));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (flag) {
+        const int pos = base + __popc(mask & ((1u << lane) - 1u));
+        a.flags[pos] = (int)row;
+        a.flag_thr[pos] = thr;
+      }
+    }
+  };
 
   if (warp == 0) {
     // ===== MMA issuer (one thread) =====
@@ -336,6 +419,10 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         }
       }
     }
+  } else if (warp >= C::kCertWarp0) {
+    // ===== certification warps (kTcTop2): lane = row of the tile quarter =====
+    if constexpr (MODE == kTcTop2)
+      for (long long i = 0; i < my_tiles; ++i) certify(i, (warp - C::kCertWarp0) * 32 + lane);
   } else {
     // ===== epilogue warps: row conversion + per-value work over TMEM =====
     const int e = warp - 1;
@@ -459,64 +546,15 @@ __global__ void __launch_bounds__(TcCfg<L>::kThreads, 1) assign_tc_kernel(Kernel
         mbar_arrive(&m->d_empty[s]);
       }
       if constexpr (MODE == kTcTop2) {
-        if (h > 0) {
-          float* mg = &m->merge.top2.part[h - 1][r][0];
-          mg[0] = m1;
-          mg[1] = __int_as_float(cnt);
-          mg[2] = __int_as_float(i1);
-        }
-        named_bar(1, 32 * C::kEpiWarps);
-        const bool badcur = qcur < 0.f;
-        float E = 0.f, M1 = m1;
-        int total = 0;
-        if (h == 0) {
-          // merge the parts: the band above the row's minimum; a part whose
-          // minimum lies above it has nothing inside
-#pragma unroll
-          for (int p = 1; p < C::kParts; ++p) M1 = fminf(M1, m->merge.top2.part[p - 1][r][0]);
-          E = tc_band<L>(M1 * inv, qcur, yn, eyw);
-          const float thr_s = fmaf(3.0f * E, dscale, M1);
-          if (m1 <= thr_s) total = cnt;
-#pragma unroll
-          for (int p = 1; p < C::kParts; ++p) {
-            const float* mg = &m->merge.top2.part[p - 1][r][0];
-            const int pc = __float_as_int(mg[1]);
-            if (mg[0] <= thr_s && pc > 0) {
-              total += pc;
-              i1 = __float_as_int(mg[2]);
-            }
-          }
-        }
-        named_bar(2, 32 * C::kEpiWarps);  // the merge area is free for the next tile
-        if (h == 0) {
-          // certification (see the header comment and assign_chunk in kernels.cu)
-          bool flag = false;
-          float thr = NAN;
-          if (valid) {
-            // certified iff the minimum is the only value within 3E of it
-            flag = badcur || total != 1;
-            thr = M1 * inv + 3.0f * E;
-            a.idx[row] = i1;
-            if (!flag && a.dists) {
-              // exact FP64 distance to the certified winner (_kernels.py:25-34);
-              // the row is L2-resident from its conversion one tile ago
-              const double d = winner_dist<float, L>(a.x32 + row * L, a.cb[st->cur] + (long long)i1 * L, L);
-              a.dists[row] = st->metric == kEuclidean ? sqrt(d) : d;
-            }
-          }
-          const unsigned mask = __ballot_sync(0xffffffffu, flag);
-          if (mask) {
-            int base = 0;
-            const int leader = __ffs(mask) - 1;
-            if (lane == leader) base = atomicAdd(&st->flag_count, __popc(mask));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (flag) {
-              const int pos = base + __popc(mask & ((1u << lane) - 1u));
-              a.flags[pos] = (int)row;
-              a.flag_thr[pos] = thr;
-            }
-          }
-        }
+        // hand the tile's per-part results to the certification warps
+        const int rb = (int)(i & 1);
+        mbar_wait(&m->res_empty[rb], (uint32_t)(((i >> 1) & 1) ^ 1));
+        m->merge.res[rb].m1[h][r] = m1;
+        m->merge.res[rb].cnt[h][r] = cnt;
+        m->merge.res[rb].i1[h][r] = i1;
+        if (h == 0) m->merge.res[rb].q[r] = qcur;
+        mbar_arrive(&m->res_full[rb]);
+        if (!C::kCertWarps && h == 0) certify(i, r);
       } else if constexpr (MODE == kTcShortlist) {
         // every part evaluates its own candidates in FP64; part 0 decides
         // overflow from the total and merges the parts' lexicographic minima
@@ -586,7 +624,7 @@ static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaS
   cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  assign_tc_kernel<L, MODE><<<grid, C::kThreads, smem, s>>>(a, dump, b_cap);
+  assign_tc_kernel<L, MODE><<<grid, C::threads(MODE), smem, s>>>(a, dump, b_cap);
   return cudaGetLastError();
 }
 
