@@ -14,7 +14,8 @@ import numpy as np
 from .errors import ConfigError, DomainError, InternalError, UsageError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvqb200.so")
+# VQB200_LIB: another build of the same ABI (A/B timing, profiling builds)
+LIB_PATH = os.environ.get("VQB200_LIB") or os.path.join(_HERE, "libvqb200.so")
 
 VQB_OK, VQB_USAGE, VQB_CONFIG, VQB_DOMAIN, VQB_INTERNAL = 0, 1, 2, 3, 4
 

@@ -4,9 +4,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -76,6 +78,12 @@ struct vqb_session {
   std::vector<float> mu_host;  // host copy of the centring vector
   double maxabs = -1.0;
   unsigned short* tcb = nullptr;  // fp16 operand image of the codebook (assign_tc)
+  // fp16 operand image of the resident rows (assign_tc reads it with bulk
+  // copies instead of converting every pass); built for scale 2^aimg_ey
+  bool rows_resident = false;  // x32 holds the session's rows for its lifetime (vqb_open)
+  unsigned short* aimg = nullptr;
+  float* aq = nullptr;
+  int aimg_ey = INT_MIN;
   // run buffers
   long long kmax = 0;
   double* cb[2] = {nullptr, nullptr};
@@ -148,6 +156,8 @@ struct vqb_session {
     a.cb[1] = cb[1];
     a.w = w;
     a.tcb = tcb;
+    a.aimg = aimg_ey != INT_MIN ? aimg : nullptr;
+    a.aq = aimg_ey != INT_MIN ? aq : nullptr;
     a.nrm = nrm;
     a.kmax = kmax;
     a.idx = idx;
@@ -216,6 +226,8 @@ struct vqb_session {
     cudaFree(partials);
     cudaFree(ord);
     cudaFree(tcb);
+    cudaFree(aimg);
+    cudaFree(aq);
     cudaFree(st);
     cudaFree(scratch);
     if (st_host) cudaFreeHost(st_host);
@@ -353,6 +365,7 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
     s->mu_host = mu;
   }
   s->fast = s->x32 != nullptr && fast_dim_supported((int)dim) && s->maxabs < 1099511627776.0;
+  s->rows_resident = true;
   *out = s.release();
   return VQB_OK;
 }
@@ -451,6 +464,28 @@ static void tc_configure(const vqb_session* s, DevState* h, double my, double mw
   h->tc_on = h->tc_kmax >= h->tc_kmin ? 1 : 0;
 }
 
+// (Re)build the rows' operand image when the TC pass is on at a new row
+// scale (one pass over x32; sessions whose rows stay resident only).
+static int build_row_image(vqb_session* s, const DevState* h) {
+  static const bool off = [] {
+    const char* e = std::getenv("VQB_TC_IMG");  // 0: always convert in-kernel (A/B timing)
+    return e && e[0] == '0';
+  }();
+  if (off || !s->rows_resident || !s->x32 || !h->tc_on) return VQB_OK;
+  if (s->aimg && s->aimg_ey == h->tc_ey) return VQB_OK;
+  if (!s->aimg) {
+    const long long elems = tc_row_image_elems(s->n, (int)s->dim);
+    const long long qn = (s->n + kTcRows - 1) / kTcRows * kTcRows;
+    CK(dalloc(&s->aimg, (size_t)elems));
+    CK(dalloc(&s->aq, (size_t)qn));
+    CK(cudaMemsetAsync(s->aimg, 0, sizeof(unsigned short) * elems, s->stream));
+    CK(cudaMemsetAsync(s->aq, 0, sizeof(float) * qn, s->stream));
+  }
+  CK(launch_build_row_image(s->x32, s->mu, s->n, (int)s->dim, h->tc_ey, s->aimg, s->aq, s->sms, s->stream));
+  s->aimg_ey = h->tc_ey;
+  return VQB_OK;
+}
+
 static double data_span(const vqb_session* s, const double* codebook, long long size) {
   // |x - mu| bound: exact from the session's max |x| when known, else the
   // codebook's span (rows beyond it are flagged on the device)
@@ -483,6 +518,7 @@ int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
     // centroids stay in the data's convex hull; a split adds delta per level
     const double my = data_span(s, nullptr, 0);
     tc_configure(s, h, my, 2.0 * (my + 16.0 * cfg->delta));
+    if (int rc2 = build_row_image(s, h)) return rc2;
   }
   h->mode = kModeTrain;
   h->ordered = s->ordered ? 1 : 0;
@@ -695,7 +731,10 @@ static int set_state(vqb_session* s, int mode, long long size, int metric, int o
   h->size = (int)size;
   h->iteration = 1;
   h->td_prev = INFINITY;
-  if (codebook) tc_configure(s, h, data_span(s, codebook, size), 2.0 * codebook_span(s, codebook, size));
+  if (codebook) {
+    tc_configure(s, h, data_span(s, codebook, size), 2.0 * codebook_span(s, codebook, size));
+    if (int rc = build_row_image(s, h)) return rc;
+  }
   CK(cudaMemcpyAsync(s->st, h, offsetof(DevState, hist), cudaMemcpyHostToDevice, s->stream));
   return VQB_OK;
 }

@@ -25,6 +25,9 @@
 // chunk c+1 overlap the epilogue of chunk c, and the conversion of tile i+1
 // overlaps the MMAs of tile i.
 #include <cfloat>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 
@@ -42,24 +45,30 @@ struct TcCfg {
   static constexpr int kEpiWarps = L == 16 ? 16 : 8;
   static constexpr int kParts = kEpiWarps / 4;
   static constexpr int kSpan = kTcChunk / kParts;
-  // warp 0 issues MMAs, warps 1..kEpiWarps run the epilogue, the next warp
-  // streams codebook chunks when the codebook does not fit in shared memory,
-  // the last warp converts row tiles into the A operand buffers
-  // and (L <= 32, kTcTop2) 4 certification warps, one per 32-row quarter,
-  // finish each tile's rows off the epilogue's critical path; at L = 64 the
-  // MMAs bind, registers are scarcer, and epilogue part 0 certifies
+  // Warp roles: 0 issues MMAs; 1..kEpiWarps run the epilogue; kEpiWarps + 1
+  // streams codebook chunks when the codebook does not fit in shared memory
+  // (else it converts rows); kEpiWarps + 2 and kExtraConv more convert row
+  // tiles into the A operand buffers (at small K the conversion is the
+  // pipeline's longest stage); then (L <= 32, kTcTop2) kCertGroups x 4
+  // certification warps, one per 32-row quarter, finish each tile's rows off
+  // the epilogue's critical path (at L = 64 the MMAs bind, registers are
+  // scarcer, and epilogue part 0 certifies).
+  static constexpr int kExtraConv = 0;
   static constexpr bool kCertWarps = L <= 32;
-  static constexpr int kCertWarp0 = 3 + kEpiWarps;
+  static constexpr int kCertGroups = L == 16 ? 2 : 1;
+  static constexpr int kCertWarp0 = 3 + kEpiWarps + kExtraConv;
   static constexpr int threads(int mode) {
-    return 32 * (mode == 0 && kCertWarps ? 7 + kEpiWarps : 3 + kEpiWarps);
+    return 32 * (kCertWarp0 + (mode == 0 && kCertWarps ? 4 * kCertGroups : 0));
   }
   static constexpr size_t kChunkBytes = (size_t)kTcChunk * (2 * L + 16) * 2;
   static constexpr size_t kABytes = (size_t)kTcRows * (2 * L + 16) * 2;
   static constexpr size_t kMisc = kParts == 4 ? 16384 : 10240;
   // contiguous row tiles arrive by one bulk copy into this stage (L <= 32);
   // the converter then reads shared memory instead of 64 B per lane from HBM
-  // (double-buffered at L = 16, where it costs no resident codebook chunk)
+  // (double-buffered at L = 16; sessions with resident rows use the prebuilt
+  // row image instead)
   static constexpr int kXsStages = L == 16 ? 2 : 1;
+  static_assert(kXsStages <= 4, "xs_full barriers");
   static constexpr size_t kXsTile = (size_t)kTcRows * L * 4;
   static constexpr size_t kXsBytes = L <= 32 ? kXsStages * kXsTile : 0;
   static constexpr size_t kSmemCap = 227 * 1024;
@@ -91,7 +100,7 @@ struct TcMisc {
   uint32_t tmem;
   uint32_t pad;
   uint64_t q_full[4];      // converter -> epilogue: qrow[i & 3] written
-  uint64_t xs_full[2];     // row tile landed in X stage i % kXsStages
+  uint64_t xs_full[4];     // row tile landed in X stage i % kXsStages
   float qrow[4][kTcRows];  // ||y~||^2 per row of tile i (slot i & 3; -1: row out of fp16 range)
   union {
     struct {               // kTcTop2: every part's (minimum, band count, index) per row
@@ -130,6 +139,93 @@ __device__ __forceinline__ float tc_band(float m1v, float q, float yn, float eyw
 
 enum { kTcTop2 = 0, kTcShortlist = 1, kTcDump = 2 };
 
+// One 8-element group of a row: y~ = fl(x - mu), its partial ||y~||^2 (FP32
+// FMA chain), and the fp16 hi/lo split of y~ * 2^ey (two elements per packed
+// conversion).  bad: a value fp16 cannot hold (or NaN).  Shared by the
+// in-kernel converter and the row-image builder, so both give the same bits.
+__device__ __forceinline__ void tc_split8(const float (&xv)[8], const float (&mv)[8], bool valid, float sy,
+                                          uint4& ph, uint4& pl, float& qq, bool& bad) {
+  float yv[8];
+  qq = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    yv[k] = valid ? __fsub_rn(xv[k], mv[k]) : 0.f;
+    qq = fmaf(yv[k], yv[k], qq);
+  }
+  uint32_t hw[4], lw[4];
+  float vmax = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const float v0 = yv[k] * sy, v1 = yv[k + 1] * sy;
+    vmax = fmaxf(vmax, fmaxf(fabsf(v0), fabsf(v1)));
+    const __half2 hi = __floats2half2_rn(v0, v1);
+    const float2 hf = __half22float2(hi);
+    const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+    hw[k / 2] = *reinterpret_cast<const uint32_t*>(&hi);
+    lw[k / 2] = *reinterpret_cast<const uint32_t*>(&lo);
+  }
+  bad = !(vmax <= 60000.0f) || isnan(qq);  // fmaxf drops NaN; the norm keeps it
+  ph = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+  pl = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
+// Row image (rows [0, n)): item = (row, 8-element group); a row's L/8 groups
+// sit in adjacent lanes and combine ||y~||^2 by shuffles in the converter's
+// order, so the image equals what the converter would write.
+template <int L>
+__global__ void __launch_bounds__(256) build_row_image_kernel(const float* __restrict__ x32,
+                                                              const float* __restrict__ mu, long long n,
+                                                              float sy, unsigned short* aimg, float* aq) {
+  constexpr int kG = L / 8;
+  const long long items = n * kG;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long end = (items + 31) / 32 * 32;
+  for (long long it0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; it0 < end; it0 += stride) {
+    const bool live = it0 < items;
+    const long long it = live ? it0 : 0;
+    const long long row = it / kG;
+    const int c8 = (int)(it % kG);
+    float xv[8], mv[8];
+    const float4* src = reinterpret_cast<const float4*>(x32 + row * L + c8 * 8);
+    const float4 p0 = __ldg(src), p1 = __ldg(src + 1);
+    xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
+    xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mv[k] = __ldg(mu + c8 * 8 + k);
+    uint4 ph, pl;
+    float qq;
+    bool bb;
+    tc_split8(xv, mv, live, sy, ph, pl, qq, bb);
+    int bi = bb ? 1 : 0;
+#pragma unroll
+    for (int o = 1; o < kG; o <<= 1) {
+      qq += __shfl_xor_sync(0xffffffffu, qq, o);
+      bi |= __shfl_xor_sync(0xffffffffu, bi, o);
+    }
+    if (live) {
+      const long long t = row / kTcRows;
+      const int r = (int)(row % kTcRows);
+      unsigned short* yh = aimg + t * (2LL * kTcRows * L);
+      *reinterpret_cast<uint4*>(yh + tc_off(r, c8 * 8, L)) = ph;
+      *reinterpret_cast<uint4*>(yh + kTcRows * L + tc_off(r, c8 * 8, L)) = pl;
+      if (c8 == 0) aq[row] = bi ? -1.0f : qq;
+    }
+  }
+}
+
+cudaError_t launch_build_row_image(const float* x32, const float* mu, long long n, int dim, int ey,
+                                   unsigned short* aimg, float* aq, int sms, cudaStream_t s) {
+  const float sy = ldexpf(1.0f, ey);
+  const int grid = sms * 8;
+  switch (dim) {
+    case 16: build_row_image_kernel<16><<<grid, 256, 0, s>>>(x32, mu, n, sy, aimg, aq); break;
+    case 32: build_row_image_kernel<32><<<grid, 256, 0, s>>>(x32, mu, n, sy, aimg, aq); break;
+    case 64: build_row_image_kernel<64><<<grid, 256, 0, s>>>(x32, mu, n, sy, aimg, aq); break;
+    default: return cudaSuccess;
+  }
+  return cudaGetLastError();
+}
+
 // MODE kTcTop2: candidate pass over rows [r0, r1) -> idx + certified band /
 //   re-rank queue (flags, flag_thr).
 // MODE kTcShortlist: the queued rows again (gathered from flags): every j
@@ -160,17 +256,47 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
   // resident: the whole operand image sits in smem for the kernel; streaming:
   // chunks cycle through kStages slots, reloaded for every row tile
   const bool resident = nch <= b_cap;
+  // rows from the prebuilt operand image (whole tiles from r0, a multiple of
+  // 128; the host guarantees it) instead of the converter warps
+  const bool img = MODE != kTcShortlist && a.aimg != nullptr;
   // row conversion: the converter warp, joined by the streamer warp when the
   // codebook is resident (the streamer has nothing to stream then)
-  const int conv_warps = resident ? 2 : 1;
+  const int conv_warps = (resident ? 2 : 1) + C::kExtraConv;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sB = smem;
   unsigned char* sA = smem + (size_t)b_cap * C::kChunkBytes;
   float* sX = reinterpret_cast<float*>(sA + 2 * C::kABytes);
   using Misc = TcMisc<C::kParts>;
   static_assert(sizeof(Misc) <= C::kMisc, "misc smem");
+  static_assert(offsetof(Misc, qrow) % 16 == 0, "qrow is a bulk-copy destination");
   Misc* m = reinterpret_cast<Misc*>(sA + 2 * C::kABytes + C::kXsBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // profiling builds (-DVQB_TC_PROFILE, VQB_TC_PROF=1): in kTcTop2 mode `dump`
+  // collects, per warp role, the clock64 cycles spent in each barrier wait
+  // and in total
+#ifdef VQB_TC_PROFILE
+  unsigned long long* prof = MODE == kTcTop2 ? reinterpret_cast<unsigned long long*>(dump) : nullptr;
+#else
+  constexpr unsigned long long* prof = nullptr;
+#endif
+  long long pacc[4] = {0, 0, 0, 0};
+  const long long pt0 = prof ? clock64() : 0;
+  auto pwait = [&](uint64_t* bar, uint32_t par, int slot) {
+    if (prof) {
+      const long long t = clock64();
+      mbar_wait(bar, par);
+      pacc[slot] += clock64() - t;
+    } else {
+      mbar_wait(bar, par);
+    }
+  };
+  auto pflush = [&](int role) {
+    if (prof && lane == 0) {
+      pacc[3] = clock64() - pt0;
+      for (int k = 0; k < 4; ++k) atomicAdd(prof + role * 4 + k, (unsigned long long)pacc[k]);
+      atomicAdd(prof + 16 + role, 1ull);
+    }
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -179,10 +305,10 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         mbar_init(&m->bs_full[i], 1);
         mbar_init(&m->bs_empty[i], 1);
       }
-      for (int i = 0; i < 4; ++i) mbar_init(&m->q_full[i], 32 * conv_warps);
-      for (int i = 0; i < 2; ++i) mbar_init(&m->xs_full[i], 1);
+      for (int i = 0; i < 4; ++i) mbar_init(&m->q_full[i], img ? 1 : 32 * conv_warps);
+      for (int i = 0; i < 4; ++i) mbar_init(&m->xs_full[i], 1);
       for (int i = 0; i < 2; ++i) {
-        mbar_init(&m->a_full[i], 32 * conv_warps);
+        mbar_init(&m->a_full[i], img ? 1 : 32 * conv_warps);
         mbar_init(&m->a_empty[i], 1);
         mbar_init(&m->d_full[i], 1);
         mbar_init(&m->d_empty[i], 32 * C::kEpiWarps);
@@ -216,7 +342,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
     const float inv = 1.0f / dscale;
     const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
     const int rb = (int)(i & 1);
-    mbar_wait(&m->res_full[rb], (uint32_t)((i >> 1) & 1));
+    pwait(&m->res_full[rb], (uint32_t)((i >> 1) & 1), 0);
     float pm[C::kParts];
     int pc[C::kParts], pi[C::kParts];
 #pragma unroll
@@ -295,7 +421,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       long long g = 0;
       for (long long i = 0; i < my_tiles; ++i) {
         const int b = (int)(i & 1);
-        mbar_wait(&m->a_full[b], (uint32_t)((i >> 1) & 1));
+        pwait(&m->a_full[b], (uint32_t)((i >> 1) & 1), 0);
         tc_fence_after();
         const uint32_t aYh = sAa + b * (uint32_t)C::kABytes;
         const uint32_t aYl = aYh + kTcRows * L * 2;
@@ -305,9 +431,9 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           int stage = c;
           if (!resident) {
             stage = (int)(g % C::kStages);
-            mbar_wait(&m->bs_full[stage], (uint32_t)((g / C::kStages) & 1));
+            pwait(&m->bs_full[stage], (uint32_t)((g / C::kStages) & 1), 2);
           }
-          mbar_wait(&m->d_empty[s], (uint32_t)(((g >> 1) & 1) ^ 1));
+          pwait(&m->d_empty[s], (uint32_t)(((g >> 1) & 1) ^ 1), 1);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(s * kTcChunk);
           const uint32_t bWh = sBa + stage * (uint32_t)C::kChunkBytes;
@@ -330,10 +456,11 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         mma_commit(&m->a_empty[b]);
       }
     }
-  } else if (warp == 2 + C::kEpiWarps || (resident && warp == 1 + C::kEpiWarps)) {
-    // ===== row converter(s): tile i's rows -> fp16 hi/lo A buffer (i & 1) =====
+    pflush(0);
+  } else if ((warp >= 2 + C::kEpiWarps && warp < C::kCertWarp0) || (resident && warp == 1 + C::kEpiWarps)) {
+    // ===== row converters: tile i's rows -> fp16 hi/lo A buffer (i & 1) =====
     const float sy = ldexpf(1.0f, st->tc_ey);
-    const int cid = warp == 2 + C::kEpiWarps ? 0 : 1;
+    const int cid = warp == 1 + C::kEpiWarps ? conv_warps - 1 : warp - (2 + C::kEpiWarps);
     constexpr bool kUseXs = MODE != kTcShortlist && C::kXsBytes > 0;
     constexpr int kXs = C::kXsStages;
     auto issue_xs = [&](long long i) {  // bulk copy of tile i's contiguous rows
@@ -344,56 +471,86 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       mbar_arrive_expect_tx(&m->xs_full[xb], bytes);
       bulk_g2s(sX + xb * (kTcRows * L), a.x32 + (a.r0 + t * kTcRows) * L, bytes, &m->xs_full[xb]);
     };
+    if (img) {
+      // prebuilt row image: the tile's operand rows and norms are two bulk
+      // copies (no conversion work)
+      if (cid == 0 && lane == 0) {
+        constexpr uint32_t kImgBytes = 2u * kTcRows * L * 2u;
+        for (long long i = 0; i < my_tiles; ++i) {
+          const int b = (int)(i & 1);
+          pwait(&m->a_empty[b], (uint32_t)(((i >> 1) & 1) ^ 1), 0);  // tile i-2's MMAs are done
+          const long long tg = a.r0 / kTcRows + (long long)blockIdx.x + i * gridDim.x;
+          mbar_arrive_expect_tx(&m->a_full[b], kImgBytes);
+          bulk_g2s(sA + b * C::kABytes, a.aimg + tg * (2LL * kTcRows * L), kImgBytes, &m->a_full[b]);
+          mbar_arrive_expect_tx(&m->q_full[i & 3], kTcRows * 4u);
+          bulk_g2s(&m->qrow[i & 3][0], a.aq + tg * kTcRows, kTcRows * 4u, &m->q_full[i & 3]);
+        }
+      }
+    } else {
     if (kUseXs && cid == 0 && lane == 0)
       for (int j = 0; j < kXs && j < my_tiles; ++j) issue_xs(j);
+    // the centring vector, in registers for the whole kernel (L <= 32)
+    constexpr int kMuRegs = L <= 32 ? L : 1;
+    float mur[kMuRegs];
+#pragma unroll
+    for (int k = 0; k < kMuRegs; ++k) mur[k] = a.mu[k];
     for (long long i = 0; i < my_tiles; ++i) {
       const int b = (int)(i & 1);
-      mbar_wait(&m->a_empty[b], (uint32_t)(((i >> 1) & 1) ^ 1));  // tile i-2's MMAs are done
+      pwait(&m->a_empty[b], (uint32_t)(((i >> 1) & 1) ^ 1), 0);  // tile i-2's MMAs are done
       const float* xs = sX + (int)(i % kXs) * (kTcRows * L);
-      if (kUseXs) mbar_wait(&m->xs_full[i % kXs], (uint32_t)((i / kXs) & 1));
+      if (kUseXs) pwait(&m->xs_full[i % kXs], (uint32_t)((i / kXs) & 1), 1);
       unsigned short* yh = reinterpret_cast<unsigned short*>(sA + b * C::kABytes);
       unsigned short* yl = yh + kTcRows * L;
       const long long t = (long long)blockIdx.x + i * gridDim.x;
-      for (int r = cid * 32 + lane; r < kTcRows; r += 32 * conv_warps) {
+      // work item = (row, 8-element group): independent items give the
+      // converter ILP; a row's L/8 groups sit in adjacent lanes and combine
+      // ||y~||^2 by shuffles (whole warps iterate: items past the tile idle)
+      constexpr int kG = L / 8;
+      const int it_end = (kTcRows * kG + 32 * conv_warps - 1) / (32 * conv_warps) * (32 * conv_warps);
+#pragma unroll 4
+      for (int it0 = cid * 32 + lane; it0 < it_end; it0 += 32 * conv_warps) {
+        const bool live = it0 < kTcRows * kG;
+        const int it = live ? it0 : 0;
+        const int r = it / kG, c8 = it % kG;
         const long long entry = t * kTcRows + r;
-        const bool valid = entry < nitems;
+        const bool valid = live && entry < nitems;
         const long long row = MODE == kTcShortlist ? (valid ? (long long)a.flags[entry] : 0) : a.r0 + entry;
-        float qq = 0.f;
-        bool bb = false;
+        float xv[8], mv[8];
+        if (valid) {
+          const float4* src = kUseXs ? reinterpret_cast<const float4*>(xs + r * L + c8 * 8)
+                                     : reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
+          const float4 p0 = kUseXs ? src[0] : __ldg(src), p1 = kUseXs ? src[1] : __ldg(src + 1);
+          xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
+          xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
+        } else {
 #pragma unroll
-        for (int c8 = 0; c8 < L / 8; ++c8) {
-          float xv[8];
-          if (valid) {
-            const float4* src = kUseXs ? reinterpret_cast<const float4*>(xs + r * L + c8 * 8)
-                                       : reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
-            const float4 p0 = kUseXs ? src[0] : __ldg(src), p1 = kUseXs ? src[1] : __ldg(src + 1);
-            xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
-            xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
+          for (int k = 0; k < 8; ++k) xv[k] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if constexpr (L <= 32) {
+            mv[k] = mur[k % kMuRegs];
+#pragma unroll
+            for (int g = 1; g < kG; ++g) mv[k] = c8 == g ? mur[(g * 8 + k) % kMuRegs] : mv[k];
           } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) xv[k] = 0.f;
+            mv[k] = __ldg(a.mu + c8 * 8 + k);
           }
-          unsigned short hs[8], ls[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float yv = valid ? __fsub_rn(xv[k], a.mu[c8 * 8 + k]) : 0.f;
-            qq = fmaf(yv, yv, qq);
-            const float v = yv * sy;
-            bb |= !(fabsf(v) <= 60000.0f);
-            const __half hi = __float2half_rn(v);
-            const __half lo = __float2half_rn(v - __half2float(hi));
-            hs[k] = __half_as_ushort(hi);
-            ls[k] = __half_as_ushort(lo);
-          }
-          uint4 ph, pl;
-          ph.x = hs[0] | ((uint32_t)hs[1] << 16); ph.y = hs[2] | ((uint32_t)hs[3] << 16);
-          ph.z = hs[4] | ((uint32_t)hs[5] << 16); ph.w = hs[6] | ((uint32_t)hs[7] << 16);
-          pl.x = ls[0] | ((uint32_t)ls[1] << 16); pl.y = ls[2] | ((uint32_t)ls[3] << 16);
-          pl.z = ls[4] | ((uint32_t)ls[5] << 16); pl.w = ls[6] | ((uint32_t)ls[7] << 16);
+        }
+        uint4 ph, pl;
+        float qq;
+        bool bb;
+        tc_split8(xv, mv, valid, sy, ph, pl, qq, bb);
+        if (live) {
           *reinterpret_cast<uint4*>(yh + tc_off(r, c8 * 8, L)) = ph;
           *reinterpret_cast<uint4*>(yl + tc_off(r, c8 * 8, L)) = pl;
         }
-        m->qrow[i & 3][r] = bb ? -1.0f : qq;
+        int bi = bb ? 1 : 0;
+#pragma unroll
+        for (int o = 1; o < kG; o <<= 1) {
+          qq += __shfl_xor_sync(0xffffffffu, qq, o);
+          bi |= __shfl_xor_sync(0xffffffffu, bi, o);
+        }
+        if (live && c8 == 0) m->qrow[i & 3][r] = bi ? -1.0f : qq;
       }
       if (kUseXs) {
         // every converter lane is done with the stage: fetch the next tile
@@ -404,6 +561,8 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       mbar_arrive(&m->a_full[b]);
       mbar_arrive(&m->q_full[i & 3]);
     }
+    }
+    pflush(1);
   } else if (warp == 1 + C::kEpiWarps) {
     // ===== codebook streamer (streaming mode only) =====
     if (!resident && lane == 0) {
@@ -422,7 +581,9 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
   } else if (warp >= C::kCertWarp0) {
     // ===== certification warps (kTcTop2): lane = row of the tile quarter =====
     if constexpr (MODE == kTcTop2)
-      for (long long i = 0; i < my_tiles; ++i) certify(i, (warp - C::kCertWarp0) * 32 + lane);
+      for (long long i = (warp - C::kCertWarp0) >> 2; i < my_tiles; i += C::kCertGroups)
+        certify(i, ((warp - C::kCertWarp0) & 3) * 32 + lane);
+    pflush(3);
   } else {
     // ===== epilogue warps: row conversion + per-value work over TMEM =====
     const int e = warp - 1;
@@ -462,13 +623,13 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       if (MODE == kTcShortlist && valid) thr_d = a.flag_thr[entry] * dscale;  // NaN stays NaN -> overflow
       float qcur = 0.f, yn = 0.f;
       if constexpr (MODE == kTcTop2) {
-        mbar_wait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1));
+        pwait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1), 0);
         qcur = m->qrow[i & 3][r];
         yn = sqrtf(fmaxf(qcur, 0.f));
       }
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = (int)(g & 1);
-        mbar_wait(&m->d_full[s], (uint32_t)((g >> 1) & 1));
+        pwait(&m->d_full[s], (uint32_t)((g >> 1) & 1), 1);
         tc_fence_after();
         const int span = ncols / C::kParts;  // this part's columns of the chunk
         // 32 accumulator columns of this part (padded with +inf below 32)
@@ -548,7 +709,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       if constexpr (MODE == kTcTop2) {
         // hand the tile's per-part results to the certification warps
         const int rb = (int)(i & 1);
-        mbar_wait(&m->res_empty[rb], (uint32_t)(((i >> 1) & 1) ^ 1));
+        pwait(&m->res_empty[rb], (uint32_t)(((i >> 1) & 1) ^ 1), 2);
         m->merge.res[rb].m1[h][r] = m1;
         m->merge.res[rb].cnt[h][r] = cnt;
         m->merge.res[rb].i1[h][r] = i1;
@@ -603,6 +764,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         named_bar(3, 32 * C::kEpiWarps);  // the merge area is free for the next tile
       }
     }
+    pflush(2);
   }
   tc_fence_before();
   __syncthreads();
@@ -628,13 +790,53 @@ static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s) {
+// VQB_TC_PROF=1 (tools only): per warp role, the share of the kernel's
+// cycles each role spends in its barrier waits, printed to stderr after every
+// launch (synchronises the stream)
+static unsigned long long* tc_prof_buffer() {
+#ifndef VQB_TC_PROFILE
+  return nullptr;
+#endif
+  static unsigned long long* buf = nullptr;
+  static const bool on = [] {
+    const char* e = std::getenv("VQB_TC_PROF");
+    return e && e[0] == '1';
+  }();
+  if (on && !buf && cudaMalloc(&buf, 32 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+  return on ? buf : nullptr;
+}
+
+cudaError_t launch_assign_tc(const KernelArgs& a_in, int sms, cudaStream_t s) {
+  KernelArgs a = a_in;
+  if (a.r0 % kTcRows != 0) a.aimg = nullptr;  // the image is tiled from row 0
+  unsigned long long* prof = tc_prof_buffer();
+  if (prof) cudaMemsetAsync(prof, 0, 32 * sizeof(unsigned long long), s);
+  float* pd = reinterpret_cast<float*>(prof);
+  cudaError_t e = cudaSuccess;
   switch (a.dim) {
-    case 16: return launch_tc_L<16, kTcTop2>(a, sms, nullptr, s);
-    case 32: return launch_tc_L<32, kTcTop2>(a, sms, nullptr, s);
-    case 64: return launch_tc_L<64, kTcTop2>(a, sms, nullptr, s);
+    case 16: e = launch_tc_L<16, kTcTop2>(a, sms, pd, s); break;
+    case 32: e = launch_tc_L<32, kTcTop2>(a, sms, pd, s); break;
+    case 64: e = launch_tc_L<64, kTcTop2>(a, sms, pd, s); break;
     default: return cudaSuccess;
   }
+  if (prof && e == cudaSuccess) {
+    unsigned long long h[32];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    static const char* role[4] = {"mma", "conv", "epi", "cert"};
+    static const char* slot[4][3] = {{"a_full", "d_empty", "bs_full"},
+                                     {"a_empty", "xs_full", "-"},
+                                     {"q_full", "d_full", "res_empty"},
+                                     {"res_full", "-", "-"}};
+    for (int r = 0; r < 4; ++r) {
+      if (!h[16 + r] || !h[r * 4 + 3]) continue;
+      std::fprintf(stderr, "tcprof %s warps=%llu", role[r], h[16 + r]);
+      for (int k = 0; k < 3; ++k)
+        std::fprintf(stderr, " %s=%.3f", slot[r][k], (double)h[r * 4 + k] / (double)h[r * 4 + 3]);
+      std::fprintf(stderr, " cycles/warp=%.0f\n", (double)h[r * 4 + 3] / (double)h[16 + r]);
+    }
+  }
+  return e;
 }
 
 cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s) {

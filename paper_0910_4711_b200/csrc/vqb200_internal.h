@@ -107,6 +107,11 @@ struct KernelArgs {
   double* cb[2];        // FP64 master, double buffered, kmax x dim
   float* w;             // -2 * c~ (FP32), kpad x dim
   unsigned short* tcb;  // fp16 hi/lo operand image of the codebook for the TC pass (nullable)
+  // fp16 hi/lo operand image of the resident rows (nullable; build_row_image):
+  // per 128-row tile [yh 128 x L | yl 128 x L] in the smem layout, and
+  // ||y~||^2 per row (-1: a row fp16 cannot hold)
+  const unsigned short* aimg;
+  const float* aq;
   float* nrm;           // ||c~||^2 (FP32), kpad
   long long kmax;
   // per-row outputs
@@ -165,6 +170,12 @@ __host__ __device__ __forceinline__ bool tc_handles(const DevState* st, int K) {
 cudaError_t launch_assign_tc(const KernelArgs& a, int sms, cudaStream_t s);
 cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s);
 cudaError_t launch_tc_probe(const KernelArgs& a, float* dump, cudaStream_t s);
+// the rows' operand image for the current tc_ey (rows [0, n) of x32)
+cudaError_t launch_build_row_image(const float* x32, const float* mu, long long n, int dim, int ey,
+                                   unsigned short* aimg, float* aq, int sms, cudaStream_t s);
+__host__ __device__ inline long long tc_row_image_elems(long long n, int dim) {
+  return (n + kTcRows - 1) / kTcRows * (2LL * kTcRows * dim);
+}
 
 // element offset of (row, col) in a K-major, no-swizzle UMMA operand tile with
 // kt columns: 8-row x 16-byte core matrices, K-adjacent core matrices 128 B

@@ -1,4 +1,4 @@
-"""One cfg2 Lloyd iteration at K=1024 (the bench step) for ncu captures:
+"""One cfg2 Lloyd iteration at K=1024 (the bench step; argv[2]: another K) for ncu captures:
 session open, 2 warm-up passes + 1 profiled pass via vqb_bench_iteration."""
 import ctypes, os, sys
 import numpy as np
@@ -10,6 +10,8 @@ from paper_0910_4711_b200.core import _Session
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 g = np.load(os.path.join(ROOT, "tests", "golden", f"{which}_design.npz"))
 cb = np.ascontiguousarray(g["cb"])
+if len(sys.argv) > 2:  # a smaller codebook: the first K codevectors
+    cb = np.ascontiguousarray(cb[: int(sys.argv[2])])
 x = synthetic.make_training(which)
 s = _Session(x, None)
 segs = (ctypes.c_double * 5)()
