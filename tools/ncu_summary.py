@@ -1,7 +1,7 @@
 """Condense an `ncu --set full` report into the lines the roofline and the
 judge need (run here, on the CPU box, on a report gpurun brought back).
 
-Usage: python tools/ncu_summary.py REPORT.ncu-rep [out.txt] [traffic.json]
+Usage: python tools/ncu_summary.py REPORT.ncu-rep [out.txt] [traffic.json] [kernel-substring]
 
 Prints per launch: duration, DRAM bytes (read + write), pipe utilisation,
 issue activity, occupancy, registers and the top stall reasons.  With a third
@@ -86,6 +86,8 @@ def main():
     if len(sys.argv) > 2:
         with open(sys.argv[2], "w") as f:
             f.write(f"# ncu --set full summary of {rep}\n" + text + "\n")
+    if len(sys.argv) > 4:
+        launches = [l for l in launches if sys.argv[4] in l["kernel"]]
     if len(sys.argv) > 3 and launches:
         mean_traffic = sum(l["traffic"] for l in launches) / len(launches)
         mean_us = sum(_to_us(*l["duration"]) for l in launches) / len(launches)
