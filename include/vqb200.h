@@ -26,7 +26,7 @@
  * Conventions.
  *  - Status codes mirror the reference's exception hierarchy (errors.py:8-29):
  *    0 ok, 1 UsageError, 2 ConfigError, 3 DomainError, 4 InternalError
- *    (CUDA failures included).  vqb_last_error() returns the message of the
+ *    (CUDA failures included), 5 FormatError.  vqb_last_error() returns the message of the
  *    calling thread's last failure.
  *  - Host buffers are caller-owned; device memory is owned by the session.
  *  - Every call is synchronous on return unless its name says `step` / `async`.
@@ -47,6 +47,7 @@ extern "C" {
 #define VQB_CONFIG 2
 #define VQB_DOMAIN 3
 #define VQB_INTERNAL 4
+#define VQB_FORMAT 5 /* FormatError (errors.py:24-25): corrupt stream / payload */
 
 const char* vqb_last_error(void);
 int vqb_version(void);
@@ -171,6 +172,45 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
 int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* codebook,
                        int64_t size, int device, double* new_codebook, int64_t* cells_out,
                        double* td, int64_t* n_empty);
+
+/* ---- data formats either side of the path ----
+ * Stateless, host buffers, synchronous.  `images` stacked uint8 rasters
+ * [images][height][width]; their block vectors are image-major, each image's
+ * ceil(h/b) x ceil(w/b) blocks row-major, each block row-major (b*b values). */
+
+/* storage.pixels_to_blocks (storage.py:281-293) / image_to_blocks
+ * (storage.py:274-278): ragged edges replicated (np.pad mode "edge").
+ * Exactly one of out64 (float64, the reference's dtype) / out32 is non-null. */
+int vqb_pixels_to_blocks(const uint8_t* pixels, int64_t images, int64_t height, int64_t width,
+                         int64_t block, int device, double* out64, float* out32);
+
+/* storage.blocks_to_image raster (storage.py:296-311): clamp to [0, 255],
+ * floor(v + 0.5), crop the padding (NaN -> 0). */
+int vqb_blocks_to_pixels(const double* vectors, int64_t images, int64_t height, int64_t width,
+                         int64_t block, int device, uint8_t* pixels);
+
+/* codec.decode (codec.py:96-114): out[j][:] = codebook[indices[j]][:];
+ * VQB_FORMAT when an index >= size. */
+int vqb_decode(const uint32_t* indices, int64_t n, const double* codebook, int64_t size, int64_t dim,
+               int device, double* out);
+
+/* decode fused with blocks_to_image: the block indices of `images` images ->
+ * pixels, without the float64 block matrix (cli.py decode of an image). */
+int vqb_decode_pixels(const uint32_t* indices, int64_t images, int64_t height, int64_t width,
+                      int64_t block, const double* codebook, int64_t size, int device, uint8_t* pixels);
+
+/* codec.reconstruction_distortion (codec.py:135-156): per-row pair_distance
+ * (_kernels.py:69-78) in the reference arithmetic; total summed in input
+ * order (sum_inorder) for n <= 2^20 rows, else per-2048-row fixed tree +
+ * in-order over tiles. */
+int vqb_reconstruction_distortion(const double* a, const double* b, int64_t n, int64_t dim, int metric,
+                                  int device, double* total);
+
+/* Session over the block vectors of `images` uint8 images, vectorised on the
+ * device (1 byte per sample over PCIe instead of the reference's float64
+ * copy, core.py:47-60): the training set of image_to_blocks + TrainingSet. */
+int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64_t width, int64_t block,
+                    int device, vqb_session** out);
 
 /* Pipe microbenchmark (0 FFMA, 1 FFMA2, 2 FFMA+top-2 mix, 3 DADD): lane-ops/s. */
 int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,

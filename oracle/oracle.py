@@ -328,3 +328,59 @@ def top2_gaps(vectors, codebook) -> np.ndarray:
         with np.errstate(divide="ignore", invalid="ignore"):
             out[lo:lo + step] = np.where(d2 > 0, (d2 - d1) / d2, 0.0)
     return out
+
+
+# ---------------------------------------------------------------------------
+# data formats either side of the path
+# ---------------------------------------------------------------------------
+# * pixels_to_blocks          <- storage.pixels_to_blocks (storage.py:281-293)
+# * blocks_to_pixels          <- storage.blocks_to_image raster (storage.py:296-311)
+# * decode                    <- codec.decode (codec.py:96-114)
+# * reconstruction_distortion <- codec.reconstruction_distortion (codec.py:135-156)
+# Restated with explicit index maps (block v = (by, bx), element q = (r, c)),
+# not the reference's reshape/swapaxes chain.
+
+def pixels_to_blocks(pixels, block: int) -> np.ndarray:
+    """float64 [ceil(h/b) * ceil(w/b)][b*b]; out-of-image samples take the
+    nearest edge pixel (np.pad mode "edge" == clamping the coordinates)."""
+    px = np.asarray(pixels, dtype=np.uint8)
+    h, w = px.shape
+    bc, br = -(-w // block), -(-h // block)
+    by, bx, r, c = np.meshgrid(np.arange(br), np.arange(bc), np.arange(block), np.arange(block),
+                               indexing="ij")
+    y = np.minimum(by * block + r, h - 1)
+    x = np.minimum(bx * block + c, w - 1)
+    return px[y, x].reshape(br * bc, block * block).astype(np.float64)
+
+
+def blocks_to_pixels(vectors, height: int, width: int, block: int) -> np.ndarray:
+    """uint8 [h][w]: pixel (y, x) is element (y % b, x % b) of block
+    (y // b, x // b), clamped to [0, 255] and rounded half up."""
+    v = np.asarray(vectors, dtype=np.float64)
+    bc = -(-width // block)
+    y, x = np.meshgrid(np.arange(height), np.arange(width), indexing="ij")
+    vals = v[(y // block) * bc + x // block, (y % block) * block + x % block]
+    return np.floor(np.clip(vals, 0.0, 255.0) + 0.5).astype(np.uint8)
+
+
+def decode(indices, codebook) -> np.ndarray:
+    cb = _f64(codebook)
+    idx = np.asarray(indices, dtype=np.int64)
+    if idx.size and (idx.max() >= cb.shape[0] or idx.min() < 0):
+        raise ValueError("corrupt stream")
+    return cb[idx]
+
+
+def reconstruction_distortion(a, b, metric=SQUARED_EUCLIDEAN) -> float:
+    """Per-row pair_distance (vq_oracle.c, _kernels.py:69-78) summed in input
+    order (sum_inorder, _kernels.py:92-98)."""
+    a, b = _f64(a), _f64(b)
+    # column by column over all rows: per row the same ascending-c sequence of
+    # separately rounded ops as the scalar kernel (numpy never contracts to FMA)
+    d = np.zeros(a.shape[0], dtype=np.float64)
+    for c in range(a.shape[1]):
+        diff = a[:, c] - b[:, c]
+        d = d + diff * diff
+    if metric_code(metric) == 1:
+        d = np.sqrt(d)
+    return sum_inorder(d) if d.size else 0.0

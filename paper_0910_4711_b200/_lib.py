@@ -11,13 +11,13 @@ import os
 
 import numpy as np
 
-from .errors import ConfigError, DomainError, InternalError, UsageError
+from .errors import ConfigError, DomainError, FormatError, InternalError, UsageError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # VQB200_LIB: another build of the same ABI (A/B timing, profiling builds)
 LIB_PATH = os.environ.get("VQB200_LIB") or os.path.join(_HERE, "libvqb200.so")
 
-VQB_OK, VQB_USAGE, VQB_CONFIG, VQB_DOMAIN, VQB_INTERNAL = 0, 1, 2, 3, 4
+VQB_OK, VQB_USAGE, VQB_CONFIG, VQB_DOMAIN, VQB_INTERNAL, VQB_FORMAT = 0, 1, 2, 3, 4, 5
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -103,6 +103,12 @@ def lib():
             "vqb_bench_assign": ([_P, _P, _I64, _I32, _P, _P, _P], _I32),
             "vqb_bench_upload": ([_P, _I64, _I32, _P], _I32),
             "vqb_debug_tc_tile": ([_P, _P, _I64, _P, _P], _I32),
+            "vqb_pixels_to_blocks": ([_P, _I64, _I64, _I64, _I64, _I32, _P, _P], _I32),
+            "vqb_blocks_to_pixels": ([_P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
+            "vqb_decode": ([_P, _I64, _P, _I64, _I64, _I32, _P], _I32),
+            "vqb_decode_pixels": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I32, _P], _I32),
+            "vqb_reconstruction_distortion": ([_P, _P, _I64, _I64, _I32, _I32, _P], _I32),
+            "vqb_open_pixels": ([_P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -123,6 +129,8 @@ def check(rc: int) -> None:
         raise UsageError(msg)
     if rc == VQB_DOMAIN:
         raise DomainError(msg)
+    if rc == VQB_FORMAT:
+        raise FormatError(msg)
     raise InternalError(msg)
 
 

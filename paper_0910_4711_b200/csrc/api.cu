@@ -266,11 +266,11 @@ int vqb_device_count(int* count) {
   return VQB_OK;
 }
 
-int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int64_t row_offset,
-             int64_t n_global, int device, vqb_session** out) {
-  *out = nullptr;
-  if ((x32 == nullptr) == (x64 == nullptr))
-    return fail(VQB_USAGE, "exactly one of x32 / x64 must be given");
+}  // extern "C"
+
+// Validation + session shell shared by vqb_open and vqb_open_pixels.
+static int new_session(int64_t rows, int64_t dim, int64_t row_offset, int64_t n_global, int device,
+                       std::unique_ptr<vqb_session>& s) {
   if (rows < 1 || dim < 1)
     return fail(VQB_USAGE, "training set must be at least 1x1, got %lldx%lld", (long long)rows,
                 (long long)dim);
@@ -286,7 +286,7 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
     return fail(VQB_INTERNAL, "no CUDA device available (the B200 path has no CPU fallback)");
   }
   CK(cudaSetDevice(device));
-  std::unique_ptr<vqb_session> s(new vqb_session());
+  s.reset(new vqb_session());
   s->device = device;
   CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device));
   if (int rc = s->make_streams()) return rc;
@@ -295,8 +295,22 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
   s->row_offset = row_offset;
   s->n_global = n_global;
   s->ntiles_global = (n_global + kTdTile - 1) / kTdTile;
-  const size_t count = (size_t)rows * dim;
   CK(dalloc(&s->scratch, 64));
+  return VQB_OK;
+}
+
+static int finish_open(std::unique_ptr<vqb_session>& s, vqb_session** out);
+
+extern "C" {
+
+int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int64_t row_offset,
+             int64_t n_global, int device, vqb_session** out) {
+  *out = nullptr;
+  if ((x32 == nullptr) == (x64 == nullptr))
+    return fail(VQB_USAGE, "exactly one of x32 / x64 must be given");
+  std::unique_ptr<vqb_session> s;
+  if (int rc = new_session(rows, dim, row_offset, n_global, device, s)) return rc;
+  const size_t count = (size_t)rows * dim;
   if (x32) {
     CK(dalloc(&s->x32, count + 16));
     CK(upload(s->x32, x32, count * sizeof(float), 16u << 20, s->copy_stream, s->stream));
@@ -320,6 +334,36 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
       cudaFree(tmp);
     }
   }
+  return finish_open(s, out);
+}
+
+int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64_t width, int64_t block,
+                    int device, vqb_session** out) {
+  *out = nullptr;
+  if (images < 1 || height < 1 || width < 1)
+    return fail(VQB_USAGE, "image must be at least 1x1, got %lldx%lld", (long long)width, (long long)height);
+  if (block < 1) return fail(VQB_USAGE, "block side must be >= 1, got %lld", (long long)block);
+  if (block > 4096) return fail(VQB_USAGE, "block side %lld too large", (long long)block);
+  const long long per_img = ((height + block - 1) / block) * ((width + block - 1) / block);
+  const long long rows = per_img * images;
+  std::unique_ptr<vqb_session> s;
+  if (int rc = new_session(rows, block * block, 0, rows, device, s)) return rc;
+  const size_t npx = (size_t)(images * height * width);
+  unsigned char* dpx = nullptr;
+  CK(dalloc(&dpx, npx));
+  std::unique_ptr<unsigned char, decltype(&cudaFree)> g(dpx, &cudaFree);
+  CK(dalloc(&s->x32, (size_t)rows * block * block + 16));
+  CK(upload(dpx, pixels, npx, 16u << 20, s->copy_stream, s->stream));
+  CK(launch_pixels_to_blocks_f32(dpx, images, height, width, (int)block, s->x32, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return finish_open(s, out);
+}
+
+}  // extern "C"
+
+static int finish_open(std::unique_ptr<vqb_session>& s, vqb_session** out) {
+  const long long rows = s->n, dim = s->dim;
+  const size_t count = (size_t)rows * dim;
   // max |x| (fixed-point scale, fast-path eligibility)
   unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
   CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
@@ -369,6 +413,8 @@ int vqb_open(const float* x32, const double* x64, int64_t rows, int64_t dim, int
   *out = s.release();
   return VQB_OK;
 }
+
+extern "C" {
 
 int vqb_close(vqb_session* s) {
   delete s;
@@ -1367,6 +1413,198 @@ int vqb_bench_upload(const void* src, int64_t bytes, int mode, double* seconds) 
   cudaStreamDestroy(ks);
   CK(e);
   *seconds = std::chrono::duration<double>(t1 - t0).count();
+  return VQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// data formats either side of the path (imaging.cu): block vectoriser, raster,
+// decode, reconstruction distortion.  Stateless, host buffers; device memory
+// from the stream-ordered pool (kept cached across calls).
+// ---------------------------------------------------------------------------
+
+}  // extern "C"
+
+namespace {
+
+struct OneShot {
+  cudaStream_t stream = nullptr, copy = nullptr;
+  int device = -1;
+  int init(int dev) {
+    CK(cudaSetDevice(dev));
+    if (device == dev && stream) return VQB_OK;
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    unsigned long long keep = ~0ULL;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    device = dev;
+    return VQB_OK;
+  }
+};
+std::mutex g_oneshot_mu;
+OneShot g_oneshot;
+
+template <typename T>
+struct PoolBuf {
+  T* p = nullptr;
+  cudaStream_t s;
+  explicit PoolBuf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t count) {
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), s);
+  }
+  ~PoolBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+int image_args(int64_t images, int64_t height, int64_t width, int64_t block, long long* count) {
+  if (images < 1 || height < 1 || width < 1)
+    return fail(VQB_USAGE, "image must be at least 1x1, got %lldx%lld", (long long)width, (long long)height);
+  if (block < 1) return fail(VQB_USAGE, "block side must be >= 1, got %lld", (long long)block);
+  if (block > 4096) return fail(VQB_USAGE, "block side %lld too large", (long long)block);
+  *count = ((height + block - 1) / block) * ((width + block - 1) / block) * images;
+  return VQB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vqb_pixels_to_blocks(const uint8_t* pixels, int64_t images, int64_t height, int64_t width, int64_t block,
+                         int device, double* out64, float* out32) {
+  long long count = 0;
+  if (int rc = image_args(images, height, width, block, &count)) return rc;
+  if ((out64 == nullptr) == (out32 == nullptr)) return fail(VQB_USAGE, "exactly one of out64 / out32 must be given");
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  if (int rc = g_oneshot.init(device)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  const size_t npx = (size_t)(images * height * width), nout = (size_t)count * block * block;
+  PoolBuf<unsigned char> px(st);
+  PoolBuf<char> out(st);
+  CK(px.alloc(npx));
+  CK(out.alloc(nout * (out64 ? 8 : 4)));
+  CK(upload(px.p, pixels, npx, 16u << 20, g_oneshot.copy, st));
+  if (out64)
+    CK(launch_pixels_to_blocks_f64(px.p, images, height, width, (int)block, reinterpret_cast<double*>(out.p), st));
+  else
+    CK(launch_pixels_to_blocks_f32(px.p, images, height, width, (int)block, reinterpret_cast<float*>(out.p), st));
+  CK(download(out64 ? static_cast<void*>(out64) : static_cast<void*>(out32), out.p, nout * (out64 ? 8 : 4), st));
+  return VQB_OK;
+}
+
+int vqb_blocks_to_pixels(const double* vectors, int64_t images, int64_t height, int64_t width, int64_t block,
+                         int device, uint8_t* pixels) {
+  long long count = 0;
+  if (int rc = image_args(images, height, width, block, &count)) return rc;
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  if (int rc = g_oneshot.init(device)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  const size_t npx = (size_t)(images * height * width), nin = (size_t)count * block * block;
+  PoolBuf<double> vin(st);
+  PoolBuf<unsigned char> px(st);
+  CK(vin.alloc(nin));
+  CK(px.alloc(npx));
+  CK(upload(vin.p, vectors, nin * sizeof(double), 16u << 20, g_oneshot.copy, st));
+  CK(launch_blocks_to_pixels(vin.p, nullptr, nullptr, images, height, width, (int)block, px.p, st));
+  CK(download(pixels, px.p, npx, st));
+  return VQB_OK;
+}
+
+int vqb_decode(const uint32_t* indices, int64_t n, const double* codebook, int64_t size, int64_t dim,
+               int device, double* out) {
+  if (n < 0 || size < 1 || dim < 1) return fail(VQB_USAGE, "decode needs a non-empty codebook");
+  if (n == 0) return VQB_OK;
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  if (int rc = g_oneshot.init(device)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  PoolBuf<double> cb(st);
+  PoolBuf<unsigned> idx(st);
+  PoolBuf<double> rows(st);
+  PoolBuf<int> bad(st);
+  CK(cb.alloc((size_t)(size * dim)));
+  CK(idx.alloc((size_t)n));
+  CK(bad.alloc(1));
+  // output in pieces of <= 2^27 doubles (1 GiB): device footprint bounded,
+  // the gather of piece i+1 overlaps nothing worth mentioning next to its D2H
+  const long long piece = std::max<long long>(1, std::min<long long>(n, (1LL << 27) / dim));
+  CK(rows.alloc((size_t)(piece * dim)));
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  CK(upload(cb.p, codebook, sizeof(double) * size * dim, 16u << 20, g_oneshot.copy, st));
+  CK(upload(idx.p, indices, sizeof(unsigned) * n, 16u << 20, g_oneshot.copy, st));
+  for (long long r0 = 0; r0 < n; r0 += piece) {
+    const long long m = std::min(piece, n - r0);
+    CK(launch_decode(idx.p + r0, m, (int)dim, cb.p, size, rows.p, bad.p, st));
+    CK(download(out + r0 * dim, rows.p, sizeof(double) * m * dim, st));
+  }
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hbad) return fail(VQB_FORMAT, "corrupt stream: index >= codebook size %lld", (long long)size);
+  return VQB_OK;
+}
+
+int vqb_decode_pixels(const uint32_t* indices, int64_t images, int64_t height, int64_t width, int64_t block,
+                      const double* codebook, int64_t size, int device, uint8_t* pixels) {
+  long long count = 0;
+  if (int rc = image_args(images, height, width, block, &count)) return rc;
+  if (size < 1) return fail(VQB_USAGE, "decode needs a non-empty codebook");
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  if (int rc = g_oneshot.init(device)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  const long long dim = block * block;
+  PoolBuf<double> cb(st);
+  PoolBuf<unsigned> idx(st);
+  PoolBuf<unsigned char> px(st);
+  PoolBuf<int> bad(st);
+  CK(cb.alloc((size_t)(size * dim)));
+  CK(idx.alloc((size_t)count));
+  CK(px.alloc((size_t)(images * height * width)));
+  CK(bad.alloc(1));
+  CK(upload(cb.p, codebook, sizeof(double) * size * dim, 16u << 20, g_oneshot.copy, st));
+  CK(upload(idx.p, indices, sizeof(unsigned) * count, 16u << 20, g_oneshot.copy, st));
+  // the raster reads codebook rows by index: validate the indices first
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  CK(launch_index_check(idx.p, count, size, bad.p, st));
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hbad) return fail(VQB_FORMAT, "corrupt stream: index >= codebook size %lld", (long long)size);
+  CK(launch_blocks_to_pixels(nullptr, idx.p, cb.p, images, height, width, (int)block, px.p, st));
+  CK(download(pixels, px.p, (size_t)(images * height * width), st));
+  return VQB_OK;
+}
+
+int vqb_reconstruction_distortion(const double* a, const double* b, int64_t n, int64_t dim, int metric,
+                                  int device, double* total) {
+  if (n < 0 || dim < 1) return fail(VQB_USAGE, "dimension must be >= 1");
+  if (metric != kSquared && metric != kEuclidean) return fail(VQB_USAGE, "unknown metric code %d", metric);
+  if (n == 0) {
+    *total = 0.0;
+    return VQB_OK;
+  }
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  if (int rc = g_oneshot.init(device)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  PoolBuf<double> da(st), db(st), d(st), tiles(st), out(st);
+  CK(da.alloc((size_t)(n * dim)));
+  CK(db.alloc((size_t)(n * dim)));
+  CK(d.alloc((size_t)n));
+  CK(tiles.alloc((size_t)((n + kTdTile - 1) / kTdTile)));
+  CK(out.alloc(1));
+  const size_t row_bytes = sizeof(double) * (size_t)dim;
+  const size_t piece = std::max<size_t>(row_bytes, ((size_t)16 << 20) / row_bytes * row_bytes);
+  CK(upload(da.p, a, row_bytes * n, piece, g_oneshot.copy, st));
+  // per-row distances of each piece of b as it lands
+  CK(upload(db.p, b, row_bytes * n, piece, g_oneshot.copy, st, [&](size_t off, size_t len) -> cudaError_t {
+    const long long r0 = (long long)(off / row_bytes), r1 = (long long)((off + len) / row_bytes);
+    return launch_pair_rows(da.p + r0 * dim, db.p + r0 * dim, r1 - r0, (int)dim, metric, d.p + r0, st);
+  }));
+  // sum_inorder (_kernels.py:92-98) for up to 2^20 rows; above, the fixed tree
+  // of 2048-row tiles (the training loop's distortion order)
+  CK(launch_distortion_sum(d.p, n, n <= (1LL << 20), tiles.p, out.p, st));
+  CK(cudaMemcpyAsync(total, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return VQB_OK;
 }
 

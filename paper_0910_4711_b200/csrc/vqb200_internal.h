@@ -154,6 +154,22 @@ cudaError_t launch_pair_distance(const double* a, const double* b, int dim, int 
                                  cudaStream_t s);
 bool fast_dim_supported(int dim);
 
+// block vectoriser / decode / reconstruction distortion (imaging.cu)
+cudaError_t launch_pixels_to_blocks_f32(const unsigned char* px, long long images, long long H, long long W,
+                                        int block, float* out, cudaStream_t s);
+cudaError_t launch_pixels_to_blocks_f64(const unsigned char* px, long long images, long long H, long long W,
+                                        int block, double* out, cudaStream_t s);
+// vecs[count][block^2] (or, with vecs == nullptr, codebook rows cb[idx[v]]) -> pixels
+cudaError_t launch_blocks_to_pixels(const double* vecs, const unsigned* idx, const double* cb, long long images,
+                                    long long H, long long W, int block, unsigned char* out, cudaStream_t s);
+cudaError_t launch_decode(const unsigned* idx, long long n, int L, const double* cb, long long K, double* out,
+                          int* bad, cudaStream_t s);
+cudaError_t launch_index_check(const unsigned* idx, long long n, long long K, int* bad, cudaStream_t s);
+cudaError_t launch_pair_rows(const double* a, const double* b, long long n, int dim, int metric, double* d,
+                             cudaStream_t s);
+cudaError_t launch_distortion_sum(const double* d, long long n, bool inorder, double* tiles, double* out,
+                                  cudaStream_t s);
+
 // tensor-core candidate pass (assign_tc.cu)
 constexpr int kTcChunk = 256;  // codewords per MMA N
 constexpr int kTcRows = 128;   // rows per tile (MMA M)

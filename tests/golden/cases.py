@@ -140,3 +140,57 @@ def encode_cases():
     cb = _f32(rng.uniform(0, 255, (1024, 16)))
     out.append(dict(x=_f32(rng.uniform(0, 255, (20000, 16))), cb=cb, workers=4))
     return out
+
+
+# ---------------------------------------------------------------------------
+# data formats either side of the path (storage.py / codec.py decode)
+# ---------------------------------------------------------------------------
+
+def image_cases():
+    """(pixels uint8 [h][w], block) -- ragged edges, every block side the band
+    kernel specialises (2, 4, 8, 16), sides it does not (1, 3, 5) and a band
+    too wide for shared memory (generic path)."""
+    rng = np.random.default_rng(5005)
+    out = []
+    out.append((np.arange(16, dtype=np.uint8).reshape(4, 4), 2))  # test_storage.py:236-241 layout
+    out.append((np.array([[1, 2], [3, 4]], dtype=np.uint8), 3))   # edge replication
+    out.append((np.array([[7]], dtype=np.uint8), 1))
+    grad = ((np.arange(9)[:, None] * 17 + np.arange(17)[None, :] * 5) % 256).astype(np.uint8)
+    out.append((grad, 5))
+    out.append((rng.integers(0, 256, (7, 13), dtype=np.uint8), 4))
+    out.append((rng.integers(0, 256, (48, 64), dtype=np.uint8), 8))
+    out.append((rng.integers(0, 256, (37, 70), dtype=np.uint8), 16))
+    out.append((rng.integers(0, 256, (65, 33), dtype=np.uint8), 4))
+    out.append((rng.integers(0, 256, (11, 10), dtype=np.uint8), 3))
+    out.append((rng.integers(0, 256, (5, 3000), dtype=np.uint8), 16))   # band = 48128 B, staged
+    out.append((rng.integers(0, 256, (7, 4000), dtype=np.uint8), 16))   # band > 48 KiB: generic
+    out.append((rng.integers(0, 256, (31, 29), dtype=np.uint8), 2))
+    return out
+
+
+def raster_vectors(vectors, seed):
+    """Block vectors perturbed past both clamps and onto exact .5 ties."""
+    rng = np.random.default_rng(seed)
+    v = np.asarray(vectors, dtype=np.float64) + rng.normal(0, 40, vectors.shape)
+    half = rng.random(vectors.shape) < 0.2
+    v[half] = np.floor(v[half]) + 0.5
+    return v
+
+
+def decode_cases():
+    rng = np.random.default_rng(6006)
+    out = []
+    for n, k, dim in ((1000, 64, 16), (777, 1, 7), (513, 256, 64), (40, 5, 3)):
+        cb = rng.normal(0, 50, (k, dim))
+        out.append(dict(idx=rng.integers(0, k, n).astype(np.uint32), cb=cb))
+    return out
+
+
+def distortion_cases():
+    rng = np.random.default_rng(7007)
+    out = []
+    for n, dim, metric in ((1000, 16, "squared_euclidean"), (513, 7, "euclidean"), (3, 1, "squared_euclidean"),
+                           (4096, 64, "squared_euclidean")):
+        a = rng.normal(0, 30, (n, dim))
+        out.append(dict(a=a, b=a + rng.normal(0, 3, (n, dim)), metric=metric))
+    return out

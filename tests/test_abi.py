@@ -124,6 +124,9 @@ def test_public_names_match_the_reference_surface():
                  "centroid", "distance", "partition_training", "parallel_assign", "integrate",
                  "parallel_update", "ChunkPlan", "UpdateAssignment", "EncodedStream",
                  "VqError", "UsageError", "ConfigError", "DomainError", "FormatError",
-                 "InternalError", "SQUARED_EUCLIDEAN", "EUCLIDEAN"):
+                 "InternalError", "SQUARED_EUCLIDEAN", "EUCLIDEAN", "decode",
+                 "reconstruction_distortion", "BlockGrid", "pixels_to_blocks", "blocks_to_image",
+                 "image_to_blocks", "parse_pgm", "pgm_bytes", "read_pgm", "save_codebook",
+                 "load_codebook", "save_encoded", "load_encoded"):
         assert hasattr(vq, name), name
         assert name in vq.__all__, name
