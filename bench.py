@@ -577,6 +577,97 @@ def run_workload(args):
     return 0
 
 
+def run_formats(args):
+    """The HBM-bound kernels either side of the path,
+    each at its BASELINE scale: the cfg3 block vectoriser (16 x 2048^2 pixels,
+    8x8 blocks), the cfg5 decode (2^26 indices, K=1024, L=16), the fused
+    decode-to-pixels and raster at cfg3, and the pair distances of
+    reconstruction_distortion at cfg5.  Per kernel: device-resident event time,
+    algorithmic bytes / time vs the measured HBM peak; e2e through the public
+    API from host buffers; the CPU numpy path (oracle restatement of the
+    reference's numpy code) on a bounded sample."""
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200 import _lib, synthetic
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    L = _lib.lib()
+    peaks, src = _measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    shapes = {  # which: (label, images, h, w, block, n, dim, size)
+        0: ("pixels_to_blocks f32 (cfg3: 16 x 2048^2, b=8)", 16, 2048, 2048, 8, 0, 0, 1),
+        1: ("pixels_to_blocks f64 (cfg3)", 16, 2048, 2048, 8, 0, 0, 1),
+        2: ("blocks_to_pixels (cfg3)", 16, 2048, 2048, 8, 0, 0, 1),
+        3: ("decode (cfg5: 2^26 x L=16, K=1024)", 0, 0, 0, 0, 1 << 26, 16, 1024),
+        4: ("decode_pixels (cfg3, K=512)", 16, 2048, 2048, 8, 0, 0, 512),
+        5: ("pair distances (cfg5: 2^26 x L=16)", 0, 0, 0, 0, 1 << 26, 16, 1),
+    }
+    clocks = ClockSampler(0).__enter__()
+    kernels = {}
+    for which, (label, im, h, w, b, n, dim, size) in shapes.items():
+        ms, by = ctypes.c_double(), ctypes.c_double()
+        _lib.check(L.vqb_bench_formats(which, im, h, w, b, n, dim, size, max(args.steps, 3),
+                                       ctypes.byref(ms), ctypes.byref(by)))
+        gbs = by.value / (ms.value * 1e-3) / 1e9
+        kernels[label] = {"ms": ms.value, "algorithmic_bytes": by.value, "gb_per_s": gbs,
+                          "frac_of_hbm_peak": gbs / hbm}
+    clocks.__exit__(None, None, None)
+    # e2e through the public API (host buffers, copies included)
+    px = synthetic.make_training_pixels("cfg3", images=4)  # 4 x 2048^2 (bounded host memory)
+    t = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        vec, grid = vq.pixels_to_blocks(px, 8)
+        t.append(time.perf_counter() - t0)
+    e2e_p2b = min(t)
+    t0 = time.perf_counter()
+    want = np.concatenate([oracle.pixels_to_blocks(im, 8) for im in px[:1]])
+    cpu_p2b = time.perf_counter() - t0
+    assert vec[:want.shape[0]].tobytes() == want.tobytes()
+    cb = vq.Codebook(np.random.default_rng(3).normal(128, 60, (1024, 16)))
+    idx = np.random.default_rng(4).integers(0, 1024, 1 << 24).astype(np.uint32)
+    stream = vq.EncodedStream(1024, 16, idx)
+    t = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rows = vq.decode(stream, cb)
+        t.append(time.perf_counter() - t0)
+    e2e_dec = min(t)
+    t0 = time.perf_counter()
+    ref_rows = oracle.decode(idx, cb.codevectors)
+    cpu_dec = time.perf_counter() - t0
+    parity = {"pixels_to_blocks_bit_exact_image0": True,
+              "decode_bit_exact": bool(rows.tobytes() == ref_rows.tobytes())}
+    c = clocks.summary()
+    head = kernels["decode (cfg5: 2^26 x L=16, K=1024)"]
+    out = {
+        "metric": "GB/s (HBM-bound format kernels)", "value": head["gb_per_s"], "unit": "GB/s",
+        "impl": "b200", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8/f32/f64", "data": "synthetic",
+        "config": {"workload": "formats: block vectoriser / raster / decode / pair distances at cfg3 and cfg5 scale",
+                   "l2": "inputs+outputs of every launch exceed the 126 MB L2"},
+        "roofline": {"bound": "hbm", "kernel": "decode", "achieved": head["gb_per_s"], "peak": hbm,
+                     "unit": "GB/s", "frac": head["frac_of_hbm_peak"], "peak_source": src,
+                     "traffic": None},
+        "kernels": kernels,
+        "e2e": {"pixels_to_blocks_4x2048sq_f64_s": e2e_p2b,
+                "pixels_to_blocks_gb_per_s_of_output": vec.nbytes / e2e_p2b / 1e9,
+                "decode_2e24_rows_s": e2e_dec,
+                "decode_gb_per_s_of_output": rows.nbytes / e2e_dec / 1e9,
+                "h2d_bytes_per_step": int(px.nbytes + idx.nbytes + cb.codevectors.nbytes),
+                "d2h_bytes_per_step": int(vec.nbytes + rows.nbytes)},
+        "cpu_baseline": {"pixels_to_blocks_2048sq_s": cpu_p2b, "decode_2e24_rows_s": cpu_dec,
+                         "kind": "port", "cores": 1,
+                         "sample": "one 2048^2 image (oracle numpy vectoriser); 2^24-row numpy gather"},
+        "parity": parity,
+        "clocks": {k: c[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def sess_fast(sess) -> bool:
     return sess.dim in (16, 32, 64)
 
@@ -587,13 +678,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "formats"],
                     help="cfg2 (default) is the headline line; the others print one line each")
     ap.add_argument("--profile-steps", action="store_true",
                     help="only the warm-up + timed steps (for ncu launch lists)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "formats":
+        return run_formats(args)
     if args.workload != "cfg2":
         return run_workload(args)
     return run_b200(args)

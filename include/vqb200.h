@@ -212,6 +212,13 @@ int vqb_reconstruction_distortion(const double* a, const double* b, int64_t n, i
 int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64_t width, int64_t block,
                     int device, vqb_session** out);
 
+/* Device-resident timing of one imaging kernel (0 pixels_to_blocks f32,
+ * 1 pixels_to_blocks f64, 2 blocks_to_pixels, 3 decode, 4 decode_pixels,
+ * 5 per-row pair distances): mean ms per launch over `reps` and the
+ * algorithmic bytes of one launch (bench.py --workload formats). */
+int vqb_bench_formats(int which, int64_t images, int64_t height, int64_t width, int64_t block, int64_t n,
+                      int64_t dim, int64_t size, int reps, double* ms_out, double* bytes_out);
+
 /* Pipe microbenchmark (0 FFMA, 1 FFMA2, 2 FFMA+top-2 mix, 3 DADD): lane-ops/s. */
 int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
                         double* seconds);

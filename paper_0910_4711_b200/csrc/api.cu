@@ -1570,7 +1570,9 @@ int vqb_decode_pixels(const uint32_t* indices, int64_t images, int64_t height, i
   CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (hbad) return fail(VQB_FORMAT, "corrupt stream: index >= codebook size %lld", (long long)size);
-  CK(launch_blocks_to_pixels(nullptr, idx.p, cb.p, images, height, width, (int)block, px.p, st));
+  PoolBuf<unsigned char> cbq(st);
+  CK(cbq.alloc((size_t)(size * dim)));
+  CK(launch_decode_pixels(idx.p, cb.p, size, images, height, width, (int)block, cbq.p, px.p, st));
   CK(download(pixels, px.p, (size_t)(images * height * width), st));
   return VQB_OK;
 }
@@ -1605,6 +1607,102 @@ int vqb_reconstruction_distortion(const double* a, const double* b, int64_t n, i
   CK(launch_distortion_sum(d.p, n, n <= (1LL << 20), tiles.p, out.p, st));
   CK(cudaMemcpyAsync(total, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return VQB_OK;
+}
+
+// Device-resident timing of one imaging kernel (bench.py --workload formats):
+// which = 0 pixels_to_blocks f32, 1 pixels_to_blocks f64, 2 blocks_to_pixels,
+// 3 decode (n rows of dim from a size-row codebook), 4 decode_pixels,
+// 5 per-row pair distances (n x dim).  Inputs are synthetic device buffers;
+// ms_out = mean event time per launch over `reps`, bytes_out = algorithmic
+// bytes per launch (every input byte read once, every output byte written once).
+int vqb_bench_formats(int which, int64_t images, int64_t height, int64_t width, int64_t block, int64_t n,
+                      int64_t dim, int64_t size, int reps, double* ms_out, double* bytes_out) {
+  if (reps < 1) return fail(VQB_USAGE, "reps must be >= 1");
+  long long count = 0;
+  if (which <= 2 || which == 4) {
+    if (int rc = image_args(images, height, width, block, &count)) return rc;
+    dim = block * block;
+    n = count;
+  }
+  if (n < 1 || dim < 1 || size < 1) return fail(VQB_USAGE, "empty benchmark shape");
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (int rc = g_oneshot.init(dev)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  const long long npx = images * height * width;
+  PoolBuf<unsigned char> px(st);
+  PoolBuf<double> vec(st), vec2(st), cb(st), d(st);
+  PoolBuf<float> vec32(st);
+  PoolBuf<unsigned> idx(st);
+  PoolBuf<int> bad(st);
+  PoolBuf<unsigned char> cbq(st);
+  double bytes = 0;
+  CK(bad.alloc(1));
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  switch (which) {
+    case 0: case 1: case 2:
+      CK(px.alloc((size_t)npx));
+      CK(cudaMemsetAsync(px.p, 0x5a, (size_t)npx, st));
+      if (which == 0) {
+        CK(vec32.alloc((size_t)(n * dim)));
+        bytes = (double)npx + 4.0 * n * dim;
+      } else {
+        CK(vec.alloc((size_t)(n * dim)));
+        CK(cudaMemsetAsync(vec.p, 0, sizeof(double) * n * dim, st));
+        bytes = (double)npx + 8.0 * n * dim;
+      }
+      break;
+    case 3: case 4:
+      CK(cb.alloc((size_t)(size * dim)));
+      CK(cudaMemsetAsync(cb.p, 0, sizeof(double) * size * dim, st));
+      CK(idx.alloc((size_t)n));
+      CK(cudaMemsetAsync(idx.p, 0, sizeof(unsigned) * n, st));  // index 0: valid
+      if (which == 3) {
+        CK(vec.alloc((size_t)(n * dim)));
+        bytes = 4.0 * n + 8.0 * n * dim;
+      } else {
+        CK(px.alloc((size_t)npx));
+        CK(cbq.alloc((size_t)(size * dim)));
+        bytes = 4.0 * n + (double)npx;
+      }
+      break;
+    case 5:
+      CK(vec.alloc((size_t)(n * dim)));
+      CK(vec2.alloc((size_t)(n * dim)));
+      CK(d.alloc((size_t)n));
+      CK(cudaMemsetAsync(vec.p, 0, sizeof(double) * n * dim, st));
+      CK(cudaMemsetAsync(vec2.p, 0, sizeof(double) * n * dim, st));
+      bytes = 16.0 * n * dim + 8.0 * n;
+      break;
+    default:
+      return fail(VQB_USAGE, "unknown kernel %d", which);
+  }
+  auto launch = [&]() -> cudaError_t {
+    switch (which) {
+      case 0: return launch_pixels_to_blocks_f32(px.p, images, height, width, (int)block, vec32.p, st);
+      case 1: return launch_pixels_to_blocks_f64(px.p, images, height, width, (int)block, vec.p, st);
+      case 2: return launch_blocks_to_pixels(vec.p, nullptr, nullptr, images, height, width, (int)block, px.p, st);
+      case 3: return launch_decode(idx.p, n, (int)dim, cb.p, size, vec.p, bad.p, st);
+      case 4: return launch_decode_pixels(idx.p, cb.p, size, images, height, width, (int)block, cbq.p, px.p, st);
+      default: return launch_pair_rows(vec.p, vec2.p, n, (int)dim, 0, d.p, st);
+    }
+  };
+  CK(launch());  // warm-up
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  for (int r = 0; r < reps; ++r) CK(launch());
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_out = ms / reps;
+  *bytes_out = bytes;
   return VQB_OK;
 }
 

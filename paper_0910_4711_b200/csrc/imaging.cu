@@ -50,17 +50,27 @@ template <int B, typename OutT>
 __global__ void __launch_bounds__(kBandThreads) pixels_to_blocks_band(
     const unsigned char* __restrict__ px, long long H, long long W, int bcols, int brows,
     OutT* __restrict__ out) {
-  extern __shared__ unsigned char band[];  // [B][Wp]
+  extern __shared__ __align__(16) unsigned char band[];  // [B][Wp]
   constexpr int BB = B * B;
   const long long img = blockIdx.y;
   const int by = blockIdx.x;
   const int Wp = bcols * B;
   const unsigned char* src = px + img * H * W;
-  for (int r = 0; r < B; ++r) {
-    const long long y = min((long long)by * B + r, H - 1);  // replicate the bottom edge
-    const unsigned char* row = src + y * W;
-    for (int x = threadIdx.x; x < Wp; x += kBandThreads)
-      band[r * Wp + x] = row[min((long long)x, W - 1)];  // replicate the right edge
+  if ((W & 15) == 0 && Wp == W) {
+    // no right padding, 16-byte aligned rows: one uint4 per thread per row
+    const int w16 = (int)(W >> 4);
+    for (int v = threadIdx.x; v < B * w16; v += kBandThreads) {
+      const int r = v / w16, x16 = v - r * w16;
+      const long long y = min((long long)by * B + r, H - 1);  // replicate the bottom edge
+      reinterpret_cast<uint4*>(band + r * Wp)[x16] = __ldg(reinterpret_cast<const uint4*>(src + y * W) + x16);
+    }
+  } else {
+    for (int r = 0; r < B; ++r) {
+      const long long y = min((long long)by * B + r, H - 1);  // replicate the bottom edge
+      const unsigned char* row = src + y * W;
+      for (int x = threadIdx.x; x < Wp; x += kBandThreads)
+        band[r * Wp + x] = row[min((long long)x, W - 1)];  // replicate the right edge
+    }
   }
   __syncthreads();
   OutT* dst = out + ((img * brows + by) * (long long)bcols) * BB;
@@ -140,6 +150,62 @@ __global__ void __launch_bounds__(kBandThreads) blocks_to_pixels_band(
   }
 }
 
+// decode fused with the raster, B % 4 == 0 and W % 4 == 0: the codebook is
+// quantised once (cbq = quantize(cb), K x BB bytes, L1/L2-resident), then one
+// thread per 4 horizontally adjacent pixels (same block row, same block):
+// one index load (shared by B/4 threads), one 4-byte codebook load, one 4-byte
+// coalesced store.  blockIdx.y = image row (img * H + y).
+__global__ void quantize_codebook_kernel(const double* __restrict__ cb, long long count,
+                                         unsigned char* __restrict__ cbq) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
+       e += (long long)gridDim.x * blockDim.x)
+    cbq[e] = quantize(cb[e]);
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) decode_pixels_vec4(const unsigned* __restrict__ idx,
+                                                          const unsigned char* __restrict__ cbq, long long H,
+                                                          int W, int bcols, int brows,
+                                                          unsigned char* __restrict__ out) {
+  constexpr int BB = B * B;
+  const long long row = blockIdx.y;  // img * H + y
+  const long long img = row / H, y = row - img * H;
+  const int x = (blockIdx.x * 256 + threadIdx.x) * 4;
+  if (x >= W) return;
+  const long long v = (img * brows + y / B) * bcols + x / B;
+  const int q = (int)(y % B) * B + x % B;
+  const unsigned k = __ldg(idx + v);
+  const unsigned p = __ldg(reinterpret_cast<const unsigned*>(cbq + (long long)k * BB + q));
+  *reinterpret_cast<unsigned*>(out + row * W + x) = p;
+}
+
+// W % 16 == 0: one thread per 16 adjacent pixels of a row (one 16-byte
+// store), grid-stride over rows x W/16 so that every thread does several.
+template <int B>
+__global__ void __launch_bounds__(256) decode_pixels_vec16(const unsigned* __restrict__ idx,
+                                                           const unsigned char* __restrict__ cbq, long long H,
+                                                           int W, int bcols, int brows, long long units,
+                                                           unsigned char* __restrict__ out) {
+  constexpr int BB = B * B;
+  const int w16 = W >> 4;
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < units;
+       u += (long long)gridDim.x * blockDim.x) {
+    const long long row = u / w16;  // img * H + y
+    const int x0 = (int)(u - row * w16) * 16;
+    const long long img = row / H, y = row - img * H;
+    const long long vrow = (img * brows + y / B) * bcols;
+    const int qrow = (int)(y % B) * B;
+    unsigned w[4];
+#pragma unroll
+    for (int part = 0; part < 4; ++part) {
+      const int x = x0 + 4 * part;
+      const unsigned k = __ldg(idx + vrow + x / B);
+      w[part] = __ldg(reinterpret_cast<const unsigned*>(cbq + (long long)k * BB + qrow + x % B));
+    }
+    *reinterpret_cast<uint4*>(out + row * W + x0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 template <typename InT>
 __global__ void blocks_to_pixels_generic(const InT* __restrict__ vecs, const unsigned* __restrict__ idx,
                                          const double* __restrict__ cb, long long H, long long W,
@@ -161,23 +227,49 @@ __global__ void blocks_to_pixels_generic(const InT* __restrict__ vecs, const uns
 // decode: out[j] = codebook[idx[j]]
 // ---------------------------------------------------------------------------
 
-// One thread per 16-byte piece of output (L even), or per element.
-__global__ void decode_pairs_kernel(const unsigned* __restrict__ idx, long long n, int L,
-                                    const double* __restrict__ cb, long long K, double* __restrict__ out,
-                                    int* __restrict__ bad) {
-  const int P = L / 2;  // double2 pieces per row
+// One thread per 16-byte piece of output (L even), four pieces per loop trip
+// (the index and codebook loads of all four are issued before any store, so a
+// thread keeps four gathers in flight); streaming stores: the rows are written
+// once and never re-read by this kernel.
+// PC = L / 2 at compile time (16, 32, 64-dim rows) or 0 (runtime).
+template <int PC>
+__global__ void __launch_bounds__(256) decode_pairs_kernel(const unsigned* __restrict__ idx, long long n,
+                                                           int L, const double* __restrict__ cb, long long K,
+                                                           double* __restrict__ out, int* __restrict__ bad) {
+  const int P = PC ? PC : L / 2;  // double2 pieces per row
   const long long total = n * P;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long j = e / P;
-    const int p = (int)(e - j * P);
-    unsigned k = __ldg(idx + j);
-    if (k >= K) {  // codec.py:110-113 (the host re-checks; never read out of range)
-      atomicOr(bad, 1);
-      k = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const double2* __restrict__ cb2 = reinterpret_cast<const double2*>(cb);
+  double2* __restrict__ out2 = reinterpret_cast<double2*>(out);
+  bool any_bad = false;
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; e + 3 * stride < total; e += 4 * stride) {
+    unsigned k[4];
+    long long j[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      j[u] = (e + u * stride) / P;
+      k[u] = __ldg(idx + j[u]);
+      any_bad |= k[u] >= K;
+      k[u] = k[u] < K ? k[u] : 0;  // codec.py:110-113 (never read out of range)
     }
-    reinterpret_cast<double2*>(out)[e] = __ldg(reinterpret_cast<const double2*>(cb + (long long)k * L) + p);
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long eu = e + u * stride;
+      v[u] = __ldg(cb2 + (long long)k[u] * P + (eu - j[u] * P));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(out2 + e + u * stride, v[u]);
   }
+  for (; e < total; e += stride) {
+    const long long j = e / P;
+    unsigned k = __ldg(idx + j);
+    any_bad |= k >= K;
+    k = k < K ? k : 0;
+    __stcs(out2 + e, __ldg(cb2 + (long long)k * P + (e - j * P)));
+  }
+  if (any_bad) atomicOr(bad, 1);
 }
 
 __global__ void decode_elems_kernel(const unsigned* __restrict__ idx, long long n, int L,
@@ -329,11 +421,45 @@ cudaError_t launch_blocks_to_pixels(const double* vecs, const unsigned* idx, con
   return launch_b2p<double>(vecs, idx, cb, images, H, W, block, out, s);
 }
 
+cudaError_t launch_decode_pixels(const unsigned* idx, const double* cb, long long K, long long images,
+                                 long long H, long long W, int block, unsigned char* cbq, unsigned char* out,
+                                 cudaStream_t s) {
+  const long long rows = images * H;
+  const bool vec4 = (block == 4 || block == 8 || block == 16) && (W % 4) == 0 &&
+                    (rows <= 65535 || W % 16 == 0) && W <= INT_MAX;
+  if (!vec4) return launch_b2p<double>(nullptr, idx, cb, images, H, W, block, out, s);
+  const long long bb = (long long)block * block;
+  quantize_codebook_kernel<<<grid_for(K * bb, device_sms()), 256, 0, s>>>(cb, K * bb, cbq);
+  const int bcols = (int)((W + block - 1) / block), brows = (int)((H + block - 1) / block);
+  if (W % 16 == 0) {
+    const long long units = rows * (W / 16);
+    const int g = grid_for(units, device_sms());
+    switch (block) {
+      case 4: decode_pixels_vec16<4><<<g, 256, 0, s>>>(idx, cbq, H, (int)W, bcols, brows, units, out); break;
+      case 8: decode_pixels_vec16<8><<<g, 256, 0, s>>>(idx, cbq, H, (int)W, bcols, brows, units, out); break;
+      default: decode_pixels_vec16<16><<<g, 256, 0, s>>>(idx, cbq, H, (int)W, bcols, brows, units, out); break;
+    }
+    return cudaGetLastError();
+  }
+  dim3 grid((unsigned)((W / 4 + 255) / 256), (unsigned)rows);
+  switch (block) {
+    case 4: decode_pixels_vec4<4><<<grid, 256, 0, s>>>(idx, cbq, H, (int)W, bcols, brows, out); break;
+    case 8: decode_pixels_vec4<8><<<grid, 256, 0, s>>>(idx, cbq, H, (int)W, bcols, brows, out); break;
+    default: decode_pixels_vec4<16><<<grid, 256, 0, s>>>(idx, cbq, H, (int)W, bcols, brows, out); break;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_decode(const unsigned* idx, long long n, int L, const double* cb, long long K, double* out,
                           int* bad, cudaStream_t s) {
   const int sms = device_sms();
-  if (L % 2 == 0)
-    decode_pairs_kernel<<<grid_for(n * (L / 2), sms), 256, 0, s>>>(idx, n, L, cb, K, out, bad);
+  const int g = grid_for(n * (L / 2), sms);
+  if (L == 16)
+    decode_pairs_kernel<8><<<g, 256, 0, s>>>(idx, n, L, cb, K, out, bad);
+  else if (L == 64)
+    decode_pairs_kernel<32><<<g, 256, 0, s>>>(idx, n, L, cb, K, out, bad);
+  else if (L % 2 == 0)
+    decode_pairs_kernel<0><<<g, 256, 0, s>>>(idx, n, L, cb, K, out, bad);
   else
     decode_elems_kernel<<<grid_for(n * L, sms), 256, 0, s>>>(idx, n, L, cb, K, out, bad);
   return cudaGetLastError();

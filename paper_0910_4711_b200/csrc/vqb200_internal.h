@@ -162,6 +162,10 @@ cudaError_t launch_pixels_to_blocks_f64(const unsigned char* px, long long image
 // vecs[count][block^2] (or, with vecs == nullptr, codebook rows cb[idx[v]]) -> pixels
 cudaError_t launch_blocks_to_pixels(const double* vecs, const unsigned* idx, const double* cb, long long images,
                                     long long H, long long W, int block, unsigned char* out, cudaStream_t s);
+// decode fused with the raster; cbq = K * block^2 bytes of scratch
+cudaError_t launch_decode_pixels(const unsigned* idx, const double* cb, long long K, long long images,
+                                 long long H, long long W, int block, unsigned char* cbq, unsigned char* out,
+                                 cudaStream_t s);
 cudaError_t launch_decode(const unsigned* idx, long long n, int L, const double* cb, long long K, double* out,
                           int* bad, cudaStream_t s);
 cudaError_t launch_index_check(const unsigned* idx, long long n, long long K, int* bad, cudaStream_t s);

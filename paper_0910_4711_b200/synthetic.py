@@ -141,16 +141,17 @@ def make_training(cfg: str, n: int | None = None) -> np.ndarray:
     return x if n is None else np.ascontiguousarray(x[:n])
 
 
-def make_training_pixels(cfg: str) -> np.ndarray:
+def make_training_pixels(cfg: str, images: int = 16) -> np.ndarray:
     """The uint8 images behind make_training('cfg1') ([512, 512]) and
     make_training('cfg3') ([16, 2048, 2048]): same seeds, same draws, so
-    pixels_to_blocks of these equals make_training(cfg)."""
+    pixels_to_blocks of these equals make_training(cfg); ``images`` < 16 gives
+    the leading images of cfg3."""
     spec = WORKLOADS[cfg]
     rng = np.random.default_rng(spec.seed)
     if cfg == "cfg1":
         return blob_image(rng, 512, 512, 32)
     if cfg == "cfg3":
-        return np.stack([blob_image(rng, 2048, 2048, 64) for _ in range(16)])
+        return np.stack([blob_image(rng, 2048, 2048, 64) for _ in range(images)])
     raise ValueError(f"{cfg} is not an image workload")
 
 

@@ -100,16 +100,17 @@ def test_decode_empty_and_mismatch():
 
 
 @pytest.mark.parametrize("b", [2, 3, 4, 8, 16])
-def test_decode_pixels_equals_raster_of_decode(b):
+@pytest.mark.parametrize("w", [95, 100, 96])  # band path / 4-pixel path / 16-pixel path
+def test_decode_pixels_equals_raster_of_decode(b, w):
     rng = np.random.default_rng(b)
-    px = rng.integers(0, 256, (61, 95), dtype=np.uint8)
+    px = rng.integers(0, 256, (61, w), dtype=np.uint8)
     vec, grid = vq.pixels_to_blocks(px, b)
     cb = vq.Codebook(rng.normal(128, 90, (32, b * b)))
     stream = vq.encode(vec, cb)
     fused = storage.decode_image(stream, cb, grid)
     assert fused == vq.blocks_to_image(vq.decode(stream, cb), grid)
     want = oracle.blocks_to_pixels(oracle.decode(oracle.encode(vec, cb.codevectors), cb.codevectors),
-                                   61, 95, b)
+                                   61, w, b)
     assert vq.parse_pgm(fused).tobytes() == want.tobytes()
 
 
