@@ -37,6 +37,12 @@
 
 namespace vqb {
 
+// suspend-time hint of the certification warps' wait for tile results
+#ifndef VQB_SLEEP_NS
+#define VQB_SLEEP_NS 20000
+#endif
+constexpr uint32_t kSleepNs = VQB_SLEEP_NS;
+
 template <int L>
 struct TcCfg {
   // epilogue warps: kParts per TMEM lane quarter, each scanning 256 / kParts
@@ -342,7 +348,10 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
     const float inv = 1.0f / dscale;
     const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
     const int rb = (int)(i & 1);
-    pwait(&m->res_full[rb], (uint32_t)((i >> 1) & 1), 0);
+    if (C::kCertWarps && !prof)  // dedicated warps: sleep, do not spin
+      mbar_wait_sleep(&m->res_full[rb], (uint32_t)((i >> 1) & 1), kSleepNs);
+    else
+      pwait(&m->res_full[rb], (uint32_t)((i >> 1) & 1), 0);
     float pm[C::kParts];
     int pc[C::kParts], pi[C::kParts];
 #pragma unroll
@@ -656,8 +665,13 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
             float v[32];
             load(q4, v);
+            // four independent FMNMX3 chains (a single chain of 16 is
+            // latency-bound: the epilogue's top stall was the fixed-latency
+            // dependency wait)
+            float c4[4] = {cm, INFINITY, INFINITY, INFINITY};
 #pragma unroll
-            for (int t = 0; t < 32; t += 2) cm = fminf(cm, fminf(v[t], v[t + 1]));
+            for (int t = 0; t < 32; t += 2) c4[(t >> 1) & 3] = fminf(c4[(t >> 1) & 3], fminf(v[t], v[t + 1]));
+            cm = fminf(fminf(c4[0], c4[1]), fminf(c4[2], c4[3]));
           }
           const float mnew = fminf(m1, cm);
           const float thr = fmaf(3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw), dscale, mnew);
@@ -670,13 +684,13 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
             float v[32];
             load(q4, v);
-            unsigned acc2[2] = {0u, 0u};  // two chains
+            unsigned acc4[4] = {0u, 0u, 0u, 0u};  // four chains
 #pragma unroll
             for (int t = 0; t < 32; ++t)  // FSETP + predicated IADD
               asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
-                  : "+r"(acc2[t & 1])
+                  : "+r"(acc4[t & 3])
                   : "f"(v[t]), "f"(thr), "r"(0x10000u + (unsigned)t));
-            const unsigned acc = acc2[0] + acc2[1];
+            const unsigned acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
             if (acc) {
               cnt += (int)(acc >> 16);
               i1 = c * kTcChunk + h * span + q4 * 32 + (int)(acc & 0xffffu);  // exact when alone
