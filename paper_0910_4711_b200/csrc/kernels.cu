@@ -946,7 +946,12 @@ __host__ __device__ inline SumsPlan sums_plan(int K, int dim) {
   p.nkc = (K + p.kc - 1) / p.kc;
   return p;
 }
-constexpr int kWStageStride = 20;  // staged row stride (elements), padded against bank conflicts
+constexpr int kWStageStride = 20;
+// block-table path: lane-sequential runs (1) or strided rows + warp segmented scan (0)
+#ifndef VQB_SUMS_RUNS
+#define VQB_SUMS_RUNS 1
+#endif
+constexpr bool kSumsRuns = VQB_SUMS_RUNS != 0;  // staged row stride (elements), padded against bank conflicts
 
 // exact int64 accumulation from two native 32-bit shared atomics
 __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, long long t) {
@@ -1102,7 +1107,58 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const long long n = a.n;
   const long long lo = n * blockIdx.x / gridDim.x;
   const long long hi = n * (blockIdx.x + 1) / gridDim.x;
-  if (!warp_sink) {
+  if (!warp_sink && kSumsRuns) {
+    // Block tables, lane-sequential runs: thread t owns a contiguous slice of
+    // the block's rows and keeps the running per-dimension sum of the current
+    // cell in registers, flushing it (one exact int64 smem add per dimension)
+    // only when the cell changes.  Rows of one cell that follow each other
+    // (image blocks of smooth regions) cost one atomic per run instead of one
+    // per row; with no runs it is one flush per row, as the strided path.
+    const long long per = (hi - lo + kSumThreads - 1) / kSumThreads;
+    const long long rb = lo + (long long)tid * per;
+    const long long re = min(hi, rb + per);
+    for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
+      const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
+      long long acc[16];
+#pragma unroll
+      for (int l = 0; l < 16; ++l) acc[l] = 0;
+      int cur = -1;
+      unsigned run = 0;
+      auto flush = [&]() {
+#pragma unroll
+        for (int l = 0; l < 16; ++l) {
+          if (l < cw) {
+            const long long w = (long long)(c0 + l - d_lo) * ncell + cur;
+            smem_add_i64(blo + w, bhi + w, acc[l]);
+          }
+          acc[l] = 0;
+        }
+        if (dy == 0 && c0 == d_lo) atomicAdd(bcounts + cur, run);
+        run = 0;
+      };
+      long long row = rb;
+      int cell_next = row < re ? (zero_cells ? 0 : a.idx[row]) : -1;
+      for (; row < re; ++row) {
+        const int cell = cell_next;
+        if (row + 1 < re) cell_next = zero_cells ? 0 : a.idx[row + 1];
+        const int lc = (cell >= c_lo && cell < c_hi) ? cell - (int)c_lo : -1;
+        if (lc != cur) {
+          if (cur >= 0) flush();
+          cur = lc;
+        }
+        if (lc >= 0) {
+          XT xr[16];
+          load_row16<XT, DIM>(X, row, dim, c0, true, xr);
+#pragma unroll
+          for (int l = 0; l < 16; ++l)
+            if (l < cw) acc[l] += to_fixed((double)xr[l], scale);
+          ++run;
+        }
+      }
+      if (cur >= 0) flush();
+    }
+  }
+  if (!warp_sink && !kSumsRuns) {
     // Block tables.  Two rows per thread per step, and every load of both
     // (cells and coordinates) issued before the first atomic: the rows'
     // HBM/L2 latency overlaps instead of chaining per row.
