@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       float m1 = INFINITY;
       int i1 = 0, cnt = 0;
       int nc = 0;
-      int cand[kTcShort];
+      int cand[kTcShort] = {0, 0, 0, 0, 0, 0, 0, 0};
       float thr_d = -INFINITY;
       long long entry;
       bool valid;
@@ -707,12 +707,23 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
               for (int t = 0; t < 32; ++t)
                 if (t < span) dump[(long long)r * K + jb + t] = v[t];
             } else {
+              // hit mask of the group (FSETP + predicated OR per value; the
+              // +inf padding and columns past K never hit), then the few hits
+              // are appended through a select network so the candidate list
+              // stays in registers (a dynamically indexed array would live in
+              // local memory)
+              unsigned msk = 0u;
 #pragma unroll
-              for (int t = 0; t < 32; ++t) {
-                if (v[t] <= thr_d && jb + t < K) {
-                  if (nc < kTcShort) cand[nc] = jb + t;
-                  ++nc;
-                }
+              for (int t = 0; t < 32; ++t)
+                asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
+                    : "+r"(msk)
+                    : "f"(v[t]), "f"(thr_d), "r"(1u << t));
+              while (msk) {
+                const int jt = jb + __ffs(msk) - 1;
+                msk &= msk - 1u;
+#pragma unroll
+                for (int k = 0; k < kTcShort; ++k) cand[k] = nc == k ? jt : cand[k];
+                ++nc;
               }
             }
           }
@@ -746,11 +757,14 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         if (valid && !over) {
           // the reference's arithmetic (_kernels.py:25-29); (d, j) order
           const double* __restrict__ cb = a.cb[st->cur];
-          for (int k = 0; k < nc; ++k) {
-            const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)cand[k] * L, L);
-            if (d < best || (d == best && cand[k] < bj)) {
-              best = d;
-              bj = cand[k];
+#pragma unroll
+          for (int k = 0; k < kTcShort; ++k) {  // unrolled: cand[] stays in registers
+            if (k < nc) {
+              const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)cand[k] * L, L);
+              if (d < best || (d == best && cand[k] < bj)) {
+                best = d;
+                bj = cand[k];
+              }
             }
           }
         }
