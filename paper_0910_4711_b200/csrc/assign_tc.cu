@@ -55,12 +55,13 @@ struct TcCfg {
   // streams codebook chunks when the codebook does not fit in shared memory
   // (else it converts rows); kEpiWarps + 2 and kExtraConv more convert row
   // tiles into the A operand buffers (at small K the conversion is the
-  // pipeline's longest stage); then (L <= 32, kTcTop2) kCertGroups x 4
-  // certification warps, one per 32-row quarter, finish each tile's rows off
-  // the epilogue's critical path (at L = 64 the MMAs bind, registers are
-  // scarcer, and epilogue part 0 certifies).
+  // pipeline's longest stage); then (kTcTop2) kCertGroups x 4 certification
+  // warps, one per 32-row quarter, finish each tile's rows (part merge, FP64
+  // winner distance, queueing) off the epilogue's critical path.  At L = 64
+  // that work (192 FP64 ops + a 768 B gather per row) on epilogue part 0
+  // stalled the MMAs 60 % of the time; dedicated warps cut the pass by 13 %.
   static constexpr int kExtraConv = 0;
-  static constexpr bool kCertWarps = L <= 32;
+  static constexpr bool kCertWarps = true;
   static constexpr int kCertGroups = L == 16 ? 2 : 1;
   static constexpr int kCertWarp0 = 3 + kEpiWarps + kExtraConv;
   static constexpr int threads(int mode) {
