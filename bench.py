@@ -168,14 +168,17 @@ def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks):
     """Roofline of the dominant kernel, assign_tc<16> (tcgen05 kind::f16 MMA
     chain into TMEM + top-2 epilogue).  achieved = ALGORITHMIC flops (3L = 48
     per vector-codeword eval) per launch / its CUDA-event time.
-    The tensor pipe is not what binds it: the argmin epilogue is ~3.5 ALU-pipe
-    ops per value (FMNMX x2, FSETP, half an FMNMX3), and the ALU pipe retires
-    16 lanes/clk/SMSP for two-register operands (profiles/r01_microbench.json
-    fmnmx_2reg), so `limiter` reports that ceiling too."""
+    The tensor pipe is not what binds it: the two-read epilogue spends per
+    value half an FMNMX3 (chunk minimum) and an FSETP (band count) on the ALU
+    pipe -- 2 lane-slots at 16 lanes/clk/SMSP for register operands
+    (profiles/r01_microbench.json fmnmx_2reg) -- plus a predicated IADD, so
+    `limiter` reports that ALU ceiling; the role profiler (VQB_TC_PROF) shows
+    the epilogue warps busy 93 % and the MMA warp waiting on them 54 %."""
     peaks, src = _measured_peaks()
     tensor_peak = float(peaks.get("bf16_tflops", 1590.0))
     mhz = (clocks.summary().get("sm_mhz") if clocks else None) or 1965.0
-    alu_ceiling = 148 * 4 * 16 / 3.5 * mhz * 1e6  # evals/s
+    alu_ops = 2.0
+    alu_ceiling = 148 * 4 * 16 / alu_ops * mhz * 1e6  # evals/s
     evals_per_s = evals / (assign_ms * 1e-3)
     return {
         "bound": "tensor", "kernel": "assign_tc<16>",
@@ -185,7 +188,7 @@ def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks):
         "issued_mma_tflops": evals * 2 * (3 * 16 + 16) / (assign_ms * 1e-3) / 1e12,
         "traffic": traffic.get("bytes_per_launch") if traffic else None,
         "algorithmic_bytes": n * 16 * 4 + n * 4,
-        "limiter": {"pipe": "ALU (top-2 over TMEM values)", "alu_ops_per_eval": 3.5,
+        "limiter": {"pipe": "ALU (minimum + band count over TMEM values)", "alu_ops_per_eval": alu_ops,
                     "ceiling_g_evals_per_s": alu_ceiling / 1e9,
                     "frac": evals_per_s / alu_ceiling},
         "vs_fp32_ffma_peak": {"peak_tflops": ffma_peak_tflops, "frac": achieved / ffma_peak_tflops,
