@@ -219,6 +219,15 @@ int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64
 int vqb_bench_formats(int which, int64_t images, int64_t height, int64_t width, int64_t block, int64_t n,
                       int64_t dim, int64_t size, int reps, double* ms_out, double* bytes_out);
 
+/* ---- host helpers of the Python types (TrainingSet, core.py:72-99) ---- */
+
+/* memcpy split over host threads (the TrainingSet snapshot of float32 rows). */
+int vqb_host_copy(void* dst, const void* src, int64_t bytes);
+
+/* Index of the first inf / NaN among n float32 values, or -1 (host threads);
+ * TrainingSet's "training vector i component j is not finite" check. */
+int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first);
+
 /* Pipe microbenchmark (0 FFMA, 1 FFMA2, 2 FFMA+top-2 mix, 3 DADD): lane-ops/s. */
 int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
                         double* seconds);

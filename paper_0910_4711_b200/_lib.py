@@ -109,6 +109,8 @@ def lib():
             "vqb_decode_pixels": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I32, _P], _I32),
             "vqb_reconstruction_distortion": ([_P, _P, _I64, _I64, _I32, _I32, _P], _I32),
             "vqb_open_pixels": ([_P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
+            "vqb_host_copy": ([_P, _P, _I64], _I32),
+            "vqb_first_nonfinite_f32": ([_P, _I64, _P], _I32),
             "vqb_bench_formats": ([_I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _P, _P], _I32),
         }
         for name, (args, res) in sig.items():

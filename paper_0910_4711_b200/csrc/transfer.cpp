@@ -239,3 +239,43 @@ cudaError_t download(void* dst, const void* src, size_t bytes, cudaStream_t stre
 }
 
 }  // namespace vqb
+
+// ---------------------------------------------------------------------------
+// host helpers of the Python types (TrainingSet, core.py:72-99): snapshot
+// copies and the finiteness check of float32 rows, split over host threads
+// ---------------------------------------------------------------------------
+
+#include "../../include/vqb200.h"
+
+extern "C" int vqb_host_copy(void* dst, const void* src, int64_t bytes) {
+  if (bytes > 0) vqb::host_parallel_copy(dst, src, (size_t)bytes);
+  return VQB_OK;
+}
+
+extern "C" int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first) {
+  *first = -1;
+  if (n <= 0) return VQB_OK;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(hw ? hw : 1, n >> 20));
+  std::vector<int64_t> found((size_t)parts, -1);
+  auto scan = [&](int p) {
+    const int64_t lo = n * p / parts, hi = n * (p + 1) / parts;
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(x);
+    for (int64_t i = lo; i < hi; ++i)
+      if ((u[i] & 0x7f800000u) == 0x7f800000u) {  // exponent all ones: inf or NaN
+        found[(size_t)p] = i;
+        return;
+      }
+  };
+  std::vector<std::thread> ts;
+  for (int p = 1; p < parts; ++p) ts.emplace_back(scan, p);
+  scan(0);
+  for (auto& t : ts) t.join();
+  for (int64_t f : found)
+    if (f >= 0) {
+      *first = f;
+      break;
+    }
+  return VQB_OK;
+}
+
