@@ -1243,6 +1243,40 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
     unsigned* tcount = reinterpret_cast<unsigned*>(smem_raw + (2 * warp + half) * wt_bytes +
                                                    (long long)ncell * dim * 8);
     XT* xs = wstage + warp * 32 * kWStageStride;
+    if (DIM == 16) {
+      // software-pipelined: the next batch's cells and rows are in flight
+      // while this batch is staged and summed (the loop was latency-bound)
+      long long row = lo + (long long)warp * 32 + lane;
+      bool valid = row < hi;
+      int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
+      XT xr[16];
+      load_row16<XT, DIM>(X, row, dim, 0, valid, xr);
+      for (long long base = lo + (long long)warp * 32; base < hi; base += (long long)kWarps * 32) {
+        const long long nrow = base + (long long)kWarps * 32 + lane;
+        const bool nvalid = nrow < hi;
+        const int ncell = nvalid ? (zero_cells ? 0 : a.idx[nrow]) : -1;
+        XT xn[16];
+        load_row16<XT, DIM>(X, nrow, dim, 0, nvalid, xn);
+        const int lc = valid ? cell : -1;  // one table piece on this path: every cell is in range
+#pragma unroll
+        for (int l = 0; l < 16; ++l) xs[lane * kWStageStride + l] = xr[l];
+        __syncwarp();
+#pragma unroll 4
+        for (int p = 0; p < 16; ++p) {
+          const int rr = 2 * p + half;
+          const int cl = __shfl_sync(0xffffffffu, lc, rr);
+          if (cl >= 0) {
+            tab[(long long)cl * dim + hl] += to_fixed((double)xs[rr * kWStageStride + hl], scale);
+            if (hl == 0) tcount[cl] += 1;
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int l = 0; l < 16; ++l) xr[l] = xn[l];
+        cell = ncell;
+        valid = nvalid;
+      }
+    } else
     for (long long base = lo + (long long)warp * 32; base < hi; base += (long long)kWarps * 32) {
       const long long row = base + lane;
       const bool valid = row < hi;
