@@ -288,36 +288,61 @@ def run_b200(args):
         _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cb), K, 1, segs, ctypes.byref(flagged)))
         return list(segs)
 
-    ex_tensor = None
-    if world > 1:
-        ex_tensor = torch.zeros(K * 16 + K + 1, dtype=torch.int64, device=f"cuda:{local_rank}")
-
+    sharded = world > 1 or getattr(args, "sharded", False)
     clocks = ClockSampler(local_rank).__enter__()
     for _ in range(args.warmup):
         flush.zero_()
         step()
-        if world > 1:
-            dist.all_reduce(ex_tensor)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     seg_hist = []
-    if True:
+    if not sharded:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            s = step()
-            if world > 1:  # the per-pass exchange of the multi-GPU loop
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev0.record()
-                dist.all_reduce(ex_tensor)
-                ev1.record()
-                torch.cuda.synchronize()
-                s = s + [ev0.elapsed_time(ev1)]
-            seg_hist.append(s)
-    torch.cuda.synchronize()
-    ms_steps = [sum(s) for s in seg_hist]
+            seg_hist.append(step())
+        torch.cuda.synchronize()
+        ms_steps = [sum(s) for s in seg_hist]
+    else:
+        # the multi-GPU Lloyd pass itself (distributed.sharded_lloyd): this
+        # rank's shard (rows [rank n, (rank+1) n) of the global set) -> local
+        # assign + epilogue -> ONE SUM allreduce of the packed int64 exchange
+        # buffer over NCCL -> finalize on every rank; CUDA events on the
+        # stream all of it runs on (torch's current stream)
+        for _ in range(2):  # per-kernel segments of this rank's local work (roofline)
+            seg_hist.append(step())
+        from paper_0910_4711_b200 import distributed as D
+
+        shard = D.DeviceShard(x, rank * n, world * n, local_rank)
+        gmax = shard.tensor([shard.maxabs()])
+        if world > 1:
+            dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+        shard.lloyd_begin(cb, float(gmax.item()))
+        ex = shard.exchange()
+
+        def pass_():
+            shard.lloyd_local()
+            if world > 1:
+                dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+            shard.finalize()
+
+        for _ in range(args.warmup):
+            flush.zero_()
+            pass_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms_steps = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            pass_()
+            ev1.record()
+            torch.cuda.synchronize()
+            ms_steps.append(ev0.elapsed_time(ev1))
+        torch.cuda.synchronize()
     ms_step = sum(ms_steps) / len(ms_steps)
     if world > 1:
         t = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{local_rank}")
@@ -415,6 +440,9 @@ def run_b200(args):
                                    "(reference's converged codebook)",
                        "rows_per_gpu": n, "codebook": K, "dim": 16,
                        "parallelism": f"dp{world}" if world > 1 else "single",
+                       "step": ("sharded Lloyd pass: local assign + epilogue, NCCL allreduce of the "
+                                "packed int64 exchange buffer, finalize (distributed.sharded_lloyd)")
+                               if sharded else "Lloyd pass on one session (vqb_bench_iteration)",
                        "l2": "flushed (256 MiB write) between timed steps"},
             "segments_ms": {"stage": seg[0], "assign": seg[1], "rerank": seg[2],
                             "epilogue": seg[3], "finalize": seg[4]},
@@ -683,6 +711,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "formats"],
                     help="cfg2 (default) is the headline line; the others print one line each")
+    ap.add_argument("--sharded", action="store_true",
+                    help="time the multi-GPU pass (shard + NCCL exchange + finalize) even at one rank")
     ap.add_argument("--profile-steps", action="store_true",
                     help="only the warm-up + timed steps (for ncu launch lists)")
     args = ap.parse_args()

@@ -158,6 +158,16 @@ int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* h
                     int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap, double* final_dists,
                     vqb_train_summary* summary);
 
+/* Fixed-size Lloyd passes over shards (the multi-GPU form of
+ * vqb_lloyd_step_f32): begin uploads the codebook and fixes the common
+ * fixed-point scale (global_maxabs < 0: this shard's); per pass
+ * vqb_lloyd_local (assign + re-rank + distortion + cell sums), the caller
+ * allreduces vqb_step_exchange's int64 buffer (SUM), then vqb_step_finalize
+ * makes the centroids of the combined sums current on every rank (same bits
+ * everywhere: integer sums). vqb_step_result reads the codebook back. */
+int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t size, double global_maxabs);
+int vqb_lloyd_local(vqb_session* s);
+
 /* ---- one-shot host-buffer calls (end-to-end path, copies included) ---- */
 
 /* encode (codec.py:62-93) of host float32 rows: pipelined H2D / assign / D2H

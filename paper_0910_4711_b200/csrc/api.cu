@@ -105,6 +105,7 @@ struct vqb_session {
   bool fast = false;
   bool ordered = false;
   bool pending_init = false;
+  long long lloyd_size = 0;  // vqb_lloyd_begin
   cudaEvent_t ev_batch[2] = {nullptr, nullptr};
   // pinned host arena for small per-call transfers (codebooks, centre) so
   // they never take the synchronous pageable-copy path; reset per call
@@ -605,6 +606,40 @@ int vqb_step_finalize(vqb_session* s) {
   return VQB_OK;
 }
 
+static int upload_codebook(vqb_session* s, const double* codebook, long long size);
+static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered,
+                     const double* codebook = nullptr);
+
+// ---- fixed-codebook Lloyd passes over shards (update_codebook after
+// assign_cells at one size, the multi-GPU bench step): begin stages the
+// codebook with the common fixed-point scale; each pass is lloyd_local ->
+// caller allreduces the exchange buffer -> vqb_step_finalize (centroids of
+// the combined sums become the current codebook on every rank).
+extern "C" int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t size, double global_maxabs) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  if (size < 1) return fail(VQB_USAGE, "codebook must be at least 1x1");
+  CK(cudaSetDevice(s->device));
+  int rc = upload_codebook(s, codebook, size);
+  if (rc) return rc;
+  const double saved = s->maxabs;
+  if (global_maxabs >= 0) s->maxabs = global_maxabs;  // one fixed-point scale on every rank
+  rc = set_state(s, kModeLloydStep, size, 0, 0, codebook);
+  s->maxabs = saved;
+  if (rc) return rc;
+  s->lloyd_size = size;
+  s->pending_init = false;
+  KernelArgs a = s->args();
+  CK(launch_clear(a, s->stream));
+  if (s->fast) CK(launch_prep_codebook(a, s->stream));
+  return VQB_OK;
+}
+
+extern "C" int vqb_lloyd_local(vqb_session* s) {
+  if (!s || s->lloyd_size < 1) return fail(VQB_USAGE, "vqb_lloyd_begin first");
+  CK(launch_reset(s->st, kModeLloydStep, (int)s->lloyd_size, 0, 0, 1, s->stream));
+  return vqb_step_local(s);
+}
+
 int vqb_session::batch_graph(int batch) {
   static int enabled = -1;
   if (enabled < 0) {
@@ -763,7 +798,7 @@ static int upload_codebook(vqb_session* s, const double* codebook, long long siz
 }
 
 static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered,
-                     const double* codebook = nullptr) {
+                     const double* codebook) {
   DevState* h = s->st_host;
   // configuration fields are written by the reset kernel + this header copy
   std::memset(h, 0, offsetof(DevState, hist));

@@ -122,6 +122,26 @@ class DeviceShard:
     def local(self) -> None:
         _lib.check(self.L.vqb_step_local(self.s.handle))
 
+    # -- fixed-size Lloyd passes (vqb_lloyd_*): update_codebook after
+    # assign_cells, sharded; the pass ends with the same exchange + finalize
+    def lloyd_begin(self, codebook: np.ndarray, global_maxabs: float) -> None:
+        cb = np.ascontiguousarray(codebook, dtype=np.float64)
+        self._lloyd_k = cb.shape[0]
+        _lib.check(self.L.vqb_lloyd_begin(self.s.handle, _lib.ptr(cb), cb.shape[0], global_maxabs))
+
+    def lloyd_local(self) -> None:
+        _lib.check(self.L.vqb_lloyd_local(self.s.handle))
+
+    def lloyd_result(self) -> tuple[np.ndarray, float]:
+        """(current codebook, distortion of the last pass)."""
+        cb = np.empty((self._lloyd_k, self.s.dim), dtype=np.float64)
+        summ = _lib.TrainSummary()
+        hist = (_lib.LevelIterationC * 1)()
+        warn = np.zeros(1, dtype=np.int64)
+        _lib.check(self.L.vqb_step_result(self.s.handle, _lib.ptr(cb), hist, 1, _lib.ptr(warn), 1,
+                                          None, ctypes.byref(summ)))
+        return cb, float(summ.total)
+
     def finalize(self) -> None:
         _lib.check(self.L.vqb_step_finalize(self.s.handle))
 
@@ -185,6 +205,30 @@ def run_sharded(backend, config, batch: int = 4, collective: bool = True):
 
             raise InternalError(f"sharded training did not terminate after {passes} passes")
     return backend.result()
+
+
+def sharded_lloyd(backend, codebook: np.ndarray, passes: int = 1, collective: bool = True,
+                  on_pass=None):
+    """``passes`` Lloyd iterations at a fixed codebook size over all ranks:
+    one MAX allreduce of |x| (the common fixed-point scale), then per pass
+    local assign + epilogue, ONE SUM allreduce of the packed int64 exchange
+    buffer, finalize (the centroids of the combined sums, identical bits on
+    every rank).  ``on_pass(i)`` runs after each pass is enqueued (timing)."""
+    import torch.distributed as dist
+
+    gmax = backend.tensor([backend.maxabs()])
+    if collective:
+        dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+    backend.lloyd_begin(codebook, float(gmax.item()))
+    ex = backend.exchange()
+    for i in range(passes):
+        backend.lloyd_local()
+        if collective:
+            dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+        backend.finalize()
+        if on_pass is not None:
+            on_pass(i)
+    return backend.lloyd_result()
 
 
 def gather_rows(local: np.ndarray, plan: ShardPlan, device: str | None):

@@ -80,3 +80,55 @@ def test_two_rank_sharded_design_matches_single_device(tmp_path):
     want = np.array(ref.history, dtype=np.float64)
     assert np.array_equal(h1[:, [0, 1, 3]], want[:, [0, 1, 3]])
     np.testing.assert_allclose(cb1.codevectors, ref.codebook, rtol=1e-12, atol=1e-12)
+
+
+def _lloyd_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_0910_4711_b200 import distributed as D
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = _data()
+        plan = D.ShardPlan(x.shape[0], world)
+        lo, hi = plan.bounds(rank)
+        shard = D.DeviceShard(np.ascontiguousarray(x[lo:hi]), lo, x.shape[0], 0)
+        cb0 = np.ascontiguousarray(x[:: x.shape[0] // 256][:256].astype(np.float64))
+        cb, td = D.sharded_lloyd(shard, cb0, passes=3)
+        if rank == 0:
+            np.savez(out_path, cb=cb, td=td)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_lloyd_passes_match_single_device(tmp_path):
+    """The multi-GPU bench step (vqb_lloyd_*: local pass, SUM allreduce of the
+    exchange buffer, finalize) over two shards equals the same passes on one
+    session holding every row, bit for bit, and the oracle's Lloyd passes."""
+    import torch.multiprocessing as mp
+
+    import oracle
+    from paper_0910_4711_b200 import distributed as D
+
+    out = str(tmp_path / "lloyd2.npz")
+    mp.start_processes(_lloyd_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    r2 = np.load(out)
+    x = _data()
+    cb0 = np.ascontiguousarray(x[:: x.shape[0] // 256][:256].astype(np.float64))
+    one = D.DeviceShard(x, 0, x.shape[0], 0)
+    cb1, td1 = D.sharded_lloyd(one, cb0, passes=3, collective=False)
+    assert r2["cb"].tobytes() == cb1.tobytes()
+    assert float(r2["td"]) == td1
+    cb = cb0
+    x64 = x.astype(np.float64)
+    for _ in range(3):
+        cells, dists = oracle.assign_all(x64, cb)
+        td = oracle.sum_inorder(dists)
+        cb, _ = oracle.update_codebook(x64, cells, cb)
+    np.testing.assert_allclose(cb1, cb, rtol=1e-12, atol=1e-12)
+    assert abs(td1 - td) <= 1e-12 * td
