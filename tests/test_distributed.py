@@ -143,6 +143,10 @@ class EmulatedShard:
         for t in range(self.ntiles):
             td += float(e[base + t: base + t + 1].view(np.float64)[0])
         e[base:] = 0
+        if getattr(self, "lloyd", False):  # kModeLloydStep: update, done
+            self._set_action(True, False)
+            self.total, self.done = td, True
+            return
         kd = self.kmax * self.dim
         empties = int(np.count_nonzero(e[kd: kd + k] == 0))
         if self.mode_final:
@@ -172,6 +176,26 @@ class EmulatedShard:
 
     def poll(self) -> bool:
         return self.done
+
+    # -- fixed-size Lloyd passes (vqb_lloyd_*, distributed.sharded_lloyd)
+    def lloyd_begin(self, codebook, global_maxabs: float) -> None:
+        import types
+
+        cb = np.asarray(codebook, dtype=np.float64)
+        self.cfg = types.SimpleNamespace(distortion_metric="squared_euclidean", delta=0.0)
+        self.kmax = cb.shape[0]
+        self.shift = _fixed_shift(self.n_global, global_maxabs)
+        self.scale = 2.0 ** self.shift
+        self.ex = self.torch.zeros(self.kmax * self.dim + self.kmax + self.ntiles, dtype=self.torch.int64)
+        self.cb = cb.copy()
+        self.size, self.done, self.lloyd, self.pending_init = cb.shape[0], False, True, False
+
+    def lloyd_local(self) -> None:
+        self.done = False
+        self.local()
+
+    def lloyd_result(self):
+        return self.cb.copy(), self.total
 
     def result(self):
         from paper_0910_4711_b200.core import LevelIteration, _max_iter_warning
@@ -284,3 +308,52 @@ def test_sharded_design_world2_matches_world1_and_reference(name, tmp_path):
     np.testing.assert_allclose(r2["cb"], ref.codebook, rtol=1e-12, atol=1e-12)
     assert int(r2["nwarn"]) == len(ref.warnings)
     np.testing.assert_allclose(r2["per_worker"], ref.per_worker, rtol=1e-12)
+
+
+def _lloyd_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    from paper_0910_4711_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = _lloyd_data()
+        plan = D.ShardPlan(x.shape[0], world)
+        lo, hi = plan.bounds(rank)
+        cb, td = D.sharded_lloyd(EmulatedShard(x[lo:hi], lo, x.shape[0]), x[:: 97][:64].astype(np.float64),
+                                 passes=2, collective=world > 1)
+        if rank == 0:
+            np.savez(out_path, cb=cb, td=td)
+    finally:
+        dist.destroy_process_group()
+
+
+def _lloyd_data():
+    rng = np.random.default_rng(11)
+    return rng.integers(0, 256, (3 * TILE + 123, 8)).astype(np.float32)
+
+
+def test_sharded_lloyd_world2_matches_world1_and_oracle(tmp_path):
+    """distributed.sharded_lloyd (the multi-GPU bench step): world 2 over gloo
+    gives the world-1 codebook and distortion bit for bit, and the oracle's
+    two Lloyd passes."""
+    import torch.multiprocessing as mp
+
+    outs = {}
+    for world in (1, 2):
+        out = str(tmp_path / f"l{world}.npz")
+        mp.start_processes(_lloyd_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                           start_method="spawn")
+        outs[world] = np.load(out)
+    assert outs[1]["cb"].tobytes() == outs[2]["cb"].tobytes()
+    assert float(outs[1]["td"]) == float(outs[2]["td"])
+    x = _lloyd_data().astype(np.float64)
+    cb = x[:: 97][:64].copy()
+    for _ in range(2):
+        cells, dists = oracle.assign_all(x, cb)
+        td = oracle.sum_inorder(dists)
+        cb, _ = oracle.update_codebook(x, cells, cb)
+    assert np.array_equal(outs[2]["cb"], cb)  # pixel-valued rows: fixed-point sums are exact
+    assert abs(float(outs[2]["td"]) - td) <= 1e-12 * td
