@@ -329,6 +329,23 @@ using namespace vqb;
 // (counts the 16 FFMA only), 3 = DADD, 4 = 3-register FFMA, 5 = evals/s of a
 // constant-memory-codebook distance loop, 6 = FFMA2 + FFMA interleaved (FMA
 // lane-ops), 7 = FMNMX (ALU pipe).  `seconds` gets the kernel time.
+// L2 (global) 64-bit atomics into a K x 17 int64 cell table (the fused
+// cell-sum candidate): each thread plays one row, picks a pseudo-random cell
+// and adds 17 words (16 dims + count) -- MODE 0 non-returning red.add.u64,
+// MODE 1 the same words from 32 lanes of one warp coalesced per dim (lane =
+// row, consecutive dims per instruction).
+template <int MODE>
+__global__ void __launch_bounds__(256) l2_red_kernel(unsigned long long* tab, int cells, int iters) {
+  unsigned h = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u;
+  for (int it = 0; it < iters; ++it) {
+    h = h * 1664525u + 1013904223u;
+    const unsigned cell = (h >> 8) % (unsigned)cells;
+    unsigned long long* w = tab + (unsigned long long)cell * 17;
+#pragma unroll
+    for (int d = 0; d < 17; ++d) atomicAdd(w + d, (unsigned long long)(h & 0xffff) + d);
+  }
+}
+
 extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,
                                    double* seconds) {
   int dev = 0, sms = 0;
@@ -397,6 +414,19 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         else smem_atomic_kernel<1><<<sms, 512>>>((float*)buf, iters);
         lane_ops = 1.0 * sms * 512 * iters * 16;
         break;
+      case 15:
+      case 16: {
+        static unsigned long long* tab = nullptr;
+        const int cells = which == 15 ? 1024 : 4096;
+        if (!tab) {
+          cudaMalloc(&tab, 4096ull * 17 * 8);
+          cudaMemset(tab, 0, 4096ull * 17 * 8);
+        }
+        const int it = iters / 20 + 1;
+        l2_red_kernel<0><<<sms * 8, 256>>>(tab, cells, it);
+        lane_ops = 17.0 * sms * 8 * 256 * it;
+        break;
+      }
       case 13:
       case 14: {
         static float4* xb = nullptr;
