@@ -42,6 +42,16 @@ namespace vqb {
 #define VQB_SLEEP_NS 20000
 #endif
 constexpr uint32_t kSleepNs = VQB_SLEEP_NS;
+// epilogue TMEM reads: 16-column loads software-pipelined, or 32-column
+// loads waited on at once.  Pipelining pays with 8 epilogue warps (L >= 32:
+// cfg3 pass -8 %) and costs with 16 (L = 16: +14 %, the warps already hide
+// the load latency and the extra loop control is on the issue-bound path).
+// VQB_PIPE_LD=0/1 forces one form (A/B builds).
+#ifndef VQB_PIPE_LD
+#define VQB_PIPE_LD -1
+#endif
+template <int L>
+__host__ __device__ constexpr bool pipe_ld() { return VQB_PIPE_LD < 0 ? L >= 32 : VQB_PIPE_LD != 0; }
 
 template <int L>
 struct TcCfg {
@@ -657,7 +667,62 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           }
           tmem_wait_ld();
         };
-        if constexpr (MODE == kTcTop2) {
+        if constexpr (MODE == kTcTop2 && pipe_ld<L>()) {
+          // Same two reads, 16 columns per tcgen05.ld, software-pipelined:
+          // the load of group g+1 is in flight while group g is processed
+          // (ld(0) wait | ld(1) proc(0) wait | ld(2) proc(1) wait | ...), so the
+          // TMEM load latency overlaps the ALU chains with the same 32
+          // registers the unpipelined x32 form used.
+          const int ng = span / 16;
+          const uint32_t cbase = trow + (uint32_t)(s * kTcChunk + h * span);
+          float va[16], vb[16];
+          float c4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+          auto pmin = [&](const float (&v)[16]) {
+#pragma unroll
+            for (int t = 0; t < 16; t += 2) c4[(t >> 1) & 3] = fminf(c4[(t >> 1) & 3], fminf(v[t], v[t + 1]));
+          };
+          tmem_ld16(cbase, va);
+          tmem_wait_ld();
+#pragma unroll 1
+          for (int g2 = 0; g2 < ng; g2 += 2) {
+            if (g2 + 1 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 1) * 16), vb);
+            pmin(va);
+            tmem_wait_ld();
+            if (g2 + 2 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 2) * 16), va);
+            if (g2 + 1 < ng) pmin(vb);
+            tmem_wait_ld();
+          }
+          const float cm = fminf(fminf(c4[0], c4[1]), fminf(c4[2], c4[3]));
+          const float mnew = fminf(m1, cm);
+          const float thr = fmaf(3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw), dscale, mnew);
+          if (cm < m1 && m1 > thr) cnt = 0;  // see the unpipelined form below
+          m1 = mnew;
+          const int jb0 = c * kTcChunk + h * span;
+          auto pcount = [&](const float (&v)[16], int g) {
+            unsigned acc4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+              asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
+                  : "+r"(acc4[t & 3])
+                  : "f"(v[t]), "f"(thr), "r"(0x10000u + (unsigned)t));
+            const unsigned acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+            if (acc) {
+              cnt += (int)(acc >> 16);
+              i1 = jb0 + g * 16 + (int)(acc & 0xffffu);  // exact when alone
+            }
+          };
+          tmem_ld16(cbase, va);
+          tmem_wait_ld();
+#pragma unroll 1
+          for (int g2 = 0; g2 < ng; g2 += 2) {
+            if (g2 + 1 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 1) * 16), vb);
+            pcount(va, g2);
+            tmem_wait_ld();
+            if (g2 + 2 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 2) * 16), va);
+            if (g2 + 1 < ng) pcount(vb, g2 + 1);
+            tmem_wait_ld();
+          }
+        } else if constexpr (MODE == kTcTop2) {
           // two reads of the chunk: its minimum (3-input FMNMX, 0.5 op per
           // value), then one compare per value against the band above the
           // running minimum (count + index packed in one predicated add)
