@@ -75,6 +75,16 @@ def _cpu_info():
     return int(cores or 1), model
 
 
+def _host_threads() -> int:
+    """Every host thread this process may run on (torchrun exports
+    OMP_NUM_THREADS=1, which would make the OpenMP default a single core; the
+    oracle's parallel loops take an explicit thread count instead)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 def cpu_iteration_rate(x: np.ndarray, cb: np.ndarray, target_s: float = 4.0, repeats: int = 3):
     """Oracle (reference arithmetic, OpenMP over all host cores) Lloyd
     iteration = parallel assign + in-order TD + round-robin update, on a
@@ -82,7 +92,7 @@ def cpu_iteration_rate(x: np.ndarray, cb: np.ndarray, target_s: float = 4.0, rep
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
-    threads = oracle.max_threads()
+    threads = _host_threads()
     k = cb.shape[0]
 
     def one(rows):
@@ -217,7 +227,6 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
-    threads = oracle.max_threads()
     # calibrate a sample so each step is ~2 s of CPU work
     rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=2.0, repeats=1)
     xs = np.ascontiguousarray(x[:rows], dtype=np.float64)
