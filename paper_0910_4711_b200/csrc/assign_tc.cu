@@ -253,6 +253,7 @@ cudaError_t launch_build_row_image(const float* x32, const float* mu, long long 
 template <int L, int MODE>
 __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(KernelArgs a, float* dump,
                                                                           int b_cap) {
+  pdl_wait();
   using C = TcCfg<L>;
   DevState* st = a.st;
   if (st->done) return;
@@ -880,7 +881,10 @@ static cudaError_t launch_tc_L(const KernelArgs& a, int grid, float* dump, cudaS
   cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<L, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  assign_tc_kernel<L, MODE><<<grid, C::threads(MODE), smem, s>>>(a, dump, b_cap);
+  {
+    cudaError_t e1 = launch_k(assign_tc_kernel<L, MODE>, grid, C::threads(MODE), smem, s, a, dump, b_cap);
+    if (e1 != cudaSuccess) return e1;
+  }
   return cudaGetLastError();
 }
 

@@ -61,6 +61,7 @@ __device__ __forceinline__ long long to_fixed(double v, double scale) {
 // ---------------------------------------------------------------------------
 
 __global__ void prep_codebook_kernel(KernelArgs a) {
+  pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
@@ -90,8 +91,7 @@ cudaError_t launch_prep_codebook(const KernelArgs& a, cudaStream_t s) {
   long long kpad = (a.kmax + 3) / 4 * 4;
   int blocks = (int)((kpad + 255) / 256);
   if (blocks > 1024) blocks = 1024;
-  prep_codebook_kernel<<<blocks, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(prep_codebook_kernel, blocks, 256, 0, s, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -112,6 +112,14 @@ template <>
 struct FastCfg<64> {
   static constexpr int NT = 256, R = 2, TK = 256;
 };
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VQB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 bool fast_dim_supported(int dim) { return dim == 16 || dim == 32 || dim == 64; }
 
@@ -307,6 +315,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
 
 template <int L, bool PACKED>
 __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelArgs a) {
+  pdl_wait();
   constexpr int NT = FastCfg<L>::NT, R = FastCfg<L>::R, TK = FastCfg<L>::TK;
   using TS = TileStream<L, TK>;
   const DevState* st = a.st;
@@ -394,7 +403,8 @@ static cudaError_t launch_fast_LP(const KernelArgs& a, int sms, cudaStream_t s) 
   cudaError_t e = cudaFuncSetAttribute(assign_fast_kernel<L, PACKED>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  assign_fast_kernel<L, PACKED><<<sms, FastCfg<L>::NT, smem, s>>>(a);
+  e = launch_k(assign_fast_kernel<L, PACKED>, sms, FastCfg<L>::NT, smem, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -434,6 +444,7 @@ __device__ __forceinline__ double ref_dist_regs(const XT (&xr)[DIM], const doubl
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT* __restrict__ X,
                                                          int use_list) {
+  pdl_wait();
   // use_list: 0 every row, 1 the assign_fast queue, 2 the shortlist overflow queue
   // T threads per row (T = pow2 >= K, capped at the block): K=2 packs 128
   // rows per block, K >= 256 gives one block per row.  Each thread scans
@@ -628,13 +639,14 @@ template <typename XT>
 static cudaError_t launch_exact_t(const KernelArgs& a, const XT* X, int use_list, int sms,
                                   cudaStream_t s) {
   const int blocks = sms * 4;
+  cudaError_t e;
   switch (a.dim) {
-    case 16: exact_rows_kernel<XT, 16><<<blocks, 256, 0, s>>>(a, X, use_list); break;
-    case 32: exact_rows_kernel<XT, 32><<<blocks, 256, 0, s>>>(a, X, use_list); break;
-    case 64: exact_rows_kernel<XT, 64><<<blocks, 256, 0, s>>>(a, X, use_list); break;
-    default: exact_rows_kernel<XT, 0><<<blocks, 256, 0, s>>>(a, X, use_list); break;
+    case 16: e = launch_k(exact_rows_kernel<XT, 16>, blocks, 256, 0, s, a, X, use_list); break;
+    case 32: e = launch_k(exact_rows_kernel<XT, 32>, blocks, 256, 0, s, a, X, use_list); break;
+    case 64: e = launch_k(exact_rows_kernel<XT, 64>, blocks, 256, 0, s, a, X, use_list); break;
+    default: e = launch_k(exact_rows_kernel<XT, 0>, blocks, 256, 0, s, a, X, use_list); break;
   }
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -662,6 +674,7 @@ constexpr int kShort = 8;
 
 template <int L>
 __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
+  pdl_wait();
   using C = ShortCfg<L>;
   constexpr int NT = C::NT, TK = C::TK;
   const DevState* st = a.st;
@@ -857,7 +870,10 @@ static cudaError_t launch_shortlist_L(const KernelArgs& a, int sms, cudaStream_t
   cudaError_t e = cudaFuncSetAttribute(shortlist_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)C::kSmem);
   if (e != cudaSuccess) return e;
-  shortlist_kernel<L><<<sms * 2, C::NT, C::kSmem, s>>>(a);
+  {
+    cudaError_t e2 = launch_k(shortlist_kernel<L>, sms * 2, C::NT, C::kSmem, s, a);
+    if (e2 != cudaSuccess) return e2;
+  }
   return cudaGetLastError();
 }
 
@@ -968,6 +984,7 @@ __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, lo
 // does not depend on the grid or on the number of GPUs -- sum_inorder's role
 // (_kernels.py:92-98).
 __global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a) {
+  pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
   __shared__ double red[8];
@@ -999,6 +1016,7 @@ __global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a) {
 // of the grid and of the number of GPUs).
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(256, 4) dist_td_kernel(KernelArgs a, const XT* __restrict__ X) {
+  pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
   __shared__ double red[8];
@@ -1068,6 +1086,7 @@ __device__ __forceinline__ void load_row16(const XT* __restrict__ X, long long r
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, const XT* __restrict__ X,
                                                              int zero_cells) {
+  pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
   const int K = zero_cells ? 1 : st->size;
@@ -1331,6 +1350,7 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
 // sum the per-block slabs into the exchange buffer: 32 words x 8 slab groups
 // per 256-thread block, int64 (any order is exact)
 __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int nblocks, int zero_cells) {
+  pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
   const int K = zero_cells ? 1 : st->size;
@@ -1373,7 +1393,8 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   if (want_td && !zero_cells) {
     // every assignment path stored the rows' exact distances (store_dist)
     const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
-    td_tiles_kernel<<<(unsigned)ntiles, 256, 0, s>>>(a);
+    e = launch_k(td_tiles_kernel, (unsigned)ntiles, 256, 0, s, a);
+    if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1387,13 +1408,15 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   if (blocks < 1) blocks = 1;
   e = cudaFuncSetAttribute(sums_kernel<XT, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEpiSmem);
   if (e != cudaSuccess) return e;
-  sums_kernel<XT, DIM><<<dim3(blocks, chunks), kSumThreads, kEpiSmem, s>>>(a, X, zero_cells ? 1 : 0);
+  e = launch_k(sums_kernel<XT, DIM>, dim3(blocks, chunks), kSumThreads, kEpiSmem, s, a, X, zero_cells ? 1 : 0);
+  if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const long long words = kmax * a.dim + kmax;
   int rb = (int)((words + 31) / 32);
   if (rb > 8192) rb = 8192;
-  reduce_partials_kernel<<<rb, 256, 0, s>>>(a, blocks, zero_cells ? 1 : 0);
+  e = launch_k(reduce_partials_kernel, rb, 256, 0, s, a, blocks, zero_cells ? 1 : 0);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1424,6 +1447,7 @@ cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums
 
 template <typename XT>
 __global__ void ordered_update_kernel(KernelArgs a, const XT* __restrict__ X) {
+  pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
@@ -1494,6 +1518,7 @@ __device__ __forceinline__ void set_action(DevState* st, int act) {
 }
 
 __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) {
+  pdl_wait();
   DevState* st = a.st;
   if (st->done) return;
   __shared__ double red[8];
@@ -1688,6 +1713,7 @@ __device__ __forceinline__ void stage_row_warp(const KernelArgs& a, long long k,
 // of the new rows for the next candidate pass.  Idempotent (speculative
 // passes after `done` may repeat it harmlessly).
 __global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
+  pdl_wait();
   const DevState* st = a.st;
   const int act = st->act;
   // zero the distortion tiles (other ranks' slots must be 0 before the next
@@ -1732,25 +1758,38 @@ __global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
 }
 
 cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s) {
-  finalize_kernel<<<1, 256, 0, s>>>(a, 1);
+  {
+    cudaError_t e1 = launch_k(finalize_kernel, 1, 256, 0, s, a, 1);
+    if (e1 != cudaSuccess) return e1;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int blocks = (int)((a.kmax + 7) / 8);  // one warp per codevector
   if (blocks < 8) blocks = 8;
-  apply_kernel<<<blocks, 256, 0, s>>>(a, stage ? 1 : 0);
+  {
+    cudaError_t e1 = launch_k(apply_kernel, blocks, 256, 0, s, a, stage ? 1 : 0);
+    if (e1 != cudaSuccess) return e1;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s) {
-  finalize_kernel<<<1, 256, 0, s>>>(a, 0);
+  {
+    cudaError_t e1 = launch_k(finalize_kernel, 1, 256, 0, s, a, 0);
+    if (e1 != cudaSuccess) return e1;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  apply_kernel<<<8, 256, 0, s>>>(a, stage ? 1 : 0);
+  {
+    cudaError_t e1 = launch_k(apply_kernel, 8, 256, 0, s, a, stage ? 1 : 0);
+    if (e1 != cudaSuccess) return e1;
+  }
   return cudaGetLastError();
 }
 
 // staging padding (rows >= K never win) and a clean exchange buffer
 __global__ void clear_kernel(KernelArgs a) {
+  pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.ex.words();
        i += (long long)gridDim.x * blockDim.x)
     a.ex.base[i] = 0;
@@ -1767,7 +1806,10 @@ __global__ void clear_kernel(KernelArgs a) {
 }
 
 cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s) {
-  clear_kernel<<<64, 256, 0, s>>>(a);
+  {
+    cudaError_t e1 = launch_k(clear_kernel, 64, 256, 0, s, a);
+    if (e1 != cudaSuccess) return e1;
+  }
   return cudaGetLastError();
 }
 
@@ -1848,6 +1890,7 @@ cudaError_t launch_sum_inorder(const double* v, long long n, double* out, cudaSt
 // reset the per-call state (one-shot assign / update / Lloyd step calls)
 __global__ void reset_kernel(DevState* st, int mode, int size, int metric, int ordered,
                              int keep_cur) {
+  pdl_wait();
   st->mode = mode;
   st->size = size;
   st->metric = metric;
@@ -1870,7 +1913,10 @@ __global__ void reset_kernel(DevState* st, int mode, int size, int metric, int o
 
 cudaError_t launch_reset(DevState* st, int mode, int size, int metric, int ordered, int keep_cur,
                          cudaStream_t s) {
-  reset_kernel<<<1, 1, 0, s>>>(st, mode, size, metric, ordered, keep_cur);
+  {
+    cudaError_t e1 = launch_k(reset_kernel, 1, 1, 0, s, st, mode, size, metric, ordered, keep_cur);
+    if (e1 != cudaSuccess) return e1;
+  }
   return cudaGetLastError();
 }
 

@@ -126,6 +126,29 @@ struct KernelArgs {
   DevState* st;
 };
 
+// Programmatic dependent launch: pass kernels are launched with
+// programmaticStreamSerialization (launch_k), so a kernel's grid is set up
+// while its predecessor drains; each begins with pdl_wait(), which returns
+// once the predecessor has completed and its writes are visible (a no-op for
+// a kernel launched without the attribute).  VQB_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // kernel launchers (kernels.cu); all asynchronous on `stream`
 cudaError_t launch_prep_codebook(const KernelArgs& a, cudaStream_t s);
 cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s);
