@@ -360,6 +360,17 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
     const float inv = 1.0f / dscale;
     const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
     const int rb = (int)(i & 1);
+    {
+      // the row's coordinates for the FP64 winner distance are fetched into
+      // L1 while the tile's results are still being computed (with the
+      // prebuilt row image nothing else brought them on chip)
+      const long long e0 = ((long long)blockIdx.x + i * gridDim.x) * kTcRows + r;
+      if (L >= 32 && e0 < nitems && MODE == kTcTop2) {  // (at L = 16 no gain measured)
+        const char* xr = reinterpret_cast<const char*>(a.x32 + (a.r0 + e0) * L);
+#pragma unroll
+        for (int off = 0; off < L * 4; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xr + off));
+      }
+    }
     if (C::kCertWarps && !prof)  // dedicated warps: sleep, do not spin
       mbar_wait_sleep(&m->res_full[rb], (uint32_t)((i >> 1) & 1), kSleepNs);
     else
