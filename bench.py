@@ -578,6 +578,23 @@ def run_workload(args):
             cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)
             e2e_runs.append(time.perf_counter() - t0)
         e2e_s = min(e2e_runs[1:])
+        pix = None
+        if name in ("cfg1", "cfg3"):
+            # the image configs from their uint8 pixels: vectorised on the
+            # device (storage.image_training_set), 1 byte per sample over PCIe
+            from paper_0910_4711_b200 import storage
+
+            px = synthetic.make_training_pixels(name)
+            runs = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                ts_px, _grid = storage.image_training_set(px, 4 if name == "cfg1" else 8)
+                cb3, st3 = vq.lbg_train(ts_px, conf)
+                runs.append(time.perf_counter() - t0)
+                del ts_px
+            pix = {"value": min(runs[1:]), "unit": "s", "api": "storage.image_training_set + lbg_train",
+                   "h2d_bytes_per_step": int(px.nbytes), "d2h_bytes_per_step": int(dcb.nbytes),
+                   "codebook_equal_to_float_path": bool(cb3.codevectors.tobytes() == cb2.codevectors.tobytes())}
         parity = None
         if g is not None:
             gh = g["hist"]
@@ -608,6 +625,7 @@ def run_workload(args):
                                 "segments_ms": list(segs), "rerank_rows": int(flagged.value)},
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(x.nbytes),
                     "d2h_bytes_per_step": int(dcb.nbytes)},
+            "e2e_from_pixels": pix,
             "parity": parity,
         })
     clocks.__exit__(None, None, None)

@@ -216,6 +216,11 @@ int vqb_decode_pixels(const uint32_t* indices, int64_t images, int64_t height, i
 int vqb_reconstruction_distortion(const double* a, const double* b, int64_t n, int64_t dim, int metric,
                                   int device, double* total);
 
+/* The session's float32 rows back to the host (out[rows][dim]); VQB_USAGE for
+ * a session that holds float64 rows.  A pixel-fed TrainingSet materialises
+ * its float64 field from this on first access. */
+int vqb_rows_f32(vqb_session* s, float* out);
+
 /* Session over the block vectors of `images` uint8 images, vectorised on the
  * device (1 byte per sample over PCIe instead of the reference's float64
  * copy, core.py:47-60): the training set of image_to_blocks + TrainingSet. */

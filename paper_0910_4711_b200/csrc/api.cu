@@ -417,6 +417,14 @@ static int finish_open(std::unique_ptr<vqb_session>& s, vqb_session** out) {
 
 extern "C" {
 
+int vqb_rows_f32(vqb_session* s, float* out) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  if (!s->x32) return fail(VQB_USAGE, "the session holds float64 rows");
+  CK(cudaSetDevice(s->device));
+  CK(download(out, s->x32, sizeof(float) * (size_t)(s->n * s->dim), s->stream));
+  return VQB_OK;
+}
+
 int vqb_close(vqb_session* s) {
   delete s;
   return VQB_OK;
