@@ -126,11 +126,11 @@ struct TcMisc {
       int i1[P][kTcRows];
       float q[kTcRows];
     } res[2];
-    struct {
-      unsigned char count[4][kTcRows];  // every part's shortlist size (saturated)
-      double best[4][kTcRows];   // every part's best FP64 distance ...
-      int bestj[4][kTcRows];     // ... and its index
-    } sl;
+    struct {                   // kTcShortlist, double-buffered by tile parity
+      double best[P][kTcRows];   // every part's best FP64 distance ...
+      int bestj[P][kTcRows];     // ... and its index
+      unsigned char count[P][kTcRows];  // every part's shortlist size (saturated)
+    } sl[2];
   } merge;
 };
 
@@ -820,19 +820,20 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         mbar_arrive(&m->res_full[rb]);
         if (!C::kCertWarps && h == 0) certify(i, r);
       } else if constexpr (MODE == kTcShortlist) {
-        // every part evaluates its own candidates in FP64; part 0 decides
-        // overflow from the total and merges the parts' lexicographic minima
-        m->merge.sl.count[h][r] = (unsigned char)min(nc, 255);
-        named_bar(1, 32 * C::kEpiWarps);
-        int total = 0;
-#pragma unroll
-        for (int p = 0; p < C::kParts; ++p) total += m->merge.sl.count[p][r];
+        // every part evaluates its own candidates in FP64 (a part holding more
+        // than kTcShort, or a row out of fp16 range, overflows the row anyway);
+        // one barrier, then part 0 decides overflow from the total and merges
+        // the parts' lexicographic minima.  The merge area alternates by tile
+        // parity: part 0 has finished reading area (i & 1) before it reaches
+        // tile i + 1's barrier, which every part passes before writing tile
+        // i + 2 into the same area.
+        auto& ml = m->merge.sl[i & 1];
+        ml.count[h][r] = (unsigned char)min(nc, 255);
         mbar_wait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1));
         const bool bad = m->qrow[i & 3][r] < 0.f;
-        const bool over = total == 0 || total > kTcShort || bad;
         double best = INFINITY;
         int bj = 0x7fffffff;
-        if (valid && !over) {
+        if (valid && !bad && nc <= kTcShort) {
           // the reference's arithmetic (_kernels.py:25-29); (d, j) order
           const double* __restrict__ cb = a.cb[st->cur];
 #pragma unroll
@@ -846,18 +847,22 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
             }
           }
         }
-        m->merge.sl.best[h][r] = best;
-        m->merge.sl.bestj[h][r] = bj;
+        ml.best[h][r] = best;
+        ml.bestj[h][r] = bj;
         named_bar(2, 32 * C::kEpiWarps);
         if (h == 0 && valid) {
+          int total = 0;
+#pragma unroll
+          for (int p = 0; p < C::kParts; ++p) total += ml.count[p][r];
+          const bool over = total == 0 || total > kTcShort || bad;
           if (over) {
             const int pos = atomicAdd(&st->flag2_count, 1);
             a.flags2[pos] = (int)row;
           } else {
 #pragma unroll
             for (int p = 1; p < C::kParts; ++p) {
-              const double d = m->merge.sl.best[p][r];
-              const int j = m->merge.sl.bestj[p][r];
+              const double d = ml.best[p][r];
+              const int j = ml.bestj[p][r];
               if (d < best || (d == best && j < bj)) {
                 best = d;
                 bj = j;
@@ -867,7 +872,6 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
             if (a.dists) a.dists[row] = st->metric == kEuclidean ? sqrt(best) : best;
           }
         }
-        named_bar(3, 32 * C::kEpiWarps);  // the merge area is free for the next tile
       }
     }
     pflush(2);
