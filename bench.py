@@ -257,6 +257,36 @@ def run_reference(args):
     return 0
 
 
+def _e2e_time(L, xp, cb, K, n, local_rank, flush, args, torch) -> float:
+    """Mean seconds of one Lloyd iteration through vqb_lloyd_step_f32 (the C
+    ABI with host buffers: H2D of this rank's rows from pinned memory + the
+    codebook, D2H of the new codebook and distortion).  xp was pinned at
+    start-up: on these VMs the DMA from freshly pinned pages runs at ~half
+    rate for about a second (tools/e2e_probe3.py)."""
+    from paper_0910_4711_b200 import _lib
+
+    new_cb = np.empty_like(cb)
+    td = ctypes.c_double()
+    empty = ctypes.c_int64()
+
+    def e2e_step():
+        # the step's result is the new codebook + distortion (what the next
+        # Lloyd pass consumes); the cell table stays on the device
+        _lib.check(L.vqb_lloyd_step_f32(_lib.ptr(xp), n, 16, _lib.ptr(cb), K, local_rank,
+                                        _lib.ptr(new_cb), None, ctypes.byref(td), ctypes.byref(empty)))
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        times.append(time.perf_counter() - t0)
+    return sum(times) / len(times)
+
+
 def run_b200(args):
     rank, world, local_rank = _rank_env()
     import torch
@@ -280,7 +310,7 @@ def run_b200(args):
         rng = np.random.default_rng(1000 + rank)
         x = synthetic.gaussian_mixture(rng, 1 << 20, 16, 1024, 2.0, 20.0)
     n = x.shape[0]
-    xp_t = torch.from_numpy(x).pin_memory() if rank == 0 else None  # e2e input, pinned early
+    xp_t = torch.from_numpy(x).pin_memory()  # e2e input (this rank's shard), pinned early
     xp = xp_t.numpy() if xp_t is not None else None
     sess = _Session(x, None, device=local_rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
@@ -297,14 +327,18 @@ def run_b200(args):
         _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cb), K, 1, segs, ctypes.byref(flagged)))
         return list(segs)
 
-    sharded = world > 1 or getattr(args, "sharded", False)
+    # --segmented: time the kernels one event pair each (vqb_bench_iteration;
+    # the events between kernels also serialise the programmatic dependent
+    # launches).  Default: per-kernel segments from that diagnostic, the value
+    # from whole passes (events only on both sides of each pass).
+    segmented = getattr(args, "segmented", False) and world == 1
     clocks = ClockSampler(local_rank).__enter__()
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
     seg_hist = []
-    if not sharded:
+    if segmented:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
@@ -312,12 +346,14 @@ def run_b200(args):
         torch.cuda.synchronize()
         ms_steps = [sum(s) for s in seg_hist]
     else:
-        # the multi-GPU Lloyd pass itself (distributed.sharded_lloyd): this
-        # rank's shard (rows [rank n, (rank+1) n) of the global set) -> local
-        # assign + epilogue -> ONE SUM allreduce of the packed int64 exchange
-        # buffer over NCCL -> finalize on every rank; CUDA events on the
-        # stream all of it runs on (torch's current stream)
-        for _ in range(2):  # per-kernel segments of this rank's local work (roofline)
+        # the Lloyd pass of the (multi-GPU) loop, distributed.sharded_lloyd:
+        # this rank's shard (rows [rank n, (rank+1) n) of the global set) ->
+        # local assign + epilogue -> ONE SUM allreduce of the packed int64
+        # exchange buffer over NCCL (N > 1) -> finalize on every rank; CUDA
+        # events on the stream all of it runs on (torch's current stream)
+        for _ in range(args.steps):  # per-kernel segments of this rank's local work (roofline)
+            flush.zero_()
+            torch.cuda.synchronize()
             seg_hist.append(step())
         from paper_0910_4711_b200 import distributed as D
 
@@ -373,33 +409,15 @@ def run_b200(args):
             print(json.dumps({"profile_steps": args.steps, "ms_per_step": ms_step,
                               "segments_ms": seg}), flush=True)
         return 0
+    # ---- e2e on every rank at once (each uploads its own shard over its own
+    # PCIe link): the slowest rank's time is the job's
+    e2e_s = _e2e_time(L, xp_t.numpy(), cb, K, n, local_rank, flush, args, torch)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    clocks.__exit__(None, None, None)  # every rank: the sampler is a child process
     if rank == 0:
-        # ---- e2e: the same iteration through the C ABI with host buffers
-        # (xp was pinned at start-up: on these VMs the DMA from freshly pinned
-        # pages runs at ~half rate for about a second, tools/e2e_probe3.py)
-        new_cb = np.empty_like(cb)
-        cells = np.empty(n, dtype=np.int64)
-        td = ctypes.c_double()
-        empty = ctypes.c_int64()
-
-        def e2e_step():
-            # the step's result is the new codebook + distortion (what the
-            # next Lloyd pass consumes); the cell table stays on the device
-            _lib.check(L.vqb_lloyd_step_f32(_lib.ptr(xp), n, 16, _lib.ptr(cb), K, local_rank,
-                                            _lib.ptr(new_cb), None, ctypes.byref(td),
-                                            ctypes.byref(empty)))
-
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        e2e_t = []
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            e2e_step()
-            e2e_t.append(time.perf_counter() - t0)
-        e2e_s = sum(e2e_t) / len(e2e_t)
-        clocks.__exit__(None, None, None)
 
         # ---- full cfg2 design (device-resident) vs the reference's run
         spec = synthetic.WORKLOADS["cfg2"]
@@ -449,15 +467,17 @@ def run_b200(args):
                                    "(reference's converged codebook)",
                        "rows_per_gpu": n, "codebook": K, "dim": 16,
                        "parallelism": f"dp{world}" if world > 1 else "single",
-                       "step": ("sharded Lloyd pass: local assign + epilogue, NCCL allreduce of the "
-                                "packed int64 exchange buffer, finalize (distributed.sharded_lloyd)")
-                               if sharded else "Lloyd pass on one session (vqb_bench_iteration)",
+                       "step": ("Lloyd pass per kernel segment (vqb_bench_iteration, --segmented)"
+                                if segmented else
+                                "Lloyd pass: local assign + re-rank + distortion + cell sums, "
+                                + ("NCCL allreduce of the packed int64 exchange buffer, " if world > 1 else "")
+                                + "finalize (distributed.sharded_lloyd); events around each whole pass"),
                        "l2": "flushed (256 MiB write) between timed steps"},
             "segments_ms": {"stage": seg[0], "assign": seg[1], "rerank": seg[2],
                             "epilogue": seg[3], "finalize": seg[4]},
             "rerank_rows_per_step": int(flagged.value),
             "roofline": _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks),
-            "e2e": {"value": evals / e2e_s / 1e9, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+            "e2e": {"value": world * evals / e2e_s / 1e9, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                     "api": "vqb_lloyd_step_f32 (C ABI), X from pinned host memory",
                     "h2d_bytes_per_step": n * 16 * 4 + K * 16 * 8,
                     "d2h_bytes_per_step": K * 16 * 8 + 8,
@@ -738,8 +758,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "formats"],
                     help="cfg2 (default) is the headline line; the others print one line each")
-    ap.add_argument("--sharded", action="store_true",
-                    help="time the multi-GPU pass (shard + NCCL exchange + finalize) even at one rank")
+    ap.add_argument("--segmented", action="store_true",
+                    help="N=1: time the step kernel by kernel (events between kernels) instead of whole passes")
     ap.add_argument("--profile-steps", action="store_true",
                     help="only the warm-up + timed steps (for ncu launch lists)")
     args = ap.parse_args()
