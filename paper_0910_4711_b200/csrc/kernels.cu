@@ -1263,37 +1263,45 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
                                                    (long long)ncell * dim * 8);
     XT* xs = wstage + warp * 32 * kWStageStride;
     if (DIM == 16) {
-      // software-pipelined: the next batch's cells and rows are in flight
-      // while this batch is staged and summed (the loop was latency-bound)
-      long long row = lo + (long long)warp * 32 + lane;
-      bool valid = row < hi;
-      int cell = valid ? (zero_cells ? 0 : a.idx[row]) : -1;
-      XT xr[16];
-      load_row16<XT, DIM>(X, row, dim, 0, valid, xr);
+      // lanes = dimensions straight from global memory: half-warp h reads
+      // rows base + 2p + h (64 contiguous bytes per half, one coalesced
+      // 128-byte request per warp), all 16 rows' loads issued before any
+      // sum; consecutive rows of one cell are summed in a register and the
+      // half-warp table is touched once per run (no staging, no per-row
+      // read-modify-write chain through shared memory)
       for (long long base = lo + (long long)warp * 32; base < hi; base += (long long)kWarps * 32) {
-        const long long nrow = base + (long long)kWarps * 32 + lane;
-        const bool nvalid = nrow < hi;
-        const int ncell = nvalid ? (zero_cells ? 0 : a.idx[nrow]) : -1;
-        XT xn[16];
-        load_row16<XT, DIM>(X, nrow, dim, 0, nvalid, xn);
-        const int lc = valid ? cell : -1;  // one table piece on this path: every cell is in range
+        XT xv[16];
+        int cv[16];
 #pragma unroll
-        for (int l = 0; l < 16; ++l) xs[lane * kWStageStride + l] = xr[l];
-        __syncwarp();
-#pragma unroll 4
         for (int p = 0; p < 16; ++p) {
-          const int rr = 2 * p + half;
-          const int cl = __shfl_sync(0xffffffffu, lc, rr);
-          if (cl >= 0) {
-            tab[(long long)cl * dim + hl] += to_fixed((double)xs[rr * kWStageStride + hl], scale);
-            if (hl == 0) tcount[cl] += 1;
+          const long long r = base + 2 * p + half;
+          const bool ok = r < hi;
+          xv[p] = ok ? __ldg(X + r * 16 + hl) : (XT)0;
+          cv[p] = ok ? (zero_cells ? 0 : __ldg(a.idx + r)) : -1;
+        }
+        long long acc = 0;
+        int cur = -1;
+        unsigned run = 0;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          if (cv[p] != cur) {  // uniform within the half-warp (one row)
+            if (cur >= 0) {
+              tab[(long long)cur * 16 + hl] += acc;
+              if (hl == 0) tcount[cur] += run;
+            }
+            cur = cv[p];
+            acc = 0;
+            run = 0;
+          }
+          if (cur >= 0) {
+            acc += to_fixed((double)xv[p], scale);
+            ++run;
           }
         }
-        __syncwarp();
-#pragma unroll
-        for (int l = 0; l < 16; ++l) xr[l] = xn[l];
-        cell = ncell;
-        valid = nvalid;
+        if (cur >= 0) {
+          tab[(long long)cur * 16 + hl] += acc;
+          if (hl == 0) tcount[cur] += run;
+        }
       }
     } else
     for (long long base = lo + (long long)warp * 32; base < hi; base += (long long)kWarps * 32) {
