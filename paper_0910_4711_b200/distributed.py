@@ -283,7 +283,8 @@ def sharded_lbg_train(ts, config, backend_factory=None):
         gdev = f"cuda:{device}"
     else:
         backend = backend_factory(rows, lo, ts.m)
-        gdev = None
+        dev = getattr(backend, "device", None)  # a DeviceShard from a caller's cache
+        gdev = f"cuda:{dev}" if dev is not None else None
     if plan.world == 1:  # replica fallback above: no collective
         cb, history, warnings, total, dists = run_sharded(backend, config, collective=False)
         all_dists = dists
