@@ -358,36 +358,37 @@ def run_b200(args):
         from paper_0910_4711_b200 import distributed as D
 
         shard = D.DeviceShard(x, rank * n, world * n, local_rank)
-        gmax = shard.tensor([shard.maxabs()])
-        if world > 1:
-            dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
-        shard.lloyd_begin(cb, float(gmax.item()))
-        ex = shard.exchange()
-
-        def pass_():
-            shard.lloyd_local()
+        with torch.cuda.stream(shard.stream):  # our kernels, NCCL and the events on one stream
+            gmax = shard.tensor([shard.maxabs()])
             if world > 1:
-                dist.all_reduce(ex, op=dist.ReduceOp.SUM)
-            shard.finalize()
+                dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+            shard.lloyd_begin(cb, float(gmax.item()))
+            ex = shard.exchange()
 
-        for _ in range(args.warmup):
-            flush.zero_()
-            pass_()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        ms_steps = []
-        for _ in range(args.steps):
-            flush.zero_()
+            def pass_():
+                shard.lloyd_local()
+                if world > 1:
+                    dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+                shard.finalize()
+
+            for _ in range(args.warmup):
+                flush.zero_()
+                pass_()
             torch.cuda.synchronize()
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            pass_()
-            ev1.record()
+            if world > 1:
+                dist.barrier()
+            ms_steps = []
+            for _ in range(args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                pass_()
+                ev1.record()
+                torch.cuda.synchronize()
+                ms_steps.append(ev0.elapsed_time(ev1))
             torch.cuda.synchronize()
-            ms_steps.append(ev0.elapsed_time(ev1))
-        torch.cuda.synchronize()
     ms_step = sum(ms_steps) / len(ms_steps)
     if world > 1:
         t = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{local_rank}")

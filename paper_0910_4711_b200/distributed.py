@@ -88,9 +88,10 @@ class DeviceShard:
         import torch
 
         self.torch = torch
-        # run our kernels on torch's stream so NCCL and the passes are ordered
-        stream = torch.cuda.current_stream(device)
-        _lib.check(self.L.vqb_set_stream(self.s.handle, ctypes.c_void_p(stream.cuda_stream)))
+        # one stream for our kernels and the collectives between them (the
+        # drivers below run the collectives under torch.cuda.stream(self.stream))
+        self.stream = torch.cuda.Stream(device=device)
+        _lib.check(self.L.vqb_set_stream(self.s.handle, ctypes.c_void_p(self.stream.cuda_stream)))
         self._ex = None
 
     def maxabs(self) -> float:
@@ -171,7 +172,52 @@ class DeviceShard:
         return cb[: int(summ.final_size)], history, warnings, float(summ.total), dists
 
 
+def _capture_batch(backend, ex, batch: int):
+    """One CUDA graph of ``batch`` passes -- our kernels and the NCCL
+    allreduce between them -- replayed per batch, so the host issues one
+    launch per batch instead of ~12 per pass (what bounds the small-codebook
+    levels when the shards are small).  Every kernel reads its size / mode from
+    the device state and passes after `done` exit at once, so the same graph
+    serves every level, as in the single-GPU vqb_train.  NCCL + DeviceShard
+    only (gloo collectives cannot be captured); VQB_SHARD_GRAPH=0 disables."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    if os.environ.get("VQB_SHARD_GRAPH", "1") == "0" or getattr(backend, "stream", None) is None:
+        return None
+    if dist.get_backend() != "nccl":
+        return None
+    backend.stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=backend.stream):
+        for _ in range(batch):
+            backend.local()
+            dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+            backend.finalize()
+    return g
+
+
+def _on_stream(backend):
+    """The backend's stream as torch's current stream (collectives, events and
+    graph replays then order with its kernels); a no-op for CPU backends."""
+    import contextlib
+
+    stream = getattr(backend, "stream", None)
+    if stream is None:
+        return contextlib.nullcontext()
+    import torch
+
+    return torch.cuda.stream(stream)
+
+
 def run_sharded(backend, config, batch: int = 4, collective: bool = True):
+    with _on_stream(backend):
+        return _run_sharded(backend, config, batch, collective)
+
+
+def _run_sharded(backend, config, batch: int, collective: bool):
     """Drive the pass loop on every rank.  Collectives: one MAX allreduce of
     |x| (common fixed-point scale), then per pass one SUM allreduce of the
     packed int64 exchange buffer.  Ranks stay in lockstep because every rank
@@ -192,11 +238,15 @@ def run_sharded(backend, config, batch: int = 4, collective: bool = True):
     levels = max(1, int(math.log2(config.target_size)))
     limit = (levels + 1) * (config.max_iterations_per_level + 1) + 2 * batch
     passes = 0
+    graph = _capture_batch(backend, ex, batch) if collective else None
     while True:
-        for _ in range(batch):
-            backend.local()
-            all_reduce(ex, dist.ReduceOp.SUM)
-            backend.finalize()
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(batch):
+                backend.local()
+                all_reduce(ex, dist.ReduceOp.SUM)
+                backend.finalize()
         passes += batch
         if backend.poll():
             break
@@ -209,6 +259,11 @@ def run_sharded(backend, config, batch: int = 4, collective: bool = True):
 
 def sharded_lloyd(backend, codebook: np.ndarray, passes: int = 1, collective: bool = True,
                   on_pass=None):
+    with _on_stream(backend):
+        return _sharded_lloyd(backend, codebook, passes, collective, on_pass)
+
+
+def _sharded_lloyd(backend, codebook: np.ndarray, passes: int, collective: bool, on_pass):
     """``passes`` Lloyd iterations at a fixed codebook size over all ranks:
     one MAX allreduce of |x| (the common fixed-point scale), then per pass
     local assign + epilogue, ONE SUM allreduce of the packed int64 exchange
