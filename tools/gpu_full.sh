@@ -13,3 +13,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:assi
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:assign_tc -s 2 -c 1 \
   -o gpurun_out/tc64_full python tools/profile_step.py cfg3 > gpurun_out/ncu_full64.log 2>&1; echo full64 rc=$?
 tail -2 gpurun_out/pytest_gpu.log
+for c in cfg2 cfg3; do
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
+    --log-file gpurun_out/launches_${c}_step.csv python tools/profile_step.py $c > /dev/null 2>&1; echo step_$c rc=$?
+done
+python tools/design_levels.py cfg2 > gpurun_out/design_levels.txt 2>&1; python tools/design_levels.py cfg4 >> gpurun_out/design_levels.txt 2>&1; echo levels rc=$?
