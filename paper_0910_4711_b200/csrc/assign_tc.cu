@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
   const long long nitems = MODE == kTcShortlist ? (long long)st->flag_count : a.r1 - a.r0;
   // a short queue is rescanned faster by shortlist_kernel's warp-per-row mode
   // (valid for TC-flagged rows: its FP32 error is below the TC band's)
-  if (MODE == kTcShortlist && nitems < kTcShortlistMin) return;
+  if (MODE == kTcShortlist && nitems * (long long)K < kTcShortlistWork) return;
   const long long ntiles = (nitems + kTcRows - 1) / kTcRows;
   const long long my_tiles = MODE == kTcDump
                                  ? 1

@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
   const long long count = st->flag_count;
   if (count == 0) return;
   const int K = st->size;
-  if (a.tcb && tc_handles(st, K) && count >= kTcShortlistMin) return;  // the TC shortlist runs
+  if (a.tcb && tc_handles(st, K) && count * (long long)K >= kTcShortlistWork) return;  // the TC shortlist runs
   const double* __restrict__ cb = a.cb[st->cur];
   if (count < (long long)gridDim.x * NT) {
     // Few queued rows (e.g. a converged codebook): one warp per row, lanes

@@ -201,7 +201,14 @@ cudaError_t launch_distortion_sum(const double* d, long long n, bool inorder, do
 constexpr int kTcChunk = 256;  // codewords per MMA N
 constexpr int kTcRows = 128;   // rows per tile (MMA M)
 constexpr int kTcShort = 8;    // shortlist candidates per row before the full FP64 scan
-constexpr int kTcShortlistMin = 0;  // queued rows below which the FP32 shortlist rescans (TC-flagged rows: either works)
+// queued rows x codebook size below which the FP32 shortlist (warp per row)
+// rescans instead of the TC shortlist pass: a short queue at a small codebook
+// does not pay the TC pass's per-CTA set-up (cfg2 K=64: 19.5 -> 13.4 us);
+// either is valid for TC-flagged rows (the FP32 error is below the TC band's)
+#ifndef VQB_TC_SL_WORK
+#define VQB_TC_SL_WORK (1LL << 19)
+#endif
+constexpr long long kTcShortlistWork = VQB_TC_SL_WORK;
 __host__ __device__ inline long long tc_chunk_elems(int dim) { return (long long)kTcChunk * (2 * dim + 16); }
 int tc_max_size(int dim);      // largest codebook whose operand image fits in smem
 // does assign_tc (rather than assign_fast) run the candidate pass at size K?
