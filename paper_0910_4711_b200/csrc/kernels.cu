@@ -918,20 +918,21 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 
 // The epilogue:
 //
-// dist_td_kernel (one block per 2048-row tile): each row's exact FP64
-// distance to its final winner and the tile's fixed-tree distortion partial
-// (sum_inorder's role, _kernels.py:92-98, in a fixed order that does not
-// depend on the grid or on the number of GPUs).
+// td_tiles_kernel (one block per 2048-row tile): the tile's fixed-tree
+// distortion partial from the per-row exact FP64 distances every assignment
+// path stored (sum_inorder's role, _kernels.py:92-98, in a fixed order that
+// does not depend on the grid or on the number of GPUs).
 //
-// sums_kernel (one persistent block per SM over a contiguous row range,
-// thread per row): int64 fixed-point cell sums + counts.  Integer adds
-// commute, so the result is deterministic for every grid shape and GPU count.
-//  * small K: warp-private smem tables, rows aggregated per cell inside the
-//    warp (match_any), lanes = dims, plain adds;
+// sums_kernel (one persistent block per SM over a contiguous row range):
+// int64 fixed-point cell sums + counts.  Integer adds commute, so the result
+// is deterministic for every grid shape and GPU count.
+//  * small K: half-warp-private smem tables, lanes = dims, plain adds, runs
+//    of one cell summed in registers first;
 //  * otherwise: a block table [dim][cell] accumulated with NATIVE 32-bit smem
 //    atomics -- an exact int64 add is atomicAdd on the low word (the returned
-//    old value gives the carry) plus atomicAdd on the high word.  Codebooks
-//    whose table would not fit are split into chunks (gridDim.y).
+//    old value gives the carry) plus atomicAdd on the high word -- one per
+//    run of equal cells in a thread's contiguous rows.  Codebooks whose table
+//    would not fit are split into chunks (gridDim.y).
 // Each block writes its table to a slab; reduce_partials_kernel sums them.
 constexpr int kSumThreads = 512;
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
@@ -963,11 +964,7 @@ __host__ __device__ inline SumsPlan sums_plan(int K, int dim) {
   return p;
 }
 constexpr int kWStageStride = 20;
-// block-table path: lane-sequential runs (1) or strided rows + warp segmented scan (0)
-#ifndef VQB_SUMS_RUNS
-#define VQB_SUMS_RUNS 1
-#endif
-constexpr bool kSumsRuns = VQB_SUMS_RUNS != 0;  // staged row stride (elements), padded against bank conflicts
+  // staged row stride (elements), padded against bank conflicts
 
 // exact int64 accumulation from two native 32-bit shared atomics
 __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, long long t) {
@@ -1007,47 +1004,6 @@ __global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a) {
     double acc = 0.0;
     for (int w = 0; w < 8; ++w) acc = __dadd_rn(acc, red[w]);
     a.ex.td()[a.tile0 + t] = __double_as_longlong(acc);
-  }
-}
-
-// One block per 2048-row tile: the final winner's distance in the
-// reference's FP64 arithmetic (_kernels.py:25-34) -> dists, and the tile's
-// fixed-tree distortion partial (sum_inorder's role, in an order independent
-// of the grid and of the number of GPUs).
-template <typename XT, int DIM>
-__global__ void __launch_bounds__(256, 4) dist_td_kernel(KernelArgs a, const XT* __restrict__ X) {
-  pdl_wait();
-  const DevState* st = a.st;
-  if (st->done) return;
-  __shared__ double red[8];
-  const int dim = DIM ? DIM : a.dim;
-  const int metric = st->metric;
-  const double* __restrict__ cb = a.cb[st->cur];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long t = blockIdx.x;
-  const long long n = a.n;
-  double tsum = 0.0;
-#pragma unroll 2
-  for (int r = 0; r < kTdTile / 256; ++r) {
-    const long long row = t * kTdTile + (long long)r * 256 + tid;
-    double d = 0.0;
-    if (row < n) {
-      const int cell = a.idx[row];
-      d = winner_dist<XT, DIM>(X + row * dim, cb + (long long)cell * dim, dim);
-      if (metric == kEuclidean) d = sqrt(d);
-      a.dists[row] = d;
-    }
-    tsum = __dadd_rn(tsum, d);
-  }
-  // fixed tree: lanes (xor butterfly), then warps in order
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) tsum = __dadd_rn(tsum, __shfl_xor_sync(0xffffffffu, tsum, off));
-  if (lane == 0) red[warp] = tsum;
-  __syncthreads();
-  if (tid == 0) {
-    double sacc = 0.0;
-    for (int w = 0; w < 8; ++w) sacc = __dadd_rn(sacc, red[w]);
-    a.ex.td()[a.tile0 + t] = __double_as_longlong(sacc);
   }
 }
 
@@ -1126,7 +1082,7 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const long long n = a.n;
   const long long lo = n * blockIdx.x / gridDim.x;
   const long long hi = n * (blockIdx.x + 1) / gridDim.x;
-  if (!warp_sink && kSumsRuns) {
+  if (!warp_sink) {
     // Block tables, lane-sequential runs: thread t owns a contiguous slice of
     // the block's rows and keeps the running per-dimension sum of the current
     // cell in registers, flushing it (one exact int64 smem add per dimension)
@@ -1175,81 +1131,6 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
         }
       }
       if (cur >= 0) flush();
-    }
-  }
-  if (!warp_sink && !kSumsRuns) {
-    // Block tables.  Two rows per thread per step, and every load of both
-    // (cells and coordinates) issued before the first atomic: the rows'
-    // HBM/L2 latency overlaps instead of chaining per row.
-    constexpr int R = 2;
-    for (long long base = lo; base < hi; base += (long long)kSumThreads * R) {
-      long long rr[R];
-      bool ok[R];
-      int lc[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        rr[k] = base + tid + (long long)k * kSumThreads;
-        ok[k] = rr[k] < hi;
-      }
-      int cell[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) cell[k] = ok[k] ? (zero_cells ? 0 : a.idx[rr[k]]) : -1;
-      // runs of equal cells among a warp's consecutive rows (image blocks of
-      // a smooth region) are summed in registers first -- a segmented scan
-      // -- so one atomic per run and dimension hits the table instead of one
-      // per row (same-address atomics serialise)
-      bool seg[R];
-      int hd[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        lc[k] = (ok[k] && cell[k] >= c_lo && cell[k] < c_hi) ? cell[k] - (int)c_lo : -1;
-        const int prev = __shfl_up_sync(0xffffffffu, lc[k], 1);
-        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != lc[k]);
-        seg[k] = heads != 0xffffffffu;
-        const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-        hd[k] = 31 - __clz(heads & upto);  // my run's head lane
-        // lanes that are not their run's tail skip the atomics below
-        if (seg[k] && !(lane == 31 || ((heads & ~upto) & (1u << (lane + 1))))) lc[k] = -2;
-      }
-      for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
-        const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
-        XT xr[R][16];
-#pragma unroll
-        for (int k = 0; k < R; ++k) load_row16<XT, DIM>(X, rr[k], dim, c0, ok[k], xr[k]);
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          if (seg[k]) {
-#pragma unroll
-            for (int l = 0; l < 16; ++l) {
-              if (l >= cw) continue;
-              long long v = ok[k] ? to_fixed((double)xr[k][l], scale) : 0;
-#pragma unroll
-              for (int off = 1; off < 32; off <<= 1) {
-                const long long t = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane - off >= hd[k]) v += t;
-              }
-              if (lc[k] >= 0) {
-                const long long w = (long long)(c0 + l - d_lo) * ncell + lc[k];
-                smem_add_i64(blo + w, bhi + w, v);
-              }
-            }
-            continue;
-          }
-          if (lc[k] < 0) continue;
-#pragma unroll
-          for (int l = 0; l < 16; ++l) {
-            if (l < cw) {
-              const long long w = (long long)(c0 + l - d_lo) * ncell + lc[k];  // [dim][cell]: spread banks
-              smem_add_i64(blo + w, bhi + w, to_fixed((double)xr[k][l], scale));
-            }
-          }
-        }
-      }
-      if (dy == 0) {
-#pragma unroll
-        for (int k = 0; k < R; ++k)  // run tails count their whole run
-          if (lc[k] >= 0) atomicAdd(bcounts + lc[k], seg[k] ? (unsigned)(lane - hd[k] + 1) : 1u);
-      }
     }
   }
   if (warp_sink) {
