@@ -132,3 +132,55 @@ def test_two_rank_lloyd_passes_match_single_device(tmp_path):
         cb, _ = oracle.update_codebook(x64, cells, cb)
     np.testing.assert_allclose(cb1, cb, rtol=1e-12, atol=1e-12)
     assert abs(td1 - td) <= 1e-12 * td
+
+
+def _nccl_one_rank(rank, port, out_path, graph):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), VQB_SHARD_GRAPH=graph)
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200.distributed import sharded_lbg_train
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        x = _data()
+        cb, stats = sharded_lbg_train(vq.TrainingSet(x), vq.LbgConfig(target_size=64, epsilon=1e-3, delta=0.01))
+        np.savez(out_path, cb=cb.codevectors, total=stats.total, passes=len(stats.history))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_graph_replayed_passes_match_plain_launches(tmp_path):
+    """The sharded loop over NCCL with batches captured into a CUDA graph
+    (kernels + allreduce) gives the bits of the plain per-pass launches."""
+    import torch.multiprocessing as mp
+
+    outs = []
+    for graph in ("1", "0"):
+        out = str(tmp_path / f"g{graph}.npz")
+        mp.start_processes(_nccl_one_rank, args=(_free_port(), out, graph), nprocs=1, join=True,
+                           start_method="spawn")
+        outs.append(np.load(out))
+    assert outs[0]["cb"].tobytes() == outs[1]["cb"].tobytes()
+    assert float(outs[0]["total"]) == float(outs[1]["total"])
+    assert int(outs[0]["passes"]) == int(outs[1]["passes"])
+
+
+def test_programmatic_dependent_launch_is_transparent():
+    """VQB_PDL=0 (plain stream order) and the default (programmatic dependent
+    launches) design the same codebook bit for bit."""
+    import subprocess
+
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_0910_4711_b200 as vq; "
+            "from paper_0910_4711_b200 import synthetic; x = synthetic.make_training('cfg2', n=1 << 16); "
+            "cb, st = vq.lbg_train(vq.TrainingSet(x), vq.LbgConfig(target_size=128, epsilon=1e-3)); "
+            "sys.stdout.write(cb.codevectors.tobytes().hex()[:4096] + ' ' + repr(st.total))") % ROOT
+    outs = []
+    for pdl in ("1", "0"):
+        env = dict(os.environ, VQB_PDL=pdl)
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                                   check=True, timeout=600).stdout)
+    assert outs[0] == outs[1] and outs[0]
