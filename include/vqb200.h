@@ -242,6 +242,7 @@ int vqb_host_copy(void* dst, const void* src, int64_t bytes);
 /* Index of the first inf / NaN among n float32 values, or -1 (host threads);
  * TrainingSet's "training vector i component j is not finite" check. */
 int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first);
+int vqb_first_nonfinite_f64(const double* x, int64_t n, int64_t* first);
 
 /* Pipe microbenchmark (0 FFMA, 1 FFMA2, 2 FFMA+top-2 mix, 3 DADD): lane-ops/s. */
 int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, double* ops_per_s,

@@ -114,6 +114,7 @@ def lib():
             "vqb_lloyd_begin": ([_P, _P, _I64, _D], _I32),
             "vqb_lloyd_local": ([_P], _I32),
             "vqb_first_nonfinite_f32": ([_P, _I64, _P], _I32),
+            "vqb_first_nonfinite_f64": ([_P, _I64, _P], _I32),
             "vqb_bench_formats": ([_I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _P, _P], _I32),
         }
         for name, (args, res) in sig.items():

@@ -252,7 +252,9 @@ extern "C" int vqb_host_copy(void* dst, const void* src, int64_t bytes) {
   return VQB_OK;
 }
 
-extern "C" int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first) {
+namespace {
+template <typename T, typename U, U kExpMask>
+int first_nonfinite(const T* x, int64_t n, int64_t* first) {
   *first = -1;
   if (n <= 0) return VQB_OK;
   const unsigned hw = std::thread::hardware_concurrency();
@@ -260,9 +262,9 @@ extern "C" int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first
   std::vector<int64_t> found((size_t)parts, -1);
   auto scan = [&](int p) {
     const int64_t lo = n * p / parts, hi = n * (p + 1) / parts;
-    const uint32_t* u = reinterpret_cast<const uint32_t*>(x);
+    const U* u = reinterpret_cast<const U*>(x);
     for (int64_t i = lo; i < hi; ++i)
-      if ((u[i] & 0x7f800000u) == 0x7f800000u) {  // exponent all ones: inf or NaN
+      if ((u[i] & kExpMask) == kExpMask) {  // exponent all ones: inf or NaN
         found[(size_t)p] = i;
         return;
       }
@@ -278,4 +280,12 @@ extern "C" int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first
     }
   return VQB_OK;
 }
+}  // namespace
 
+extern "C" int vqb_first_nonfinite_f64(const double* x, int64_t n, int64_t* first) {
+  return first_nonfinite<double, uint64_t, 0x7ff0000000000000ull>(x, n, first);
+}
+
+extern "C" int vqb_first_nonfinite_f32(const float* x, int64_t n, int64_t* first) {
+  return first_nonfinite<float, uint32_t, 0x7f800000u>(x, n, first);
+}
