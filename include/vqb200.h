@@ -75,6 +75,12 @@ int vqb_column_sums(const double* vectors, int64_t m, int64_t dim, double* out);
 /* _kernels.sum_inorder (_kernels.py:92-98), strict left-to-right. */
 int vqb_sum_inorder(const double* values, int64_t n, double* out);
 
+/* core.split_codebook (core.py:277-289): out[2*size][dim], rows 2i = c_i +
+ * delta and 2i+1 = c_i - delta (one rounding each); VQB_CONFIG unless
+ * delta > 0. */
+int vqb_split_codebook(const double* codebook, int64_t size, int64_t dim, double delta, int device,
+                       double* out);
+
 /* _kernels.pair_distance (_kernels.py:69-78). */
 int vqb_pair_distance(const double* a, const double* b, int64_t dim, int metric, double* out);
 

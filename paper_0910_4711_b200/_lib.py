@@ -83,6 +83,7 @@ def lib():
             "vqb_column_sums": ([_P, _I64, _I64, _P], _I32),
             "vqb_sum_inorder": ([_P, _I64, _P], _I32),
             "vqb_pair_distance": ([_P, _P, _I64, _I32, _P], _I32),
+            "vqb_split_codebook": ([_P, _I64, _I64, _D, _I32, _P], _I32),
             "vqb_open": ([_P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
             "vqb_close": ([_P], _I32),
             "vqb_set_stream": ([_P, _P], _I32),

@@ -1749,4 +1749,21 @@ int vqb_bench_formats(int which, int64_t images, int64_t height, int64_t width, 
   return VQB_OK;
 }
 
+int vqb_split_codebook(const double* codebook, int64_t size, int64_t dim, double delta, int device,
+                       double* out) {
+  if (size < 1 || dim < 1) return fail(VQB_USAGE, "codebook must be at least 1x1");
+  if (!(delta > 0)) return fail(VQB_CONFIG, "split offset delta must be > 0, got %g", delta);
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  if (int rc = g_oneshot.init(device)) return rc;
+  cudaStream_t st = g_oneshot.stream;
+  PoolBuf<double> cb(st), o(st);
+  CK(cb.alloc((size_t)(size * dim)));
+  CK(o.alloc((size_t)(2 * size * dim)));
+  CK(cudaMemcpyAsync(cb.p, codebook, sizeof(double) * size * dim, cudaMemcpyHostToDevice, st));
+  CK(launch_split_rows(cb.p, size, (int)dim, delta, o.p, st));
+  CK(cudaMemcpyAsync(out, o.p, sizeof(double) * 2 * size * dim, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return VQB_OK;
+}
+
 }  // extern "C"

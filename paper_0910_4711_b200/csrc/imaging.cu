@@ -343,6 +343,19 @@ __global__ void inorder_kernel(const double* v, long long n, double* out) {
   *out = s;
 }
 
+// core._split_rows (core.py:277-281): rows 2i = c + delta, 2i+1 = c - delta,
+// each component rounded once (the device loop's apply_kernel does the same)
+__global__ void split_rows_kernel(const double* __restrict__ cb, long long count, int dim, double delta,
+                                  double* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / dim, l = e - i * dim;
+    const double c = cb[e];
+    out[(2 * i) * dim + l] = __dadd_rn(c, delta);
+    out[(2 * i + 1) * dim + l] = __dsub_rn(c, delta);
+  }
+}
+
 int grid_for(long long work, int sms) {
   const long long g = (work + 255) / 256;
   return (int)std::max<long long>(1, std::min<long long>(g, (long long)sms * 8));
@@ -462,6 +475,13 @@ cudaError_t launch_decode(const unsigned* idx, long long n, int L, const double*
     decode_pairs_kernel<0><<<g, 256, 0, s>>>(idx, n, L, cb, K, out, bad);
   else
     decode_elems_kernel<<<grid_for(n * L, sms), 256, 0, s>>>(idx, n, L, cb, K, out, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_rows(const double* cb, long long size, int dim, double delta, double* out,
+                              cudaStream_t s) {
+  const long long count = size * dim;
+  split_rows_kernel<<<grid_for(count, device_sms()), 256, 0, s>>>(cb, count, dim, delta, out);
   return cudaGetLastError();
 }
 

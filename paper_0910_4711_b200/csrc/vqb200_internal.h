@@ -191,6 +191,8 @@ cudaError_t launch_decode_pixels(const unsigned* idx, const double* cb, long lon
                                  cudaStream_t s);
 cudaError_t launch_decode(const unsigned* idx, long long n, int L, const double* cb, long long K, double* out,
                           int* bad, cudaStream_t s);
+cudaError_t launch_split_rows(const double* cb, long long size, int dim, double delta, double* out,
+                              cudaStream_t s);
 cudaError_t launch_index_check(const unsigned* idx, long long n, long long K, int* bad, cudaStream_t s);
 cudaError_t launch_pair_rows(const double* a, const double* b, long long n, int dim, int metric, double* d,
                              cudaStream_t s);

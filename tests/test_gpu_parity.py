@@ -407,3 +407,20 @@ def test_tc_accumulators_vs_float64_emulation(dim, k):
     n_mma = 3 * dim // 16 + 1
     assert rel.max() <= 0.5 * 2 * n_mma * 2.0 ** -22, rel.max()
     assert np.array_equal(np.argmin(dump, 1), np.argmin(v, 1))
+
+
+# ---------------------------------------------------------------------------
+# split_codebook on the device (core.py:277-289)
+# ---------------------------------------------------------------------------
+
+def test_split_codebook_known_answers_and_oracle():
+    # the reference's split KATs (pkg/tests/test_core.py split tests)
+    assert vq.split_codebook(vq.Codebook([(2.0, 0.5)]), 0.5).codevectors.tolist() == [[2.5, 1.0], [1.5, 0.0]]
+    got = vq.split_codebook(vq.Codebook([(0.0, 0.0), (4.0, 4.0)]), 0.01).codevectors.tolist()
+    assert got == [[0.01, 0.01], [-0.01, -0.01], [4.01, 4.01], [3.99, 3.99]]
+    rows = np.random.default_rng(5).normal(0, 100, (37, 13))
+    for delta in (0.01, 0.005, 1e-9):
+        out = vq.split_codebook(vq.Codebook(rows), delta).codevectors
+        assert out.tobytes() == oracle.split_rows(rows, delta).tobytes()
+    with pytest.raises(vq.ConfigError):
+        vq.split_codebook(vq.Codebook(rows), 0.0)
