@@ -1061,6 +1061,17 @@ int set_centre_from_codebook(vqb_session* s, const double* codebook, long long s
   return VQB_OK;
 }
 
+// H2D piece size of the host-buffer paths (VQB_PIECE_MB, default 8): the
+// candidate pass of piece i runs while piece i+1 is in flight
+size_t piece_bytes() {
+  static const size_t b = [] {
+    const char* e = getenv("VQB_PIECE_MB");
+    const long v = e ? atol(e) : 8;
+    return (size_t)(v > 0 ? v : 8) << 20;
+  }();
+  return b;
+}
+
 // Enqueue the H2D of `rows` host rows into s->x32 in pieces, each piece's
 // max |x| and FP32 candidate pass launched as soon as it lands (the copy of
 // piece i+1 overlaps the distance pass of piece i).  For dims without a fast
@@ -1068,7 +1079,7 @@ int set_centre_from_codebook(vqb_session* s, const double* codebook, long long s
 int stream_rows_and_assign(vqb_session* s, const KernelArgs& a, const float* x, long long rows,
                            unsigned long long* maxabs_bits) {
   const size_t row_bytes = sizeof(float) * (size_t)s->dim;
-  const size_t piece = std::max<size_t>(row_bytes, ((size_t)8 << 20) / row_bytes * row_bytes);
+  const size_t piece = std::max<size_t>(row_bytes, piece_bytes() / row_bytes * row_bytes);
   CK(cudaMemsetAsync(maxabs_bits, 0, sizeof(unsigned long long), s->stream));
   CK(upload(s->x32, x, row_bytes * rows, piece, s->copy_stream, s->stream,
             [&](size_t off, size_t len) -> cudaError_t {
@@ -1141,7 +1152,7 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   Trace tr(s->stream);
   tr.mark("start");
   const size_t row_bytes = sizeof(float) * (size_t)dim;
-  const size_t piece = std::max<size_t>(row_bytes, ((size_t)8 << 20) / row_bytes * row_bytes);
+  const size_t piece = std::max<size_t>(row_bytes, piece_bytes() / row_bytes * row_bytes);
   const bool pinned_x = host_is_pinned(x);
   if (tr.on) fprintf(stderr, "[trace] pinned=%d\n", pinned_x ? 1 : 0);
   // the small uploads (centre, codebook, state) go first: they share the
