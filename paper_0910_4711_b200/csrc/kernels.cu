@@ -934,13 +934,17 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
 //    run of equal cells in a thread's contiguous rows.  Codebooks whose table
 //    would not fit are split into chunks (gridDim.y).
 // Each block writes its table to a slab; reduce_partials_kernel sums them.
-constexpr int kSumThreads = 512;
+// threads per sums block: 768 at L = 16 (more rows in flight: cfg2 -3 % at
+// K = 1024, -12 % at K = 2), 512 for wider rows (their registers; 768 was
+// +6 % at L = 64)
+template <int DIM>
+__host__ __device__ constexpr int sum_threads() { return DIM == 16 ? 768 : 512; }
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
 
-__host__ __device__ inline bool sums_warp_sink(int K, int dim) {
+__host__ __device__ inline bool sums_warp_sink(int K, int dim, int nthreads) {
   // 2 half-warp tables per warp + the 32-row staging slices (double rows)
-  const long long tables = ((long long)K * dim * 8 + K * 4 + 15) / 16 * 16 * 2 * (kSumThreads / 32);
-  const long long stage = (long long)(kSumThreads / 32) * 32 * 20 * 8;
+  const long long tables = ((long long)K * dim * 8 + K * 4 + 15) / 16 * 16 * 2 * (nthreads / 32);
+  const long long stage = (long long)(nthreads / 32) * 32 * 20 * 8;
   return tables + stage <= kEpiSmem;
 }
 // Block-table split when K x L does not fit one table: first split the
@@ -950,11 +954,11 @@ struct SumsPlan {
   int dc, ndc;
   long long kc, nkc;
 };
-__host__ __device__ inline SumsPlan sums_plan(int K, int dim) {
+__host__ __device__ inline SumsPlan sums_plan(int K, int dim, int nthreads) {
   SumsPlan p;
   p.dc = dim;
   p.kc = K;
-  if (!sums_warp_sink(K, dim)) {
+  if (!sums_warp_sink(K, dim, nthreads)) {
     while (p.dc > 8 && (long long)K * (p.dc * 8 + 4) > kEpiSmem - 64) p.dc = (p.dc / 2 + 7) / 8 * 8;
     const long long kc = (kEpiSmem - 64) / ((long long)p.dc * 8 + 4);
     p.kc = kc < K ? kc : K;
@@ -1040,7 +1044,7 @@ __device__ __forceinline__ void load_row16(const XT* __restrict__ X, long long r
 }
 
 template <typename XT, int DIM>
-__global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, const XT* __restrict__ X,
+__global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs a, const XT* __restrict__ X,
                                                              int zero_cells) {
   pdl_wait();
   const DevState* st = a.st;
@@ -1049,10 +1053,11 @@ __global__ void __launch_bounds__(kSumThreads, 1) sums_kernel(KernelArgs a, cons
   const int dim = DIM ? DIM : a.dim;
   const double scale = ldexp(1.0, st->fixed_shift);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kSumThreads = sum_threads<DIM>();
   constexpr int kWarps = kSumThreads / 32;
 
-  const bool warp_sink = sums_warp_sink(K, dim);
-  const SumsPlan plan = sums_plan(K, dim);
+  const bool warp_sink = sums_warp_sink(K, dim, kSumThreads);
+  const SumsPlan plan = sums_plan(K, dim, kSumThreads);
   const int chunk = blockIdx.y;
   const long long cy = chunk / plan.ndc;
   const int dy = chunk % plan.ndc;
@@ -1289,7 +1294,8 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   }
   if (!want_sums) return cudaSuccess;
   const long long kmax = zero_cells ? 1 : a.kmax;
-  const SumsPlan plan = sums_plan((int)kmax, a.dim);
+  constexpr int kSumThreads = sum_threads<DIM>();
+  const SumsPlan plan = sums_plan((int)kmax, a.dim, kSumThreads);
   const int chunks = (int)(plan.nkc * plan.ndc);
   const long long rows_per_block = 4LL * kSumThreads;
   int blocks = (int)((a.n + rows_per_block - 1) / rows_per_block);
