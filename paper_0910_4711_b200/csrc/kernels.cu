@@ -100,9 +100,13 @@ cudaError_t launch_prep_codebook(const KernelArgs& a, cudaStream_t s) {
 
 template <int L>
 struct FastCfg;
+#ifndef VQB_FAST16_NT
+#define VQB_FAST16_NT 512
+#define VQB_FAST16_R 4
+#endif
 template <>
 struct FastCfg<16> {
-  static constexpr int NT = 512, R = 4, TK = 1024;
+  static constexpr int NT = VQB_FAST16_NT, R = VQB_FAST16_R, TK = 1024;
 };
 template <>
 struct FastCfg<32> {
