@@ -946,9 +946,10 @@ __host__ __device__ constexpr int sum_threads() { return DIM == 16 ? 768 : 512; 
 constexpr int kEpiSmem = 224 * 1024;  // + static smem stays under the 227 KB opt-in
 
 __host__ __device__ inline bool sums_warp_sink(int K, int dim, int nthreads) {
-  // 2 half-warp tables per warp + the 32-row staging slices (double rows)
+  // 2 half-warp tables per warp + the 32-row staging slices (double rows;
+  // the 16-dimension path reads rows straight from global memory, no stage)
   const long long tables = ((long long)K * dim * 8 + K * 4 + 15) / 16 * 16 * 2 * (nthreads / 32);
-  const long long stage = (long long)(nthreads / 32) * 32 * 20 * 8;
+  const long long stage = dim == 16 ? 0 : (long long)(nthreads / 32) * 32 * 20 * 8;
   return tables + stage <= kEpiSmem;
 }
 // Block-table split when K x L does not fit one table: first split the
