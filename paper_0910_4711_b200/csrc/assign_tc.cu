@@ -9,21 +9,27 @@
 //
 //   D = yh.wh + yh.wl + yl.wh + 2^kn (nh + nl) = 2^(ey+ew) v      (fp32, TMEM)
 //
-// so the epilogue only does the top-2 bookkeeping (5 ALU ops per value) on
-// values read straight from TMEM.  The certification band is the FP32 one
-// widened for the split (4 x 2^-22) and for tensor-core accumulation (2 x
-// 2^-22 of the magnitude sum per MMA instruction; tools/tc_probe.py measures
-// <= 0.5 x 2^-22 per MMA against a float64 emulation of the same operands);
-// rows that do not certify go to the same shortlist / FP64 re-rank as the
-// FP32 pass, so a certified index is the reference's index.
+// so the epilogue only does the minimum / band bookkeeping on values read
+// straight from TMEM (per value half a 3-input FMNMX for the chunk minimum,
+// then one FSETP + predicated add for the count inside the band).  The
+// certification band is the FP32 one widened for the split (4 x 2^-22) and
+// for tensor-core accumulation (2 x 2^-22 of the magnitude sum per MMA
+// instruction; tools/tc_probe.py measures <= 0.5 x 2^-22 per MMA against a
+// float64 emulation of the same operands); rows that do not certify go to the
+// same shortlist / FP64 re-rank as the FP32 pass, so a certified index is the
+// reference's index.
 //
-// CTA = 1 MMA-issuer warp + 8 epilogue warps, persistent over 128-row tiles.
-// The codebook's operand image (staged by apply_kernel / prep_codebook in the
-// exact smem layout) is bulk-copied into smem once; the row tile's operands
-// are converted by the epilogue warps into a double-buffered smem tile;
+// CTA (persistent, one per SM, over 128-row tiles) = 1 MMA-issuer warp +
+// 16 (L = 16) or 8 epilogue warps (4 lane quarters x column parts) + a
+// streamer / converter pair + 8 (L = 16) or 4 certification warps.  The
+// codebook's operand image (staged by apply_kernel / prep_codebook in the
+// exact smem layout) is bulk-copied into smem once, or streamed through a TMA
+// ring when it does not fit; row tiles come from the prebuilt fp16 row image
+// of a resident training set (bulk copies) or are converted from x32;
 // accumulators are double-buffered in TMEM (2 x 256 columns), so the MMAs of
-// chunk c+1 overlap the epilogue of chunk c, and the conversion of tile i+1
-// overlaps the MMAs of tile i.
+// chunk c+1 overlap the epilogue of chunk c.  The certification warps merge
+// the parts' results, compute the certified row's exact FP64 distance and
+// queue the rest, off the epilogue's critical path.
 #include <cfloat>
 #include <cstddef>
 #include <cstdio>
