@@ -114,6 +114,20 @@ def test_product_never_imports_the_oracle():
         assert "vq_oracle" not in src and "vqo_" not in src, fn
 
 
+def test_every_reference_export_exists():
+    """Every name of vqkit.__all__ (pkg/src/vqkit/__init__.py:79-135) is
+    importable from the package (the GPU sweep harness stands in for the
+    thread sweep of bench.py)."""
+    import paper_0910_4711_b200 as vq
+
+    for name in ("AmdahlParams", "BenchRecord", "amdahl_speedup", "run_sweep", "speedup_report",
+                 "synthetic_training_set", "write_bench_csv", "load_training_csv", "save_vectors_csv",
+                 "BlockGrid", "blocks_to_image", "image_to_blocks", "load_codebook", "load_encoded",
+                 "parse_pgm", "pgm_bytes", "pixels_to_blocks", "read_pgm", "save_codebook",
+                 "save_encoded", "RateReport", "rate", "decode", "reconstruction_distortion"):
+        assert hasattr(vq, name) and name in vq.__all__, name
+
+
 def test_public_names_match_the_reference_surface():
     """The hot-path names of vqkit.__all__ (pkg/src/vqkit/__init__.py:79-135)."""
     import paper_0910_4711_b200 as vq
