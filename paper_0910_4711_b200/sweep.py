@@ -137,11 +137,13 @@ def _rank_main(rank, world, port, backend, data_path, cells, repeats, out_path, 
 def run_sweep(ts: TrainingSet, sizes=DEFAULT_SIZES, gpu_counts=(1,), repeats: int = DEFAULT_REPEATS,
               epsilon: float = 1e-3, delta: float = 0.01, metric: str = SQUARED_EUCLIDEAN,
               max_iterations: int = 100, progress=None, backend: str = "nccl",
-              backend_factory: str | None = None) -> list[BenchRecord]:
+              backend_factory: str | None = None, thread_counts=None) -> list[BenchRecord]:
     """bench.run_sweep (bench.py:72-120) over GPU counts.  Every (N, P) cell
     is trained ``repeats`` times and the minimum wall time kept; only the
     design is timed.  ``backend``/``backend_factory`` ("module:callable" of a
     DeviceShard stand-in) exist so the P > 1 protocol runs on CPU with gloo."""
+    if thread_counts is not None:  # the reference's keyword (bench.py:72-76): counts of GPUs here
+        gpu_counts = tuple(thread_counts)
     if repeats < 1:
         raise UsageError(f"repeats must be >= 1, got {repeats}")
     for p in gpu_counts:
