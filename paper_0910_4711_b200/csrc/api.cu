@@ -748,7 +748,11 @@ int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
   // Speculative batches: passes early-exit on the device once `done` is set,
   // so the host only checks the flag of the previous batch while the next
   // one is already queued (the GPU never waits on the host).
-  const int batch = 4;
+  static const int batch = [] {  // passes per captured graph (VQB_BATCH, default 4)
+    const char* e = getenv("VQB_BATCH");
+    const int v = e ? atoi(e) : 4;
+    return v >= 1 && v <= 64 ? v : 4;
+  }();
   long long issued = 0;
   int b = 0;
   const long long max_passes = (long long)(std::log2((double)cfg->target_size) + 1) *
