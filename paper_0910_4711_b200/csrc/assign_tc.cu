@@ -21,7 +21,7 @@
 //
 // CTA (persistent, one per SM, over 128-row tiles) = 1 MMA-issuer warp +
 // 16 (L = 16) or 8 epilogue warps (4 lane quarters x column parts) + a
-// streamer / converter pair + 8 (L = 16) or 4 certification warps.  The
+// streamer / converter pair + 8 certification warps (two groups of 4).  The
 // codebook's operand image (staged by apply_kernel / prep_codebook in the
 // exact smem layout) is bulk-copied into smem once, or streamed through a TMA
 // ring when it does not fit; row tiles come from the prebuilt fp16 row image
@@ -59,6 +59,13 @@ constexpr uint32_t kSleepNs = VQB_SLEEP_NS;
 template <int L>
 __host__ __device__ constexpr bool pipe_ld() { return VQB_PIPE_LD < 0 ? L >= 32 : VQB_PIPE_LD != 0; }
 
+// certification groups of 4 warps at L >= 32: the role profile showed the
+// certification warps busy 94 % at cfg3 (64-dimension FP64 distances) with
+// the epilogue waiting on them; a second group cuts the pass 14 % (96
+// registers, no spills)
+#ifndef VQB_CERT_GROUPS_WIDE
+#define VQB_CERT_GROUPS_WIDE 2
+#endif
 template <int L>
 struct TcCfg {
   // epilogue warps: kParts per TMEM lane quarter, each scanning 256 / kParts
@@ -78,7 +85,7 @@ struct TcCfg {
   // stalled the MMAs 60 % of the time; dedicated warps cut the pass by 13 %.
   static constexpr int kExtraConv = 0;
   static constexpr bool kCertWarps = true;
-  static constexpr int kCertGroups = L == 16 ? 2 : 1;
+  static constexpr int kCertGroups = L == 16 ? 2 : VQB_CERT_GROUPS_WIDE;
   static constexpr int kCertWarp0 = 3 + kEpiWarps + kExtraConv;
   static constexpr int threads(int mode) {
     return 32 * (kCertWarp0 + (mode == 0 && kCertWarps ? 4 * kCertGroups : 0));
