@@ -73,6 +73,47 @@ def test_assign_shapes_vs_oracle(dim, k):
     assert np.array_equal(table.cells, cells)
 
 
+def _adversarial_cases():
+    rng = np.random.default_rng(77)
+    out = []
+    # large common offset: distances tiny against the norms (cancellation in
+    # |x|^2 - 2xc + |c|^2); the certified band must queue, never mis-rank
+    x = (1.0e5 + rng.normal(0, 1, (12345, 16))).astype(np.float32)
+    out.append(("offset-L16", x, x[rng.choice(len(x), 1024, replace=False)].astype(np.float64) + 0.25))
+    # tiny magnitudes, L=32
+    x = rng.uniform(0, 1e-3, (9001, 32)).astype(np.float32)
+    out.append(("tiny-L32", x, rng.uniform(0, 1e-3, (256, 32))))
+    # negative values, every codevector twice (exact ties), L=64
+    x = rng.integers(-128, 128, (7777, 64)).astype(np.float32)
+    cb = rng.integers(-128, 128, (32, 64)).astype(np.float64)
+    out.append(("dup-neg-L64", x, np.repeat(cb, 2, axis=0)))
+    # rows sitting exactly on codevectors (zero distances), L=16, K=512
+    cb = rng.integers(0, 256, (512, 16)).astype(np.float64)
+    x = cb[rng.integers(0, 512, 10000)].astype(np.float32)
+    out.append(("on-codevector-L16", x, cb))
+    # dimensions off the tensor-core set
+    for dim, k in ((3, 100), (48, 200), (100, 64), (128, 256)):
+        x = rng.integers(0, 256, (5003, dim)).astype(np.float32)
+        out.append((f"dim{dim}", x, x[rng.choice(5003, k, replace=False)].astype(np.float64) + 0.5))
+    return out
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_assign_adversarial_vs_oracle(i):
+    """Offsets, tiny magnitudes, negative duplicates, zero distances, ragged
+    row counts and dimensions outside 16/32/64: indices and per-row distances
+    stay the oracle's bit for bit."""
+    name, x, cb = _adversarial_cases()[i]
+    cells, dists = oracle.assign_all(x.astype(np.float64), cb, workers=8)
+    from paper_0910_4711_b200.core import _session_of, _matrix_keep_f32
+    table, _ = vq.assign_cells(x, vq.Codebook(cb))
+    assert np.array_equal(table.cells, cells), name
+    _, got, _ = _session_of(_matrix_keep_f32(x)).assign(cb, 0)
+    assert got.tobytes() == dists.tobytes(), name
+    stream = vq.encode(x, vq.Codebook(cb))
+    assert np.array_equal(stream.indices, cells.astype(np.uint32)), name
+
+
 def test_first_split_tie_density_exact():
     """K=2 additive split of a GMM centroid: the tie-densest point of the whole
     design.  Indices must still be bit-exact."""
