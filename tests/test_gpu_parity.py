@@ -167,6 +167,22 @@ def test_design_matches_reference(golden_small, i):
     np.testing.assert_allclose(stats.per_worker, golden_small[f"design{i}_per_worker"], rtol=1e-12)
 
 
+@pytest.mark.parametrize("dim,k,offset", [(16, 64, 1000.0), (32, 32, -300.0), (64, 16, 0.0)])
+def test_design_offset_integer_data_vs_oracle(dim, k, offset):
+    """Whole designs on integer-valued rows far from the origin (and
+    negative): every FP64 cell sum is exact on both sides, so the codebooks
+    are bit-identical and the schedules match pass for pass."""
+    rng = np.random.default_rng(dim + k)
+    x = (offset + rng.integers(-50, 51, (20011, dim))).astype(np.float32)
+    want = oracle.lbg_train(x.astype(np.float64), k, epsilon=1e-3, delta=0.01, workers=8)
+    cb, stats = vq.lbg_train(vq.TrainingSet(x), vq.LbgConfig(target_size=k, epsilon=1e-3, delta=0.01))
+    hist = np.array([(h.codebook_size, h.iteration, h.td, h.empty_cells) for h in stats.history])
+    ref = np.array(want.history, dtype=np.float64)
+    assert np.array_equal(hist[:, [0, 1, 3]], ref[:, [0, 1, 3]])
+    np.testing.assert_allclose(hist[:, 2], ref[:, 2], rtol=2 * x.shape[0] * 2.0 ** -53)
+    assert cb.codevectors.tobytes() == np.ascontiguousarray(want.codebook).tobytes()
+
+
 def test_trace_kat_exact():
     trace = vq.TrainingSet(np.array([[0.0, 0.0], [0.0, 1.0], [4.0, 0.0], [4.0, 1.0]]))
     cb, stats = vq.lbg_train(trace, vq.LbgConfig(target_size=2, epsilon=1e-3, delta=0.5))
