@@ -86,6 +86,10 @@ struct TcCfg {
   static constexpr int kExtraConv = 0;
   static constexpr bool kCertWarps = true;
   static constexpr int kCertGroups = L == 16 ? 2 : VQB_CERT_GROUPS_WIDE;
+  // the tile results are double-buffered (res[i & 1]) and each buffer's
+  // res_empty barrier expects one group's 4 warps: group g owns buffer g, so
+  // a third group would arrive out of phase and deadlock
+  static_assert(kCertGroups == 1 || kCertGroups == 2, "certification groups: 1 or 2");
   static constexpr int kCertWarp0 = 3 + kEpiWarps + kExtraConv;
   static constexpr int threads(int mode) {
     return 32 * (kCertWarp0 + (mode == 0 && kCertWarps ? 4 * kCertGroups : 0));
