@@ -359,10 +359,10 @@ def run_b200(args):
 
         shard = D.DeviceShard(x, rank * n, world * n, local_rank)
         with torch.cuda.stream(shard.stream):  # our kernels, NCCL and the events on one stream
-            gmax = shard.tensor([shard.maxabs()])
+            gstats = shard.tensor(shard.colstats())
             if world > 1:
-                dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
-            shard.lloyd_begin(cb, float(gmax.item()))
+                dist.all_reduce(gstats, op=dist.ReduceOp.MAX)
+            shard.lloyd_begin(cb, gstats.cpu().numpy())
             ex = shard.exchange()
 
             def pass_():

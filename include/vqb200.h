@@ -100,6 +100,12 @@ int vqb_close(vqb_session* s);
 int vqb_set_stream(vqb_session* s, void* stream);
 /* max |x| over this shard (+inf when any value is non-finite). */
 int vqb_local_maxabs(vqb_session* s, double* out);
+/* Per-column stats of this shard's rows: colmax[dim] = max |x| (+inf when a
+ * value is non-finite), collow[dim] = exponent of the lowest set bit
+ * (INT32_MAX for a column of zeros).  Ranks combine them (MAX / MIN) into the
+ * global stats that fix the two-word fixed-point plan of the cell sums
+ * (vqb_train_config.global_colmax / global_collow). */
+int vqb_local_colstats(vqb_session* s, double* colmax, int32_t* collow);
 
 typedef struct {
   int64_t target_size;               /* LbgConfig.target_size (power of two) */
@@ -107,8 +113,9 @@ typedef struct {
   double delta;                      /* additive split offset */
   int64_t max_iterations_per_level;  /* guard (warning, not error) */
   int32_t metric;                    /* 0 squared_euclidean, 1 euclidean */
-  int32_t ordered;                   /* -1 auto, 0 fixed-point sums, 1 reference order */
-  double global_maxabs;              /* < 0: use this shard's max |x| */
+  int32_t ordered;                   /* -1 auto, 0 two-word fixed-point sums, 1 reference order */
+  const double* global_colmax;       /* [dim] or NULL: this shard's column stats */
+  const int32_t* global_collow;      /* [dim] or NULL */
 } vqb_train_config;
 
 typedef struct {
@@ -130,12 +137,17 @@ typedef struct {
   int32_t fast_path;     /* 1: FP32 candidate + FP64 re-rank; 0: exact FP64 scan */
   int32_t ordered;
   int64_t flagged_full;  /* of flagged_rows, those whose shortlist overflowed (full FP64 scan) */
+  int32_t sums_exact;    /* 1: every coordinate is exact on the two-word fixed-point grid */
+  int32_t ref_exact;     /* 1: the reference's own FP64 cell sums are provably exact too (so the
+                            fixed-point centroids equal update_rows' bit for bit) */
 } vqb_train_summary;
 
 /* Full LBG design on the device (lbg_train / parallel_lbg_train).  Outputs:
- * codebook_out[target_size][dim], hist[hist_cap], warn_sizes[warn_cap] (level
- * sizes whose guard tripped), final_dists[rows] (nullable: distances of the
- * last allocation pass, for DistortionStats.per_worker). */
+ * codebook_out[target_size][dim], hist[hist_cap] (nullable: fetch the whole
+ * history afterwards with vqb_step_history, sized from summary->n_hist),
+ * warn_sizes[warn_cap] (level sizes whose guard tripped), final_dists[rows]
+ * (nullable: distances of the last allocation pass, for
+ * DistortionStats.per_worker). */
 int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
               vqb_level_iteration* hist, int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap,
               double* final_dists, vqb_train_summary* summary);
@@ -163,15 +175,19 @@ int vqb_step_poll(vqb_session* s, int* done);
 int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* hist,
                     int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap, double* final_dists,
                     vqb_train_summary* summary);
+/* The last finished run's history (DistortionStats.history, core.py:175-197):
+ * up to cap records into hist, *count = records recorded. */
+int vqb_step_history(vqb_session* s, vqb_level_iteration* hist, int64_t cap, int64_t* count);
 
 /* Fixed-size Lloyd passes over shards (the multi-GPU form of
  * vqb_lloyd_step_f32): begin uploads the codebook and fixes the common
- * fixed-point scale (global_maxabs < 0: this shard's); per pass
+ * fixed-point plan (global column stats; NULL: this shard's); per pass
  * vqb_lloyd_local (assign + re-rank + distortion + cell sums), the caller
  * allreduces vqb_step_exchange's int64 buffer (SUM), then vqb_step_finalize
  * makes the centroids of the combined sums current on every rank (same bits
  * everywhere: integer sums). vqb_step_result reads the codebook back. */
-int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t size, double global_maxabs);
+int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t size, const double* global_colmax,
+                    const int32_t* global_collow);
 int vqb_lloyd_local(vqb_session* s);
 
 /* ---- one-shot host-buffer calls (end-to-end path, copies included) ---- */

@@ -33,7 +33,8 @@ class TrainConfig(ctypes.Structure):
         ("max_iterations_per_level", ctypes.c_int64),
         ("metric", ctypes.c_int32),
         ("ordered", ctypes.c_int32),
-        ("global_maxabs", ctypes.c_double),
+        ("global_colmax", ctypes.c_void_p),   # const double[dim] or NULL
+        ("global_collow", ctypes.c_void_p),   # const int32[dim] or NULL
     ]
 
 
@@ -59,6 +60,8 @@ class TrainSummary(ctypes.Structure):
         ("fast_path", ctypes.c_int32),
         ("ordered", ctypes.c_int32),
         ("flagged_full", ctypes.c_int64),
+        ("sums_exact", ctypes.c_int32),
+        ("ref_exact", ctypes.c_int32),
     ]
 
 
@@ -88,6 +91,8 @@ def lib():
             "vqb_close": ([_P], _I32),
             "vqb_set_stream": ([_P, _P], _I32),
             "vqb_local_maxabs": ([_P, _P], _I32),
+            "vqb_local_colstats": ([_P, _P, _P], _I32),
+            "vqb_step_history": ([_P, _P, _I64, _P], _I32),
             "vqb_train": ([_P, _P, _P, _P, _I64, _P, _I64, _P, _P], _I32),
             "vqb_assign": ([_P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
             "vqb_update": ([_P, _P, _P, _I64, _P, _P, _P], _I32),
@@ -112,7 +117,7 @@ def lib():
             "vqb_open_pixels": ([_P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
             "vqb_rows_f32": ([_P, _P], _I32),
             "vqb_host_copy": ([_P, _P, _I64], _I32),
-            "vqb_lloyd_begin": ([_P, _P, _I64, _D], _I32),
+            "vqb_lloyd_begin": ([_P, _P, _I64, _P, _P], _I32),
             "vqb_lloyd_local": ([_P], _I32),
             "vqb_first_nonfinite_f32": ([_P, _I64, _P], _I32),
             "vqb_first_nonfinite_f64": ([_P, _I64, _P], _I32),

@@ -21,6 +21,10 @@
 
 using namespace vqb;
 
+// the part of DevState the host writes / reads back (everything before the
+// history buffer fields)
+static constexpr size_t kStateHeader = offsetof(DevState, hist_cap);
+
 namespace {
 
 thread_local std::string g_err;
@@ -50,18 +54,6 @@ cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
 }
 
-int fixed_shift_for(long long n_global, double maxabs) {
-  int e_n = 0;
-  while ((1LL << e_n) < n_global && e_n < 62) ++e_n;
-  int e_x = 0;
-  if (maxabs > 0) {
-    std::frexp(maxabs, &e_x);  // maxabs < 2^e_x
-  }
-  int s = 62 - e_n - e_x - 1;
-  if (s > 1000) s = 1000;
-  if (s < -1000) s = -1000;
-  return s;
-}
 
 }  // namespace
 
@@ -77,6 +69,31 @@ struct vqb_session {
   float* mu = nullptr;
   std::vector<float> mu_host;  // host copy of the centring vector
   double maxabs = -1.0;
+  // per-column stats of this shard's rows (colstats): max |x| and the lowest
+  // set bit exponent -- the two-word fixed-point plan of the cell sums
+  std::vector<double> colmax;
+  std::vector<int> collow;
+  std::vector<int> cshift_host;
+  unsigned long long* cmax = nullptr;  // device copies (host-buffer paths recompute them per call)
+  int* clow = nullptr;
+  int* cshift = nullptr;               // per-column shifts of the current run
+  bool sums_exact = true, ref_exact = true;
+  // history: a device ring the finalize kernel writes, drained by the host
+  // after every batch of passes (so a run may record any number of passes)
+  HistRec* hist = nullptr;
+  int hist_cap = 0;
+  long long drained = 0;                       // records copied to hist_raw so far
+  std::vector<HistRec> hist_raw;
+  std::vector<vqb_level_iteration> hist_host;  // the last run's history (vqb_step_history)
+  // reference-order cell sums (ordered.cu), allocated on first use
+  int* operm = nullptr;
+  int* obase = nullptr;
+  int* oscan = nullptr;
+  int oblocks = 0;
+  long long obase_k = 0;
+  // one caller at a time: ctypes releases the GIL, and every call below uses
+  // the session's buffers, state and pinned arena
+  std::recursive_mutex lock_mu;
   unsigned short* tcb = nullptr;  // fp16 operand image of the codebook (assign_tc)
   // fp16 operand image of the resident rows (assign_tc reads it with bulk
   // copies instead of converting every pass); built for scale 2^aimg_ey
@@ -153,6 +170,7 @@ struct vqb_session {
     a.dim = (int)dim;
     a.tile0 = row_offset / kTdTile;
     a.mu = mu;
+    a.cshift = cshift;
     a.cb[0] = cb[0];
     a.cb[1] = cb[1];
     a.w = w;
@@ -172,6 +190,10 @@ struct vqb_session {
     a.ex.ntiles = ntiles_global;
     a.partials = partials;
     a.ord = ord;
+    a.operm = operm;
+    a.obase = obase;
+    a.oscan = oscan;
+    a.oblocks = oblocks;
     a.st = st;
     return a;
   }
@@ -199,12 +221,12 @@ struct vqb_session {
     CK(dalloc(&cb[1], (size_t)(k * dim)));
     CK(dalloc(&w, (size_t)(kpad * dim + 64)));
     CK(dalloc(&nrm, (size_t)(kpad + 64)));
-    CK(dalloc(&ex, (size_t)(k * dim + k + ntiles_global)));
+    CK(dalloc(&ex, (size_t)(2 * k * dim + k + ntiles_global)));  // Exchange::words()
     CK(dalloc(&partials, (size_t)sms * (size_t)(k * dim + k)));
     CK(dalloc(&ord, (size_t)(k * dim)));
     if (fast_dim_supported((int)dim))
       CK(dalloc(&tcb, (size_t)(((k + kTcChunk - 1) / kTcChunk) * tc_chunk_elems((int)dim))));
-    CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (k * dim + k + ntiles_global), stream));
+    CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (2 * k * dim + k + ntiles_global), stream));
     return VQB_OK;
   }
 
@@ -229,6 +251,13 @@ struct vqb_session {
     cudaFree(tcb);
     cudaFree(aimg);
     cudaFree(aq);
+    cudaFree(cmax);
+    cudaFree(clow);
+    cudaFree(cshift);
+    cudaFree(hist);
+    cudaFree(operm);
+    cudaFree(obase);
+    cudaFree(oscan);
     cudaFree(st);
     cudaFree(scratch);
     if (st_host) cudaFreeHost(st_host);
@@ -246,6 +275,110 @@ struct vqb_session {
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     own_stream = true;
+    return VQB_OK;
+  }
+
+  // device buffers every session needs besides the rows
+  int alloc_common() {
+    CK(dalloc(&idx, (size_t)n + 32));
+    CK(dalloc(&flags, (size_t)n + 32));
+    CK(dalloc(&flag_thr, (size_t)n + 32));
+    CK(dalloc(&flags2, (size_t)n + 32));
+    CK(dalloc(&dists, (size_t)n + 32));
+    CK(dalloc(&st, 1));
+    CK(dalloc(&mu, (size_t)dim + 4));
+    CK(dalloc(&cmax, (size_t)dim));
+    CK(dalloc(&clow, (size_t)dim));
+    CK(dalloc(&cshift, (size_t)dim));
+    CK(cudaMemset(cshift, 0, sizeof(int) * dim));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&st_host), sizeof(DevState)));
+    std::memset(st_host, 0, sizeof(DevState));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&done_host), 4 * sizeof(int)));
+    return alloc_hist();
+  }
+
+  // the history ring (VQB_HIST_RING overrides its size, for tests); the
+  // device state points at it
+  int alloc_hist() {
+    static const int ring = [] {
+      const char* e = getenv("VQB_HIST_RING");
+      const int v = e ? atoi(e) : kHistRing;
+      return v >= 16 ? v : kHistRing;
+    }();
+    CK(dalloc(&hist, (size_t)ring));
+    hist_cap = ring;
+    // hist_cap / hist close DevState: the header copies (kStateHeader bytes)
+    // never overwrite them
+    CK(cudaMemcpy(reinterpret_cast<char*>(st) + offsetof(DevState, hist_cap), &hist_cap, sizeof(int),
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(reinterpret_cast<char*>(st) + offsetof(DevState, hist), &hist, sizeof(HistRec*),
+                  cudaMemcpyHostToDevice));
+    return VQB_OK;
+  }
+
+  // copy the ring's records [drained, upto) to the host (they were written by
+  // passes that have completed; the copy runs on the copy stream, so it does
+  // not queue behind the batch the device is executing now)
+  int drain_hist(long long upto) {
+    if (upto <= drained) return VQB_OK;
+    if (upto - drained > hist_cap)
+      return fail(VQB_INTERNAL, "history ring overrun (%lld records pending, ring %d)", upto - drained, hist_cap);
+    const size_t old = hist_raw.size();
+    hist_raw.resize((size_t)upto);
+    long long i = drained;
+    while (i < upto) {
+      const long long slot = i % hist_cap;
+      const long long run = std::min<long long>(upto - i, hist_cap - slot);
+      CK(cudaMemcpyAsync(hist_raw.data() + old + (i - drained), hist + slot, sizeof(HistRec) * run,
+                         cudaMemcpyDeviceToHost, copy_stream));
+      i += run;
+    }
+    CK(cudaStreamSynchronize(copy_stream));
+    drained = upto;
+    return VQB_OK;
+  }
+
+  // buffers of the reference-order path for codebooks up to k
+  int ensure_ordered(long long k) {
+    const int B = ordered_blocks(n);
+    if (operm && obase_k >= k && oblocks == B) return VQB_OK;
+    drop_graph();
+    cudaFree(operm);
+    cudaFree(obase);
+    cudaFree(oscan);
+    operm = obase = oscan = nullptr;
+    oblocks = B;
+    obase_k = k;
+    CK(dalloc(&operm, (size_t)n + 32));
+    CK(dalloc(&obase, (size_t)(k * B)));
+    CK(dalloc(&oscan, (size_t)((k * B + 4095) / 4096 + 256)));
+    return VQB_OK;
+  }
+
+  // Two-word fixed-point plan of the cell sums from column stats (this
+  // shard's, or the global ones every rank agreed on): per-column shifts to
+  // the device, lo_shift and the exactness flags into the host state `h`.
+  int plan_fixed(DevState* h, const double* gmax = nullptr, const int* glow = nullptr) {
+    cshift_host.assign((size_t)dim, 0);
+    bool ex = true, rex = true;
+    const bool have = (long long)colmax.size() == dim;  // host-buffer sessions plan on the device
+    for (long long l = 0; l < dim; ++l) {
+      const double m = gmax ? gmax[l] : (have ? colmax[(size_t)l] : 0.0);
+      const int lw = glow ? glow[l] : (have ? collow[(size_t)l] : 0x7fffffff);
+      const FixedCol f = fixed_plan(n_global, m, lw);
+      cshift_host[(size_t)l] = f.s;
+      ex = ex && f.exact;
+      rex = rex && f.ref_exact;
+    }
+    sums_exact = ex;
+    ref_exact = rex;
+    h->lo_shift = fixed_lo_shift(n_global);
+    h->sums_exact = ex ? 1 : 0;
+    h->ref_exact = rex ? 1 : 0;
+    char* p = pin_alloc(sizeof(int) * dim);
+    if (p) std::memcpy(p, cshift_host.data(), sizeof(int) * dim);
+    CK(cudaMemcpyAsync(cshift, p ? static_cast<const void*>(p) : cshift_host.data(), sizeof(int) * dim,
+                       cudaMemcpyHostToDevice, stream));
     return VQB_OK;
   }
 };
@@ -364,27 +497,39 @@ int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64
 
 static int finish_open(std::unique_ptr<vqb_session>& s, vqb_session** out) {
   const long long rows = s->n, dim = s->dim;
-  const size_t count = (size_t)rows * dim;
-  // max |x| (fixed-point scale, fast-path eligibility)
-  unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
-  CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
-  CK(launch_maxabs(s->x32, s->x64, (long long)count, mb, s->sms, s->stream));
-  unsigned long long bits = 0;
-  CK(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
-  CK(dalloc(&s->idx, (size_t)rows + 32));
-  CK(dalloc(&s->flags, (size_t)rows + 32));
-  CK(dalloc(&s->flag_thr, (size_t)rows + 32));
-  CK(dalloc(&s->flags2, (size_t)rows + 32));
-  CK(dalloc(&s->dists, (size_t)rows + 32));
-  CK(dalloc(&s->st, 1));
-  CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
-  CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
-  CK(dalloc(&s->mu, (size_t)dim + 4));
+  if (int rc = s->alloc_common()) return rc;
+  // per-column max |x| and lowest set bit (fixed-point plan of the cell
+  // sums; max |x| also decides fast-path eligibility)
+  CK(launch_colstats_reset(s->cmax, s->clow, (int)dim, s->stream));
+  CK(launch_colstats(s->x32, s->x64, rows, (int)dim, s->cmax, s->clow, s->sms, s->stream));
+  std::vector<unsigned long long> cm((size_t)dim);
+  s->collow.assign((size_t)dim, 0);
+  CK(cudaMemcpyAsync(cm.data(), s->cmax, sizeof(unsigned long long) * dim, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->collow.data(), s->clow, sizeof(int) * dim, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaEventCreateWithFlags(&s->ev_batch[0], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s->ev_batch[1], cudaEventDisableTiming));
   CK(cudaStreamSynchronize(s->stream));
-  std::memcpy(&s->maxabs, &bits, sizeof(double));
-  if (!(s->maxabs <= 1.7976931348623157e308)) s->maxabs = INFINITY;
+  s->colmax.assign((size_t)dim, 0.0);
+  s->maxabs = 0.0;
+  for (long long l = 0; l < dim; ++l) {
+    double v;
+    std::memcpy(&v, &cm[(size_t)l], sizeof(double));
+    if (!(v <= 1.7976931348623157e308)) v = INFINITY;
+    s->colmax[(size_t)l] = v;
+    s->maxabs = std::max(s->maxabs, v);
+  }
+  {
+    // exactness of this shard's own fixed-point plan (the summation mode of
+    // single-device calls; a sharded run re-plans from the global stats)
+    bool ex = true, rex = true;
+    for (long long l = 0; l < dim; ++l) {
+      const FixedCol f = fixed_plan(s->n_global, s->colmax[(size_t)l], s->collow[(size_t)l]);
+      ex = ex && f.exact;
+      rex = rex && f.ref_exact;
+    }
+    s->sums_exact = ex;
+    s->ref_exact = rex;
+  }
   // centring vector: the shard's first row mean is as good as any; use a
   // cheap, deterministic one -- the midpoint of [-maxabs, maxabs] is 0, so
   // centre at the column means of up to 4096 leading rows (FP32, host-free:
@@ -419,6 +564,7 @@ extern "C" {
 
 int vqb_rows_f32(vqb_session* s, float* out) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   if (!s->x32) return fail(VQB_USAGE, "the session holds float64 rows");
   CK(cudaSetDevice(s->device));
   CK(download(out, s->x32, sizeof(float) * (size_t)(s->n * s->dim), s->stream));
@@ -432,6 +578,7 @@ int vqb_close(vqb_session* s) {
 
 int vqb_set_stream(vqb_session* s, void* stream) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   CK(cudaSetDevice(s->device));
   CK(cudaStreamSynchronize(s->stream));
   if (s->own_stream) cudaStreamDestroy(s->stream);
@@ -441,7 +588,19 @@ int vqb_set_stream(vqb_session* s, void* stream) {
 }
 
 int vqb_local_maxabs(vqb_session* s, double* out) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   *out = s->maxabs;
+  return VQB_OK;
+}
+
+int vqb_local_colstats(vqb_session* s, double* colmax, int32_t* collow) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
+  for (long long l = 0; l < s->dim; ++l) {
+    colmax[l] = s->colmax[(size_t)l];
+    collow[l] = s->collow[(size_t)l];
+  }
   return VQB_OK;
 }
 
@@ -464,13 +623,19 @@ static int check_config(const vqb_train_config* cfg) {
   return VQB_OK;
 }
 
-static bool choose_ordered(const vqb_session* s, int requested, long long kmax) {
+// Summation mode of the cell sums.  Auto: the two-word fixed-point sums
+// (exact, order-free, identical for every GPU count) unless (a) the data's
+// column span defeats the two-word grid, or (b) the rows are float64 that
+// float32 cannot hold and the set is small enough that the reference's own
+// rounding sequence is affordable (kOrderedAutoRows): then the ordered path
+// reproduces the reference's ascending-index FP64 sums bit for bit.  The
+// ordered path needs the whole set on one device.
+constexpr long long kOrderedAutoRows = 1LL << 20;
+static bool choose_ordered(const vqb_session* s, int requested) {
   if (requested == 1) return true;
   if (requested == 0) return false;
-  // auto: float64 rows that are not float32-exact keep the reference's own
-  // summation order (bit-identical) while the per-pass cost stays modest.
-  return s->x64 != nullptr && s->n == s->n_global &&
-         (double)s->n * (double)kmax * (double)s->dim <= 2.7e8;
+  if (s->n != s->n_global) return false;
+  return !s->sums_exact || (s->x64 != nullptr && s->n <= kOrderedAutoRows);
 }
 
 static bool tc_enabled() {
@@ -551,21 +716,30 @@ static double data_span(const vqb_session* s, const double* codebook, long long 
 }
 
 int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   int rc = check_config(cfg);
   if (rc) return rc;
   CK(cudaSetDevice(s->device));
   rc = s->ensure(cfg->target_size);
   if (rc) return rc;
-  s->ordered = choose_ordered(s, cfg->ordered, cfg->target_size);
+  s->drained = 0;
+  s->hist_raw.clear();
+  DevState* h = s->st_host;
+  std::memset(h, 0, kStateHeader);
+  // fixed-point plan from the column stats every rank agreed on (or this shard's)
+  rc = s->plan_fixed(h, cfg->global_colmax, cfg->global_collow);
+  if (rc) return rc;
+  s->ordered = choose_ordered(s, cfg->ordered);
   if (s->ordered && s->n != s->n_global)
     return fail(VQB_USAGE, "reference-order mode needs the whole training set on one device");
-  DevState* h = s->st_host;
-  std::memset(h, 0, sizeof(DevState));
+  if (s->ordered) {
+    rc = s->ensure_ordered(cfg->target_size);
+    if (rc) return rc;
+  }
   h->target = (int)cfg->target_size;
   h->max_iter = (int)cfg->max_iterations_per_level;
   h->metric = cfg->metric;
-  const double gmax = cfg->global_maxabs >= 0 ? cfg->global_maxabs : s->maxabs;
-  h->fixed_shift = fixed_shift_for(s->n_global, gmax);
   h->eps = cfg->epsilon;
   h->delta = cfg->delta;
   h->n_global = s->n_global;
@@ -581,12 +755,11 @@ int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
   h->iteration = 1;
   h->td_prev = INFINITY;
   // copy only the header part of the state (history is written on device)
-  CK(cudaMemcpyAsync(s->st, h, offsetof(DevState, hist), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->st, h, kStateHeader, cudaMemcpyHostToDevice, s->stream));
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
   if (s->ordered) {
-    CK(cudaMemsetAsync(s->idx, 0, sizeof(int) * s->n, s->stream));
-    CK(launch_ordered_update(a, s->stream));
+    CK(launch_ordered_update(a, true, s->sms, s->stream));  // column sums in row order
   } else {
     CK(launch_epilogue(a, false, true, true, s->sms, s->stream));
   }
@@ -595,15 +768,19 @@ int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
 }
 
 int vqb_step_local(vqb_session* s) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   KernelArgs a = s->args();
   CK(launch_assign(a, s->fast, s->sms, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
   CK(launch_epilogue(a, true, !s->ordered, false, s->sms, s->stream));
-  if (s->ordered) CK(launch_ordered_update(a, s->stream));
+  if (s->ordered) CK(launch_ordered_update(a, false, s->sms, s->stream));
   return VQB_OK;
 }
 
 int vqb_step_finalize(vqb_session* s) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   KernelArgs a = s->args();
   if (s->pending_init) {
     CK(launch_init_centroid(a, s->fast, s->stream));
@@ -616,24 +793,32 @@ int vqb_step_finalize(vqb_session* s) {
 
 static int upload_codebook(vqb_session* s, const double* codebook, long long size);
 static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered,
-                     const double* codebook = nullptr);
+                     const double* codebook = nullptr, const double* gmax = nullptr,
+                     const int* glow = nullptr);
 
 // ---- fixed-codebook Lloyd passes over shards (update_codebook after
 // assign_cells at one size, the multi-GPU bench step): begin stages the
 // codebook with the common fixed-point scale; each pass is lloyd_local ->
 // caller allreduces the exchange buffer -> vqb_step_finalize (centroids of
 // the combined sums become the current codebook on every rank).
-extern "C" int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t size, double global_maxabs) {
+extern "C" int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t size,
+                               const double* global_colmax, const int32_t* global_collow) {
   if (!s) return fail(VQB_USAGE, "null session");
   if (size < 1) return fail(VQB_USAGE, "codebook must be at least 1x1");
+  std::lock_guard<std::recursive_mutex> lock(s->lock_mu);
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
-  const double saved = s->maxabs;
-  if (global_maxabs >= 0) s->maxabs = global_maxabs;  // one fixed-point scale on every rank
-  rc = set_state(s, kModeLloydStep, size, 0, 0, codebook);
-  s->maxabs = saved;
+  // one fixed-point plan on every rank (the column stats they agreed on)
+  rc = set_state(s, kModeLloydStep, size, 0, 0, codebook, global_colmax, global_collow);
   if (rc) return rc;
+  s->ordered = choose_ordered(s, -1);
+  if (s->ordered) {
+    rc = s->ensure_ordered(size);
+    if (rc) return rc;
+    s->st_host->ordered = 1;
+    CK(cudaMemcpyAsync(&s->st->ordered, &s->st_host->ordered, sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  }
   s->lloyd_size = size;
   s->pending_init = false;
   KernelArgs a = s->args();
@@ -644,7 +829,8 @@ extern "C" int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t s
 
 extern "C" int vqb_lloyd_local(vqb_session* s) {
   if (!s || s->lloyd_size < 1) return fail(VQB_USAGE, "vqb_lloyd_begin first");
-  CK(launch_reset(s->st, kModeLloydStep, (int)s->lloyd_size, 0, 0, 1, s->stream));
+  std::lock_guard<std::recursive_mutex> lock(s->lock_mu);
+  CK(launch_reset(s->st, kModeLloydStep, (int)s->lloyd_size, 0, s->ordered ? 1 : 0, 1, s->stream));
   return vqb_step_local(s);
 }
 
@@ -680,42 +866,49 @@ int vqb_session::batch_graph(int batch) {
 }
 
 int vqb_step_exchange(vqb_session* s, int64_t** device_words, int64_t* count) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   *device_words = reinterpret_cast<int64_t*>(s->ex);
-  *count = s->kmax * s->dim + s->kmax + s->ntiles_global;
+  *count = s->args().ex.words();
   return VQB_OK;
 }
 
 int vqb_step_poll(vqb_session* s, int* done) {
-  CK(cudaMemcpyAsync(s->done_host, &s->st->done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
+  CK(cudaMemcpyAsync(s->done_host, &s->st->done, 2 * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   *done = s->done_host[0];
-  return VQB_OK;
+  return s->drain_hist(s->done_host[1]);
 }
 
 int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* hist,
                     int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap, double* final_dists,
                     vqb_train_summary* summary) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock(s->lock_mu);
   CK(cudaSetDevice(s->device));
   CK(cudaStreamSynchronize(s->stream));
   DevState* h = s->st_host;
-  CK(cudaMemcpy(h, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h, s->st, kStateHeader, cudaMemcpyDeviceToHost));
   if (!h->done) return fail(VQB_INTERNAL, "training loop has not finished");
-  const long long nh = std::min<long long>(h->n_hist, kMaxHist);
-  std::vector<HistRec> recs((size_t)nh);
-  if (nh > 0)
-    CK(cudaMemcpy(recs.data(), reinterpret_cast<char*>(s->st) + offsetof(DevState, hist),
-                  sizeof(HistRec) * nh, cudaMemcpyDeviceToHost));
+  const long long nh = h->n_hist;
+  if (int rc = s->drain_hist(nh)) return rc;
+  const std::vector<HistRec>& recs = s->hist_raw;
   const long long size = h->size;
   if (codebook_out)
     CK(cudaMemcpy(codebook_out, s->cb[h->cur], sizeof(double) * size * s->dim,
                   cudaMemcpyDeviceToHost));
   if (final_dists) CK(cudaMemcpy(final_dists, s->dists, sizeof(double) * s->n, cudaMemcpyDeviceToHost));
-  for (long long i = 0; i < nh && i < hist_cap; ++i) {
-    hist[i].codebook_size = recs[(size_t)i].size;
-    hist[i].iteration = recs[(size_t)i].iteration;
-    hist[i].td = recs[(size_t)i].td;
-    hist[i].empty_cells = recs[(size_t)i].empty;
-    hist[i].seconds = (double)(recs[(size_t)i].t_ns - h->t0_ns) * 1e-9;
+  s->hist_host.resize((size_t)nh);
+  for (long long i = 0; i < nh; ++i) {
+    vqb_level_iteration& r = s->hist_host[(size_t)i];
+    r.codebook_size = recs[(size_t)i].size;
+    r.iteration = recs[(size_t)i].iteration;
+    r.td = recs[(size_t)i].td;
+    r.empty_cells = recs[(size_t)i].empty;
+    r.seconds = (double)(recs[(size_t)i].t_ns - h->t0_ns) * 1e-9;
+    if (hist && i < hist_cap) hist[i] = r;
   }
   for (long long i = 0; i < std::min<long long>(h->n_warn, kMaxWarn) && i < warn_cap; ++i)
     warn_sizes[i] = h->warn_sizes[i];
@@ -730,8 +923,18 @@ int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* h
     summary->final_size = size;
     summary->fast_path = s->fast ? 1 : 0;
     summary->ordered = s->ordered ? 1 : 0;
+    summary->sums_exact = s->sums_exact ? 1 : 0;
+    summary->ref_exact = s->ref_exact ? 1 : 0;
   }
-  if (h->n_hist > kMaxHist) return fail(VQB_INTERNAL, "history overflow (%d records)", h->n_hist);
+  return VQB_OK;
+}
+
+int vqb_step_history(vqb_session* s, vqb_level_iteration* hist, int64_t cap, int64_t* count) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock(s->lock_mu);
+  const long long nh = (long long)s->hist_host.size();
+  for (long long i = 0; i < nh && i < cap; ++i) hist[i] = s->hist_host[(size_t)i];
+  if (count) *count = nh;
   return VQB_OK;
 }
 
@@ -739,6 +942,7 @@ int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
               vqb_level_iteration* hist, int64_t hist_cap, int64_t* warn_sizes, int64_t warn_cap,
               double* final_dists, vqb_train_summary* summary) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   if (s->n != s->n_global)
     return fail(VQB_USAGE, "vqb_train drives one device; use the vqb_step_* loop for shards");
   int rc = vqb_step_begin(s, cfg);
@@ -775,15 +979,18 @@ int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
       }
     }
     issued += batch;
-    CK(cudaMemcpyAsync(&s->done_host[b], &s->st->done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    // {done, n_hist} of this batch, read once the batch has run
+    CK(cudaMemcpyAsync(&s->done_host[2 * b], &s->st->done, 2 * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaEventRecord(s->ev_batch[b], s->stream));
     if (issued > batch) {
       CK(cudaEventSynchronize(s->ev_batch[b ^ 1]));
-      if (s->done_host[b ^ 1]) break;
+      rc = s->drain_hist(s->done_host[2 * (b ^ 1) + 1]);
+      if (rc) return rc;
+      if (s->done_host[2 * (b ^ 1)]) break;
     }
     if (issued > max_passes + 2 * batch) {
       CK(cudaStreamSynchronize(s->stream));
-      if (s->done_host[b]) break;
+      if (s->done_host[2 * b]) break;
       return fail(VQB_INTERNAL, "training loop did not terminate after %lld passes", issued);
     }
     b ^= 1;
@@ -810,14 +1017,14 @@ static int upload_codebook(vqb_session* s, const double* codebook, long long siz
 }
 
 static int set_state(vqb_session* s, int mode, long long size, int metric, int ordered,
-                     const double* codebook) {
+                     const double* codebook, const double* gmax, const int* glow) {
   DevState* h = s->st_host;
   // configuration fields are written by the reset kernel + this header copy
-  std::memset(h, 0, offsetof(DevState, hist));
+  std::memset(h, 0, kStateHeader);
   h->target = (int)size;
   h->max_iter = 1;
   h->metric = metric;
-  h->fixed_shift = fixed_shift_for(s->n_global, s->maxabs);
+  if (int rc = s->plan_fixed(h, gmax, glow)) return rc;
   h->n_global = s->n_global;
   h->mode = mode;
   h->ordered = ordered;
@@ -828,13 +1035,14 @@ static int set_state(vqb_session* s, int mode, long long size, int metric, int o
     tc_configure(s, h, data_span(s, codebook, size), 2.0 * codebook_span(s, codebook, size));
     if (int rc = build_row_image(s, h)) return rc;
   }
-  CK(cudaMemcpyAsync(s->st, h, offsetof(DevState, hist), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->st, h, kStateHeader, cudaMemcpyHostToDevice, s->stream));
   return VQB_OK;
 }
 
 int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric, int64_t* cells64,
                uint32_t* idx32, double* dists, double* total) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   if (size < 1) return fail(VQB_USAGE, "codebook must be at least 1x1");
   if (size > (1LL << 30)) return fail(VQB_USAGE, "codebook too large");
   CK(cudaSetDevice(s->device));
@@ -862,7 +1070,7 @@ int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric,
     }
   }
   if (dists) CK(cudaMemcpyAsync(dists, s->dists, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, kStateHeader, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   if (cells64) {
     if (idx32)
@@ -877,19 +1085,24 @@ int vqb_assign(vqb_session* s, const double* codebook, int64_t size, int metric,
 int vqb_update(vqb_session* s, const int64_t* cells, const double* old_codebook, int64_t size,
                double* new_codebook, int64_t* counts, int64_t* n_empty) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, old_codebook, size);
   if (rc) return rc;
-  const int ordered = choose_ordered(s, -1, size) ? 1 : 0;
+  const int ordered = choose_ordered(s, -1) ? 1 : 0;
   rc = set_state(s, kModeUpdateOnly, size, 0, ordered);
   if (rc) return rc;
+  if (ordered) {
+    rc = s->ensure_ordered(size);
+    if (rc) return rc;
+  }
   // cells (int64) staged through the dists buffer, narrowed on the device
   CK(cudaMemcpyAsync(s->dists, cells, sizeof(int64_t) * s->n, cudaMemcpyHostToDevice, s->stream));
   CK(launch_cells_to_idx(reinterpret_cast<const long long*>(s->dists), s->idx, s->n, s->sms, s->stream));
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
   if (ordered)
-    CK(launch_ordered_update(a, s->stream));
+    CK(launch_ordered_update(a, false, s->sms, s->stream));
   else
     CK(launch_epilogue(a, false, true, false, s->sms, s->stream));
   CK(launch_finalize(a, false, s->stream));
@@ -898,7 +1111,7 @@ int vqb_update(vqb_session* s, const int64_t* cells, const double* old_codebook,
                      s->stream));
   CK(cudaMemcpyAsync(hc.data(), s->ex + s->kmax * s->dim, sizeof(long long) * size,
                      cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, kStateHeader, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   if (counts)
     for (long long i = 0; i < size; ++i) counts[i] = hc[(size_t)i];
@@ -1024,18 +1237,10 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
   s->dim = dim;
   s->ntiles_global = (n + kTdTile - 1) / kTdTile;
   CK(dalloc(&s->x32, (size_t)(n * dim + 16)));
-  CK(dalloc(&s->idx, (size_t)n + 32));
-  CK(dalloc(&s->flags, (size_t)n + 32));
-  CK(dalloc(&s->flag_thr, (size_t)n + 32));
-  CK(dalloc(&s->flags2, (size_t)n + 32));
-  CK(dalloc(&s->dists, (size_t)n + 32));
-  CK(dalloc(&s->st, 1));
   CK(dalloc(&s->scratch, 64));
-  CK(dalloc(&s->mu, (size_t)dim + 4));
+  if (int rc = s->alloc_common()) return rc;
   CK(cudaMemset(s->mu, 0, sizeof(float) * dim));
   s->mu_host.assign((size_t)dim, 0.f);
-  CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
-  CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
   s->fast = fast_dim_supported((int)dim);
   g_cache.s = s.release();
   g_cache.n = n;
@@ -1080,16 +1285,15 @@ size_t piece_bytes() {
 // max |x| and FP32 candidate pass launched as soon as it lands (the copy of
 // piece i+1 overlaps the distance pass of piece i).  For dims without a fast
 // path the exact scan runs after the last piece.
-int stream_rows_and_assign(vqb_session* s, const KernelArgs& a, const float* x, long long rows,
-                           unsigned long long* maxabs_bits) {
+int stream_rows_and_assign(vqb_session* s, const KernelArgs& a, const float* x, long long rows) {
   const size_t row_bytes = sizeof(float) * (size_t)s->dim;
   const size_t piece = std::max<size_t>(row_bytes, piece_bytes() / row_bytes * row_bytes);
-  CK(cudaMemsetAsync(maxabs_bits, 0, sizeof(unsigned long long), s->stream));
+  CK(launch_colstats_reset(s->cmax, s->clow, (int)s->dim, s->stream));
   CK(upload(s->x32, x, row_bytes * rows, piece, s->copy_stream, s->stream,
             [&](size_t off, size_t len) -> cudaError_t {
               const long long r0 = (long long)(off / row_bytes), r1 = (long long)((off + len) / row_bytes);
-              cudaError_t e = launch_maxabs(s->x32 + r0 * s->dim, nullptr, (r1 - r0) * s->dim, maxabs_bits,
-                                            s->sms, s->stream);
+              cudaError_t e = launch_colstats(s->x32 + r0 * s->dim, nullptr, r1 - r0, (int)s->dim, s->cmax,
+                                              s->clow, s->sms, s->stream);
               if (e != cudaSuccess || !s->fast) return e;
               KernelArgs c = a;
               c.r0 = r0;
@@ -1190,14 +1394,13 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   CK(launch_clear(a, s->stream));
   if (s->fast) CK(launch_prep_codebook(a, s->stream));
   tr.mark("prepped");
-  unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
   if (pinned_x) {
-    CK(cudaMemsetAsync(mb, 0, sizeof(unsigned long long), s->stream));
+    CK(launch_colstats_reset(s->cmax, s->clow, (int)dim, s->stream));
     for (size_t i = 0; i < npieces; ++i) {
       const long long r0 = (long long)(i * piece / row_bytes);
       const long long r1 = std::min<long long>(n, (long long)((i + 1) * piece / row_bytes));
       CK(cudaStreamWaitEvent(s->stream, s->piece_ev[i], 0));
-      CK(launch_maxabs(s->x32 + r0 * dim, nullptr, (r1 - r0) * dim, mb, s->sms, s->stream));
+      CK(launch_colstats(s->x32 + r0 * dim, nullptr, r1 - r0, (int)dim, s->cmax, s->clow, s->sms, s->stream));
       if (s->fast) {
         KernelArgs c = a;
         c.r0 = r0;
@@ -1207,11 +1410,12 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
     }
     if (!s->fast) CK(launch_assign(a, false, s->sms, s->stream));
   } else {
-    rc = stream_rows_and_assign(s, a, x, n, mb);
+    rc = stream_rows_and_assign(s, a, x, n);
     if (rc) return rc;
   }
   tr.mark("assigned");
-  CK(launch_set_shift(s->st, mb, s->n_global, s->stream));
+  // the fixed-point plan of these rows' column stats, on the device
+  CK(launch_set_shift(s->st, s->cmax, s->clow, (int)dim, s->n_global, s->cshift, nullptr, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
   tr.mark("reranked");
   CK(launch_epilogue(a, true, true, false, s->sms, s->stream));  // distortion + cell sums
@@ -1221,7 +1425,7 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   char* cb_pin = s->pin_alloc(sizeof(double) * size * dim);
   CK(cudaMemcpyAsync(cb_pin ? cb_pin : reinterpret_cast<char*>(new_codebook), s->cb[1],
                      sizeof(double) * size * dim, cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, kStateHeader, cudaMemcpyDeviceToHost, s->stream));
   if (cells_out) {
     long long* wide = reinterpret_cast<long long*>(s->dists);  // dists are consumed by now
     CK(launch_widen_idx(s->idx, wide, n, s->sms, s->stream));
@@ -1229,8 +1433,24 @@ int vqb_lloyd_step_f32(const float* x, int64_t n, int64_t dim, const double* cod
   }
   CK(cudaStreamSynchronize(s->stream));
   tr.mark("synced", false);
-  if (cb_pin) std::memcpy(new_codebook, cb_pin, sizeof(double) * size * dim);
   if (s->st_host->nonfinite) return fail(VQB_USAGE, "training vectors contain non-finite values");
+  if (!s->st_host->sums_exact) {
+    // the rows' span defeats the two-word grid: redo the update in the
+    // reference's order from the cell table already on the device
+    rc = s->ensure_ordered(size);
+    if (rc) return rc;
+    KernelArgs o = s->args();
+    CK(launch_reset(s->st, kModeUpdateOnly, (int)size, 0, 1, 0, s->stream));
+    CK(launch_ordered_update(o, false, s->sms, s->stream));
+    CK(launch_finalize(o, false, s->stream));
+    CK(cudaMemcpyAsync(cb_pin ? cb_pin : reinterpret_cast<char*>(new_codebook), s->cb[1],
+                       sizeof(double) * size * dim, cudaMemcpyDeviceToHost, s->stream));
+    const double td_keep = s->st_host->total;
+    CK(cudaMemcpyAsync(s->st_host, s->st, kStateHeader, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    s->st_host->total = td_keep;
+  }
+  if (cb_pin) std::memcpy(new_codebook, cb_pin, sizeof(double) * size * dim);
   if (td) *td = s->st_host->total;
   if (n_empty) *n_empty = s->st_host->last_empty;
   return VQB_OK;
@@ -1260,16 +1480,8 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     s->dim = dim;
     s->ntiles_global = (chunk + kTdTile - 1) / kTdTile;
     CK(dalloc(&s->x32, (size_t)(chunk * dim + 16)));
-    CK(dalloc(&s->idx, (size_t)chunk + 32));
-    CK(dalloc(&s->flags, (size_t)chunk + 32));
-    CK(dalloc(&s->flag_thr, (size_t)chunk + 32));
-    CK(dalloc(&s->flags2, (size_t)chunk + 32));
-    CK(dalloc(&s->dists, (size_t)chunk + 32));
-    CK(dalloc(&s->st, 1));
     CK(dalloc(&s->scratch, 64));
-    CK(dalloc(&s->mu, (size_t)dim + 4));
-    CK(cudaMallocHost(reinterpret_cast<void**>(&s->st_host), sizeof(DevState)));
-    CK(cudaMallocHost(reinterpret_cast<void**>(&s->done_host), 2 * sizeof(int)));
+    if (int rc = s->alloc_common()) return rc;
     s->maxabs = 0;
     s->fast = fast_dim_supported((int)dim);
     int rc = set_centre_from_codebook(s, codebook, size);
@@ -1298,8 +1510,7 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     CK(launch_reset(s->st, kModeAssignOnly, (int)size, 0, 0, 0, s->stream));
     CK(launch_clear(a, s->stream));
     if (s->fast) CK(launch_prep_codebook(a, s->stream));
-    unsigned long long* mb = reinterpret_cast<unsigned long long*>(s->scratch) + 1;
-    int rc = stream_rows_and_assign(s, a, x + r0 * dim, rows, mb);
+    int rc = stream_rows_and_assign(s, a, x + r0 * dim, rows);
     if (rc) return rc;
     if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
     CK(launch_epilogue(a, total != nullptr, false, false, s->sms, s->stream));
@@ -1329,6 +1540,7 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
 int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, int reps,
                         double* ms_segments, int64_t* flagged) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
   if (rc) return rc;
@@ -1379,6 +1591,7 @@ int vqb_bench_iteration(vqb_session* s, const double* codebook, int64_t size, in
 int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int reps, double* ms_out,
                      double* total_out, int64_t* flagged) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   if (reps < 1) return fail(VQB_USAGE, "reps must be >= 1");
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
@@ -1405,7 +1618,7 @@ int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int r
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  CK(cudaMemcpy(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(s->st_host, s->st, kStateHeader, cudaMemcpyDeviceToHost));
   *ms_out = ms / reps;
   if (total_out) *total_out = s->st_host->total;
   if (flagged) *flagged = s->st_host->flagged_total / reps;
@@ -1418,6 +1631,7 @@ int vqb_bench_assign(vqb_session* s, const double* codebook, int64_t size, int r
 int vqb_debug_tc_tile(vqb_session* s, const double* codebook, int64_t size, float* dump,
                       int32_t* scales) {
   if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   if (size % kTcChunk != 0 || size > tc_max_size((int)s->dim))
     return fail(VQB_USAGE, "probe needs a codebook size that is a multiple of %d and <= %d", kTcChunk,
                 tc_max_size((int)s->dim));
@@ -1435,7 +1649,7 @@ int vqb_debug_tc_tile(vqb_session* s, const double* codebook, int64_t size, floa
   CK(cudaMemsetAsync(d, 0xff, sizeof(float) * kTcRows * size, s->stream));
   CK(launch_tc_probe(a, d, s->stream));
   CK(cudaMemcpyAsync(dump, d, sizeof(float) * kTcRows * size, cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaMemcpyAsync(s->st_host, s->st, offsetof(DevState, hist), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, kStateHeader, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   scales[0] = s->st_host->tc_ey;
   scales[1] = s->st_host->tc_ew;

@@ -17,6 +17,7 @@
 //                     centroid update / empty cells (_kernels.py:59-66), split
 //                     (core.py:277-281), level/guard logic (core.py:384-415), history
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -52,8 +53,99 @@ __device__ __forceinline__ void store_dist(const KernelArgs& a, long long row, d
   if (a.dists) a.dists[row] = a.st->metric == kEuclidean ? sqrt(d) : d;
 }
 
-__device__ __forceinline__ long long to_fixed(double v, double scale) {
-  return __double2ll_rn(v * scale);  // scale is a power of two: the product is exact
+// Exact two-word fixed-point split of one coordinate (vqb200_internal.h
+// fixed_plan): x * 2^s = hi + lo * 2^-t, hi the integer part of |x| 2^s, lo
+// the remainder in units of 2^-t, both carrying x's sign.  Pure integer work
+// on the IEEE fields; exact whenever x has no set bit below 2^-(s + t) (the
+// column's colstats decide that before any pass runs).
+__device__ __forceinline__ void split_fixed(float x, int s, int t, long long& hi, long long& lo) {
+  const unsigned u = __float_as_uint(x);
+  const unsigned E = (u >> 23) & 0xffu;
+  unsigned long long m = u & 0x7fffffu;
+  int e0 = -149;
+  if (E) {
+    m |= 0x800000u;
+    e0 = (int)E - 150;
+  }
+  long long h = 0, l = 0;
+  if (m) {
+    const int k = e0 + s;  // x = m 2^e0, so |x| 2^s = m 2^k
+    if (k >= 0) {
+      h = (long long)(m << k);  // < 2^61 by the choice of s
+    } else {
+      const int nk = -k;
+      const unsigned long long rem = nk >= 64 ? m : (m & ((1ull << nk) - 1));
+      h = nk >= 64 ? 0 : (long long)(m >> nk);
+      const int sh = t - nk;  // rem < 2^nk, so rem 2^sh < 2^t
+      l = sh >= 0 ? (long long)(rem << sh) : (sh > -64 ? (long long)(rem >> -sh) : 0);
+    }
+    if (u >> 31) {
+      h = -h;
+      l = -l;
+    }
+  }
+  hi = h;
+  lo = l;
+}
+__device__ __forceinline__ void split_fixed(double x, int s, int t, long long& hi, long long& lo) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  const unsigned E = (unsigned)((u >> 52) & 0x7ffu);
+  unsigned long long m = u & 0xfffffffffffffull;
+  int e0 = -1074;
+  if (E) {
+    m |= 1ull << 52;
+    e0 = (int)E - 1075;
+  }
+  long long h = 0, l = 0;
+  if (m) {
+    const int k = e0 + s;
+    if (k >= 0) {
+      h = (long long)(m << k);
+    } else {
+      const int nk = -k;
+      const unsigned long long rem = nk >= 64 ? m : (m & ((1ull << nk) - 1));
+      h = nk >= 64 ? 0 : (long long)(m >> nk);
+      const int sh = t - nk;
+      l = sh >= 0 ? (long long)(rem << sh) : (sh > -64 ? (long long)(rem >> -sh) : 0);
+    }
+    if (u >> 63) {
+      h = -h;
+      l = -l;
+    }
+  }
+  hi = h;
+  lo = l;
+}
+
+// low words are rare for float32 data (only coordinates with bits below the
+// column's 2^-s_l): added straight into the exchange buffer's lo section
+// (64-bit global atomics; integer adds commute, so still deterministic)
+__device__ __forceinline__ void add_lo(const KernelArgs& a, long long cell, int l, long long lo) {
+  if (lo) atomicAdd(reinterpret_cast<unsigned long long*>(a.ex.lo() + cell * a.dim + l), (unsigned long long)lo);
+}
+
+// (hi 2^t + lo) 2^e rounded once to the nearest double (ties to even): the
+// exact two-word cell sum as the FP64 numerator of the centroid
+__device__ __forceinline__ double fixed_to_double(long long hi, long long lo, int t, int e) {
+  __int128 T = ((__int128)hi << t) + (__int128)lo;
+  const bool neg = T < 0;
+  unsigned __int128 M = neg ? (unsigned __int128)(-T) : (unsigned __int128)T;
+  if (M == 0) return 0.0;
+  const unsigned long long mh = (unsigned long long)(M >> 64), ml = (unsigned long long)M;
+  const int p = mh ? 127 - __clzll((long long)mh) : 63 - __clzll((long long)ml);  // top bit
+  double d;
+  if (p <= 52) {
+    d = (double)ml;
+    d = ldexp(d, e);
+  } else {
+    const int sh = p - 52;
+    unsigned long long mant = (unsigned long long)(M >> sh);
+    const unsigned __int128 rem = M & ((((unsigned __int128)1) << sh) - 1);
+    const unsigned __int128 half = ((unsigned __int128)1) << (sh - 1);
+    if (rem > half || (rem == half && (mant & 1))) ++mant;  // 2^53 after a carry is still exact
+    d = ldexp((double)mant, sh + e);
+  }
+  return neg ? -d : d;
 }
 
 // ---------------------------------------------------------------------------
@@ -989,10 +1081,27 @@ __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, lo
 // ... of the tile, then a lane butterfly, then the 8 warps in order) that
 // does not depend on the grid or on the number of GPUs -- sum_inorder's role
 // (_kernels.py:92-98).
-__global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a) {
+// Zero the low words of the exchange buffer for cells [0, K) before this
+// pass's cell sums add into them (the previous pass's apply has read them).
+__device__ __forceinline__ void zero_lo_words(const KernelArgs& a, int K) {
+  const long long words = (long long)K * a.dim;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x)
+    a.ex.lo()[i] = 0;
+}
+
+__global__ void zero_lo_kernel(KernelArgs a, int zero_cells) {
   pdl_wait();
   const DevState* st = a.st;
   if (st->done) return;
+  zero_lo_words(a, zero_cells ? 1 : st->size);
+}
+
+__global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a, int zero_lo) {
+  pdl_wait();
+  const DevState* st = a.st;
+  if (st->done) return;
+  if (zero_lo) zero_lo_words(a, st->size);
   __shared__ double red[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long t = blockIdx.x;
@@ -1056,7 +1165,7 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
   if (st->done) return;
   const int K = zero_cells ? 1 : st->size;
   const int dim = DIM ? DIM : a.dim;
-  const double scale = ldexp(1.0, st->fixed_shift);
+  const int t_lo = st->lo_shift;  // per-column shifts: a.cshift
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kSumThreads = sum_threads<DIM>();
   constexpr int kWarps = kSumThreads / 32;
@@ -1105,8 +1214,12 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
     for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
       const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
       long long acc[16];
+      int shl[16];
 #pragma unroll
-      for (int l = 0; l < 16; ++l) acc[l] = 0;
+      for (int l = 0; l < 16; ++l) {
+        acc[l] = 0;
+        shl[l] = l < cw ? __ldg(a.cshift + c0 + l) : 0;
+      }
       int cur = -1;
       unsigned run = 0;
       auto flush = [&]() {
@@ -1136,7 +1249,12 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
           load_row16<XT, DIM>(X, row, dim, c0, true, xr);
 #pragma unroll
           for (int l = 0; l < 16; ++l)
-            if (l < cw) acc[l] += to_fixed((double)xr[l], scale);
+            if (l < cw) {
+              long long h, lo;
+              split_fixed(xr[l], shl[l], t_lo, h, lo);
+              acc[l] += h;
+              add_lo(a, cell, c0 + l, lo);
+            }
           ++run;
         }
       }
@@ -1160,6 +1278,7 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
       // sum; consecutive rows of one cell are summed in a register and the
       // half-warp table is touched once per run (no staging, no per-row
       // read-modify-write chain through shared memory)
+      const int shl = __ldg(a.cshift + hl);
       for (long long base = lo + (long long)warp * 32; base < hi; base += (long long)kWarps * 32) {
         XT xv[16];
         int cv[16];
@@ -1170,7 +1289,7 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
           xv[p] = ok ? __ldg(X + r * 16 + hl) : (XT)0;
           cv[p] = ok ? (zero_cells ? 0 : __ldg(a.idx + r)) : -1;
         }
-        long long acc = 0;
+        long long acc = 0, acc_lo = 0;
         int cur = -1;
         unsigned run = 0;
 #pragma unroll
@@ -1178,19 +1297,25 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
           if (cv[p] != cur) {  // uniform within the half-warp (one row)
             if (cur >= 0) {
               tab[(long long)cur * 16 + hl] += acc;
+              add_lo(a, cur, hl, acc_lo);
               if (hl == 0) tcount[cur] += run;
             }
             cur = cv[p];
             acc = 0;
+            acc_lo = 0;
             run = 0;
           }
           if (cur >= 0) {
-            acc += to_fixed((double)xv[p], scale);
+            long long h, l2;
+            split_fixed(xv[p], shl, t_lo, h, l2);
+            acc += h;
+            acc_lo += l2;
             ++run;
           }
         }
         if (cur >= 0) {
           tab[(long long)cur * 16 + hl] += acc;
+          add_lo(a, cur, hl, acc_lo);
           if (hl == 0) tcount[cur] += run;
         }
       }
@@ -1211,7 +1336,12 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
           const int rr = 2 * p + half;
           const int cl = __shfl_sync(0xffffffffu, lc, rr);
           if (cl >= 0) {
-            if (c0 + hl < dim) tab[(long long)cl * dim + c0 + hl] += to_fixed((double)xs[rr * kWStageStride + hl], scale);
+            if (c0 + hl < dim) {
+              long long h, l2;
+              split_fixed(xs[rr * kWStageStride + hl], __ldg(a.cshift + c0 + hl), t_lo, h, l2);
+              tab[(long long)cl * dim + c0 + hl] += h;
+              add_lo(a, cl, c0 + hl, l2);
+            }
             if (c0 == 0 && hl == 0) tcount[cl] += 1;
           }
         }
@@ -1290,11 +1420,15 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
                                   bool zero_cells, int sms, cudaStream_t s) {
   cudaError_t e;
   if (want_td && !zero_cells) {
-    // every assignment path stored the rows' exact distances (store_dist)
+    // every assignment path stored the rows' exact distances (store_dist);
+    // the same grid clears the low words the cell sums below add into
     const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
-    e = launch_k(td_tiles_kernel, (unsigned)ntiles, 256, 0, s, a);
+    e = launch_k(td_tiles_kernel, (unsigned)ntiles, 256, 0, s, a, want_sums ? 1 : 0);
     if (e != cudaSuccess) return e;
     e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  } else if (want_sums) {
+    e = launch_k(zero_lo_kernel, 64, 256, 0, s, a, zero_cells ? 1 : 0);
     if (e != cudaSuccess) return e;
   }
   if (!want_sums) return cudaSuccess;
@@ -1339,49 +1473,6 @@ cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums
 }
 
 // ---------------------------------------------------------------------------
-// ordered update: the reference's own summation order (update_rows,
-// _kernels.py:47-58: members of cell i summed in ascending training index),
-// one thread per (cell, dim).  Writes the new centroids to the `ord` buffer;
-// apply_kernel picks them up.
-// ---------------------------------------------------------------------------
-
-template <typename XT>
-__global__ void ordered_update_kernel(KernelArgs a, const XT* __restrict__ X) {
-  pdl_wait();
-  const DevState* st = a.st;
-  if (st->done) return;
-  const int K = st->size;
-  const int dim = a.dim;
-  const double* old = a.cb[st->cur];
-  const long long n = a.n;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)K * dim;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(t / dim), l = (int)(t % dim);
-    double s = 0.0;
-    long long cnt = 0;
-    for (long long j = 0; j < n; ++j) {
-      if (a.idx[j] == k) {
-        s = __dadd_rn(s, load_x(X, j * dim + l));
-        ++cnt;
-      }
-    }
-    a.ord[t] = cnt > 0 ? __ddiv_rn(s, (double)cnt) : old[t];
-    if (l == 0) a.ex.counts()[k] = cnt;
-  }
-}
-
-cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s) {
-  long long work = a.kmax * a.dim;
-  int blocks = (int)((work + 127) / 128);
-  if (blocks > 4096) blocks = 4096;
-  if (a.x32)
-    ordered_update_kernel<float><<<blocks, 128, 0, s>>>(a, a.x32);
-  else
-    ordered_update_kernel<double><<<blocks, 128, 0, s>>>(a, a.x64);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
 // finalize (one block): the pass's distortion, the convergence test
 // (core.py:342-356), level / guard logic (core.py:384-415) and history.  It
 // only DECIDES: the codebook work (centroids, split, FP32 staging) is done
@@ -1389,8 +1480,8 @@ cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 
 __device__ void record_hist(DevState* st, int size, int it, double td, long long empty) {
-  if (st->n_hist < kMaxHist) {
-    HistRec& h = st->hist[st->n_hist];
+  {
+    HistRec& h = st->hist[st->n_hist % st->hist_cap];  // ring: the host drains it per batch
     h.size = size;
     h.iteration = it;
     h.td = td;
@@ -1626,7 +1717,7 @@ __global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
   const int dim = a.dim;
   const double* src = a.cb[st->act_src];
   double* dst = a.cb[st->act_src ^ 1];
-  const double inv_scale = ldexp(1.0, -st->fixed_shift);
+  const int t_lo = st->lo_shift;
   const double delta = st->delta;
   const int ordered = st->ordered;
   const int lane = threadIdx.x & 31;
@@ -1637,7 +1728,9 @@ __global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
       const long long i = k * dim + l;
       double v = src[i];
       if ((act & kActUpdate) && cnt > 0)
-        v = ordered ? a.ord[i] : __ddiv_rn((double)a.ex.sums()[i] * inv_scale, (double)cnt);
+        v = ordered ? a.ord[i]
+                    : __ddiv_rn(fixed_to_double(a.ex.sums()[i], a.ex.lo()[i], t_lo, -(a.cshift[l] + t_lo)),
+                                (double)cnt);
       if (act & kActSplit) {
         dst[(2 * k) * dim + l] = __dadd_rn(v, delta);
         dst[(2 * k + 1) * dim + l] = __dsub_rn(v, delta);
@@ -1745,23 +1838,131 @@ cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
   return cudaGetLastError();
 }
 
-// fixed-point scale from a device-side max |x| (api.cu fixed_shift_for, on
-// the device so the host-buffer Lloyd step needs no host round trip)
-__global__ void set_shift_kernel(DevState* st, const unsigned long long* maxabs_bits, long long n_global) {
-  const double m = __longlong_as_double((long long)*maxabs_bits);
-  int e_n = 0;
-  while ((1LL << e_n) < n_global && e_n < 62) ++e_n;
-  int e_x = 0;
-  if (m > 0 && m <= DBL_MAX) frexp(m, &e_x);
-  int sft = 62 - e_n - e_x - 1;
-  sft = sft > 1000 ? 1000 : (sft < -1000 ? -1000 : sft);
-  st->fixed_shift = sft;
-  st->nonfinite = !(m <= DBL_MAX);
+// Per-column statistics of a row block for the two-word fixed-point plan:
+// max |x| (FP64 bit patterns; NaN bits when a value is not finite) and the
+// exponent of the lowest set bit (INT_MAX when the column is all zeros).
+// Thread t keeps column t % dim when the grid's thread count is a multiple of
+// dim (dim divides 256), else it walks elements with shared-memory atomics.
+__device__ __forceinline__ int lowbit_exp(float x) {
+  const unsigned u = __float_as_uint(x);
+  const unsigned E = (u >> 23) & 0xffu;
+  unsigned m = u & 0x7fffffu;
+  if (E == 0xffu) return INT_MIN;  // non-finite: flagged through the max
+  int e0 = -149;
+  if (E) {
+    m |= 0x800000u;
+    e0 = (int)E - 150;
+  }
+  return m ? e0 + __ffs((int)m) - 1 : INT_MAX;
+}
+__device__ __forceinline__ int lowbit_exp(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  const unsigned E = (unsigned)((u >> 52) & 0x7ffu);
+  unsigned long long m = u & 0xfffffffffffffull;
+  if (E == 0x7ffu) return INT_MIN;
+  int e0 = -1074;
+  if (E) {
+    m |= 1ull << 52;
+    e0 = (int)E - 1075;
+  }
+  return m ? e0 + __ffsll((long long)m) - 1 : INT_MAX;
 }
 
-cudaError_t launch_set_shift(DevState* st, const unsigned long long* maxabs_bits, long long n_global,
-                             cudaStream_t s) {
-  set_shift_kernel<<<1, 1, 0, s>>>(st, maxabs_bits, n_global);
+template <typename T>
+__global__ void __launch_bounds__(256) colstats_kernel(const T* __restrict__ x, long long rows, int dim,
+                                                       unsigned long long* cmax, int* clow) {
+  const long long count = rows * dim;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (stride % dim == 0) {
+    double m = 0.0;
+    bool bad = false;
+    int low = INT_MAX;
+    for (long long i = i0; i < count; i += stride) {
+      const T v = x[i];
+      const double av = fabs((double)v);
+      bad |= !(av <= DBL_MAX);
+      m = fmax(m, av);
+      low = min(low, lowbit_exp(v));
+    }
+    if (i0 < count) {
+      const int c = (int)(i0 % dim);
+      atomicMax(cmax + c, bad ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(m));
+      if (low != INT_MAX) atomicMin(clow + c, low);
+    }
+    return;
+  }
+  for (long long i = i0; i < count; i += stride) {
+    const T v = x[i];
+    const double av = fabs((double)v);
+    const int c = (int)(i % dim);
+    atomicMax(cmax + c, !(av <= DBL_MAX) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(av));
+    const int low = lowbit_exp(v);
+    if (low != INT_MAX) atomicMin(clow + c, low);
+  }
+}
+
+__global__ void colstats_reset_kernel(unsigned long long* cmax, int* clow, int dim) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < dim; c += gridDim.x * blockDim.x) {
+    cmax[c] = 0;
+    clow[c] = INT_MAX;
+  }
+}
+
+cudaError_t launch_colstats_reset(unsigned long long* cmax, int* clow, int dim, cudaStream_t s) {
+  colstats_reset_kernel<<<(dim + 255) / 256, 256, 0, s>>>(cmax, clow, dim);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colstats(const float* x32, const double* x64, long long rows, int dim,
+                            unsigned long long* cmax, int* clow, int sms, cudaStream_t s) {
+  if (rows < 1) return cudaSuccess;
+  const long long count = rows * dim;
+  long long blocks = (count + 255) / 256;
+  const long long cap = (long long)sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (x32)
+    colstats_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(x32, rows, dim, cmax, clow);
+  else
+    colstats_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(x64, rows, dim, cmax, clow);
+  return cudaGetLastError();
+}
+
+// fixed-point plan from column stats, on the device (the host-buffer Lloyd
+// step needs no host round trip): cshift, lo_shift, exactness flags, and the
+// overall max |x| for the non-finite check
+__global__ void set_shift_kernel(DevState* st, const unsigned long long* cmax, const int* clow, int dim,
+                                 long long n_global, int* cshift, unsigned long long* maxabs_bits) {
+  __shared__ int s_exact, s_ref, s_bad;
+  if (threadIdx.x == 0) {
+    s_exact = 1;
+    s_ref = 1;
+    s_bad = 0;
+  }
+  __syncthreads();
+  unsigned long long mb = 0;
+  for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+    const double m = __longlong_as_double((long long)cmax[c]);
+    const FixedCol f = fixed_plan(n_global, m, clow[c]);
+    cshift[c] = f.s;
+    if (!f.exact) atomicAnd(&s_exact, 0);
+    if (!f.ref_exact) atomicAnd(&s_ref, 0);
+    if (!(m <= DBL_MAX)) atomicOr(&s_bad, 1);
+    mb = cmax[c] > mb ? cmax[c] : mb;
+  }
+  if (maxabs_bits) atomicMax(maxabs_bits, mb);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->lo_shift = fixed_lo_shift(n_global);
+    st->sums_exact = s_exact;
+    st->ref_exact = s_ref;
+    st->nonfinite = s_bad;
+  }
+}
+
+cudaError_t launch_set_shift(DevState* st, const unsigned long long* cmax, const int* clow, int dim,
+                             long long n_global, int* cshift, unsigned long long* maxabs_bits, cudaStream_t s) {
+  set_shift_kernel<<<1, 256, 0, s>>>(st, cmax, clow, dim, n_global, cshift, maxabs_bits);
   return cudaGetLastError();
 }
 

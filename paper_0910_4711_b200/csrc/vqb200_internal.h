@@ -9,7 +9,7 @@
 
 namespace vqb {
 
-constexpr int kMaxHist = 8192;   // levels x max_iterations_per_level records
+constexpr int kHistRing = 8192;  // device ring of history records, drained by the host per batch
 constexpr int kMaxWarn = 64;     // one warning per level at most
 constexpr int kTdTile = 2048;    // rows per distortion partial (fixed, global)
 constexpr int kEpiThreads = 1024; // dist/TD block: 2 rows per thread per 2048-row tile
@@ -41,7 +41,9 @@ struct DevState {
   int target;
   int max_iter;
   int metric;
-  int fixed_shift;     // sums are int64 fixed point with 2^-fixed_shift resolution
+  int lo_shift;        // t: the low word of a two-word fixed-point value has 2^-(s_l + t) units
+  int sums_exact;      // 1: every coordinate is exact on its column's two-word grid
+  int ref_exact;       // 1: the reference's own FP64 cell sums are provably exact too
   double eps;
   double delta;
   long long n_global;  // rows over all shards (for the centroid of size 1)
@@ -51,12 +53,12 @@ struct DevState {
   int size;
   int iteration;
   int done;
+  int n_hist;          // records written so far (adjacent to done: one 8-byte poll reads both)
   int cur;             // which codebook buffer holds the current codebook
   double td_prev;
   double total;
   double last_td;
   long long last_empty;
-  int n_hist;
   int n_warn;
   int warn_sizes[kMaxWarn];
   int flag_count;      // rows queued for the re-rank this pass (assign_fast -> shortlist)
@@ -77,12 +79,15 @@ struct DevState {
   int act_src;         // buffer holding the source codebook of the action
   int act_k;           // source codebook size
   unsigned long long t0_ns;  // %globaltimer at the initial centroid
-  HistRec hist[kMaxHist];
+  int hist_cap;        // ring capacity: record i lives in hist[i % hist_cap]
+  HistRec* hist;       // device ring, session-owned; the host drains it as passes complete
 };
 
 // Packed exchange buffer (int64 words), one allreduce per pass in the
-// multi-GPU loop: [sums K*L | counts K | td tile partials (FP64 bit patterns,
-// zero on tiles another rank owns)].
+// multi-GPU loop: [hi sums K*L | counts K | td tile partials (FP64 bit
+// patterns, zero on tiles another rank owns) | lo sums K*L].  A cell sum is
+// the two-word fixed-point integer hi * 2^t + lo in units of 2^-(s_l + t)
+// (per-column shift s_l, common t; see fixed_plan).
 struct Exchange {
   long long* base;
   long long kmax;
@@ -91,8 +96,49 @@ struct Exchange {
   __host__ __device__ long long* sums() const { return base; }
   __host__ __device__ long long* counts() const { return base + kmax * dim; }
   __host__ __device__ long long* td() const { return base + kmax * dim + kmax; }
-  __host__ __device__ long long words() const { return kmax * dim + kmax + ntiles; }
+  __host__ __device__ long long* lo() const { return base + kmax * dim + kmax + ntiles; }
+  __host__ __device__ long long words() const { return 2 * kmax * dim + kmax + ntiles; }
 };
+
+// ---- two-word fixed-point cell sums (the centroid numerators) ----
+// Column l is scaled by 2^s_l with s_l = 61 - e_n - e_l (rows < 2^e_n,
+// max |x_l| < 2^e_l), so the high words of n rows cannot overflow int64.  A
+// coordinate x splits EXACTLY as x * 2^s_l = hi + lo * 2^-t (hi = the integer
+// part of the magnitude, lo its remainder in units of 2^-t, t = 62 - e_n):
+// exact whenever x has no set bit below 2^-(s_l + t) = 2^(2 e_n + e_l - 123)
+// (at N = 2^20 and |x| < 512: every float32 |x| >= 2^-50), which is checked
+// up front (colstats: the lowest set bit of every column; otherwise the
+// reference-order path runs).  Integer
+// sums commute, so the result is the exact cell sum -- deterministic,
+// grid-independent and identical for every GPU count -- rounded once when it
+// becomes a centroid.  When the reference's own ascending-order FP64 sum is
+// exact as well (ref_exact: e_n + e_l - lowbit_l <= 53), the centroids are
+// bit-identical to the reference's.
+__host__ __device__ inline int ceil_log2_rows(long long n) {
+  int e = 0;
+  while (e < 62 && (1LL << e) < n) ++e;
+  return e;
+}
+struct FixedCol {
+  int s;          // column shift
+  int exact;      // two-word split exact for every coordinate of the column
+  int ref_exact;  // the reference's FP64 sums of this column are exact in any order
+};
+__host__ __device__ inline FixedCol fixed_plan(long long n_global, double maxabs, int minlow) {
+  FixedCol f;
+  const int e_n = ceil_log2_rows(n_global);
+  const int t = 62 - e_n;
+  int e_x = 0;
+  if (maxabs > 0 && maxabs <= 1.7976931348623157e308) frexp(maxabs, &e_x);
+  int s = 61 - e_n - e_x;
+  s = s > 960 ? 960 : (s < -1020 ? -1020 : s);
+  const bool zero = minlow == 0x7fffffff;  // column of zeros
+  f.s = s;
+  f.exact = (maxabs <= 1.7976931348623157e308) && (zero || (minlow + s + t >= 0 && s + t <= 1020));
+  f.ref_exact = f.exact && (zero || e_n + e_x - minlow <= 53);
+  return f;
+}
+__host__ __device__ inline int fixed_lo_shift(long long n_global) { return 62 - ceil_log2_rows(n_global); }
 
 struct KernelArgs {
   // training data (this shard): exactly one of x32/x64 is non-null
@@ -103,6 +149,7 @@ struct KernelArgs {
   int dim;
   long long tile0;      // global index of this shard's first TD tile
   const float* mu;      // centring vector (FP32, dim)
+  const int* cshift;    // per-column fixed-point shifts s_l (dim)
   // codebooks
   double* cb[2];        // FP64 master, double buffered, kmax x dim
   float* w;             // -2 * c~ (FP32), kpad x dim
@@ -123,6 +170,10 @@ struct KernelArgs {
   Exchange ex;
   long long* partials;  // per-block fixed-point slabs, sms x (kmax*dim + kmax)
   double* ord;          // reference-order centroids (ordered mode), kmax x dim
+  int* operm;           // ordered mode: rows sorted by cell, ascending within a cell (n)
+  int* obase;           // ordered mode: per (cell, row block) offsets, kmax x oblocks
+  int* oscan;           // ordered mode: scan scratch
+  int oblocks;          // ordered mode: row blocks of the counting sort
   DevState* st;
 };
 
@@ -156,14 +207,25 @@ cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s);
 bool shortlist_enabled();
 cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums, bool zero_cells,
                             int sms, cudaStream_t s);
-cudaError_t launch_ordered_update(const KernelArgs& a, cudaStream_t s);
+// reference-order FP64 cell sums (update_rows' ascending-index order): stable
+// counting sort of the rows by cell, then one sequential FP64 chain per
+// (cell, dimension); zero_cells: every row in cell 0 (the initial centroid)
+cudaError_t launch_ordered_update(const KernelArgs& a, bool zero_cells, int sms, cudaStream_t s);
+int ordered_blocks(long long n);
 cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s);
 cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s);
 cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s);
 cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,
                           unsigned long long* out_bits, int sms, cudaStream_t s);
-cudaError_t launch_set_shift(DevState* st, const unsigned long long* maxabs_bits, long long n_global,
-                             cudaStream_t s);
+// per-column max |x| (FP64 bit patterns, NaN bits for a non-finite value) and
+// lowest set bit exponent (INT_MAX for a column of zeros) of rows x[rows][dim]
+cudaError_t launch_colstats(const float* x32, const double* x64, long long rows, int dim,
+                            unsigned long long* cmax, int* clow, int sms, cudaStream_t s);
+cudaError_t launch_colstats_reset(unsigned long long* cmax, int* clow, int dim, cudaStream_t s);
+// per-column shifts (cshift) + lo_shift / sums_exact / ref_exact / nonfinite
+// from column stats, on the device (the host-buffer Lloyd step)
+cudaError_t launch_set_shift(DevState* st, const unsigned long long* cmax, const int* clow, int dim,
+                             long long n_global, int* cshift, unsigned long long* maxabs_bits, cudaStream_t s);
 cudaError_t launch_widen_idx(const int* idx, long long* out, long long n, int sms, cudaStream_t s);
 cudaError_t launch_sum_inorder(const double* v, long long n, double* out, cudaStream_t s);
 cudaError_t launch_reset(DevState* st, int mode, int size, int metric, int ordered, int keep_cur,

@@ -11,8 +11,9 @@ tables and distortions) maps onto ranks as follows:
 * every rank holds a codebook replica and runs allocation + epilogue on its
   shard (the C ABI's ``vqb_step_local``);
 * the partial cell tables never move: each rank reduces them on the device
-  into one packed int64 buffer [K*L fixed-point sums | K counts | distortion
-  tile partials] and ONE ``all_reduce(SUM)`` over NVLink combines them --
+  into one packed int64 buffer [K*L fixed-point high words | K counts |
+  distortion tile partials | K*L low words] (the two-word exact cell sums,
+  vqb200_internal.h) and ONE ``all_reduce(SUM)`` over NVLink combines them --
   integer addition is exact, so the combined buffer is identical on every
   rank and for every world size;
 * every rank then runs the same finalize (convergence test, centroids, split)
@@ -34,6 +35,15 @@ import numpy as np
 from . import _lib
 
 TILE = 2048  # vqb200_internal.h kTdTile
+
+
+def _split_stats(gstats: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """The MAX-reduced [colmax | -collow] vector back to the C ABI's arrays."""
+    g = np.asarray(gstats, dtype=np.float64)
+    dim = g.shape[0] // 2
+    cmax = np.ascontiguousarray(g[:dim])
+    clow = np.ascontiguousarray(-g[dim:]).astype(np.int32)
+    return cmax, clow
 
 
 def world_size() -> int:
@@ -94,19 +104,25 @@ class DeviceShard:
         _lib.check(self.L.vqb_set_stream(self.s.handle, ctypes.c_void_p(self.stream.cuda_stream)))
         self._ex = None
 
-    def maxabs(self) -> float:
-        return self.s.maxabs()
+    def colstats(self) -> np.ndarray:
+        """[max |x| per column | -(lowest set bit) per column] as float64: one
+        MAX allreduce gives the global column stats of the fixed-point plan."""
+        cmax, clow = self.s.colstats()
+        return np.concatenate([cmax, -clow.astype(np.float64)])
 
     def tensor(self, values):
         return self.torch.tensor(values, dtype=self.torch.float64, device=f"cuda:{self.device}")
 
-    def begin(self, config, global_maxabs: float) -> None:
+    def begin(self, config, gstats: np.ndarray) -> None:
         from .core import metric_code
 
         self.config = config
+        cmax, clow = _split_stats(gstats)
+        self._stats = (cmax, clow)  # alive for the call
         cfg = _lib.TrainConfig(config.target_size, config.epsilon, config.delta,
                                config.max_iterations_per_level,
-                               metric_code(config.distortion_metric), 0, global_maxabs)
+                               metric_code(config.distortion_metric), 0,
+                               cmax.ctypes.data, clow.ctypes.data)
         self._cfg = cfg
         _lib.check(self.L.vqb_step_begin(self.s.handle, ctypes.byref(cfg)))
 
@@ -125,10 +141,12 @@ class DeviceShard:
 
     # -- fixed-size Lloyd passes (vqb_lloyd_*): update_codebook after
     # assign_cells, sharded; the pass ends with the same exchange + finalize
-    def lloyd_begin(self, codebook: np.ndarray, global_maxabs: float) -> None:
+    def lloyd_begin(self, codebook: np.ndarray, gstats: np.ndarray) -> None:
         cb = np.ascontiguousarray(codebook, dtype=np.float64)
         self._lloyd_k = cb.shape[0]
-        _lib.check(self.L.vqb_lloyd_begin(self.s.handle, _lib.ptr(cb), cb.shape[0], global_maxabs))
+        cmax, clow = _split_stats(gstats)
+        _lib.check(self.L.vqb_lloyd_begin(self.s.handle, _lib.ptr(cb), cb.shape[0], _lib.ptr(cmax),
+                                          _lib.ptr(clow)))
 
     def lloyd_local(self) -> None:
         _lib.check(self.L.vqb_lloyd_local(self.s.handle))
@@ -155,18 +173,13 @@ class DeviceShard:
         from .core import LevelIteration, _max_iter_warning
 
         config = self.config
-        levels = max(1, int(math.log2(config.target_size)))
-        cap = levels * config.max_iterations_per_level + 8
-        hist = (_lib.LevelIterationC * cap)()
         warn = np.zeros(64, dtype=np.int64)
         cb = np.empty((config.target_size, self.s.dim), dtype=np.float64)
         dists = np.empty(self.s.rows, dtype=np.float64)
         summ = _lib.TrainSummary()
-        _lib.check(self.L.vqb_step_result(self.s.handle, _lib.ptr(cb), hist, cap, _lib.ptr(warn), 64,
+        _lib.check(self.L.vqb_step_result(self.s.handle, _lib.ptr(cb), None, 0, _lib.ptr(warn), 64,
                                           _lib.ptr(dists), ctypes.byref(summ)))
-        history = [LevelIteration(int(h.codebook_size), int(h.iteration), float(h.td),
-                                  int(h.empty_cells), float(h.seconds))
-                   for h in hist[: int(summ.n_hist)]]
+        history = self.s.history(int(summ.n_hist))
         warnings = [_max_iter_warning(int(s), config.max_iterations_per_level)
                     for s in warn[: int(summ.n_warn)]]
         return cb[: int(summ.final_size)], history, warnings, float(summ.total), dists
@@ -219,8 +232,8 @@ def run_sharded(backend, config, batch: int = 4, collective: bool = True):
 
 def _run_sharded(backend, config, batch: int, collective: bool):
     """Drive the pass loop on every rank.  Collectives: one MAX allreduce of
-    |x| (common fixed-point scale), then per pass one SUM allreduce of the
-    packed int64 exchange buffer.  Ranks stay in lockstep because every rank
+    the column stats (the common two-word fixed-point plan), then per pass
+    one SUM allreduce of the packed int64 exchange buffer.  Ranks stay in lockstep because every rank
     derives `done` from identical combined bits.  ``collective=False`` runs
     the same loop on one rank without any collective."""
     import torch.distributed as dist
@@ -229,9 +242,9 @@ def _run_sharded(backend, config, batch: int, collective: bool):
         if collective:
             dist.all_reduce(t, op=op)
 
-    gmax = backend.tensor([backend.maxabs()])
-    all_reduce(gmax, dist.ReduceOp.MAX)
-    backend.begin(config, float(gmax.item()))
+    gstats = backend.tensor(backend.colstats())
+    all_reduce(gstats, dist.ReduceOp.MAX)
+    backend.begin(config, gstats.cpu().numpy())
     ex = backend.exchange()
     all_reduce(ex, dist.ReduceOp.SUM)
     backend.finalize()
@@ -265,16 +278,16 @@ def sharded_lloyd(backend, codebook: np.ndarray, passes: int = 1, collective: bo
 
 def _sharded_lloyd(backend, codebook: np.ndarray, passes: int, collective: bool, on_pass):
     """``passes`` Lloyd iterations at a fixed codebook size over all ranks:
-    one MAX allreduce of |x| (the common fixed-point scale), then per pass
+    one MAX allreduce of the column stats (the common fixed-point plan), then per pass
     local assign + epilogue, ONE SUM allreduce of the packed int64 exchange
     buffer, finalize (the centroids of the combined sums, identical bits on
     every rank).  ``on_pass(i)`` runs after each pass is enqueued (timing)."""
     import torch.distributed as dist
 
-    gmax = backend.tensor([backend.maxabs()])
+    gstats = backend.tensor(backend.colstats())
     if collective:
-        dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
-    backend.lloyd_begin(codebook, float(gmax.item()))
+        dist.all_reduce(gstats, op=dist.ReduceOp.MAX)
+    backend.lloyd_begin(codebook, gstats.cpu().numpy())
     ex = backend.exchange()
     for i in range(passes):
         backend.lloyd_local()

@@ -28,13 +28,23 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TILE = 2048
 
 
-def _fixed_shift(n_global: int, maxabs: float) -> int:
-    """api.cu fixed_shift_for: int64 sums of n rows of |x| < 2^e_x cannot overflow."""
+def _fixed_plan(n_global: int, cmax: np.ndarray) -> tuple[np.ndarray, int]:
+    """vqb200_internal.h fixed_plan: per-column shifts s_l = 61 - e_n - e_l
+    (int64 high words of n rows cannot overflow) and the common low-word
+    shift t = 62 - e_n."""
     e_n = 0
     while (1 << e_n) < n_global and e_n < 62:
         e_n += 1
-    e_x = math.frexp(maxabs)[1] if maxabs > 0 else 0
-    return max(-1000, min(1000, 62 - e_n - e_x - 1))
+    s = [max(-1020, min(960, 61 - e_n - (math.frexp(m)[1] if m > 0 else 0))) for m in cmax]
+    return np.array(s, dtype=np.int64), 62 - e_n
+
+
+def _lowbit(v: float) -> int:
+    if v == 0.0:
+        return 2**31 - 1
+    m, e = math.frexp(abs(v))  # |v| = m 2^e, m in [0.5, 1)
+    q = int(m * 2**53)
+    return e - 53 + ((q & -q).bit_length() - 1)
 
 
 class EmulatedShard:
@@ -53,18 +63,27 @@ class EmulatedShard:
         self.ntiles = -(-n_global // TILE)
 
     # -- backend surface used by run_sharded ------------------------------
-    def maxabs(self) -> float:
-        return float(np.max(np.abs(self.x))) if self.x.size else 0.0
+    def colstats(self) -> np.ndarray:
+        cmax = np.max(np.abs(self.x), axis=0)
+        clow = np.array([min(_lowbit(float(v)) for v in col) for col in self.x.T], dtype=np.float64)
+        return np.concatenate([cmax, -clow])
 
     def tensor(self, values):
         return self.torch.tensor(values, dtype=self.torch.float64)
 
-    def begin(self, config, global_maxabs: float) -> None:
+    def _plan(self, gstats) -> None:
+        g = np.asarray(gstats, dtype=np.float64)
+        self.shift, self.t = _fixed_plan(self.n_global, g[: self.dim])
+
+    def _alloc_exchange(self) -> None:
+        # [hi K*L | counts K | td tiles | lo K*L] (vqb200_internal.h Exchange)
+        self.ex = self.torch.zeros(2 * self.kmax * self.dim + self.kmax + self.ntiles, dtype=self.torch.int64)
+
+    def begin(self, config, gstats) -> None:
         self.cfg = config
         self.kmax = config.target_size
-        self.shift = _fixed_shift(self.n_global, global_maxabs)
-        self.scale = 2.0 ** self.shift
-        self.ex = self.torch.zeros(self.kmax * self.dim + self.kmax + self.ntiles, dtype=self.torch.int64)
+        self._plan(gstats)
+        self._alloc_exchange()
         self.cb = np.zeros((self.kmax, self.dim))
         self.size, self.iteration, self.td_prev = 1, 1, math.inf
         self.done, self.mode_final = False, False
@@ -77,16 +96,24 @@ class EmulatedShard:
     def exchange(self):
         return self.ex
 
-    def _fixed(self, v: np.ndarray) -> np.ndarray:
-        return np.rint(v * self.scale).astype(np.int64)  # __double2ll_rn(v * 2^shift)
+    def _split(self) -> tuple[np.ndarray, np.ndarray]:
+        """kernels.cu split_fixed: x 2^s = hi + lo 2^-t, hi truncated toward 0."""
+        v = self.x * np.exp2(self.shift.astype(np.float64))
+        h = np.trunc(v)
+        return h.astype(np.int64), ((v - h) * 2.0 ** self.t).astype(np.int64)
 
     def _write_sums(self, cells: np.ndarray, k: int) -> None:
         e = self.ex.numpy()
         kd = self.kmax * self.dim
+        hi, lo = self._split()
         sums = np.zeros((k, self.dim), dtype=np.int64)
-        np.add.at(sums, cells, self._fixed(self.x))
+        los = np.zeros((k, self.dim), dtype=np.int64)
+        np.add.at(sums, cells, hi)
+        np.add.at(los, cells, lo)
         e[: k * self.dim] = sums.reshape(-1)
         e[kd: kd + k] = np.bincount(cells, minlength=k)
+        lo0 = kd + self.kmax + self.ntiles
+        e[lo0: lo0 + k * self.dim] = los.reshape(-1)
 
     def local(self) -> None:
         if self.done:
@@ -111,10 +138,20 @@ class EmulatedShard:
         k = self.size
         src = self.cb[:k].copy()
         if update:
+            from fractions import Fraction
+
             counts = e[kd: kd + k]
-            sums = e[: k * self.dim].reshape(k, self.dim).astype(np.float64) * (2.0 ** -self.shift)
-            nz = counts > 0
-            src[nz] = sums[nz] / counts[nz, None]
+            lo0 = kd + self.kmax + self.ntiles
+            his = e[: k * self.dim].reshape(k, self.dim)
+            los = e[lo0: lo0 + k * self.dim].reshape(k, self.dim)
+            for c in range(k):
+                if counts[c] == 0:
+                    continue
+                for l in range(self.dim):
+                    # kernels.cu fixed_to_double: the exact sum rounded once
+                    T = int(his[c, l]) * 2 ** self.t + int(los[c, l])
+                    num = float(Fraction(T, 2 ** (int(self.shift[l]) + self.t)))
+                    src[c, l] = np.float64(num) / np.float64(counts[c])
         if split:
             out = np.empty((2 * k, self.dim))
             out[0::2] = src + self.cfg.delta
@@ -136,13 +173,13 @@ class EmulatedShard:
                 self._set_action(True, False)
             else:
                 self._set_action(True, True)
-            e[base:] = 0
+            e[base: base + self.ntiles] = 0
             return
         k = self.size
         td = 0.0
         for t in range(self.ntiles):
             td += float(e[base + t: base + t + 1].view(np.float64)[0])
-        e[base:] = 0
+        e[base: base + self.ntiles] = 0
         if getattr(self, "lloyd", False):  # kModeLloydStep: update, done
             self._set_action(True, False)
             self.total, self.done = td, True
@@ -178,15 +215,14 @@ class EmulatedShard:
         return self.done
 
     # -- fixed-size Lloyd passes (vqb_lloyd_*, distributed.sharded_lloyd)
-    def lloyd_begin(self, codebook, global_maxabs: float) -> None:
+    def lloyd_begin(self, codebook, gstats) -> None:
         import types
 
         cb = np.asarray(codebook, dtype=np.float64)
         self.cfg = types.SimpleNamespace(distortion_metric="squared_euclidean", delta=0.0)
         self.kmax = cb.shape[0]
-        self.shift = _fixed_shift(self.n_global, global_maxabs)
-        self.scale = 2.0 ** self.shift
-        self.ex = self.torch.zeros(self.kmax * self.dim + self.kmax + self.ntiles, dtype=self.torch.int64)
+        self._plan(gstats)
+        self._alloc_exchange()
         self.cb = cb.copy()
         self.size, self.done, self.lloyd, self.pending_init = cb.shape[0], False, True, False
 
