@@ -1,29 +1,37 @@
 """Benchmark of the B200 LBG hot path (BASELINE.json metric: G vector-codeword
 distance evals/s per Lloyd iteration; codebook design wall time).
 
-Workload (N=1): BASELINE configs[1] (cfg2) -- N = 2^20 float32 vectors, L = 16,
-from the seeded 1024-component Gaussian mixture (paper_0910_4711_b200/
-synthetic.py); a step is ONE Lloyd iteration at the final level K = 1024
-(assign over all rows + FP64 re-rank + exact distortion + centroid update),
-starting from the reference's own converged K=1024 codebook
-(tests/golden/cfg2_design.npz, produced by the reference).  Evals per step =
-N * K.  L2 is flushed (256 MiB write) between timed steps.
+Headline (default, N=1): BASELINE configs[3] (cfg4, the largest config that
+fits one B200) -- N = 2^24 float32 vectors, L = 16, from the seeded
+4096-component Dirichlet-weighted Gaussian mixture (paper_0910_4711_b200/
+synthetic.py); a step is ONE Lloyd iteration at the final level K = 4096
+(assign over all rows + FP64 re-rank + exact distortion + exact cell sums +
+centroid update), starting from the reference's own converged K=4096 codebook
+(tests/golden/cfg4_design.npz, produced by the reference).  Evals per step =
+N * K.  L2 is flushed (256 MiB write) between timed steps (the 1 GiB input is
+larger than L2 anyway).
+
+N > 1 (torchrun): STRONG scaling -- every rank holds a contiguous tile-aligned
+shard of the same global 2^24-row set (distributed.ShardPlan); each pass ends
+with one NCCL allreduce of the packed int64 exchange buffer; time = max over
+ranks; value = N * K / that time.
 
 Keys beyond the base contract:
-  e2e          same iteration through the C ABI with HOST buffers
-               (vqb_lloyd_step_f32: H2D of X + codebook, D2H of cells + codebook)
-  roofline     dominant kernel (assign_tc<16>): algorithmic 3L flops per
-               eval / its CUDA-event time, against the measured tensor peak,
-               with the ALU-pipe ceiling of its argmin epilogue and the
-               FP32 FFMA peak (the north star's denominator) beside it
-  cpu_baseline oracle/ (C + OpenMP restatement of the reference kernels) on a
-               bounded row sample of the same iteration, all host cores
-  design       one full cfg2 design (1 -> 1024, 244 passes in the reference):
-               device-resident wall time and through the host API
---impl reference times the CPU oracle port alone (the reference itself is
-Python+numba and cannot travel to the GPU box).
-N>1 (torchrun): weak scaling, every rank a cfg2-sized shard (rank-seeded),
-one int64 allreduce per pass over NCCL; time = max over ranks.
+  e2e           same iteration through the C ABI with HOST buffers from pinned
+                memory (vqb_lloyd_step_f32: H2D of X + codebook, D2H of the
+                new codebook + distortion); e2e_pageable: from a plain numpy array
+  roofline      dominant kernel (assign_tc<16>): algorithmic 3L flops per
+                eval / its CUDA-event time, against the measured tensor peak,
+                with the ALU-pipe ceiling of its argmin epilogue and the FP32
+                FFMA peak (the north star's denominator) beside it
+  cpu_baseline  oracle/ (C + OpenMP restatement of the reference kernels) on a
+                bounded row sample of the same iteration, all host cores
+  design        one full cfg4 design (1 -> 4096, 338 passes in the reference):
+                device-resident wall time and through lbg_train from numpy
+  cfg2          the cfg2 Lloyd iteration (BASELINE configs[1]) and its design
+--impl reference prints the CPU arm on the same config dict (the reference is
+Python + numba and cannot travel to the GPU box: its arithmetic runs as the
+oracle/ port).
 """
 
 from __future__ import annotations
@@ -174,7 +182,7 @@ def _measured_peaks():
         return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks):
+def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks, k):
     """Roofline of the dominant kernel, assign_tc<16> (tcgen05 kind::f16 MMA
     chain into TMEM + top-2 epilogue).  achieved = ALGORITHMIC flops (3L = 48
     per vector-codeword eval) per launch / its CUDA-event time.
@@ -194,7 +202,7 @@ def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks):
         "bound": "tensor", "kernel": "assign_tc<16>",
         "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s", "frac": achieved / tensor_peak,
         "peak_source": f"{src} bf16_tflops (dense burst; kind::f16 runs at the bf16 rate)",
-        "algorithmic": "3L = 48 flops per vector-codeword eval, N*K evals per launch",
+        "algorithmic": f"3L = 48 flops per vector-codeword eval, N*K = {n}*{k} evals per launch",
         "issued_mma_tflops": evals * 2 * (3 * 16 + 16) / (assign_ms * 1e-3) / 1e12,
         "traffic": traffic.get("bytes_per_launch") if traffic else None,
         "algorithmic_bytes": n * 16 * 4 + n * 4,
@@ -206,8 +214,10 @@ def _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks):
     }
 
 
-def _load_traffic():
-    path = os.path.join(ROOT, "profiles", "assign_traffic.json")
+def _load_traffic(name):
+    """DRAM bytes per launch of assign_tc<16> from the committed ncu --set full
+    capture of this workload (profiles/assign_traffic_<cfg>.json)."""
+    path = os.path.join(ROOT, "profiles", f"assign_traffic_{name}.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -215,40 +225,76 @@ def _load_traffic():
         return None
 
 
+LLOYD_WORKLOADS = ("cfg4", "cfg2")  # the Lloyd-iteration lines; cfg4 is the headline (largest 1-GPU config)
+
+
+def _lloyd_case(name):
+    """(spec, reference's converged codebook, golden npz) of a Lloyd-line workload."""
+    from paper_0910_4711_b200 import synthetic
+
+    g = np.load(os.path.join(ROOT, "tests", "golden", f"{name}_design.npz"))
+    return synthetic.WORKLOADS[name], np.ascontiguousarray(g["cb"]), g
+
+
+def _lloyd_config(name, n, k, world):
+    """The `config` dict of a Lloyd-iteration line -- identical in both arms
+    (bench.py --impl reference prints the same dict)."""
+    from paper_0910_4711_b200 import synthetic
+
+    spec = synthetic.WORKLOADS[name]
+    return {"workload": f"{name}: {spec.name} N=2^{int(np.log2(n))} L=16, one Lloyd iteration at K={k} "
+                        f"(reference's converged codebook)",
+            "rows": n, "codebook": k, "dim": 16,
+            "parallelism": f"dp{world}" if world > 1 else "single",
+            "sharding": "contiguous tile-aligned row shards of the same global set (strong scaling)",
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+def _cpu_lloyd(x, cb, target_s, warmup, steps):
+    """Oracle (reference arithmetic, OpenMP over every host thread) Lloyd
+    iteration on a bounded leading-row sample: parallel assign + in-order TD
+    + update.  Returns (G evals/s, rows, threads, mean s per step)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    rate, rows, threads, _ = cpu_iteration_rate(x, cb, target_s=target_s, repeats=1)
+    xs = np.ascontiguousarray(x[:rows], dtype=np.float64)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        cells, dists = oracle.assign_all(xs, cb, workers=threads)
+        oracle.sum_inorder(dists)
+        oracle.update_all(xs, cells, cb, workers=threads)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    return rows * cb.shape[0] / t / 1e9, rows, threads, t
+
+
 def run_reference(args):
+    """The CPU arm: the reference's own arithmetic (oracle/ C + OpenMP port of
+    vqkit._kernels) on the SAME workload/config as the GPU arm, each step a
+    bounded row sample of it.  Under torchrun only rank 0 runs."""
     rank, world, _ = _rank_env()
     if rank != 0:
         return 0
     from paper_0910_4711_b200 import synthetic
 
-    cb, _ = _golden_codebook()
-    x = synthetic.make_training("cfg2")
+    name = args.workload if args.workload in LLOYD_WORKLOADS else "cfg4"
+    spec, cb, _ = _lloyd_case(name)
+    x = synthetic.make_training(name)
     cores, model = _cpu_info()
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle
-
-    # calibrate a sample so each step is ~2 s of CPU work
-    rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=2.0, repeats=1)
-    xs = np.ascontiguousarray(x[:rows], dtype=np.float64)
-    times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        cells, dists = oracle.assign_all(xs, cb, workers=threads)
-        oracle.sum_inorder(dists)
-        oracle.update_all(xs, cells, cb, workers=threads)
-        if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
-    value = rows * cb.shape[0] / t / 1e9
-    sample = (f"{rows} leading rows of cfg2 x K=1024 (reference's converged codebook): "
-              f"assign + in-order TD + update per step")
+    steps = max(1, min(args.steps, 5))  # a bounded sample per step: the run stays within minutes
+    value, rows, threads, t = _cpu_lloyd(x, cb, 2.0, min(args.warmup, 1), steps)
+    sample = (f"{rows} leading rows of {name} x K={cb.shape[0]} (reference's converged codebook): "
+              f"assign + in-order TD + update per step, {steps} steps")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2 gmm1024 N=2^20 L=16 K=1024 Lloyd iteration (sampled rows)",
-                   "rows_sampled": rows, "cpu_model": model},
+        "config": _lloyd_config(name, x.shape[0], cb.shape[0], world),
+        "cpu_model": model, "rows_sampled": rows,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -257,28 +303,29 @@ def run_reference(args):
     return 0
 
 
-def _e2e_time(L, xp, cb, K, n, local_rank, flush, args, torch) -> float:
+def _e2e_time(L, xh, cb, K, local_rank, flush, args, torch) -> float:
     """Mean seconds of one Lloyd iteration through vqb_lloyd_step_f32 (the C
-    ABI with host buffers: H2D of this rank's rows from pinned memory + the
-    codebook, D2H of the new codebook and distortion).  xp was pinned at
-    start-up: on these VMs the DMA from freshly pinned pages runs at ~half
-    rate for about a second (tools/e2e_probe3.py)."""
+    ABI with host buffers: H2D of this rank's rows + the codebook, D2H of the
+    new codebook and distortion).  xh pinned (torch pin_memory, pinned at
+    start-up: freshly pinned pages DMA at ~half rate for about a second,
+    tools/e2e_probe3.py) or pageable numpy."""
     from paper_0910_4711_b200 import _lib
 
     new_cb = np.empty_like(cb)
     td = ctypes.c_double()
     empty = ctypes.c_int64()
+    n = xh.shape[0]
 
     def e2e_step():
         # the step's result is the new codebook + distortion (what the next
         # Lloyd pass consumes); the cell table stays on the device
-        _lib.check(L.vqb_lloyd_step_f32(_lib.ptr(xp), n, 16, _lib.ptr(cb), K, local_rank,
+        _lib.check(L.vqb_lloyd_step_f32(_lib.ptr(xh), n, 16, _lib.ptr(cb), K, local_rank,
                                         _lib.ptr(new_cb), None, ctypes.byref(td), ctypes.byref(empty)))
 
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, min(args.warmup, 2))):
         e2e_step()
     times = []
-    for _ in range(args.steps):
+    for _ in range(max(1, min(args.steps, 10))):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -287,14 +334,91 @@ def _e2e_time(L, xp, cb, K, n, local_rank, flush, args, torch) -> float:
     return sum(times) / len(times)
 
 
+def _timed_lloyd(shard, cb, world, dist, flush, warmup, steps, torch):
+    """Lloyd passes of distributed.sharded_lloyd on one rank: local assign +
+    re-rank + distortion + cell sums, ONE SUM allreduce of the packed int64
+    exchange buffer over NCCL (world > 1), finalize; CUDA events on the stream
+    all of it runs on.  Returns the per-step ms of this rank."""
+    with torch.cuda.stream(shard.stream):  # our kernels, NCCL and the events on one stream
+        gstats = shard.tensor(shard.colstats())
+        if world > 1:
+            dist.all_reduce(gstats, op=dist.ReduceOp.MAX)
+        shard.lloyd_begin(cb, gstats.cpu().numpy())
+        ex = shard.exchange()
+
+        def pass_():
+            shard.lloyd_local()
+            if world > 1:
+                dist.all_reduce(ex, op=dist.ReduceOp.SUM)
+            shard.finalize()
+
+        for _ in range(warmup):
+            flush.zero_()
+            pass_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            pass_()
+            ev1.record()
+            torch.cuda.synchronize()
+            ms.append(ev0.elapsed_time(ev1))
+        torch.cuda.synchronize()
+    return ms
+
+
+def _design_entry(sess, x, conf, golden, vq, torch, e2e_runs=2):
+    """One full design: device-resident wall time (vqb_train on the resident
+    session) and through lbg_train from a numpy float32 matrix, with the
+    reference schedule check."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dcb, hist, warns, total, _d, summ = sess.train(conf)
+    design_s = time.perf_counter() - t0
+    walls = []
+    for _ in range(e2e_runs):  # the first call also pays one-time staging / module setup
+        t0 = time.perf_counter()
+        vq.lbg_train(vq.TrainingSet(x), conf)  # host buffer -> device -> host
+        walls.append(time.perf_counter() - t0)
+    ghist = golden["hist"]
+    return {
+        "wall_s": design_s, "e2e_wall_s": min(walls[1:] if len(walls) > 1 else walls),
+        "passes": int(summ.passes), "evals": int(summ.evals),
+        "g_evals_per_s": summ.evals / design_s / 1e9,
+        "flagged_rows": int(summ.flagged_rows), "flagged_full_scan_rows": int(summ.flagged_full),
+        "sums_exact": int(summ.sums_exact), "sums_ref_exact": int(summ.ref_exact),
+        "reference_passes": int(ghist.shape[0]),
+        "schedule_matches_reference": bool(
+            len(hist) == ghist.shape[0] and all(
+                (h.codebook_size, h.iteration, h.empty_cells) == (int(g[0]), int(g[1]), int(g[3]))
+                for h, g in zip(hist, ghist))),
+        "total_rel_err_vs_reference": abs(total - float(golden["total"])) / float(golden["total"]),
+        "codebook_max_rel_err_vs_reference": float(np.max(np.abs(dcb - golden["cb"]) /
+                                                          np.maximum(np.abs(golden["cb"]), 1e-300))),
+        "reference_wall_s": float(golden["seconds"]),
+        "reference_workers": int(golden["workers"]) if "workers" in golden.files else None,
+    }
+
+
 def run_b200(args):
+    """The headline Lloyd-iteration line (default cfg4; --workload cfg2 for
+    the cfg2 line).  N > 1: strong scaling -- every rank holds a contiguous
+    tile-aligned shard (distributed.ShardPlan) of the same global set."""
     rank, world, local_rank = _rank_env()
     import torch
 
     import paper_0910_4711_b200 as vq
     from paper_0910_4711_b200 import _lib, synthetic
+    from paper_0910_4711_b200 import distributed as D
     from paper_0910_4711_b200.core import _Session
 
+    name = args.workload if args.workload in LLOYD_WORKLOADS else "cfg4"
     torch.cuda.set_device(local_rank)
     L = _lib.lib()
     dist = None
@@ -302,17 +426,15 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
 
-    cb, golden = _golden_codebook()
+    spec, cb, golden = _lloyd_case(name)
     K = cb.shape[0]
-    if world == 1:
-        x = synthetic.make_training("cfg2")
-    else:  # weak scaling: a cfg2-sized shard per rank, rank-seeded
-        rng = np.random.default_rng(1000 + rank)
-        x = synthetic.gaussian_mixture(rng, 1 << 20, 16, 1024, 2.0, 20.0)
+    x = synthetic.make_training(name)  # every rank: the same global set
     n = x.shape[0]
-    xp_t = torch.from_numpy(x).pin_memory()  # e2e input (this rank's shard), pinned early
-    xp = xp_t.numpy() if xp_t is not None else None
-    sess = _Session(x, None, device=local_rank)
+    plan = D.ShardPlan(n, world)
+    lo, hi = plan.bounds(rank)
+    xs = np.ascontiguousarray(x[lo:hi])
+    n_local = xs.shape[0]
+    xp_t = torch.from_numpy(xs).pin_memory()  # e2e input (this rank's shard), pinned early
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
 
     # ---- peak: measured FFMA throughput (lane FMA/s -> FLOP/s)
@@ -320,90 +442,41 @@ def run_b200(args):
     _lib.check(L.vqb_pipe_microbench(0, 4, 4000, ctypes.byref(ops), ctypes.byref(sec)))
     ffma_peak_tflops = 2 * ops.value / 1e12
 
+    # ---- per-kernel segments of this rank's local pass (roofline diagnostic)
+    sess = _Session(xs, None, device=local_rank, row_offset=lo, n_global=n)
     segs = (ctypes.c_double * 5)()
     flagged = ctypes.c_int64()
 
-    def step():
+    def seg_step():
         _lib.check(L.vqb_bench_iteration(sess.handle, _lib.ptr(cb), K, 1, segs, ctypes.byref(flagged)))
         return list(segs)
 
-    # --segmented: time the kernels one event pair each (vqb_bench_iteration;
-    # the events between kernels also serialise the programmatic dependent
-    # launches).  Default: per-kernel segments from that diagnostic, the value
-    # from whole passes (events only on both sides of each pass).
-    segmented = getattr(args, "segmented", False) and world == 1
     clocks = ClockSampler(local_rank).__enter__()
     for _ in range(args.warmup):
         flush.zero_()
-        step()
-    torch.cuda.synchronize()
+        seg_step()
     seg_hist = []
-    if segmented:
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            seg_hist.append(step())
+    for _ in range(args.steps):
+        flush.zero_()
         torch.cuda.synchronize()
-        ms_steps = [sum(s) for s in seg_hist]
-    else:
-        # the Lloyd pass of the (multi-GPU) loop, distributed.sharded_lloyd:
-        # this rank's shard (rows [rank n, (rank+1) n) of the global set) ->
-        # local assign + epilogue -> ONE SUM allreduce of the packed int64
-        # exchange buffer over NCCL (N > 1) -> finalize on every rank; CUDA
-        # events on the stream all of it runs on (torch's current stream)
-        for _ in range(args.steps):  # per-kernel segments of this rank's local work (roofline)
-            flush.zero_()
-            torch.cuda.synchronize()
-            seg_hist.append(step())
-        from paper_0910_4711_b200 import distributed as D
+        seg_hist.append(seg_step())
+    seg = [sum(s[k] for s in seg_hist) / len(seg_hist) for k in range(5)]
 
-        shard = D.DeviceShard(x, rank * n, world * n, local_rank)
-        with torch.cuda.stream(shard.stream):  # our kernels, NCCL and the events on one stream
-            gstats = shard.tensor(shard.colstats())
-            if world > 1:
-                dist.all_reduce(gstats, op=dist.ReduceOp.MAX)
-            shard.lloyd_begin(cb, gstats.cpu().numpy())
-            ex = shard.exchange()
-
-            def pass_():
-                shard.lloyd_local()
-                if world > 1:
-                    dist.all_reduce(ex, op=dist.ReduceOp.SUM)
-                shard.finalize()
-
-            for _ in range(args.warmup):
-                flush.zero_()
-                pass_()
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            ms_steps = []
-            for _ in range(args.steps):
-                flush.zero_()
-                torch.cuda.synchronize()
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev0.record()
-                pass_()
-                ev1.record()
-                torch.cuda.synchronize()
-                ms_steps.append(ev0.elapsed_time(ev1))
-            torch.cuda.synchronize()
+    # ---- the timed step: whole Lloyd passes of the (multi-GPU) loop
+    shard = D.DeviceShard(xs, lo, n, local_rank)
+    ms_steps = _timed_lloyd(shard, cb, world, dist, flush, args.warmup, args.steps, torch)
     ms_step = sum(ms_steps) / len(ms_steps)
     if world > 1:
         t = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
         dist.barrier()
-    seg = [sum(s[k] for s in seg_hist) / len(seg_hist) for k in range(5)]
     evals = n * K
-    value = world * evals / (ms_step * 1e-3) / 1e9
+    value = evals / (ms_step * 1e-3) / 1e9
     assign_ms = seg[1]
-    flops = 3 * 16 * evals
-    achieved = flops / (assign_ms * 1e-3) / 1e12
-    traffic = _load_traffic()
+    achieved = 3 * 16 * n_local * K / (assign_ms * 1e-3) / 1e12
+    traffic = _load_traffic(name)
 
-    result = None
     if getattr(args, "profile_steps", False):
         clocks.__exit__(None, None, None)
         if rank == 0:
@@ -412,85 +485,75 @@ def run_b200(args):
         return 0
     # ---- e2e on every rank at once (each uploads its own shard over its own
     # PCIe link): the slowest rank's time is the job's
-    e2e_s = _e2e_time(L, xp_t.numpy(), cb, K, n, local_rank, flush, args, torch)
+    e2e_s = _e2e_time(L, xp_t.numpy(), cb, K, local_rank, flush, args, torch)
+    e2e_pg_s = _e2e_time(L, xs, cb, K, local_rank, flush, args, torch)  # pageable numpy rows
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local_rank}")
+        t = torch.tensor([e2e_s, e2e_pg_s], dtype=torch.float64, device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s, e2e_pg_s = (float(v) for v in t.tolist())
     clocks.__exit__(None, None, None)  # every rank: the sampler is a child process
+    c = clocks.summary()
     if rank == 0:
-
-        # ---- full cfg2 design (device-resident) vs the reference's run
-        spec = synthetic.WORKLOADS["cfg2"]
-        conf = vq.LbgConfig(target_size=spec.target_size, epsilon=spec.epsilon, delta=spec.delta)
-        design = {}
+        design, second = {}, {}
         if world == 1:
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            dcb, hist, warns, total, _d, summ = sess.train(conf)
-            design_s = time.perf_counter() - t0
-            e2e_runs = []
-            for _ in range(3):  # first call pays one-time staging-buffer / module setup
-                t0 = time.perf_counter()
-                cb2, st2 = vq.lbg_train(vq.TrainingSet(x), conf)   # host buffer -> device -> host
-                e2e_runs.append(time.perf_counter() - t0)
-            design_e2e_s = min(e2e_runs[1:])
-            ghist = golden["hist"]
-            design = {
-                "wall_s": design_s, "e2e_wall_s": design_e2e_s, "passes": int(summ.passes),
-                "evals": int(summ.evals), "g_evals_per_s": summ.evals / design_s / 1e9,
-                "flagged_rows": int(summ.flagged_rows),
-                "flagged_full_scan_rows": int(summ.flagged_full),
-                "reference_passes": int(ghist.shape[0]),
-                "schedule_matches_reference": bool(
-                    len(hist) == ghist.shape[0] and all(
-                        (h.codebook_size, h.iteration, h.empty_cells) ==
-                        (int(g[0]), int(g[1]), int(g[3])) for h, g in zip(hist, ghist))),
-                "total_rel_err_vs_reference": abs(total - float(golden["total"])) / float(golden["total"]),
-                "reference_wall_s": float(golden["seconds"]),
-                "reference_workers": int(golden["workers"]) if "workers" in golden.files else None,
-            }
+            del shard
+            conf = vq.LbgConfig(target_size=spec.target_size, epsilon=spec.epsilon, delta=spec.delta)
+            design = _design_entry(sess, x, conf, golden, vq, torch, e2e_runs=1 if name == "cfg4" else 3)
+            if name == "cfg4":
+                # the cfg2 line (BASELINE configs[1]) beside the headline
+                del sess
+                torch.cuda.empty_cache()
+                s2, cb2, g2 = _lloyd_case("cfg2")
+                x2 = synthetic.make_training("cfg2")
+                sh2 = D.DeviceShard(x2, 0, x2.shape[0], local_rank)
+                ms2 = _timed_lloyd(sh2, cb2, 1, None, flush, args.warmup, args.steps, torch)
+                del sh2
+                sess2 = _Session(x2, None, device=local_rank)
+                conf2 = vq.LbgConfig(target_size=s2.target_size, epsilon=s2.epsilon, delta=s2.delta)
+                m2 = sum(ms2) / len(ms2)
+                second = {"cfg2": {"config": _lloyd_config("cfg2", x2.shape[0], cb2.shape[0], 1),
+                                   "value": x2.shape[0] * cb2.shape[0] / (m2 * 1e-3) / 1e9, "unit": UNIT,
+                                   "ms_per_step": m2,
+                                   "design": _design_entry(sess2, x2, conf2, g2, vq, torch)}}
 
         # ---- CPU baseline: oracle on a bounded sample, all host cores
         cpu_rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=4.0)
         cores, model = _cpu_info()
-        c = clocks.summary()
-        # per step (vqb_bench_iteration): reset, assign_fast + assign_tc (one
-        # of them exits at once), TC shortlist + FP32 shortlist + exact re-rank,
-        # td_tiles + sums + reduce_partials, finalize + apply
-        launches_per_step = 11 if sess_fast(sess) else 8
+        # per step: reset, assign_fast + assign_tc (one of them exits at once),
+        # TC shortlist + FP32 shortlist + exact re-rank, td_tiles (+ low-word
+        # clear) + sums + reduce_partials, finalize + apply
+        launches_per_step = 11
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32+f64", "data": "synthetic",
-            "config": {"workload": "cfg2: gmm1024 N=2^20 L=16, Lloyd iteration at K=1024 "
-                                   "(reference's converged codebook)",
-                       "rows_per_gpu": n, "codebook": K, "dim": 16,
-                       "parallelism": f"dp{world}" if world > 1 else "single",
-                       "step": ("Lloyd pass per kernel segment (vqb_bench_iteration, --segmented)"
-                                if segmented else
-                                "Lloyd pass: local assign + re-rank + distortion + cell sums, "
-                                + ("NCCL allreduce of the packed int64 exchange buffer, " if world > 1 else "")
-                                + "finalize (distributed.sharded_lloyd); events around each whole pass"),
-                       "l2": "flushed (256 MiB write) between timed steps"},
+            "config": _lloyd_config(name, n, K, world),
+            "step": ("Lloyd pass: local assign + re-rank + distortion + cell sums, "
+                     + ("NCCL allreduce of the packed int64 exchange buffer, " if world > 1 else "")
+                     + "finalize (distributed.sharded_lloyd); CUDA events around each whole pass"),
             "segments_ms": {"stage": seg[0], "assign": seg[1], "rerank": seg[2],
                             "epilogue": seg[3], "finalize": seg[4]},
             "rerank_rows_per_step": int(flagged.value),
-            "roofline": _roofline(achieved, evals, assign_ms, ffma_peak_tflops, traffic, n, clocks),
-            "e2e": {"value": world * evals / e2e_s / 1e9, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
-                    "api": "vqb_lloyd_step_f32 (C ABI), X from pinned host memory",
-                    "h2d_bytes_per_step": n * 16 * 4 + K * 16 * 8,
+            "roofline": _roofline(achieved, n_local * K, assign_ms, ffma_peak_tflops, traffic, n_local,
+                                  clocks, K),
+            "e2e": {"value": evals / e2e_s / 1e9, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+                    "api": "vqb_lloyd_step_f32 (C ABI), X from pinned host memory"
+                           + (", per rank on its shard" if world > 1 else ""),
+                    "h2d_bytes_per_step": n_local * 16 * 4 + K * 16 * 8,
                     "d2h_bytes_per_step": K * 16 * 8 + 8,
                     "result": "new codebook + distortion"},
+            "e2e_pageable": {"value": evals / e2e_pg_s / 1e9, "unit": UNIT, "ms_per_step": e2e_pg_s * 1e3,
+                             "api": "vqb_lloyd_step_f32, X from pageable numpy (staged copy engine)"},
             "cpu_baseline": {"value": cpu_rate, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{rows} leading rows x K=1024, assign+TD+update "
+                             "sample": f"{rows} leading rows of {name} x K={K}, assign+TD+update "
                                        f"(oracle/ C+OpenMP, reference arithmetic), min of 3",
                              "cpu_model": model},
             "design": design,
             "clocks": {k: c[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "gpu_launches": launches_per_step * args.steps,
         }
+        result.update(second)
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
@@ -834,21 +897,26 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "formats"],
-                    help="cfg2 (default) is the headline line; the others print one line each")
-    ap.add_argument("--segmented", action="store_true",
-                    help="N=1: time the step kernel by kernel (events between kernels) instead of whole passes")
+    ap.add_argument("--workload", default="lloyd",
+                    choices=["lloyd", "cfg1", "cfg2", "cfg3", "cfg4", "cfg4-design", "cfg5", "formats"],
+                    help="lloyd (default): the headline cfg4 Lloyd-iteration line (+ cfg2 beside it); "
+                         "cfg2: the cfg2 Lloyd line; cfg1/cfg3/cfg4-design/cfg5/formats: one line each")
     ap.add_argument("--profile-steps", action="store_true",
                     help="only the warm-up + timed steps (for ncu launch lists)")
     args = ap.parse_args()
+    if args.workload in ("lloyd", "cfg4"):
+        args.workload = "cfg4"
+    elif args.workload == "cfg4-design":
+        args.workload = "cfg4"
+        args.design = True
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "formats":
         return run_formats(args)
-    if args.workload in ("cfg1", "cfg3", "cfg4") and (
-            _rank_env()[1] > 1 or os.environ.get("VQB_BENCH_SHARDED") == "1"):  # (the latter: test hook, 1 rank)
+    design = getattr(args, "design", False) or args.workload in ("cfg1", "cfg3")
+    if design and (_rank_env()[1] > 1 or os.environ.get("VQB_BENCH_SHARDED") == "1"):  # (the latter: test hook)
         return run_workload_sharded(args)
-    if args.workload != "cfg2":
+    if design or args.workload == "cfg5":
         return run_workload(args)
     return run_b200(args)
 

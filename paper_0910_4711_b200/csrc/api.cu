@@ -165,6 +165,7 @@ struct vqb_session {
     a.x32 = x32;
     a.x64 = x64;
     a.n = n;
+    a.n_global = n_global;
     a.r0 = 0;
     a.r1 = n;
     a.dim = (int)dim;

@@ -58,8 +58,7 @@ __device__ __forceinline__ void store_dist(const KernelArgs& a, long long row, d
 // the remainder in units of 2^-t, both carrying x's sign.  Pure integer work
 // on the IEEE fields; exact whenever x has no set bit below 2^-(s + t) (the
 // column's colstats decide that before any pass runs).
-__device__ __forceinline__ void split_fixed(float x, int s, int t, long long& hi, long long& lo) {
-  const unsigned u = __float_as_uint(x);
+__device__ __forceinline__ void split_fixed_slow(unsigned u, int s, int t, long long& hi, long long& lo) {
   const unsigned E = (u >> 23) & 0xffu;
   unsigned long long m = u & 0x7fffffu;
   int e0 = -149;
@@ -86,6 +85,40 @@ __device__ __forceinline__ void split_fixed(float x, int s, int t, long long& hi
   }
   hi = h;
   lo = l;
+}
+// the common case of split_fixed for float32: zero, or a normal value that is
+// an integer multiple of the column's grid 2^-s (no low word); false = take
+// the general split
+__device__ __forceinline__ bool split_fast(float x, int s, long long& h) {
+  const unsigned u = __float_as_uint(x);
+  const int E = (int)((u >> 23) & 0xffu);
+  const int k = E - 150 + s;
+  const long long v = (long long)((u & 0x7fffffu) | 0x800000u) << (k & 63);
+  const bool zero = (u << 1) == 0;
+  h = zero ? 0 : ((int)u < 0 ? -v : v);
+  return zero || (E != 0 && k >= 0);
+}
+__device__ __forceinline__ bool split_fast(double x, int s, long long& h) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  const int E = (int)((u >> 52) & 0x7ffu);
+  const int k = E - 1075 + s;
+  const long long v = (long long)((u & 0xfffffffffffffull) | (1ull << 52)) << (k & 63);
+  const bool zero = (u << 1) == 0;
+  h = zero ? 0 : ((long long)u < 0 ? -v : v);
+  return zero || (E != 0 && k >= 0);
+}
+__device__ __forceinline__ void split_fixed(float x, int s, int t, long long& hi, long long& lo) {
+  const unsigned u = __float_as_uint(x);
+  const int k = (int)((u >> 23) & 0xffu) - 150 + s;
+  if (((u >> 23) & 0xffu) != 0 && k >= 0) {
+    // the usual case: a normal float32 that is an integer multiple of the
+    // column's grid 2^-s (k < 61 - 23 by the choice of s): no low word
+    const long long h = (long long)((u & 0x7fffffu) | 0x800000u) << k;
+    hi = (u >> 31) ? -h : h;
+    lo = 0;
+    return;
+  }
+  split_fixed_slow(u, s, t, hi, lo);
 }
 __device__ __forceinline__ void split_fixed(double x, int s, int t, long long& hi, long long& lo) {
   const unsigned long long u = (unsigned long long)__double_as_longlong(x);
@@ -218,6 +251,12 @@ bool pdl_enabled() {
 }
 
 bool fast_dim_supported(int dim) { return dim == 16 || dim == 32 || dim == 64; }
+
+// integer environment switch (A/B timing), read once per name
+static int getenv_flag(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 template <int L, int TK>
 struct TileStream {
@@ -1083,11 +1122,16 @@ __device__ __forceinline__ void smem_add_i64(unsigned* lo_word, int* hi_word, lo
 // (_kernels.py:92-98).
 // Zero the low words of the exchange buffer for cells [0, K) before this
 // pass's cell sums add into them (the previous pass's apply has read them).
+// The limb-RED cell sums below add straight into the exchange buffer's high
+// words and counts, so those are cleared here too for cells [0, K).
 __device__ __forceinline__ void zero_lo_words(const KernelArgs& a, int K) {
   const long long words = (long long)K * a.dim;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
-       i += (long long)gridDim.x * blockDim.x)
+       i += (long long)gridDim.x * blockDim.x) {
     a.ex.lo()[i] = 0;
+    a.ex.sums()[i] = 0;
+    if (i < K) a.ex.counts()[i] = 0;
+  }
 }
 
 __global__ void zero_lo_kernel(KernelArgs a, int zero_cells) {
@@ -1214,12 +1258,8 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
     for (int c0 = d_lo; c0 < d_hi; c0 += 16) {
       const int cw = d_hi - c0 < 16 ? d_hi - c0 : 16;
       long long acc[16];
-      int shl[16];
 #pragma unroll
-      for (int l = 0; l < 16; ++l) {
-        acc[l] = 0;
-        shl[l] = l < cw ? __ldg(a.cshift + c0 + l) : 0;
-      }
+      for (int l = 0; l < 16; ++l) acc[l] = 0;
       int cur = -1;
       unsigned run = 0;
       auto flush = [&]() {
@@ -1251,7 +1291,7 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
           for (int l = 0; l < 16; ++l)
             if (l < cw) {
               long long h, lo;
-              split_fixed(xr[l], shl[l], t_lo, h, lo);
+              split_fixed(xr[l], __ldg(a.cshift + c0 + l), t_lo, h, lo);  // uniform: an L1 broadcast
               acc[l] += h;
               add_lo(a, cell, c0 + l, lo);
             }
@@ -1376,6 +1416,206 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cell sums for larger codebooks without returning atomics ("limb REDs").
+//
+// A coordinate's high word h (|h| < 2^(t-1), t = lo_shift = 62 - e_n) is
+// biased to u = h + 2^(t-1) in [0, 2^t) and cut into m limbs of w bits; each
+// limb is added to a 32-bit shared-memory counter with a NON-returning RED
+// (one ATOMS.ADD, no carry to wait for).  A counter absorbs 2^(32-w) adds, and
+// w is chosen so that exceeds the rows one CTA visits, so no limb can wrap.
+// At the end the CTA recombines sum_j limb_j 2^(w j) - count * 2^(t-1) --
+// exactly its share of the cell sum -- and adds it into the exchange buffer
+// with one 64-bit global atomic per (cell, dim) (integer adds commute: the
+// result does not depend on the order).  Codebooks too large for a table of
+// all dims are split into dimension pieces (blockIdx.x % pieces, adjacent in
+// launch order so the pieces of one row chunk share its rows through L2).
+// ---------------------------------------------------------------------------
+struct LimbPlan {
+  int m, w;         // limbs per coordinate, bits per limb
+  int lp, pieces;   // dims per piece (template LP), pieces
+  int chunks;       // row chunks
+  long long rows;   // rows per chunk
+};
+__host__ __device__ inline LimbPlan limb_plan(long long n, int K, int dim, int lo_shift, int sms) {
+  LimbPlan p{};
+  const int t = lo_shift;
+  // dims per piece: the widest of 32 / 16 / 8 / 4 whose table fits
+  const long long budget = kEpiSmem - 1024;
+  int lp = 32;
+  while (lp > 4 && (long long)K * (lp * 4 * 3 + 4) > budget) lp >>= 1;
+  if (lp > 16 && dim <= 16) lp = 16;
+  p.lp = lp;
+  p.pieces = (dim + lp - 1) / lp;
+  p.chunks = sms / p.pieces > 0 ? sms / p.pieces : 1;
+  if ((long long)p.chunks * 4096 > n) p.chunks = (int)((n + 4095) / 4096) > 0 ? (int)((n + 4095) / 4096) : 1;
+  p.rows = (n + p.chunks - 1) / p.chunks;
+  int hb = 0;
+  while (hb < 40 && (1LL << hb) <= p.rows) ++hb;  // rows < 2^hb
+  p.w = 32 - hb;                                     // 2^(32-w) = 2^hb > rows
+  if (p.w > 31) p.w = 31;
+  p.m = p.w > 0 ? (t + p.w - 1) / p.w : 99;
+  return p;
+}
+__host__ __device__ inline bool limb_ok(const LimbPlan& p, int K) {
+  return p.w >= 8 && p.m <= 4 && (long long)K * (p.lp * 4 * p.m + 4) <= kEpiSmem - 1024;
+}
+
+// 4 consecutive coordinates of a row (one 16-byte load for float rows)
+template <typename XT>
+__device__ __forceinline__ void load4(const XT* __restrict__ p, int valid, bool vec, XT (&v)[4]) {
+  if (valid == 4 && vec) {
+    if constexpr (sizeof(XT) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 q0 = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 q1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y;
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) v[g] = g < valid ? __ldg(p + g) : (XT)0;
+  }
+}
+
+template <typename XT, int LP, int M>
+__global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT* __restrict__ X, int zero_cells,
+                                                          LimbPlan pl) {
+  pdl_wait();
+  const DevState* st = a.st;
+  if (st->done) return;
+  const int K = zero_cells ? 1 : st->size;
+  const int dim = a.dim;
+  const int t = st->lo_shift;  // == fixed_lo_shift(n_global), what the plan was made for
+  constexpr int m = M;
+  const int w = pl.w;
+  const int piece = blockIdx.x % pl.pieces;
+  const long long chunk = blockIdx.x / pl.pieces;
+  const int d0 = piece * LP;
+  constexpr int TPR = LP / 4;  // threads per row: 4 coordinates each
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned* tab = reinterpret_cast<unsigned*>(smem_raw);     // [K][LP][m]
+  unsigned* cnt = tab + (long long)K * LP * m;                // [K]
+  const long long twords = (long long)K * (LP * m + 1);
+  for (long long i = threadIdx.x; i < twords; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  const long long r0 = chunk * pl.rows;
+  const long long r1 = r0 + pl.rows < a.n ? r0 + pl.rows : a.n;
+  const int g0 = (threadIdx.x % TPR) * 4;  // first of this thread's 4 dims within the piece
+  const int d = d0 + g0;
+  const int valid = dim - d >= 4 ? 4 : (dim - d > 0 ? dim - d : 0);
+  const bool vec = (dim & 3) == 0;  // 16-byte aligned row slices
+  int sh[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) sh[g] = g < valid ? __ldg(a.cshift + d + g) : 0;
+  const long long bias = 1LL << (t - 1);
+  const unsigned long long mask = (1ull << w) - 1;
+  const int rstep = blockDim.x / TPR;
+  constexpr int U = sizeof(XT) == 4 ? 8 : 4;  // rows per thread per batch; the next batch is in flight meanwhile
+  // dims past `dim` load as 0 and add into table entries the flush skips
+  XT xv[U][4];
+  int cv[U];
+  auto fetch = [&](long long rb) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long row = rb + (long long)u * rstep;
+      const bool ok = row < r1;
+      cv[u] = ok ? (zero_cells ? 0 : __ldg(a.idx + row)) : -1;
+      load4<XT>(X + row * dim + d, ok ? valid : 0, vec, xv[u]);
+    }
+  };
+  long long rb = r0 + threadIdx.x / TPR;
+  if (rb < r1) fetch(rb);
+  while (rb < r1) {
+    XT cx[U][4];
+    int cc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cc[u] = cv[u];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) cx[u][g] = xv[u][g];
+    }
+    const long long nb = rb + (long long)rstep * U;
+    if (nb < r1) fetch(nb);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = cc[u];
+      if (c < 0) continue;
+      if (g0 == 0) atomicAdd(cnt + c, 1u);
+      unsigned* e = tab + (unsigned)c * (unsigned)(LP * M) + (unsigned)(g0 * M);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        long long h;
+        if (!split_fast(cx[u][g], sh[g], h)) {  // rare for float32 rows: bits below the grid
+          long long lo;
+          split_fixed(cx[u][g], sh[g], t, h, lo);
+          add_lo(a, c, d + g, lo);
+        }
+        const unsigned long long uv = (unsigned long long)(h + bias);
+#pragma unroll
+        for (int j = 0; j < M; ++j) atomicAdd(e + g * M + j, (unsigned)((uv >> (w * j)) & mask));
+      }
+    }
+    rb = nb;
+  }
+  __syncthreads();
+  // this chunk's share of the sums into its slab (reduce_partials_kernel adds
+  // the slabs in a fixed order; every word of cells < K is written)
+  long long* slab = a.partials + chunk * ((long long)a.kmax * dim + a.kmax);
+  for (long long i = threadIdx.x; i < (long long)K * LP; i += blockDim.x) {
+    const long long c = i / LP;
+    const int ll = (int)(i % LP);
+    if (d0 + ll >= dim) continue;
+    const unsigned* e = tab + i * m;
+    long long v = 0;
+    for (int j = 0; j < m; ++j) v += (long long)e[j] << (w * j);
+    slab[c * dim + d0 + ll] = v - (long long)cnt[c] * bias;
+  }
+  if (piece == 0)
+    for (long long c = threadIdx.x; c < K; c += blockDim.x) slab[(long long)K * dim + c] = cnt[c];
+}
+
+// Launch the limb-RED sums when the plan fits (K large enough that the
+// warp-private tables are out, small enough that a table of >= 4 dims fits);
+// *used tells the caller whether the slab reduction is still needed.
+template <typename XT, int LP, int M>
+static cudaError_t launch_red_lpm(const KernelArgs& a, const XT* X, const LimbPlan& pl, bool zero_cells,
+                                  cudaStream_t s) {
+  const size_t smem = (size_t)a.kmax * (LP * M + 1) * 4;
+  cudaError_t e = cudaFuncSetAttribute(sums_red_kernel<XT, LP, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_k(sums_red_kernel<XT, LP, M>, (unsigned)(pl.chunks * pl.pieces), 512, smem, s, a, X,
+                  zero_cells ? 1 : 0, pl);
+}
+template <typename XT, int LP>
+static cudaError_t launch_red_lp(const KernelArgs& a, const XT* X, const LimbPlan& pl, bool zero_cells,
+                                 cudaStream_t s) {
+  switch (pl.m) {
+    case 2: return launch_red_lpm<XT, LP, 2>(a, X, pl, zero_cells, s);
+    case 3: return launch_red_lpm<XT, LP, 3>(a, X, pl, zero_cells, s);
+    default: return launch_red_lpm<XT, LP, 4>(a, X, pl, zero_cells, s);
+  }
+}
+
+template <typename XT>
+static cudaError_t launch_sums_red(const KernelArgs& a, const XT* X, bool zero_cells, int sms, cudaStream_t s,
+                                   bool* used, int* chunks) {
+  *used = false;
+  if (zero_cells) return cudaSuccess;
+  const LimbPlan pl = limb_plan(a.n, (int)a.kmax, a.dim, fixed_lo_shift(a.n_global), sms);
+  if (!limb_ok(pl, (int)a.kmax)) return cudaSuccess;
+  *used = true;
+  *chunks = pl.chunks;
+  switch (pl.lp) {
+    case 32: return launch_red_lp<XT, 32>(a, X, pl, zero_cells, s);
+    case 16: return launch_red_lp<XT, 16>(a, X, pl, zero_cells, s);
+    case 8: return launch_red_lp<XT, 8>(a, X, pl, zero_cells, s);
+    default: return launch_red_lp<XT, 4>(a, X, pl, zero_cells, s);
+  }
+}
+
 // sum the per-block slabs into the exchange buffer: 32 words x 8 slab groups
 // per 256-thread block, int64 (any order is exact)
 __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int nblocks, int zero_cells) {
@@ -1434,6 +1674,19 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   if (!want_sums) return cudaSuccess;
   const long long kmax = zero_cells ? 1 : a.kmax;
   constexpr int kSumThreads = sum_threads<DIM>();
+  const long long words = kmax * a.dim + kmax;
+  int rb = (int)((words + 31) / 32);
+  if (rb > 8192) rb = 8192;
+  const SumsPlan plan0 = sums_plan((int)kmax, a.dim, kSumThreads);
+  const int red_mode = getenv_flag("VQB_SUMS_RED", 1);  // 0 never, 1 always, 2 where the block table splits
+  if (!sums_warp_sink((int)kmax, a.dim, kSumThreads) &&
+      (red_mode == 1 || (red_mode == 2 && plan0.nkc * plan0.ndc > 1))) {
+    bool used = false;
+    int chunks = 0;
+    e = launch_sums_red<XT>(a, X, zero_cells, sms, s, &used, &chunks);
+    if (e != cudaSuccess) return e;
+    if (used) return launch_k(reduce_partials_kernel, rb, 256, 0, s, a, chunks, zero_cells ? 1 : 0);
+  }
   const SumsPlan plan = sums_plan((int)kmax, a.dim, kSumThreads);
   const int chunks = (int)(plan.nkc * plan.ndc);
   const long long rows_per_block = 4LL * kSumThreads;
@@ -1446,9 +1699,6 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const long long words = kmax * a.dim + kmax;
-  int rb = (int)((words + 31) / 32);
-  if (rb > 8192) rb = 8192;
   e = launch_k(reduce_partials_kernel, rb, 256, 0, s, a, blocks, zero_cells ? 1 : 0);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

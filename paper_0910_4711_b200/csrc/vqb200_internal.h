@@ -145,6 +145,7 @@ struct KernelArgs {
   const float* x32;
   const double* x64;
   long long n;          // local rows
+  long long n_global;   // rows over all shards (fixed-point plan)
   long long r0, r1;     // row range of the candidate pass (a chunk of [0, n))
   int dim;
   long long tile0;      // global index of this shard's first TD tile
