@@ -644,6 +644,105 @@ def run_workload_sharded(args):
     return 0
 
 
+def run_encode(args):
+    """cfg5 (BASELINE configs[4]): encode 2^26 queries against the fixed
+    K=1024 codebook, sharded over N GPUs (torchrun, one process per GPU):
+    every rank holds a contiguous tile-aligned shard of the same query set;
+    value = N * K / the slowest rank's device-resident allocation pass
+    (candidate pass + re-rank + exact distances + distortion; CUDA events).
+    e2e = distributed.sharded_encode / codec.encode from host numpy (H2D,
+    encode, D2H, index all-gather), the public call."""
+    import hashlib
+
+    import torch
+
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200 import _lib, synthetic
+    from paper_0910_4711_b200 import distributed as D
+    from paper_0910_4711_b200.core import _Session
+
+    rank, world, local_rank = _rank_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    L = _lib.lib()
+    cb32, q = synthetic.make_encode_case()
+    cb = cb32.astype(np.float64)
+    n, K = q.shape[0], cb.shape[0]
+    plan = D.ShardPlan(n, world)
+    lo, hi = plan.bounds(rank)
+    g = _workload_golden("cfg5")
+    clocks = ClockSampler(local_rank).__enter__()
+    sess = _Session(np.ascontiguousarray(q[lo:hi]), None, device=local_rank, row_offset=lo, n_global=n)
+    ms, total, fl = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    _lib.check(L.vqb_bench_assign(sess.handle, _lib.ptr(cb), K, max(1, args.warmup),
+                                  ctypes.byref(ms), ctypes.byref(total), ctypes.byref(fl)))
+    if world > 1:
+        dist.barrier()
+    _lib.check(L.vqb_bench_assign(sess.handle, _lib.ptr(cb), K, args.steps,
+                                  ctypes.byref(ms), ctypes.byref(total), ctypes.byref(fl)))
+    dev_ms = ms.value
+    local_idx = sess.assign_u32(cb)
+    sess.close()
+    del sess
+    torch.cuda.empty_cache()
+    t = torch.tensor([dev_ms, total.value, float(fl.value)], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if world > 1:
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dev_ms, tot, flagged = float(tm[0]), float(t[1]), int(t[2])
+    else:
+        tot, flagged = total.value, int(fl.value)
+    # e2e through the public call (every rank: its shard H2D + encode + the gather)
+    e2e_runs = []
+    stream = None
+    for _ in range(2):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        stream = vq.encode(q, vq.Codebook(cb))
+        t1 = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local_rank}")
+        if world > 1:
+            dist.all_reduce(t1, op=dist.ReduceOp.MAX)
+        e2e_runs.append(float(t1.item()))
+    e2e_s = min(e2e_runs)
+    clocks.__exit__(None, None, None)
+    if rank == 0:
+        c = clocks.summary()
+        parity = None
+        if g is not None:
+            want = g["idx_sha256"].item().decode()
+            parity = {
+                "encode_api_sha256_match": hashlib.sha256(stream.indices.tobytes()).hexdigest() == want,
+                "shard0_head_match": bool(np.array_equal(local_idx[:65536], g["head"][: min(65536, hi - lo)])),
+                "total_rel_err": abs(tot - float(g["total"])) / float(g["total"]),
+                "reference_encode_s": float(g["seconds"]), "reference_workers": int(g["workers"]),
+            }
+        print(json.dumps({
+            "metric": "G vector·codeword distance evals/s (encode pass)", "impl": "b200",
+            "value": n * K / (dev_ms * 1e-3) / 1e9, "unit": "G evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": "cfg5: encode N=2^26 L=16 K=1024 (fixed seeded codebook)",
+                       "rows": n, "codebook": K, "dim": 16,
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "sharding": "contiguous tile-aligned query shards, indices all-gathered"},
+            "rerank_rows_per_step": flagged,
+            "e2e": {"value": n * K / e2e_s / 1e9, "unit": "G evals/s", "seconds": e2e_s,
+                    "api": "codec.encode (distributed.sharded_encode under torchrun)",
+                    "h2d_bytes_per_step": int(q.nbytes + cb.nbytes), "d2h_bytes_per_step": int(n * 4)},
+            "parity": parity,
+            "clocks": {k: c[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+        }), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def run_workload(args):
     """One BASELINE config end to end on one GPU (parity-checked against the
     reference's committed outputs where they exist):
@@ -916,7 +1015,9 @@ def main():
     design = getattr(args, "design", False) or args.workload in ("cfg1", "cfg3")
     if design and (_rank_env()[1] > 1 or os.environ.get("VQB_BENCH_SHARDED") == "1"):  # (the latter: test hook)
         return run_workload_sharded(args)
-    if design or args.workload == "cfg5":
+    if args.workload == "cfg5":
+        return run_encode(args)
+    if design:
         return run_workload(args)
     return run_b200(args)
 

@@ -299,22 +299,103 @@ def _sharded_lloyd(backend, codebook: np.ndarray, passes: int, collective: bool,
     return backend.lloyd_result()
 
 
-def gather_rows(local: np.ndarray, plan: ShardPlan, device: str | None):
-    """All-gather this rank's per-row values into the global order."""
+def _local_device() -> int:
+    """This rank's GPU: LOCAL_RANK when torchrun set it, else torch's current
+    device (a caller that never called set_device still gets its own GPU)."""
+    import os
+
+    import torch
+
+    lr = os.environ.get("LOCAL_RANK")
+    dev = int(lr) if lr is not None else torch.cuda.current_device()
+    torch.cuda.set_device(dev)
+    return dev
+
+
+def sharded_per_worker(dists: np.ndarray, plan: ShardPlan, rank: int, workers: int,
+                       device: str | None) -> list[float]:
+    """DistortionStats.per_worker (parallel.py:321: sum_inorder of each worker
+    chunk's distances, chunks from partition_training) from sharded per-row
+    distances WITHOUT gathering them: a chunk that spans ranks is summed left
+    to right by relaying its running FP64 sum from rank to rank (one scalar
+    send/recv per shard boundary inside a chunk), so every chunk sum is the
+    reference's exact sequential sum.  One SUM allreduce of the `workers`
+    values (each set by the rank holding the chunk's end) finishes it."""
     import torch
     import torch.distributed as dist
 
-    world = plan.world
-    longest = max(hi - lo for lo, hi in (plan.bounds(r) for r in range(world)))
-    buf = torch.zeros(longest, dtype=torch.float64, device=device)
-    buf[: local.shape[0]] = torch.from_numpy(local).to(device)
+    from .parallel import partition_training
+
+    a, b = plan.bounds(rank)
+    vals = np.zeros(max(1, workers), dtype=np.float64)
+    for w, (lo, hi) in enumerate(partition_training(plan.n, workers).ranges):
+        s_lo, s_hi = max(lo, a), min(hi, b)
+        if s_lo >= s_hi:
+            continue
+        carry = 0.0
+        if lo < a:  # the chunk began on an earlier rank: continue its running sum
+            t = torch.zeros(1, dtype=torch.float64, device=device)
+            dist.recv(t, src=rank - 1)
+            carry = float(t.item())
+        piece = dists[s_lo - a: s_hi - a]
+        # sequential: carry, carry + d0, ... (cumsum accumulates left to right)
+        acc = float(np.cumsum(np.concatenate([[carry], piece]))[-1])
+        if hi > b:
+            dist.send(torch.tensor([acc], dtype=torch.float64, device=device), dst=rank + 1)
+        else:
+            vals[w] = acc
+    t = torch.from_numpy(vals).to(device) if device else torch.from_numpy(vals)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.cpu().numpy()[:workers]]
+
+
+def sharded_encode(rows: np.ndarray, codebook: np.ndarray, want_total: bool = False):
+    """codec.encode (codec.py:62-93) over every rank of the default process
+    group: each rank encodes its contiguous tile-aligned shard of the rows
+    (the reference's chunk fan-out, codec.py:79-87 / parallel.py:93-107, one
+    GPU per chunk), the indices are all-gathered so every rank returns the
+    full uint32 array, and the distortion (when asked for) is one FP64 SUM
+    allreduce.  Every rank passes the same rows."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n, dim = rows.shape
+    plan = ShardPlan(n, world)
+    if plan.tiles < world:
+        plan = ShardPlan(n, 1)  # too few rows to shard: rank 0's answer everywhere
+    lo, hi = plan.bounds(rank) if plan.world > 1 else (0, n)
+    dev = _local_device()
+    gdev = f"cuda:{dev}" if dist.get_backend() == "nccl" else None
+    cb = np.ascontiguousarray(codebook, dtype=np.float64)
+    part = np.ascontiguousarray(rows[lo:hi])
+    idx = np.empty(hi - lo, dtype=np.uint32)
+    total = ctypes.c_double(0.0)
+    if part.dtype == np.float32:
+        _lib.check(_lib.lib().vqb_encode_f32(_lib.ptr(part), part.shape[0], dim, _lib.ptr(cb), cb.shape[0],
+                                             dev, _lib.ptr(idx), ctypes.byref(total) if want_total else None))
+    else:
+        from .core import _Session
+
+        s = _Session(None, np.ascontiguousarray(part, dtype=np.float64), device=dev)
+        _c, _d, tot = s.assign(cb, 0, want_dists=False)
+        idx[:] = _c.astype(np.uint32)
+        total.value = tot
+    if plan.world == 1:
+        return idx, total.value
+    longest = max(b - a for a, b in (plan.bounds(r) for r in range(world)))
+    buf = torch.zeros(longest, dtype=torch.int32, device=gdev)
+    buf[: idx.shape[0]] = torch.from_numpy(idx.view(np.int32)).to(buf.device)
     parts = [torch.zeros_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf)
-    out = np.empty(plan.n, dtype=np.float64)
+    out = np.empty(n, dtype=np.uint32)
     for r in range(world):
-        lo, hi = plan.bounds(r)
-        out[lo:hi] = parts[r][: hi - lo].cpu().numpy()
-    return out
+        a, b = plan.bounds(r)
+        out[a:b] = parts[r][: b - a].cpu().numpy().view(np.uint32)
+    tot = torch.tensor([total.value], dtype=torch.float64, device=gdev)
+    if want_total:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    return out, float(tot.item())
 
 
 def sharded_lbg_train(ts, config, backend_factory=None):
@@ -346,7 +427,7 @@ def sharded_lbg_train(ts, config, backend_factory=None):
     x32 = ts.__dict__.get("_x32")
     rows = (x32 if x32 is not None else ts.vectors)[lo:hi]
     if backend_factory is None:
-        device = torch.cuda.current_device()
+        device = _local_device()
         backend = DeviceShard(np.ascontiguousarray(rows), lo, ts.m, device)
         gdev = f"cuda:{device}"
     else:
@@ -356,10 +437,11 @@ def sharded_lbg_train(ts, config, backend_factory=None):
     if plan.world == 1:  # replica fallback above: no collective
         cb, history, warnings, total, dists = run_sharded(backend, config, collective=False)
         all_dists = dists
+        per_worker = [_inorder(all_dists[a:b]) for a, b in partition_training(ts.m, config.workers).ranges]
     else:
         cb, history, warnings, total, dists = run_sharded(backend, config)
-        all_dists = gather_rows(dists, plan, gdev)
-    per_worker = [_inorder(all_dists[a:b]) for a, b in partition_training(ts.m, config.workers).ranges]
+        per_worker = sharded_per_worker(dists, plan, rank, config.workers,
+                                        gdev if dist.get_backend() == "nccl" else None)
     stats = DistortionStats(per_worker=per_worker, total=total, history=history,
                             warnings=warnings, vector_count=ts.m)
     return Codebook(cb), stats

@@ -393,3 +393,43 @@ def test_sharded_lloyd_world2_matches_world1_and_oracle(tmp_path):
         cb, _ = oracle.update_codebook(x, cells, cb)
     assert np.array_equal(outs[2]["cb"], cb)  # pixel-valued rows: fixed-point sums are exact
     assert abs(float(outs[2]["td"]) - td) <= 1e-12 * td
+
+
+def _per_worker_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_0910_4711_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 5 * TILE + 777
+        d = np.random.default_rng(5).exponential(3.0, n)
+        plan = D.ShardPlan(n, world)
+        lo, hi = plan.bounds(rank)
+        res = {w: D.sharded_per_worker(d[lo:hi], plan, rank, w, None) for w in (1, 2, 3, 7, 16)}
+        if rank == 0:
+            np.savez(out_path, **{str(w): np.array(v) for w, v in res.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_per_worker_relay_is_the_inorder_sum(world, tmp_path):
+    """per_worker from sharded distances without gathering them: chunks that
+    span ranks are summed left to right by relaying the running sum, so
+    every value equals sum_inorder over the chunk (parallel.py:321)."""
+    import torch.multiprocessing as mp
+
+    from paper_0910_4711_b200.parallel import _inorder, partition_training
+
+    out = str(tmp_path / "pw.npz")
+    mp.start_processes(_per_worker_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    r = np.load(out)
+    n = 5 * TILE + 777
+    d = np.random.default_rng(5).exponential(3.0, n)
+    for w in (1, 2, 3, 7, 16):
+        want = [_inorder(d[a:b]) for a, b in partition_training(n, w).ranges]
+        assert r[str(w)].tolist() == want, w

@@ -184,3 +184,56 @@ def test_programmatic_dependent_launch_is_transparent():
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                                    check=True, timeout=600).stdout)
     assert outs[0] == outs[1] and outs[0]
+
+
+def _encode_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    for p in (ROOT, os.path.join(ROOT, "oracle")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    import torch
+    import torch.distributed as dist
+
+    import paper_0910_4711_b200 as vq
+    from paper_0910_4711_b200 import distributed as D
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = _data()
+        rng = np.random.default_rng(77)
+        cb = rng.uniform(0, 255, (1024, 16))
+        stream = vq.encode(x, vq.Codebook(cb))          # the public API shards under a group
+        idx, total = D.sharded_encode(x, cb, want_total=True)
+        x64 = np.ascontiguousarray(x[:40000], dtype=np.float64) + 1e-9  # not float32-exact
+        idx64, _ = D.sharded_encode(x64, cb)
+        if rank == 0:
+            np.savez(out_path, idx=stream.indices, idx2=idx, total=total, idx64=idx64)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_encode_matches_single_device(tmp_path):
+    """cfg5's sharding: every rank encodes its contiguous shard,
+    the indices are all-gathered -- identical to one device and the oracle."""
+    import torch.multiprocessing as mp
+
+    import oracle
+    import paper_0910_4711_b200 as vq
+
+    out = str(tmp_path / "enc2.npz")
+    mp.start_processes(_encode_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    r2 = np.load(out)
+    x = _data()
+    rng = np.random.default_rng(77)
+    cb = rng.uniform(0, 255, (1024, 16))
+    one = vq.encode(x, vq.Codebook(cb)).indices
+    assert r2["idx"].dtype == np.uint32 and np.array_equal(r2["idx"], one)
+    assert np.array_equal(r2["idx2"], one)
+    cells, dists = oracle.assign_all(x.astype(np.float64), cb, workers=oracle.max_threads())
+    assert np.array_equal(one, cells.astype(np.uint32))
+    assert abs(float(r2["total"]) - float(np.sum(dists))) <= 1e-12 * float(np.sum(dists))
+    x64 = np.ascontiguousarray(x[:40000], dtype=np.float64) + 1e-9
+    c64, _ = oracle.assign_all(x64, cb)
+    assert np.array_equal(r2["idx64"], c64.astype(np.uint32))
