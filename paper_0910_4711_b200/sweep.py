@@ -82,8 +82,12 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, backend, data_path, cells, repeats, out_path, factory_spec):
-    """One rank of a P > 1 sweep column (spawned; one process per GPU)."""
+def _rank_main(rank, world, port, backend, data_path, cells, repeats, out_path, factory_spec, devices=0):
+    """One rank of a P > 1 sweep column (spawned; one process per GPU, or --
+    with fewer GPUs than ranks -- ranks sharing the visible GPUs over gloo,
+    whose host-mediated collectives never make one rank's kernel wait on
+    another's: the protocol and the results are the same, the times are not
+    a scaling measurement)."""
     import importlib
 
     import torch
@@ -98,9 +102,10 @@ def _rank_main(rank, world, port, backend, data_path, cells, repeats, out_path, 
     if factory_spec:
         mod, attr = factory_spec.split(":")
         factory = getattr(importlib.import_module(mod), attr)
-    cuda = backend == "nccl"
+    cuda = backend == "nccl" or devices > 0
     if cuda:
-        torch.cuda.set_device(rank)
+        os.environ["LOCAL_RANK"] = str(rank % max(1, devices) if devices else rank)
+        torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     ts = TrainingSet(np.load(data_path))
 
     def sync():
@@ -149,12 +154,17 @@ def run_sweep(ts: TrainingSet, sizes=DEFAULT_SIZES, gpu_counts=(1,), repeats: in
     for p in gpu_counts:
         if p < 1:
             raise UsageError(f"GPU count must be >= 1, got {p}")
+    devices = 0
     if backend == "nccl":
         import torch
 
         have = torch.cuda.device_count()
+        if have < 1:
+            raise UsageError("the sweep needs a CUDA device")
         if max(gpu_counts) > have:
-            raise UsageError(f"sweep asks for {max(gpu_counts)} GPUs, {have} visible")
+            # more ranks than GPUs: ranks share the GPUs over gloo (the
+            # reference's thread counts stay meaningful as a protocol check)
+            backend, devices = "gloo", have
     from .parallel import parallel_lbg_train
 
     cells = {}
@@ -182,7 +192,7 @@ def run_sweep(ts: TrainingSet, sizes=DEFAULT_SIZES, gpu_counts=(1,), repeats: in
                 np.save(data_path, x32 if x32 is not None else ts.vectors)
                 out_path = os.path.join(tmp, "out.json")
                 mp.spawn(_rank_main, args=(gpus, _free_port(), backend, data_path, kws, repeats,
-                                           out_path, backend_factory),
+                                           out_path, backend_factory, devices),
                          nprocs=gpus, join=True, start_method="spawn")
                 with open(out_path) as f:
                     out = json.load(f)
