@@ -106,6 +106,11 @@ int vqb_local_maxabs(vqb_session* s, double* out);
  * global stats that fix the two-word fixed-point plan of the cell sums
  * (vqb_train_config.global_colmax / global_collow). */
 int vqb_local_colstats(vqb_session* s, double* colmax, int32_t* collow);
+/* info[5] = {candidate pass on (FP32 / tensor-core fast path), candidate
+ * width (16/32/64, rows zero-padded; 0: L > 64, FP64 scan only), rows held as
+ * float64 (not float32-exact), cell sums exact on the two-word grid, the
+ * reference's own FP64 cell sums provably exact}. */
+int vqb_session_info(vqb_session* s, int32_t* info);
 
 typedef struct {
   int64_t target_size;               /* LbgConfig.target_size (power of two) */

@@ -92,6 +92,7 @@ def lib():
             "vqb_set_stream": ([_P, _P], _I32),
             "vqb_local_maxabs": ([_P, _P], _I32),
             "vqb_local_colstats": ([_P, _P, _P], _I32),
+            "vqb_session_info": ([_P, _P], _I32),
             "vqb_step_history": ([_P, _P, _I64, _P], _I32),
             "vqb_train": ([_P, _P, _P, _P, _I64, _P, _I64, _P, _P], _I32),
             "vqb_assign": ([_P, _P, _I64, _I32, _P, _P, _P, _P], _I32),

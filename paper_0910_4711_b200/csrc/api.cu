@@ -66,6 +66,11 @@ struct vqb_session {
   long long n = 0, dim = 0, row_offset = 0, n_global = 0;
   float* x32 = nullptr;
   double* x64 = nullptr;
+  // candidate rows of the FP32 / TC passes (KernelArgs::xc): fl32 + zero pad
+  // to cdim (== x32 when the rows are float32 of a candidate width)
+  float* xc_own = nullptr;
+  float* rin = nullptr;  // float64 rows: per-row rounding bound
+  int cdim = 0;          // 16 / 32 / 64, or 0: no candidate pass
   float* mu = nullptr;
   std::vector<float> mu_host;  // host copy of the centring vector
   double maxabs = -1.0;
@@ -164,6 +169,9 @@ struct vqb_session {
     KernelArgs a{};
     a.x32 = x32;
     a.x64 = x64;
+    a.cdim = cdim ? cdim : (int)dim;
+    a.xc = xc_own ? xc_own : (cdim == dim ? x32 : nullptr);
+    a.rin = rin;
     a.n = n;
     a.n_global = n_global;
     a.r0 = 0;
@@ -220,13 +228,14 @@ struct vqb_session {
     const long long kpad = (k + 3) / 4 * 4;
     CK(dalloc(&cb[0], (size_t)(k * dim)));
     CK(dalloc(&cb[1], (size_t)(k * dim)));
-    CK(dalloc(&w, (size_t)(kpad * dim + 64)));
+    const long long wd = cdim > dim ? cdim : dim;
+    CK(dalloc(&w, (size_t)(kpad * wd + 64)));
     CK(dalloc(&nrm, (size_t)(kpad + 64)));
     CK(dalloc(&ex, (size_t)(2 * k * dim + k + ntiles_global)));  // Exchange::words()
     CK(dalloc(&partials, (size_t)sms * (size_t)(k * dim + k)));
     CK(dalloc(&ord, (size_t)(k * dim)));
-    if (fast_dim_supported((int)dim))
-      CK(dalloc(&tcb, (size_t)(((k + kTcChunk - 1) / kTcChunk) * tc_chunk_elems((int)dim))));
+    if (fast_dim_supported(cdim))
+      CK(dalloc(&tcb, (size_t)(((k + kTcChunk - 1) / kTcChunk) * tc_chunk_elems(cdim))));
     CK(cudaMemsetAsync(ex, 0, sizeof(long long) * (2 * k * dim + k + ntiles_global), stream));
     return VQB_OK;
   }
@@ -236,6 +245,8 @@ struct vqb_session {
     if (stream) cudaStreamSynchronize(stream);
     cudaFree(x32);
     cudaFree(x64);
+    cudaFree(xc_own);
+    cudaFree(rin);
     cudaFree(mu);
     cudaFree(cb[0]);
     cudaFree(cb[1]);
@@ -287,7 +298,8 @@ struct vqb_session {
     CK(dalloc(&flags2, (size_t)n + 32));
     CK(dalloc(&dists, (size_t)n + 32));
     CK(dalloc(&st, 1));
-    CK(dalloc(&mu, (size_t)dim + 4));
+    CK(dalloc(&mu, (size_t)dim + 68));  // zero-padded up to the candidate width
+    CK(cudaMemset(mu, 0, sizeof(float) * (dim + 68)));
     CK(dalloc(&cmax, (size_t)dim));
     CK(dalloc(&clow, (size_t)dim));
     CK(dalloc(&cshift, (size_t)dim));
@@ -555,7 +567,17 @@ static int finish_open(std::unique_ptr<vqb_session>& s, vqb_session** out) {
     CK(cudaMemcpy(s->mu, mu.data(), dim * sizeof(float), cudaMemcpyHostToDevice));
     s->mu_host = mu;
   }
-  s->fast = s->x32 != nullptr && fast_dim_supported((int)dim) && s->maxabs < 1099511627776.0;
+  // candidate rows: the FP32 / tensor-core pass runs for every L <= 64 (rows
+  // zero-padded to 16 / 32 / 64) and for float64 rows (rounded to float32,
+  // the rounding bounded per row and added to the certified band)
+  s->cdim = candidate_dim((int)dim);
+  if (s->cdim && (s->x64 || s->cdim != dim)) {
+    CK(dalloc(&s->xc_own, (size_t)rows * s->cdim + 16));
+    if (s->x64) CK(dalloc(&s->rin, (size_t)rows + 16));
+    CK(launch_candidate_rows(s->x32, s->x64, rows, (int)dim, s->cdim, s->xc_own, s->rin, s->sms, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  s->fast = s->cdim != 0 && s->maxabs < 1099511627776.0;
   s->rows_resident = true;
   *out = s.release();
   return VQB_OK;
@@ -592,6 +614,17 @@ int vqb_local_maxabs(vqb_session* s, double* out) {
   if (!s) return fail(VQB_USAGE, "null session");
   std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   *out = s->maxabs;
+  return VQB_OK;
+}
+
+int vqb_session_info(vqb_session* s, int32_t* info) {
+  if (!s) return fail(VQB_USAGE, "null session");
+  std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
+  info[0] = s->fast ? 1 : 0;
+  info[1] = s->cdim;
+  info[2] = s->x64 ? 1 : 0;
+  info[3] = s->sums_exact ? 1 : 0;
+  info[4] = s->ref_exact ? 1 : 0;
   return VQB_OK;
 }
 
@@ -681,7 +714,7 @@ static void tc_configure(const vqb_session* s, DevState* h, double my, double mw
   h->tc_ew = ew;
   h->tc_kn = kn;
   h->tc_kmin = 64;
-  h->tc_kmax = (int)std::min<long long>(tc_max_size((int)s->dim), s->kmax);
+  h->tc_kmax = (int)std::min<long long>(tc_max_size(s->cdim), s->kmax);
   h->tc_on = h->tc_kmax >= h->tc_kmin ? 1 : 0;
 }
 
@@ -692,17 +725,18 @@ static int build_row_image(vqb_session* s, const DevState* h) {
     const char* e = std::getenv("VQB_TC_IMG");  // 0: always convert in-kernel (A/B timing)
     return e && e[0] == '0';
   }();
-  if (off || !s->rows_resident || !s->x32 || !h->tc_on) return VQB_OK;
+  const float* xc = s->args().xc;
+  if (off || !s->rows_resident || !xc || !h->tc_on) return VQB_OK;
   if (s->aimg && s->aimg_ey == h->tc_ey) return VQB_OK;
   if (!s->aimg) {
-    const long long elems = tc_row_image_elems(s->n, (int)s->dim);
+    const long long elems = tc_row_image_elems(s->n, s->cdim);
     const long long qn = (s->n + kTcRows - 1) / kTcRows * kTcRows;
     CK(dalloc(&s->aimg, (size_t)elems));
     CK(dalloc(&s->aq, (size_t)qn));
     CK(cudaMemsetAsync(s->aimg, 0, sizeof(unsigned short) * elems, s->stream));
     CK(cudaMemsetAsync(s->aq, 0, sizeof(float) * qn, s->stream));
   }
-  CK(launch_build_row_image(s->x32, s->mu, s->n, (int)s->dim, h->tc_ey, s->aimg, s->aq, s->sms, s->stream));
+  CK(launch_build_row_image(xc, s->mu, s->n, s->cdim, h->tc_ey, s->aimg, s->aq, s->sms, s->stream));
   s->aimg_ey = h->tc_ey;
   return VQB_OK;
 }
@@ -1243,6 +1277,7 @@ int cached_session(long long n, long long dim, int device, vqb_session** out) {
   CK(cudaMemset(s->mu, 0, sizeof(float) * dim));
   s->mu_host.assign((size_t)dim, 0.f);
   s->fast = fast_dim_supported((int)dim);
+  s->cdim = s->fast ? (int)dim : 0;
   g_cache.s = s.release();
   g_cache.n = n;
   g_cache.dim = dim;
@@ -1485,6 +1520,7 @@ int vqb_encode_f32(const float* x, int64_t n, int64_t dim, const double* codeboo
     if (int rc = s->alloc_common()) return rc;
     s->maxabs = 0;
     s->fast = fast_dim_supported((int)dim);
+    s->cdim = s->fast ? (int)dim : 0;
     int rc = set_centre_from_codebook(s, codebook, size);
     if (rc) return rc;
     rc = upload_codebook(s, codebook, size);
@@ -1633,9 +1669,9 @@ int vqb_debug_tc_tile(vqb_session* s, const double* codebook, int64_t size, floa
                       int32_t* scales) {
   if (!s) return fail(VQB_USAGE, "null session");
   std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
-  if (size % kTcChunk != 0 || size > tc_max_size((int)s->dim))
+  if (size % kTcChunk != 0 || size > tc_max_size(s->cdim))
     return fail(VQB_USAGE, "probe needs a codebook size that is a multiple of %d and <= %d", kTcChunk,
-                tc_max_size((int)s->dim));
+                tc_max_size(s->cdim));
   CK(cudaSetDevice(s->device));
   int rc = upload_codebook(s, codebook, size);
   if (rc) return rc;

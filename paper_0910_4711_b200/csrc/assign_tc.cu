@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       // L1 while the tile's results are still being computed (with the
       // prebuilt row image nothing else brought them on chip)
       const long long e0 = ((long long)blockIdx.x + i * gridDim.x) * kTcRows + r;
-      if (L >= 32 && e0 < nitems && MODE == kTcTop2) {  // (at L = 16 no gain measured)
+      if (L >= 32 && e0 < nitems && MODE == kTcTop2 && a.x32 && a.dim == L) {  // (at L = 16 no gain measured)
         const char* xr = reinterpret_cast<const char*>(a.x32 + (a.r0 + e0) * L);
 #pragma unroll
         for (int off = 0; off < L * 4; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xr + off));
@@ -412,7 +412,10 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
 #pragma unroll
     for (int p = 1; p < C::kParts; ++p) M1 = fminf(M1, pm[p]);
     const float E = tc_band<L>(M1 * inv, qcur, sqrtf(fmaxf(qcur, 0.f)), eyw);
-    const float thr_s = fmaf(3.0f * E, dscale, M1);
+    // float64 rows: + the band of their float32 rounding (the epilogue's
+    // count used the same widened band)
+    const float band = 3.0f * E + input_band(valid ? rin_of(a, row) : 0.f, M1 * inv + qcur, 3.0f * E);
+    const float thr_s = fmaf(band, dscale, M1);
     int total = 0, i1 = 0;
 #pragma unroll
     for (int p = 0; p < C::kParts; ++p) {
@@ -427,12 +430,12 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
     float thr = NAN;
     if (valid) {
       flag = qcur < 0.f || total != 1;
-      thr = M1 * inv + 3.0f * E;
+      thr = M1 * inv + band;
       a.idx[row] = i1;
       if (!flag && a.dists) {
         // exact FP64 distance to the certified winner (_kernels.py:25-34);
         // the row is L2-resident from its conversion
-        const double d = winner_dist<float, L>(a.x32 + row * L, a.cb[st->cur] + (long long)i1 * L, L);
+        const double d = row_dist<L>(a, row, a.cb[st->cur], i1);
         a.dists[row] = st->metric == kEuclidean ? sqrt(d) : d;
       }
     }
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       const uint32_t bytes = (uint32_t)(rows * L * 4);
       const int xb = (int)(i % kXs);
       mbar_arrive_expect_tx(&m->xs_full[xb], bytes);
-      bulk_g2s(sX + xb * (kTcRows * L), a.x32 + (a.r0 + t * kTcRows) * L, bytes, &m->xs_full[xb]);
+      bulk_g2s(sX + xb * (kTcRows * L), a.xc + (a.r0 + t * kTcRows) * L, bytes, &m->xs_full[xb]);
     };
     if (img) {
       // prebuilt row image: the tile's operand rows and norms are two bulk
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         float xv[8], mv[8];
         if (valid) {
           const float4* src = kUseXs ? reinterpret_cast<const float4*>(xs + r * L + c8 * 8)
-                                     : reinterpret_cast<const float4*>(a.x32 + row * L + c8 * 8);
+                                     : reinterpret_cast<const float4*>(a.xc + row * L + c8 * 8);
           const float4 p0 = kUseXs ? src[0] : __ldg(src), p1 = kUseXs ? src[1] : __ldg(src + 1);
           xv[0] = p0.x; xv[1] = p0.y; xv[2] = p0.z; xv[3] = p0.w;
           xv[4] = p1.x; xv[5] = p1.y; xv[6] = p1.z; xv[7] = p1.w;
@@ -670,11 +673,12 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       bool valid;
       const long long row = row_of(i, entry, valid);
       if (MODE == kTcShortlist && valid) thr_d = a.flag_thr[entry] * dscale;  // NaN stays NaN -> overflow
-      float qcur = 0.f, yn = 0.f;
+      float qcur = 0.f, yn = 0.f, rn = 0.f;
       if constexpr (MODE == kTcTop2) {
         pwait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1), 0);
         qcur = m->qrow[i & 3][r];
         yn = sqrtf(fmaxf(qcur, 0.f));
+        rn = valid ? rin_of(a, row) : 0.f;  // float64 rows: rounding band
       }
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = (int)(g & 1);
@@ -723,7 +727,8 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           }
           const float cm = fminf(fminf(c4[0], c4[1]), fminf(c4[2], c4[3]));
           const float mnew = fminf(m1, cm);
-          const float thr = fmaf(3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw), dscale, mnew);
+          const float e3 = 3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw);
+          const float thr = fmaf(e3 + input_band(rn, mnew * inv + qcur, e3), dscale, mnew);
           if (cm < m1 && m1 > thr) cnt = 0;  // see the unpipelined form below
           m1 = mnew;
           const int jb0 = c * kTcChunk + h * span;
@@ -769,7 +774,8 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
             cm = fminf(fminf(c4[0], c4[1]), fminf(c4[2], c4[3]));
           }
           const float mnew = fminf(m1, cm);
-          const float thr = fmaf(3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw), dscale, mnew);
+          const float e3 = 3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw);
+          const float thr = fmaf(e3 + input_band(rn, mnew * inv + qcur, e3), dscale, mnew);
           // a new minimum far below the old one: every earlier value is >= the
           // old minimum > thr, so the count restarts (otherwise it is kept,
           // which can only over-count)
@@ -856,7 +862,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
 #pragma unroll
           for (int k = 0; k < kTcShort; ++k) {  // unrolled: cand[] stays in registers
             if (k < nc) {
-              const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)cand[k] * L, L);
+              const double d = row_dist<L>(a, row, cb, cand[k]);
               if (d < best || (d == best && cand[k] < bj)) {
                 best = d;
                 bj = cand[k];
@@ -943,7 +949,7 @@ cudaError_t launch_assign_tc(const KernelArgs& a_in, int sms, cudaStream_t s) {
   if (prof) cudaMemsetAsync(prof, 0, 32 * sizeof(unsigned long long), s);
   float* pd = reinterpret_cast<float*>(prof);
   cudaError_t e = cudaSuccess;
-  switch (a.dim) {
+  switch (a.cdim) {
     case 16: e = launch_tc_L<16, kTcTop2>(a, sms, pd, s); break;
     case 32: e = launch_tc_L<32, kTcTop2>(a, sms, pd, s); break;
     case 64: e = launch_tc_L<64, kTcTop2>(a, sms, pd, s); break;
@@ -970,7 +976,7 @@ cudaError_t launch_assign_tc(const KernelArgs& a_in, int sms, cudaStream_t s) {
 }
 
 cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s) {
-  switch (a.dim) {
+  switch (a.cdim) {
     case 16: return launch_tc_L<16, kTcShortlist>(a, sms, nullptr, s);
     case 32: return launch_tc_L<32, kTcShortlist>(a, sms, nullptr, s);
     case 64: return launch_tc_L<64, kTcShortlist>(a, sms, nullptr, s);
@@ -979,7 +985,7 @@ cudaError_t launch_shortlist_tc(const KernelArgs& a, int sms, cudaStream_t s) {
 }
 
 cudaError_t launch_tc_probe(const KernelArgs& a, float* dump, cudaStream_t s) {
-  switch (a.dim) {
+  switch (a.cdim) {
     case 16: return launch_tc_L<16, kTcDump>(a, 1, dump, s);
     case 32: return launch_tc_L<32, kTcDump>(a, 1, dump, s);
     case 64: return launch_tc_L<64, kTcDump>(a, 1, dump, s);

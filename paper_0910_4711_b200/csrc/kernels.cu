@@ -190,23 +190,23 @@ __global__ void prep_codebook_kernel(KernelArgs a) {
   const DevState* st = a.st;
   if (st->done) return;
   const int K = st->size;
-  const int dim = a.dim;
+  const int dim = a.dim, cdim = a.cdim;  // codevectors zero-padded to the candidate width
   const double* cb = a.cb[st->cur];
   const long long kpad = (a.kmax + 3) / 4 * 4;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < kpad;
        k += (long long)gridDim.x * blockDim.x) {
-    float* w = a.w + k * dim;
+    float* w = a.w + k * cdim;
     if (k < K) {
       double n = 0.0;
-      for (int l = 0; l < dim; ++l) {
-        float c = (float)(cb[k * dim + l] - (double)a.mu[l]);
+      for (int l = 0; l < cdim; ++l) {
+        float c = l < dim ? (float)(cb[k * dim + l] - (double)a.mu[l]) : 0.0f;
         n += (double)c * (double)c;
         w[l] = -2.0f * c;
       }
       a.nrm[k] = (float)n;
       stage_tc_row(a, k, w, n);
     } else {
-      for (int l = 0; l < dim; ++l) w[l] = 0.0f;
+      for (int l = 0; l < cdim; ++l) w[l] = 0.0f;
       a.nrm[k] = INFINITY;  // padding never wins
     }
   }
@@ -279,7 +279,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
     long long row = row0 + tid + (long long)r * NT;
     valid[r] = row < row_end;
     q[r] = 0.f;
-    const float4* src = reinterpret_cast<const float4*>(a.x32 + (valid[r] ? row : row0) * L);
+    const float4* src = reinterpret_cast<const float4*>(a.xc + (valid[r] ? row : row0) * L);
 #pragma unroll
     for (int v = 0; v < L / 4; ++v) {
       float4 t = __ldg(src + v);
@@ -426,11 +426,12 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
       const float sd = sqrtf(d2) * 1.01f + 1.0f;
       const float S = 2.02f * yn + sd;
       const float E = (float)(L + 3) * u * S * S + 2.5f * u * sd * S + 1e-14f * S * S;
-      ok = (m2[r] - m1[r]) > 3.0f * E;
-      thr = m1[r] + 3.0f * E;  // shortlist band (shortlist_kernel)
+      // float64 rows: + the band of their float32 rounding (input_band)
+      const float band = 3.0f * E + input_band(rin_of(a, row), m1[r] + q[r], 3.0f * E);
+      ok = (m2[r] - m1[r]) > band;
+      thr = m1[r] + band;  // shortlist band (shortlist_kernel)
       a.idx[row] = i1[r];
-      if (ok && a.dists)
-        store_dist(a, row, winner_dist<float, L>(a.x32 + row * L, a.cb[a.st->cur] + (long long)i1[r] * L, L));
+      if (ok && a.dists) store_dist(a, row, row_dist<L>(a, row, a.cb[a.st->cur], i1[r]));
     }
     const bool flag = valid[r] && !ok;
     const unsigned mask = __ballot_sync(0xffffffffu, flag);
@@ -830,7 +831,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
       const long long row = a.flags[i];
       const float thr = a.flag_thr[i];
       float y[L];
-      const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L);
+      const float4* src = reinterpret_cast<const float4*>(a.xc + row * L);
 #pragma unroll
       for (int v = 0; v < L / 4; ++v) {
         const float4 t = __ldg(src + v);
@@ -885,7 +886,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
       double d = INFINITY;
       int dj = 0x7fffffff;
       if (mine >= 0) {
-        d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)mine * L, L);
+        d = row_dist<L>(a, row, cb, mine);
         dj = mine;
         if (!(d < INFINITY)) {  // NaN / inf never wins a strict < (index 0 if nothing does)
           d = INFINITY;
@@ -919,7 +920,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
     const float thr = valid ? a.flag_thr[i] : -INFINITY;
     float y[L];
     {
-      const float4* src = reinterpret_cast<const float4*>(a.x32 + row * L);
+      const float4* src = reinterpret_cast<const float4*>(a.xc + row * L);
 #pragma unroll
       for (int v = 0; v < L / 4; ++v) {
         const float4 t = __ldg(src + v);
@@ -978,7 +979,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
     int bj = 0;  // nothing < inf -> index 0 (_kernels.py:23-32)
     for (int c = 0; c < nc; ++c) {
       const int j = list[c];
-      const double d = winner_dist<float, L>(a.x32 + row * L, cb + (long long)j * L, L);
+      const double d = row_dist<L>(a, row, cb, j);
       if (d < best) {
         best = d;
         bj = j;
@@ -1012,21 +1013,26 @@ static cudaError_t launch_shortlist_L(const KernelArgs& a, int sms, cudaStream_t
   return cudaGetLastError();
 }
 
+// the full FP64 scan on the rows the reference sees
+static cudaError_t launch_exact_rows(const KernelArgs& a, int use_list, int sms, cudaStream_t s) {
+  if (a.x64) return launch_exact_t<double>(a, a.x64, use_list, sms, s);
+  return launch_exact_t<float>(a, a.x32, use_list, sms, s);
+}
+
 cudaError_t launch_rerank(const KernelArgs& a, int sms, cudaStream_t s) {
-  if (a.x32 && shortlist_enabled()) {
+  if (a.xc && shortlist_enabled()) {
     cudaError_t e = a.tcb ? launch_shortlist_tc(a, sms, s) : cudaSuccess;
     if (e != cudaSuccess) return e;
-    switch (a.dim) {
+    switch (a.cdim) {
       case 16: e = launch_shortlist_L<16>(a, sms, s); break;
       case 32: e = launch_shortlist_L<32>(a, sms, s); break;
       case 64: e = launch_shortlist_L<64>(a, sms, s); break;
       default: e = cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
-    return launch_exact_t<float>(a, a.x32, 2, sms, s);
+    return launch_exact_rows(a, 2, sms, s);
   }
-  if (a.x32) return launch_exact_t<float>(a, a.x32, 1, sms, s);
-  return launch_exact_t<double>(a, a.x64, 1, sms, s);
+  return launch_exact_rows(a, 1, sms, s);
 }
 
 cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t s) {
@@ -1034,7 +1040,7 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
     // both candidate kernels are enqueued; each reads the device-side codebook
     // size and exactly one of them runs (assign_tc for tc_kmin <= K <= tc_kmax)
     cudaError_t e;
-    switch (a.dim) {
+    switch (a.cdim) {
       case 16: e = launch_fast_L<16>(a, sms, s); break;
       case 32: e = launch_fast_L<32>(a, sms, s); break;
       case 64: e = launch_fast_L<64>(a, sms, s); break;
@@ -1043,8 +1049,7 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
     if (e != cudaSuccess || !a.tcb) return e;
     return launch_assign_tc(a, sms, s);
   }
-  if (a.x32) return launch_exact_t<float>(a, a.x32, 0, sms, s);
-  return launch_exact_t<double>(a, a.x64, 0, sms, s);
+  return launch_exact_rows(a, 0, sms, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1905,34 +1910,36 @@ __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) 
 // operand image for the TC pass (stage_tc_row's layout).
 __device__ __forceinline__ void stage_row_warp(const KernelArgs& a, long long k, const double* row, int dim,
                                                int lane) {
+  // row has `dim` values; the staging is zero-padded to the candidate width
+  const int cdim = a.cdim;
   double part = 0.0;
   float wv[2] = {0.f, 0.f};
-  for (int l = lane, t = 0; l < dim; l += 32, ++t) {
-    const float c = (float)(row[l] - (double)a.mu[l]);
+  for (int l = lane, t = 0; l < cdim; l += 32, ++t) {
+    const float c = l < dim ? (float)(row[l] - (double)a.mu[l]) : 0.0f;
     part += (double)c * (double)c;
     const float w = -2.0f * c;
-    a.w[k * dim + l] = w;
+    a.w[k * cdim + l] = w;
     if (t < 2) wv[t] = w;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
   if (lane == 0) a.nrm[k] = (float)part;
-  if (!a.tcb || dim > 64 || (dim % 16) != 0) return;
+  if (!a.tcb || cdim > 64 || (cdim % 16) != 0) return;
   DevState* st = a.st;
-  unsigned short* img = a.tcb + (k / kTcChunk) * tc_chunk_elems(dim);
+  unsigned short* img = a.tcb + (k / kTcChunk) * tc_chunk_elems(cdim);
   const int r = (int)(k % kTcChunk);
   unsigned short* wh = img;
-  unsigned short* wl = img + (long long)kTcChunk * dim;
-  unsigned short* wn = img + 2LL * kTcChunk * dim;
+  unsigned short* wl = img + (long long)kTcChunk * cdim;
+  unsigned short* wn = img + 2LL * kTcChunk * cdim;
   const float sw = ldexpf(1.0f, st->tc_ew);
   bool bad = false;
-  for (int l = lane, t = 0; l < dim; l += 32, ++t) {
+  for (int l = lane, t = 0; l < cdim; l += 32, ++t) {
     const float v = wv[t] * sw;
     const __half h = __float2half_rn(v);
     const __half lo = __float2half_rn(v - __half2float(h));
     bad |= !(fabsf(v) <= 60000.0f);
-    wh[tc_off(r, l, dim)] = __half_as_ushort(h);
-    wl[tc_off(r, l, dim)] = __half_as_ushort(lo);
+    wh[tc_off(r, l, cdim)] = __half_as_ushort(h);
+    wl[tc_off(r, l, cdim)] = __half_as_ushort(lo);
   }
   if (lane < 16) {
     unsigned short val = 0;
@@ -2040,7 +2047,7 @@ __global__ void clear_kernel(KernelArgs a) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < kpad;
        k += (long long)gridDim.x * blockDim.x) {
     a.nrm[k] = INFINITY;
-    for (int l = 0; l < a.dim; ++l) a.w[k * a.dim + l] = 0.0f;
+    for (int l = 0; l < a.cdim; ++l) a.w[k * a.cdim + l] = 0.0f;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.st->flag_count = 0;
@@ -2319,6 +2326,33 @@ cudaError_t launch_column_sums_ordered(const double* x64, const float* x32, long
     column_sums_kernel<float><<<blocks, 64, 0, s>>>(x32, m, dim, out);
   else
     column_sums_kernel<double><<<blocks, 64, 0, s>>>(x64, m, dim, out);
+  return cudaGetLastError();
+}
+
+// Candidate rows: fl32 of each value, zero-padded to cdim; for float64 rows
+// also rin = 2^-24 ||x|| (x 1.0001, + a subnormal floor), the bound of the
+// rounding ||x - fl32(x)|| the certified band widens by (input_band)
+template <typename XT>
+__global__ void candidate_rows_kernel(const XT* __restrict__ x, long long n, int dim, int cdim, float* xc,
+                                      float* rin) {
+  for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
+       row += (long long)gridDim.x * blockDim.x) {
+    double nn = 0.0;
+    for (int l = 0; l < cdim; ++l) {
+      const double v = l < dim ? (double)x[row * dim + l] : 0.0;
+      xc[row * cdim + l] = (float)v;
+      nn += v * v;
+    }
+    if (rin) rin[row] = (float)(sqrt(nn) * 5.9604644775390625e-8 * 1.0001 + 1e-37);
+  }
+}
+
+cudaError_t launch_candidate_rows(const float* x32, const double* x64, long long n, int dim, int cdim,
+                                  float* xc, float* rin, int sms, cudaStream_t s) {
+  if (x64)
+    candidate_rows_kernel<double><<<sms * 8, 256, 0, s>>>(x64, n, dim, cdim, xc, rin);
+  else
+    candidate_rows_kernel<float><<<sms * 8, 256, 0, s>>>(x32, n, dim, cdim, xc, nullptr);
   return cudaGetLastError();
 }
 

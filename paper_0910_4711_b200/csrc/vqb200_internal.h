@@ -7,6 +7,8 @@
 
 #include <cstdint>
 
+#include "refarith.cuh"
+
 namespace vqb {
 
 constexpr int kHistRing = 8192;  // device ring of history records, drained by the host per batch
@@ -141,9 +143,17 @@ __host__ __device__ inline FixedCol fixed_plan(long long n_global, double maxabs
 __host__ __device__ inline int fixed_lo_shift(long long n_global) { return 62 - ceil_log2_rows(n_global); }
 
 struct KernelArgs {
-  // training data (this shard): exactly one of x32/x64 is non-null
+  // training data (this shard): exactly one of x32/x64 is non-null (x64 only
+  // for float64 rows float32 cannot hold); dim = L
   const float* x32;
   const double* x64;
+  // candidate rows of the FP32 / tensor-core passes: the rows rounded to
+  // float32 and zero-padded to cdim in {16, 32, 64} (== x32 when L is one of
+  // those and the rows are float32); rin[row] (nullable) bounds the rounding
+  // ||x - fl32(x)|| <= 2^-24 ||x|| of float64 rows, widening the certified band
+  const float* xc;
+  int cdim;
+  const float* rin;
   long long n;          // local rows
   long long n_global;   // rows over all shards (fixed-point plan)
   long long r0, r1;     // row range of the candidate pass (a chunk of [0, n))
@@ -178,6 +188,18 @@ struct KernelArgs {
   DevState* st;
 };
 
+// The reference's distance (_kernels.py:25-29) of row `row` to codevector j
+// (FP64 master codebook cb), from the rows the reference sees: the float64
+// rows when the session holds them, else the float32 rows (vectorised when L
+// is the candidate width W).
+template <int W>
+__device__ __forceinline__ double row_dist(const KernelArgs& a, long long row, const double* cb, long long j) {
+  if (a.x64) return ref_dist(a.x64 + row * a.dim, cb + j * a.dim, a.dim);
+  if (a.dim == W) return winner_dist<float, W>(a.x32 + row * W, cb + j * W, W);
+  return ref_dist(a.x32 + row * a.dim, cb + j * a.dim, a.dim);
+}
+__device__ __forceinline__ float rin_of(const KernelArgs& a, long long row) { return a.rin ? a.rin[row] : 0.f; }
+
 // Programmatic dependent launch: pass kernels are launched with
 // programmaticStreamSerialization (launch_k), so a kernel's grid is set up
 // while its predecessor drains; each begins with pdl_wait(), which returns
@@ -199,6 +221,18 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// Extra certified band for float64 rows rounded to float32 (rn = rin[row]):
+// the reference compares d_j = ||x - c_j||^2 while the candidate pass sees
+// x^ = fl32(x); d_j - d_1 moves by 2 (x - x^).(c_1 - c_j), at most
+// 2 rn (sqrt d_1 + sqrt d_j).  With B >= every sqrt d inside the band (from
+// the best value m1 + q and the FP band 3E) the extra term 4 rn B + 2 rn^2
+// keeps "certified" and "the reference's winner lies inside the band" true.
+__host__ __device__ __forceinline__ float input_band(float rn, float d1, float e3) {
+  if (!(rn > 0.f)) return 0.f;
+  const float B = (sqrtf(fmaxf(d1 + e3, 0.f)) + 4.0f * rn) * 1.02f;
+  return 4.0f * rn * B + 2.0f * rn * rn;
 }
 
 // kernel launchers (kernels.cu); all asynchronous on `stream`
@@ -239,6 +273,12 @@ cudaError_t launch_column_sums_ordered(const double* x64, const float* x32, long
 cudaError_t launch_pair_distance(const double* a, const double* b, int dim, int metric, double* out,
                                  cudaStream_t s);
 bool fast_dim_supported(int dim);
+// candidate width of a row length: 16 / 32 / 64, or 0 (no fast path, L > 64)
+inline int candidate_dim(int dim) { return dim <= 16 ? 16 : (dim <= 32 ? 32 : (dim <= 64 ? 64 : 0)); }
+// fl32 + zero-padded candidate copy of rows (x64 or x32, [n][dim] -> [n][cdim])
+// and, for float64 rows, the per-row rounding bound rin
+cudaError_t launch_candidate_rows(const float* x32, const double* x64, long long n, int dim, int cdim,
+                                  float* xc, float* rin, int sms, cudaStream_t s);
 
 // block vectoriser / decode / reconstruction distortion (imaging.cu)
 cudaError_t launch_pixels_to_blocks_f32(const unsigned char* px, long long images, long long H, long long W,
@@ -306,7 +346,7 @@ __host__ __device__ __forceinline__ long long tc_off(int row, int col, int kt) {
 __device__ __forceinline__ void stage_tc_row(const KernelArgs& a, long long k, const float* w, double nrm) {
   if (!a.tcb) return;
   DevState* st = a.st;
-  const int L = a.dim;
+  const int L = a.cdim;
   unsigned short* img = a.tcb + (k / kTcChunk) * tc_chunk_elems(L);
   const int r = (int)(k % kTcChunk);
   unsigned short* wh = img;

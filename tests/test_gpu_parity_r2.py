@@ -405,3 +405,52 @@ def test_threads_share_a_training_set():
     for i, r in enumerate(results):
         c, d, cbk = serial[i % len(books)]
         assert np.array_equal(r[0], c) and r[1] == d and r[2].tobytes() == cbk.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# the candidate pass for float64 rows and every L <= 64
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dim", [2, 5, 9, 16, 36])
+def test_float64_rows_any_dim_fast_path_bit_exact(dim):
+    """float64 normals (not float32-exact), N=2^20, K=1024: the FP32 /
+    tensor-core candidate pass on the rounded, zero-padded rows with the
+    rounding added to the certified band, FP64 re-rank against the float64
+    rows -> indices and per-row distances bit-identical to the reference."""
+    from paper_0910_4711_b200.core import _Session
+    rng = np.random.default_rng(100 + dim)
+    x = rng.normal(0, 1, (1 << 20, dim)) * rng.uniform(0.5, 3.0, dim) + rng.uniform(-2, 2, dim)
+    cb = x[rng.choice(x.shape[0], 1024, replace=False)] + rng.normal(0, 0.05, (1024, dim))
+    s = _Session(None, x)
+    info = s.info()
+    assert info["fast"] and info["float64_rows"] and info["cdim"] in (16, 32, 64)
+    cells, dists, total = s.assign(cb, 0)
+    want_c, want_d = oracle.assign_all(x, cb, workers=oracle.max_threads())
+    assert np.array_equal(cells, want_c)
+    assert dists.tobytes() == want_d.tobytes()
+    assert total == oracle.sum_inorder(want_d)
+
+
+@pytest.mark.parametrize("dim", [3, 5, 36])
+def test_float32_rows_any_dim_fast_path_bit_exact(dim):
+    from paper_0910_4711_b200.core import _Session
+    rng = np.random.default_rng(200 + dim)
+    x = rng.uniform(0, 255, (200000, dim)).astype(np.float32)
+    cb = rng.uniform(0, 255, (512, dim))
+    s = _Session(x, None)
+    assert s.info()["fast"] and not s.info()["float64_rows"]
+    cells, dists, _ = s.assign(cb, 0)
+    want_c, want_d = oracle.assign_all(x.astype(np.float64), cb, workers=oracle.max_threads())
+    assert np.array_equal(cells, want_c)
+    assert dists.tobytes() == want_d.tobytes()
+
+
+def test_float64_design_fast_path_matches_reference():
+    """A whole float64 design on the candidate pass: schedule, TD and
+    codebook bit-identical to the reference (reference-order sums, n <= 2^20)."""
+    rng = np.random.default_rng(9)
+    x = rng.normal(0, 1, (50000, 7)) * np.array([1.0, 3.0, 0.2, 10.0, 1.0, 0.5, 2.0])
+    cb, stats = vq.lbg_train(vq.TrainingSet(x), vq.LbgConfig(target_size=64, epsilon=1e-3))
+    ref = oracle.lbg_train(x, 64, epsilon=1e-3, workers=oracle.max_threads())
+    assert stats.td_history() == [(s_, i, td) for s_, i, td, _ in ref.history]
+    assert cb.codevectors.tobytes() == ref.codebook.tobytes()
