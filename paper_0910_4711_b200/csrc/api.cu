@@ -126,6 +126,7 @@ struct vqb_session {
   double* scratch = nullptr;    // small device scratch
   bool fast = false;
   bool ordered = false;
+  bool fused_ok = false;  // vqb_train on one device: the fused small-codebook pass leads every pass
   bool pending_init = false;
   long long lloyd_size = 0;  // vqb_lloyd_begin
   cudaEvent_t ev_batch[2] = {nullptr, nullptr};
@@ -298,6 +299,7 @@ struct vqb_session {
     CK(dalloc(&flags2, (size_t)n + 32));
     CK(dalloc(&dists, (size_t)n + 32));
     CK(dalloc(&st, 1));
+    CK(cudaMemset(st, 0, sizeof(DevState)));  // every field starts defined (skip, barriers, ...)
     CK(dalloc(&mu, (size_t)dim + 68));  // zero-padded up to the candidate width
     CK(cudaMemset(mu, 0, sizeof(float) * (dim + 68)));
     CK(dalloc(&cmax, (size_t)dim));
@@ -806,6 +808,7 @@ int vqb_step_local(vqb_session* s) {
   if (!s) return fail(VQB_USAGE, "null session");
   std::lock_guard<std::recursive_mutex> lock_(s->lock_mu);
   KernelArgs a = s->args();
+  if (s->fused_ok) CK(launch_pass_small(a, s->sms, s->stream));
   CK(launch_assign(a, s->fast, s->sms, s->stream));
   if (s->fast) CK(launch_rerank(a, s->sms, s->stream));
   CK(launch_epilogue(a, true, !s->ordered, false, s->sms, s->stream));
@@ -876,7 +879,7 @@ int vqb_session::batch_graph(int batch) {
     enabled = (e && strcmp(e, "0") == 0) ? 0 : 1;
   }
   if (!enabled || !own_stream) return VQB_OK;  // a caller's stream: plain launches
-  const int key = (fast ? 1 : 0) | (ordered ? 2 : 0) | (batch << 2);
+  const int key = (fast ? 1 : 0) | (ordered ? 2 : 0) | (fused_ok ? 4 : 0) | (batch << 3);
   if (graph && graph_kmax == kmax && graph_key == key) return VQB_OK;
   drop_graph();
   cudaGraph_t g = nullptr;
@@ -984,6 +987,12 @@ int vqb_train(vqb_session* s, const vqb_train_config* cfg, double* codebook_out,
   if (rc) return rc;
   rc = vqb_step_finalize(s);  // global centroid + first split
   if (rc) return rc;
+  // one device holds every row: small-codebook passes run as one fused kernel
+  s->fused_ok = s->fast && !s->ordered && s->n == s->n_global;
+  struct Reset {
+    vqb_session* s;
+    ~Reset() { s->fused_ok = false; }
+  } reset_fused{s};
   // Speculative batches: passes early-exit on the device once `done` is set,
   // so the host only checks the flag of the previous batch while the next
   // one is already queued (the GPU never waits on the host).

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
   pdl_wait();
   using C = TcCfg<L>;
   DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = st->size;
   if (MODE != kTcDump && !tc_handles(st, K)) return;
   const int ncols = K < kTcChunk ? K : kTcChunk;  // MMA N (64 / 128 for small codebooks)

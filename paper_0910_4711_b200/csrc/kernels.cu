@@ -188,7 +188,7 @@ __device__ __forceinline__ double fixed_to_double(long long hi, long long lo, in
 __global__ void prep_codebook_kernel(KernelArgs a) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = st->size;
   const int dim = a.dim, cdim = a.cdim;  // codevectors zero-padded to the candidate width
   const double* cb = a.cb[st->cur];
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelAr
   constexpr int NT = FastCfg<L>::NT, R = FastCfg<L>::R, TK = FastCfg<L>::TK;
   using TS = TileStream<L, TK>;
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = st->size;
   if (a.tcb && tc_handles(st, K)) return;  // assign_tc runs this pass
   const int ntiles = (K + TK - 1) / TK;
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(256) exact_rows_kernel(KernelArgs a, const XT*
   // j = t, t+T, ... (ascending) with the reference's strict <, then a
   // lexicographic (d, j) reduction over the T threads.
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = st->size;
   const int dim = DIM ? DIM : a.dim;
   const double* __restrict__ cb = a.cb[st->cur];
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(256) shortlist_kernel(KernelArgs a) {
   using C = ShortCfg<L>;
   constexpr int NT = C::NT, TK = C::TK;
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const long long count = st->flag_count;
   if (count == 0) return;
   const int K = st->size;
@@ -1142,14 +1142,14 @@ __device__ __forceinline__ void zero_lo_words(const KernelArgs& a, int K) {
 __global__ void zero_lo_kernel(KernelArgs a, int zero_cells) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   zero_lo_words(a, zero_cells ? 1 : st->size);
 }
 
 __global__ void __launch_bounds__(256) td_tiles_kernel(KernelArgs a, int zero_lo) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   if (zero_lo) zero_lo_words(a, st->size);
   __shared__ double red[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1208,12 +1208,16 @@ __device__ __forceinline__ void load_row16(const XT* __restrict__ X, long long r
 
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs a, const XT* __restrict__ X,
-                                                             int zero_cells) {
+                                                             int zero_cells, int small_only) {
   pdl_wait();
-  const DevState* st = a.st;
-  if (st->done) return;
+  DevState* st = a.st;
+  if (pass_off(st)) return;
   const int K = zero_cells ? 1 : st->size;
   const int dim = DIM ? DIM : a.dim;
+  // small_only: launched beside sums_red_kernel (one graph serves every
+  // level); this kernel takes the passes whose codebook fits warp tables
+  if (small_only && !sums_warp_sink(K, dim, sum_threads<DIM>())) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) st->slabs = gridDim.x;
   const int t_lo = st->lo_shift;  // per-column shifts: a.cshift
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kSumThreads = sum_threads<DIM>();
@@ -1441,6 +1445,7 @@ struct LimbPlan {
   int lp, pieces;   // dims per piece (template LP), pieces
   int chunks;       // row chunks
   long long rows;   // rows per chunk
+  int small_cut;    // codebooks up to this size are left to sums_kernel's warp tables (0: none)
 };
 __host__ __device__ inline LimbPlan limb_plan(long long n, int K, int dim, int lo_shift, int sms) {
   LimbPlan p{};
@@ -1488,10 +1493,12 @@ template <typename XT, int LP, int M>
 __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT* __restrict__ X, int zero_cells,
                                                           LimbPlan pl) {
   pdl_wait();
-  const DevState* st = a.st;
-  if (st->done) return;
+  DevState* st = a.st;
+  if (pass_off(st)) return;
   const int K = zero_cells ? 1 : st->size;
   const int dim = a.dim;
+  if (pl.small_cut > 0 && K <= pl.small_cut) return;  // sums_kernel's warp tables take this pass
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->slabs = pl.chunks;
   const int t = st->lo_shift;  // == fixed_lo_shift(n_global), what the plan was made for
   constexpr int m = M;
   const int w = pl.w;
@@ -1606,10 +1613,11 @@ static cudaError_t launch_red_lp(const KernelArgs& a, const XT* X, const LimbPla
 
 template <typename XT>
 static cudaError_t launch_sums_red(const KernelArgs& a, const XT* X, bool zero_cells, int sms, cudaStream_t s,
-                                   bool* used, int* chunks) {
+                                   bool* used, int* chunks, int small_cut) {
   *used = false;
   if (zero_cells) return cudaSuccess;
-  const LimbPlan pl = limb_plan(a.n, (int)a.kmax, a.dim, fixed_lo_shift(a.n_global), sms);
+  LimbPlan pl = limb_plan(a.n, (int)a.kmax, a.dim, fixed_lo_shift(a.n_global), sms);
+  pl.small_cut = small_cut;
   if (!limb_ok(pl, (int)a.kmax)) return cudaSuccess;
   *used = true;
   *chunks = pl.chunks;
@@ -1626,7 +1634,8 @@ static cudaError_t launch_sums_red(const KernelArgs& a, const XT* X, bool zero_c
 __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int nblocks, int zero_cells) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
+  if (nblocks < 0) nblocks = st->slabs;  // whichever sums kernel ran this pass
   const int K = zero_cells ? 1 : st->size;
   const long long dim = a.dim;
   const long long words = (long long)K * dim + K;
@@ -1682,25 +1691,35 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   const long long words = kmax * a.dim + kmax;
   int rb = (int)((words + 31) / 32);
   if (rb > 8192) rb = 8192;
-  const SumsPlan plan0 = sums_plan((int)kmax, a.dim, kSumThreads);
-  const int red_mode = getenv_flag("VQB_SUMS_RED", 1);  // 0 never, 1 always, 2 where the block table splits
-  if (!sums_warp_sink((int)kmax, a.dim, kSumThreads) &&
-      (red_mode == 1 || (red_mode == 2 && plan0.nkc * plan0.ndc > 1))) {
-    bool used = false;
-    int chunks = 0;
-    e = launch_sums_red<XT>(a, X, zero_cells, sms, s, &used, &chunks);
-    if (e != cudaSuccess) return e;
-    if (used) return launch_k(reduce_partials_kernel, rb, 256, 0, s, a, chunks, zero_cells ? 1 : 0);
-  }
-  const SumsPlan plan = sums_plan((int)kmax, a.dim, kSumThreads);
-  const int chunks = (int)(plan.nkc * plan.ndc);
+  const int red_mode = getenv_flag("VQB_SUMS_RED", 1);  // 0 never, 1 for codebooks past the warp tables
   const long long rows_per_block = 4LL * kSumThreads;
   int blocks = (int)((a.n + rows_per_block - 1) / rows_per_block);
   if (blocks > sms) blocks = sms;
   if (blocks < 1) blocks = 1;
   e = cudaFuncSetAttribute(sums_kernel<XT, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEpiSmem);
   if (e != cudaSuccess) return e;
-  e = launch_k(sums_kernel<XT, DIM>, dim3(blocks, chunks), kSumThreads, kEpiSmem, s, a, X, zero_cells ? 1 : 0);
+  if (!zero_cells && red_mode == 1 && !sums_warp_sink((int)kmax, a.dim, kSumThreads)) {
+    // one graph serves every level: the warp-table kernel takes the small
+    // codebooks (no shared-address contention), the limb-RED kernel the rest
+    bool used = false;
+    int chunks = 0;
+    int cut = 0;
+    while (cut < kmax && sums_warp_sink(cut + 1, a.dim, kSumThreads)) ++cut;
+    e = launch_sums_red<XT>(a, X, zero_cells, sms, s, &used, &chunks, cut);
+    if (e != cudaSuccess) return e;
+    if (used) {
+      if (cut > 0) {
+        const SumsPlan p1 = sums_plan(cut, a.dim, kSumThreads);
+        e = launch_k(sums_kernel<XT, DIM>, dim3(blocks, (unsigned)(p1.nkc * p1.ndc)), kSumThreads, kEpiSmem, s, a,
+                     X, 0, 1);
+        if (e != cudaSuccess) return e;
+      }
+      return launch_k(reduce_partials_kernel, rb, 256, 0, s, a, -1, 0);
+    }
+  }
+  const SumsPlan plan = sums_plan((int)kmax, a.dim, kSumThreads);
+  const int chunks = (int)(plan.nkc * plan.ndc);
+  e = launch_k(sums_kernel<XT, DIM>, dim3(blocks, chunks), kSumThreads, kEpiSmem, s, a, X, zero_cells ? 1 : 0, 0);
   if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1763,12 +1782,11 @@ __device__ __forceinline__ void set_action(DevState* st, int act) {
   }
 }
 
-__global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) {
-  pdl_wait();
+// The decision step of a pass, one block of any size (<= 1024 threads).
+__device__ void finalize_body(const KernelArgs& a, int phase) {
   DevState* st = a.st;
-  if (st->done) return;
-  __shared__ double red[8];
-  __shared__ long long s_empty[8];
+  __shared__ double red[32];
+  __shared__ long long s_empty[32];
   __shared__ double s_td;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -1805,11 +1823,15 @@ __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) 
         s_td = s;
       }
     } else {
+      // a fixed tree of 256 leaves whatever the block size (the fused pass
+      // runs this with 512 threads: its extra warps add exact zeros), so the
+      // distortion has the same bits on every path
       const long long nt = a.ex.ntiles;
-      const long long per = (nt + blockDim.x - 1) / blockDim.x;
+      const long long per = (nt + 255) / 256;
       double s = 0.0;
-      for (long long i = tid * per; i < (tid + 1) * per && i < nt; ++i)
-        s = __dadd_rn(s, __longlong_as_double(a.ex.td()[i]));
+      if (tid < 256)
+        for (long long i = tid * per; i < (tid + 1) * per && i < nt; ++i)
+          s = __dadd_rn(s, __longlong_as_double(a.ex.td()[i]));
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
       if (lane == 0) red[warp] = s;
@@ -1896,6 +1918,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) 
   }
 }
 
+__global__ void __launch_bounds__(256) finalize_kernel(KernelArgs a, int phase) {
+  pdl_wait();
+  if (pass_off(a.st)) return;
+  finalize_body(a, phase);
+}
+
 // ---------------------------------------------------------------------------
 // apply: one thread per source codevector.  Update (update_rows,
 // _kernels.py:59-66: sum / n with the int64 fixed-point sum, empty cells keep
@@ -1960,8 +1988,10 @@ __device__ __forceinline__ void stage_row_warp(const KernelArgs& a, long long k,
 // 2i+1 = c - delta) or both, into the other codebook buffer, then the staging
 // of the new rows for the next candidate pass.  Idempotent (speculative
 // passes after `done` may repeat it harmlessly).
-__global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
-  pdl_wait();
+// The codebook work of a pass over any grid: one warp per source codevector.
+// zero_lo: consume (read, then clear) the pass's low words -- the fused pass,
+// whose action runs exactly once, uses it; the kernel form is idempotent.
+__device__ void apply_body(const KernelArgs& a, int stage, bool zero_lo) {
   const DevState* st = a.st;
   const int act = st->act;
   // zero the distortion tiles (other ranks' slots must be 0 before the next
@@ -1984,10 +2014,11 @@ __global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
     for (int l = lane; l < dim; l += 32) {
       const long long i = k * dim + l;
       double v = src[i];
+      const long long lo = a.ex.lo()[i];
+      if (zero_lo && lo) a.ex.lo()[i] = 0;  // consumed: the next pass adds from zero
       if ((act & kActUpdate) && cnt > 0)
         v = ordered ? a.ord[i]
-                    : __ddiv_rn(fixed_to_double(a.ex.sums()[i], a.ex.lo()[i], t_lo, -(a.cshift[l] + t_lo)),
-                                (double)cnt);
+                    : __ddiv_rn(fixed_to_double(a.ex.sums()[i], lo, t_lo, -(a.cshift[l] + t_lo)), (double)cnt);
       if (act & kActSplit) {
         dst[(2 * k) * dim + l] = __dadd_rn(v, delta);
         dst[(2 * k + 1) * dim + l] = __dsub_rn(v, delta);
@@ -2005,6 +2036,419 @@ __global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) apply_kernel(KernelArgs a, int stage) {
+  pdl_wait();
+  if (a.st->skip) return;  // (not `done`: speculative passes re-apply harmlessly)
+  apply_body(a, stage, false);
+}
+
+// ---------------------------------------------------------------------------
+// Fused pass for small codebooks (K <= 512 / L): ONE cooperative persistent
+// kernel does the whole training pass -- FP32 candidate pass + certification,
+// the reference's FP64 scan for the rows it cannot certify (a warp per row,
+// lanes = codevectors), exact winner distances, the distortion tile partials
+// in the fixed tree of td_tiles_kernel, two-word cell sums in half-warp
+// tables, the slab reduction, finalize (one block) and apply (all blocks) --
+// separated by three grid barriers.  Each row is read from HBM once.  The
+// per-kernel path of the same pass sees `skip` and idles (one graph serves
+// every level).  Reference: _kernels.py:18-66, core.py:384-415.
+// ---------------------------------------------------------------------------
+constexpr int kFuseThreads = 512;
+template <int L>
+__host__ __device__ constexpr int fused_kmax() { return 512 / L; }
+
+// grid-wide barrier (cooperative launch: every CTA is resident)
+__device__ __forceinline__ void grid_sync(DevState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* genp = &st->bar_gen;
+    const unsigned g = *genp;
+    __threadfence();
+    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
+      st->bar_count = 0;
+      __threadfence();
+      atomicAdd(&st->bar_gen, 1u);
+    } else {
+      while (*genp == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int L>
+struct FuseSmem {
+  static constexpr int KF = fused_kmax<L>();
+  float w[KF * L];
+  float nrm[KF];
+  double cb[KF * L];
+  long long tab[32][KF * L];   // half-warp tables (2 per warp)
+  unsigned tcnt[32][KF];
+  double red[32];
+};
+
+// reference-arithmetic distance of a row (x32 / x64, dim values) to a
+// codevector staged in shared memory, 16 values loaded at a time
+template <typename XT>
+__device__ __forceinline__ double smem_dist(const XT* __restrict__ x, const double* c, int dim) {
+  double d = 0.0;
+  for (int c0 = 0; c0 < dim; c0 += 16) {
+    XT xr[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) xr[l] = c0 + l < dim ? x[c0 + l] : (XT)0;
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      if (c0 + l < dim) {
+        const double diff = __dsub_rn((double)xr[l], c[c0 + l]);
+        d = __dadd_rn(d, __dmul_rn(diff, diff));
+      }
+    }
+  }
+  return d;
+}
+
+// Phase A of the fused pass, warp-independent: the grid's warps take
+// 128-row chunks round-robin (lane: rows base + lane + 32 k, k < 4): the
+// candidate pass and certification (assign_chunk's arithmetic and band),
+// the reference's FP64 scan for rows the band cannot certify (lanes =
+// codevectors, lexicographic (d, j) minimum), exact winner distances,
+// cells / distances out, and the two-word cell sums into the warp's
+// half-warp tables (lanes = dimensions, 16 rows' values loaded together, runs
+// of one cell summed in registers).  No block-wide synchronisation.
+template <int L, typename XT>
+__device__ __forceinline__ void fused_rows(const KernelArgs& a, const XT* __restrict__ X, FuseSmem<L>& sm,
+                                           int K, int t_lo, int metric, const float (&mu)[L]) {
+  constexpr int kChunk = 128, R = 4;
+  constexpr int RB = L == 16 ? 4 : (L == 32 ? 2 : 1);
+  const int dim = a.dim;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane >> 4, hl = lane & 15;
+  long long* tab = sm.tab[2 * warp + half];
+  unsigned* tcnt = sm.tcnt[2 * warp + half];
+  const float u = 5.9604645e-8f;
+  const long long nchunks = (a.n + kChunk - 1) / kChunk;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  int nflag = 0;
+  for (long long ch = gw; ch < nchunks; ch += nw) {
+    const long long base = ch * kChunk;
+    int cell[R];
+    double dist[R];
+    unsigned flagm = 0;  // bit k: row k of this lane needs the exact scan
+#pragma unroll 1
+    for (int kb = 0; kb < R; kb += RB) {
+      float y[RB][L];
+      float q[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const long long row = base + lane + 32 * (kb + k);
+        const float4* src = reinterpret_cast<const float4*>(a.xc + (row < a.n ? row : base) * L);
+#pragma unroll
+        for (int v = 0; v < L / 4; ++v) {
+          const float4 t4 = __ldg(src + v);
+          y[k][4 * v + 0] = t4.x;
+          y[k][4 * v + 1] = t4.y;
+          y[k][4 * v + 2] = t4.z;
+          y[k][4 * v + 3] = t4.w;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        q[k] = 0.f;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          y[k][l] = __fsub_rn(y[k][l], mu[l]);
+          q[k] = fmaf(y[k][l], y[k][l], q[k]);
+        }
+      }
+      float m1[RB], m2[RB];
+      int i1[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        m1[k] = INFINITY;
+        m2[k] = INFINITY;
+        i1[k] = 0;
+      }
+#pragma unroll 1
+      for (int j = 0; j < K; ++j) {
+        float v[RB];
+        const float nj = sm.nrm[j];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) v[k] = nj;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const float wl = sm.w[j * L + l];
+#pragma unroll
+          for (int k = 0; k < RB; ++k) v[k] = fmaf(wl, y[k][l], v[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const float n2 = fminf(m2[k], fmaxf(m1[k], v[k]));
+          const bool p = v[k] < m1[k];
+          m1[k] = fminf(m1[k], v[k]);
+          i1[k] = p ? j : i1[k];
+          m2[k] = n2;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const long long row = base + lane + 32 * (kb + k);
+        const float yn = sqrtf(q[k]);
+        const float d2 = fmaxf(m2[k] + q[k], 0.f);
+        const float sd = sqrtf(d2) * 1.01f + 1.0f;
+        const float Sm = 2.02f * yn + sd;
+        const float E = (float)(L + 3) * u * Sm * Sm + 2.5f * u * sd * Sm + 1e-14f * Sm * Sm;
+        const float band = 3.0f * E + input_band(row < a.n ? rin_of(a, row) : 0.f, m1[k] + q[k], 3.0f * E);
+        const bool ok = row >= a.n || (m2[k] - m1[k]) > band;
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk)
+          if (kk == kb + k) cell[kk] = i1[k];
+        if (!ok) flagm |= 1u << (kb + k);
+      }
+    }
+    // exact distances of the certified winners (the rows the reference sees)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const long long row = base + lane + 32 * k;
+      dist[k] = (row < a.n && !(flagm >> k & 1)) ? smem_dist(X + row * dim, sm.cb + cell[k] * dim, dim) : 0.0;
+    }
+    // rows the band could not certify: the warp scans each in FP64
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      unsigned fl = __ballot_sync(0xffffffffu, (flagm >> k) & 1);
+      nflag += __popc(fl);
+      while (fl) {
+        const int src = __ffs(fl) - 1;
+        fl &= fl - 1;
+        const long long row = base + src + 32 * k;
+        double d = INFINITY;
+        int j = lane;
+        if (lane < K) {
+          d = smem_dist(X + row * dim, sm.cb + lane * dim, dim);
+          if (!(d < INFINITY)) d = INFINITY;  // NaN / inf never win a strict <
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, d, off);
+          const int oj = __shfl_xor_sync(0xffffffffu, j, off);
+          if (od < d || (od == d && oj < j)) {
+            d = od;
+            j = oj;
+          }
+        }
+        if (lane == src) {
+          cell[k] = d < INFINITY ? j : 0;
+          dist[k] = d;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const long long row = base + lane + 32 * k;
+      if (row >= a.n) continue;
+      a.idx[row] = cell[k];
+      if (a.dists) a.dists[row] = metric == kEuclidean ? sqrt(dist[k]) : dist[k];
+    }
+    // two-word cell sums: 32 rows (k) at a time, half-warp h takes row 2p + h
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+      for (int c0 = 0; c0 < dim; c0 += 16) {
+        const int l = c0 + hl;
+        const bool lon = l < dim;
+        const int shl = lon ? __ldg(a.cshift + l) : 0;
+        XT xv[16];
+        int cv[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const int rl = 2 * p + half;  // row base + rl + 32 k, held by lane rl
+          const long long row = base + rl + 32 * k;
+          int c = 0;
+#pragma unroll
+          for (int kk = 0; kk < R; ++kk) c = kk == k ? __shfl_sync(0xffffffffu, cell[kk], rl) : c;
+          const bool ok = row < a.n;
+          cv[p] = ok ? c : -1;
+          xv[p] = (ok && lon) ? X[row * dim + l] : (XT)0;
+        }
+        long long acc = 0, acc_lo = 0;
+        int cur = -1;
+        unsigned run = 0;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          if (cv[p] != cur) {  // uniform within the half-warp (one row)
+            if (cur >= 0) {
+              if (lon) {
+                tab[cur * L + l] += acc;
+                add_lo(a, cur, l, acc_lo);
+              }
+              if (c0 == 0 && hl == 0) tcnt[cur] += run;
+            }
+            cur = cv[p];
+            acc = 0;
+            acc_lo = 0;
+            run = 0;
+          }
+          if (cur >= 0) {
+            long long h, lo2;
+            split_fixed(xv[p], shl, t_lo, h, lo2);
+            acc += h;
+            acc_lo += lo2;
+            ++run;
+          }
+        }
+        if (cur >= 0) {
+          if (lon) {
+            tab[cur * L + l] += acc;
+            add_lo(a, cur, l, acc_lo);
+          }
+          if (c0 == 0 && hl == 0) tcnt[cur] += run;
+        }
+      }
+    }
+  }
+  if (lane == 0 && nflag) atomicAdd(&a.st->flag_count, nflag);
+}
+
+template <int L, typename XT>
+__device__ __forceinline__ void fused_pass(const KernelArgs& a, const XT* __restrict__ X) {
+  using S = FuseSmem<L>;
+  constexpr int KF = S::KF;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  DevState* st = a.st;
+  const int K = st->size;
+  const int dim = a.dim;
+  const int tid = threadIdx.x;
+  const double* cbg = a.cb[st->cur];
+  for (int i = tid; i < K * L; i += blockDim.x) sm.w[i] = a.w[i];
+  for (int i = tid; i < K; i += blockDim.x) sm.nrm[i] = a.nrm[i];
+  for (int i = tid; i < K * dim; i += blockDim.x) sm.cb[i] = cbg[i];
+  for (int i = tid; i < 32 * KF * L; i += blockDim.x) (&sm.tab[0][0])[i] = 0;
+  for (int i = tid; i < 32 * KF; i += blockDim.x) (&sm.tcnt[0][0])[i] = 0;
+  float mu[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) mu[l] = a.mu[l];
+  __syncthreads();
+  fused_rows<L, XT>(a, X, sm, K, st->lo_shift, st->metric, mu);
+  __syncthreads();
+  // this CTA's slab: its half-warp tables summed (int64, any order exact)
+  long long* slab = a.partials + (long long)blockIdx.x * ((long long)a.kmax * dim + a.kmax);
+  for (int i = tid; i < K * dim; i += blockDim.x) {
+    const int c = i / dim, l = i % dim;
+    long long v = 0;
+    for (int tb2 = 0; tb2 < 32; ++tb2) v += sm.tab[tb2][c * L + l];
+    slab[i] = v;
+  }
+  for (int c = tid; c < K; c += blockDim.x) {
+    long long v = 0;
+    for (int tb2 = 0; tb2 < 32; ++tb2) v += sm.tcnt[tb2][c];
+    slab[(long long)K * dim + c] = v;
+  }
+}
+
+// the distortion partial of 2048-row tile t from the stored distances, in
+// td_tiles_kernel's order (threads 0..255 of the block)
+__device__ __forceinline__ void tile_partial(const KernelArgs& a, long long t, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 256) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int r = 0; r < kTdTile / 256; ++r) {
+      const long long row = t * kTdTile + (long long)r * 256 + tid;
+      sacc = __dadd_rn(sacc, row < a.n ? a.dists[row] : 0.0);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sacc = __dadd_rn(sacc, __shfl_xor_sync(0xffffffffu, sacc, off));
+    if (lane == 0) red[warp] = sacc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t2 = 0.0;
+    for (int w = 0; w < 8; ++w) t2 = __dadd_rn(t2, red[w]);
+    a.ex.td()[a.tile0 + t] = __double_as_longlong(t2);
+  }
+  __syncthreads();
+}
+
+template <int L>
+__global__ void __launch_bounds__(kFuseThreads, 1) pass_small_kernel(KernelArgs a) {
+  DevState* st = a.st;
+  if (st->done) return;
+  const int K = st->size;
+  if (st->mode != kModeTrain || st->ordered || K > fused_kmax<L>()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->skip = 0;  // the per-kernel path runs this pass
+    return;
+  }
+  if (a.x64)
+    fused_pass<L, double>(a, a.x64);
+  else
+    fused_pass<L, float>(a, a.x32);
+  grid_sync(st);
+  // distortion tile partials (every row's distance is stored now)
+  {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* red = reinterpret_cast<FuseSmem<L>*>(smem_raw)->red;
+    const long long ntiles = (a.n + kTdTile - 1) / kTdTile;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) tile_partial(a, t, red);
+  }
+  // slabs -> the exchange buffer (fixed order over CTAs; integer sums)
+  {
+    const int dim = a.dim;
+    const long long words = (long long)K * dim + K;
+    const long long stride = (long long)a.kmax * dim + a.kmax;
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < words;
+         w += (long long)gridDim.x * blockDim.x) {
+      long long v = 0;
+      for (int b = 0; b < (int)gridDim.x; ++b) v += a.partials[(long long)b * stride + w];
+      if (w < (long long)K * dim)
+        a.ex.sums()[w] = v;
+      else
+        a.ex.counts()[w - (long long)K * dim] = v;
+    }
+  }
+  grid_sync(st);
+  if (blockIdx.x == 0) {
+    finalize_body(a, 1);
+    if (threadIdx.x == 0) st->skip = 1;  // the rest of this pass's kernels idle
+  }
+  grid_sync(st);
+  apply_body(a, 1, true);
+}
+
+// Launch the fused pass (one CTA per SM, cooperative); it returns at once
+// for passes it does not take.  Opt-in (VQB_FUSE=1): measured on the B200 it
+// is correct but slower than the per-kernel pass (cfg2 K=2: 177 vs 110 us per
+// pass; instruction-bound at 16 warps per SM -- DESIGN.md section 9).
+cudaError_t launch_pass_small(const KernelArgs& a, int sms, cudaStream_t s) {
+  static const bool on = getenv_flag("VQB_FUSE", 0) != 0;
+  if (!on || !a.xc) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(kFuseThreads);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.stream = s;
+  cudaError_t e = cudaSuccess;
+  switch (a.cdim) {
+#define VQB_FUSE_L(LL)                                                                                      \
+  case LL: {                                                                                                \
+    cfg.dynamicSmemBytes = sizeof(FuseSmem<LL>);                                                            \
+    e = cudaFuncSetAttribute(pass_small_kernel<LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                             (int)sizeof(FuseSmem<LL>));                                                    \
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, pass_small_kernel<LL>, a);                           \
+    break;                                                                                                  \
+  }
+    VQB_FUSE_L(16)
+    VQB_FUSE_L(32)
+    VQB_FUSE_L(64)
+#undef VQB_FUSE_L
+    default: return cudaSuccess;
+  }
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s) {
@@ -2034,6 +2478,10 @@ cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s
     cudaError_t e1 = launch_k(apply_kernel, 8, 256, 0, s, a, stage ? 1 : 0);
     if (e1 != cudaSuccess) return e1;
   }
+  // the column sums' low words are consumed: clear them (the fused pass adds
+  // from zero and clears after itself)
+  e = launch_k(zero_lo_kernel, 64, 256, 0, s, a, 0);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -2254,6 +2702,7 @@ __global__ void reset_kernel(DevState* st, int mode, int size, int metric, int o
   st->metric = metric;
   st->ordered = ordered;
   st->done = 0;
+  st->skip = 0;
   if (!keep_cur) st->cur = 0;
   st->flag_count = 0;
   st->flag2_count = 0;

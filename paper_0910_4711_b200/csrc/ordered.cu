@@ -46,7 +46,7 @@ __device__ __forceinline__ long long ord_rows_per_block(long long n, int B) {
 __global__ void __launch_bounds__(256) ord_count_kernel(KernelArgs a) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = st->size;
   const int B = a.oblocks;
   const long long R = ord_rows_per_block(a.n, B);
@@ -73,7 +73,7 @@ constexpr int kScanChunk = 4096;  // elements per scan block (256 threads x 16)
 __global__ void __launch_bounds__(256) ord_scan_sums_kernel(KernelArgs a) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const long long total = (long long)st->size * a.oblocks;
   const long long c0 = blockIdx.x * (long long)kScanChunk;
   if (c0 >= total) return;
@@ -112,7 +112,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot) {
 __global__ void __launch_bounds__(256) ord_scan_top_kernel(KernelArgs a) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const long long total = (long long)st->size * a.oblocks;
   const int chunks = (int)((total + kScanChunk - 1) / kScanChunk);
   __shared__ int warp_tot[8];
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) ord_scan_top_kernel(KernelArgs a) {
 __global__ void __launch_bounds__(256) ord_scan_apply_kernel(KernelArgs a) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const long long total = (long long)st->size * a.oblocks;
   const long long c0 = blockIdx.x * (long long)kScanChunk;
   if (c0 >= total) return;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) ord_scan_apply_kernel(KernelArgs a) {
 __global__ void __launch_bounds__(32) ord_scatter_kernel(KernelArgs a) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = st->size;
   const int B = a.oblocks;
   const long long R = ord_rows_per_block(a.n, B);
@@ -199,7 +199,7 @@ template <typename XT>
 __global__ void __launch_bounds__(32) ord_chain_kernel(KernelArgs a, const XT* __restrict__ X, int zero_cells) {
   pdl_wait();
   const DevState* st = a.st;
-  if (st->done) return;
+  if (pass_off(st)) return;
   const int K = zero_cells ? 1 : st->size;
   const int dim = a.dim;
   const int dchunks = (dim + 31) / 32;

@@ -67,6 +67,10 @@ struct DevState {
   int flag2_count;     // rows whose shortlist overflowed -> full FP64 scan
   unsigned int cmax_bits;  // float bits of max_j ||c~_j|| (centred FP32 codebook)
   int passes;          // allocation passes executed
+  int slabs;           // per-block cell-sum slabs the sums kernel of this pass wrote
+  int skip;            // 1: the fused small-codebook pass did this whole pass (the per-kernel path idles)
+  unsigned bar_count;  // grid barrier of the fused pass (arrivals, generation)
+  unsigned bar_gen;
   int nonfinite;       // set_shift saw a non-finite |x| (host-buffer Lloyd step)
   // tensor-core candidate pass (assign_tc.cu): power-of-two scales of the
   // fp16 hi/lo operand split, chosen on the host from |x| / codebook bounds
@@ -200,6 +204,10 @@ __device__ __forceinline__ double row_dist(const KernelArgs& a, long long row, c
 }
 __device__ __forceinline__ float rin_of(const KernelArgs& a, long long row) { return a.rin ? a.rin[row] : 0.f; }
 
+// A pass kernel has nothing to do once the design is done or when the fused
+// small-codebook pass (pass_small_kernel) already ran this pass.
+__device__ __forceinline__ bool pass_off(const DevState* st) { return st->done || st->skip; }
+
 // Programmatic dependent launch: pass kernels are launched with
 // programmaticStreamSerialization (launch_k), so a kernel's grid is set up
 // while its predecessor drains; each begins with pdl_wait(), which returns
@@ -248,6 +256,8 @@ cudaError_t launch_epilogue(const KernelArgs& a, bool want_dists, bool want_sums
 cudaError_t launch_ordered_update(const KernelArgs& a, bool zero_cells, int sms, cudaStream_t s);
 int ordered_blocks(long long n);
 cudaError_t launch_finalize(const KernelArgs& a, bool stage, cudaStream_t s);
+// the fused single-kernel pass for small codebooks (training loop, one device)
+cudaError_t launch_pass_small(const KernelArgs& a, int sms, cudaStream_t s);
 cudaError_t launch_init_centroid(const KernelArgs& a, bool stage, cudaStream_t s);
 cudaError_t launch_clear(const KernelArgs& a, cudaStream_t s);
 cudaError_t launch_maxabs(const float* x32, const double* x64, long long count,

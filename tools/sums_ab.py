@@ -14,7 +14,8 @@ for which in sys.argv[1:]:
     s = _Session(x, None)
     segs = (ctypes.c_double * 5)()
     fl = ctypes.c_int64()
-    for k in (g["cb"].shape[0], 256, 64):
+    for k in [int(v) for v in os.environ.get("KS", "0,256,64").split(",")]:
+        k = k or g["cb"].shape[0]
         cb = np.ascontiguousarray(g["cb"][:k])
         acc = np.zeros(5)
         for r in range(8):
