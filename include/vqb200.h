@@ -254,6 +254,20 @@ int vqb_rows_f32(vqb_session* s, float* out);
 int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64_t width, int64_t block,
                     int device, vqb_session** out);
 
+/* Session over `rows` rows of an isotropic Gaussian mixture drawn on the
+ * device (replaces the host generators behind the benchmark training sets,
+ * reference bench.py:59-62 / SURVEY 8(f) row 1; no row crosses PCIe).
+ * Component c has mean means[c][dim] and standard deviation sigmas[c]; it is
+ * picked uniformly, or as the first c with u < cum_weights[c] when the
+ * (nondecreasing, ending at 1) cumulative weights are given.  Row g (global
+ * index row_offset + r) draws from Philox4x32-10 with counter (g, call) and
+ * key `seed`, so a shard [row_offset, row_offset + rows) of n_global rows is
+ * the same slice of the same set on any device count.  Every bit is
+ * reproducible on the host (oracle/vq_oracle.c vq_gmm_rows). */
+int vqb_open_gmm(const float* means, const float* sigmas, const double* cum_weights, int64_t components,
+                 int64_t rows, int64_t dim, int64_t row_offset, int64_t n_global, uint64_t seed, int device,
+                 vqb_session** out);
+
 /* Device-resident timing of one imaging kernel (0 pixels_to_blocks f32,
  * 1 pixels_to_blocks f64, 2 blocks_to_pixels, 3 decode, 4 decode_pixels,
  * 5 per-row pair distances): mean ms per launch over `reps` and the

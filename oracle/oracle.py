@@ -69,6 +69,7 @@ def _load():
         lib.vqo_assign_parallel.argtypes = [P, P, I64, I64, P, I64, I, I, P, P]
         lib.vqo_update_parallel.argtypes = [P, I64, I64, P, P, I64, I, P, P]
         lib.vqo_max_threads.restype = ctypes.c_int
+        lib.vqo_gmm_rows.argtypes = [P, P, P, I64, I64, I64, I64, ctypes.c_uint64, P]
         _lib = lib
     return _lib
 
@@ -339,6 +340,19 @@ def top2_gaps(vectors, codebook) -> np.ndarray:
 # * reconstruction_distortion <- codec.reconstruction_distortion (codec.py:135-156)
 # Restated with explicit index maps (block v = (by, bx), element q = (r, c)),
 # not the reference's reshape/swapaxes chain.
+
+def gmm_rows(means, sigmas, cum_weights, rows: int, seed: int, row_offset: int = 0) -> np.ndarray:
+    """Host restatement of the device Gaussian-mixture generator
+    (csrc/gmm.cu gmm_rows_kernel; vq_oracle.c vqo_gmm_rows): float32 rows
+    [row_offset, row_offset + rows) of the set drawn with ``seed``."""
+    m = np.ascontiguousarray(means, dtype=np.float32)
+    sg = np.ascontiguousarray(sigmas, dtype=np.float32)
+    cw = None if cum_weights is None else np.ascontiguousarray(cum_weights, dtype=np.float64)
+    out = np.empty((rows, m.shape[1]), dtype=np.float32)
+    _load().vqo_gmm_rows(_p(m), _p(sg), None if cw is None else _p(cw), m.shape[0], rows, m.shape[1],
+                         row_offset, seed, _p(out))
+    return out
+
 
 def pixels_to_blocks(pixels, block: int) -> np.ndarray:
     """float64 [ceil(h/b) * ceil(w/b)][b*b]; out-of-image samples take the

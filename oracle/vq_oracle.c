@@ -188,3 +188,103 @@ int vqo_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ---- Gaussian-mixture rows: host restatement of the device generator ----
+ * paper_0910_4711_b200/csrc/gmm.cu (gmm_rows_kernel), operation for
+ * operation, so a GPU test can compare every float bit of a device-drawn
+ * training set (and the oracle trains on the same rows).  Philox4x32-10 with
+ * counter (row_lo, row_hi, call, 0) and key (seed_lo, seed_hi); call 0 picks
+ * the component, call 1 + j / 4 gives the uniforms of dimensions j .. j + 3
+ * as two Box-Muller pairs; log and sin / cos by the same fixed series. */
+static void vqo_philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = (uint32_t)p1;
+    c[2] = n2;
+    c[3] = (uint32_t)p0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+static double vqo_unit(uint32_t x) { return ((double)x + 0.5) * 2.3283064365386963e-10; }
+
+static double vqo_gmm_log(double u) {
+  uint64_t b;
+  memcpy(&b, &u, sizeof b);
+  const int e = (int)((b >> 52) & 0x7ff) - 1023;
+  const uint64_t mb = (b & 0xfffffffffffffull) | 0x3ff0000000000000ull;
+  double m;
+  memcpy(&m, &mb, sizeof m);
+  const double s = (m - 1.0) / (m + 1.0);
+  const double s2 = s * s;
+  double t = 1.0 / 27.0;
+  for (int k = 12; k >= 0; --k) t = 1.0 / (double)(2 * k + 1) + s2 * t;
+  return (double)e * 0.6931471805599453 + 2.0 * s * t;
+}
+
+static void vqo_gmm_sincos(double u, double *sn, double *cs) {
+  double fact[22];
+  fact[0] = 1.0;
+  for (int k = 1; k < 22; ++k) fact[k] = fact[k - 1] * (double)k; /* exact below 2^53 * 2^16 */
+  const double t = u * 4.0;
+  const int q = (int)t;
+  const double x = (t - (double)q) * 1.5707963267948966;
+  const double x2 = x * x;
+  double ps = 1.0 / fact[21], pc = 1.0 / fact[20];
+  for (int k = 9; k >= 0; --k) {
+    ps = 1.0 / fact[2 * k + 1] - x2 * ps;
+    pc = 1.0 / fact[2 * k] - x2 * pc;
+  }
+  const double s0 = x * ps, c0 = pc;
+  switch (q & 3) {
+    case 0: *sn = s0; *cs = c0; break;
+    case 1: *sn = c0; *cs = -s0; break;
+    case 2: *sn = -s0; *cs = -c0; break;
+    default: *sn = -c0; *cs = s0; break;
+  }
+}
+
+void vqo_gmm_rows(const float *means, const float *sigmas, const double *cw, int64_t comps, int64_t rows,
+                  int64_t dim, int64_t row0, uint64_t seed, float *out) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    const int64_t g = row0 + r;
+    uint32_t c[4] = {(uint32_t)g, (uint32_t)(g >> 32), 0u, 0u};
+    vqo_philox10(c, k0, k1);
+    const double uc = vqo_unit(c[0]);
+    int64_t comp;
+    if (cw) {
+      int64_t lo = 0, hi = comps - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (uc < cw[mid]) hi = mid; else lo = mid + 1;
+      }
+      comp = lo;
+    } else {
+      comp = (int64_t)(uc * (double)comps);
+      if (comp >= comps) comp = comps - 1;
+    }
+    const double sg = (double)sigmas[comp];
+    const float *mu = means + comp * dim;
+    float *o = out + r * dim;
+    for (int64_t l0 = 0; l0 < dim; l0 += 4) {
+      uint32_t v[4] = {(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)(1 + l0 / 4), 0u};
+      vqo_philox10(v, k0, k1);
+      for (int p = 0; p < 2; ++p) {
+        const double u1 = vqo_unit(v[2 * p]), u2 = vqo_unit(v[2 * p + 1]);
+        const double rad = sqrt(-2.0 * vqo_gmm_log(u1));
+        double sn, cs;
+        vqo_gmm_sincos(u2, &sn, &cs);
+        const int64_t l = l0 + 2 * p;
+        if (l < dim) o[l] = (float)((double)mu[l] + sg * (rad * cs));
+        if (l + 1 < dim) o[l + 1] = (float)((double)mu[l + 1] + sg * (rad * sn));
+      }
+    }
+  }
+}

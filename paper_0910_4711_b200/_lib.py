@@ -116,6 +116,7 @@ def lib():
             "vqb_decode_pixels": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I32, _P], _I32),
             "vqb_reconstruction_distortion": ([_P, _P, _I64, _I64, _I32, _I32, _P], _I32),
             "vqb_open_pixels": ([_P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
+            "vqb_open_gmm": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I64, ctypes.c_uint64, _I32, _P], _I32),
             "vqb_rows_f32": ([_P, _P], _I32),
             "vqb_host_copy": ([_P, _P, _I64], _I32),
             "vqb_lloyd_begin": ([_P, _P, _I64, _P, _P], _I32),

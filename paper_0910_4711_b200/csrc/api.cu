@@ -508,6 +508,43 @@ int vqb_open_pixels(const uint8_t* pixels, int64_t images, int64_t height, int64
   return finish_open(s, out);
 }
 
+int vqb_open_gmm(const float* means, const float* sigmas, const double* cum_weights, int64_t components,
+                 int64_t rows, int64_t dim, int64_t row_offset, int64_t n_global, uint64_t seed, int device,
+                 vqb_session** out) {
+  *out = nullptr;
+  if (!means || !sigmas) return fail(VQB_USAGE, "means and sigmas are required");
+  if (components < 1) return fail(VQB_USAGE, "mixture needs at least one component, got %lld", (long long)components);
+  for (int64_t i = 0; i < components * dim; ++i)
+    if (!std::isfinite(means[i])) return fail(VQB_USAGE, "mean %lld is not finite", (long long)i);
+  for (int64_t i = 0; i < components; ++i)
+    if (!std::isfinite(sigmas[i]) || sigmas[i] < 0.f)
+      return fail(VQB_USAGE, "sigma %lld must be finite and >= 0", (long long)i);
+  if (cum_weights) {
+    for (int64_t i = 0; i < components; ++i)
+      if (!(cum_weights[i] >= (i ? cum_weights[i - 1] : 0.0)) || cum_weights[i] > 1.0)
+        return fail(VQB_USAGE, "cumulative weights must be nondecreasing in [0, 1] (entry %lld)", (long long)i);
+    if (cum_weights[components - 1] != 1.0) return fail(VQB_USAGE, "cumulative weights must end at 1");
+  }
+  std::unique_ptr<vqb_session> s;
+  if (int rc = new_session(rows, dim, row_offset, n_global, device, s)) return rc;
+  float *dm = nullptr, *dsg = nullptr;
+  double* dcw = nullptr;
+  CK(dalloc(&dm, (size_t)(components * dim)));
+  std::unique_ptr<float, decltype(&cudaFree)> g0(dm, &cudaFree);
+  CK(dalloc(&dsg, (size_t)components));
+  std::unique_ptr<float, decltype(&cudaFree)> g1(dsg, &cudaFree);
+  if (cum_weights) CK(dalloc(&dcw, (size_t)components));
+  std::unique_ptr<double, decltype(&cudaFree)> g2(dcw, &cudaFree);
+  CK(cudaMemcpyAsync(dm, means, sizeof(float) * components * dim, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(dsg, sigmas, sizeof(float) * components, cudaMemcpyHostToDevice, s->stream));
+  if (dcw) CK(cudaMemcpyAsync(dcw, cum_weights, sizeof(double) * components, cudaMemcpyHostToDevice, s->stream));
+  CK(dalloc(&s->x32, (size_t)rows * dim + 16));
+  CK(launch_gmm_rows(dm, dsg, dcw, components, rows, (int)dim, row_offset, (unsigned long long)seed, s->x32,
+                     s->sms, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return finish_open(s, out);
+}
+
 }  // extern "C"
 
 static int finish_open(std::unique_ptr<vqb_session>& s, vqb_session** out) {

@@ -290,6 +290,12 @@ inline int candidate_dim(int dim) { return dim <= 16 ? 16 : (dim <= 32 ? 32 : (d
 cudaError_t launch_candidate_rows(const float* x32, const double* x64, long long n, int dim, int cdim,
                                   float* xc, float* rin, int sms, cudaStream_t s);
 
+// Gaussian-mixture rows on the device (gmm.cu): means [comps][dim] f32,
+// sigmas [comps] f32, cw [comps] cumulative weights (nullable: uniform)
+cudaError_t launch_gmm_rows(const float* means, const float* sigmas, const double* cw, long long comps,
+                            long long rows, int dim, long long row0, unsigned long long seed, float* out, int sms,
+                            cudaStream_t s);
+
 // block vectoriser / decode / reconstruction distortion (imaging.cu)
 cudaError_t launch_pixels_to_blocks_f32(const unsigned char* px, long long images, long long H, long long W,
                                         int block, float* out, cudaStream_t s);

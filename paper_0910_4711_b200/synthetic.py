@@ -25,6 +25,10 @@ __all__ = [
     "gaussian_mixture",
     "make_training",
     "make_encode_case",
+    "MixtureParams",
+    "mixture_params",
+    "device_mixture",
+    "make_training_device",
 ]
 
 
@@ -163,3 +167,72 @@ def make_encode_case(n: int | None = None) -> tuple[np.ndarray, np.ndarray]:
     q = gaussian_mixture(np.random.default_rng(spec.seed), spec.n if n is None else n,
                          16, 1024, 2.0, 20.0)
     return cb, q
+
+
+# ---- device-drawn mixtures ----------------------------
+
+@dataclass(frozen=True)
+class MixtureParams:
+    """Component parameters of an isotropic mixture: means [C, dim] f32,
+    sigmas [C] f32, cumulative weights [C] f64 (None: uniform labels)."""
+    means: np.ndarray
+    sigmas: np.ndarray
+    cum_weights: np.ndarray | None
+
+
+def mixture_params(rng: np.random.Generator, dim: int, components: int, sigma_lo: float,
+                   sigma_hi: float, dirichlet: bool = False) -> MixtureParams:
+    """The component draws of ``gaussian_mixture`` (same rng calls, same
+    order), so a device-drawn set samples the same mixture as the host one."""
+    means = rng.uniform(0, 255, (components, dim)).astype(np.float32)
+    sig = rng.uniform(sigma_lo, sigma_hi, components).astype(np.float32)
+    cw = None
+    if dirichlet:
+        cw = np.minimum(np.cumsum(rng.dirichlet(np.ones(components))), 1.0)
+        cw[-1] = 1.0
+    return MixtureParams(means, sig, cw)
+
+
+def device_mixture(params: MixtureParams, n: int, seed: int, row_offset: int = 0,
+                   n_global: int | None = None, device: int | None = None):
+    """A TrainingSet of ``n`` mixture rows drawn on the device (vqb_open_gmm):
+    rows [row_offset, row_offset + n) of the ``n_global``-row set of ``seed``.
+    Nothing but the component parameters crosses PCIe; the host ``vectors``
+    field is downloaded only if something asks for it."""
+    import ctypes
+
+    from . import _lib
+    from .core import TrainingSet, _Session, _device
+
+    m = np.ascontiguousarray(params.means, dtype=np.float32)
+    sg = np.ascontiguousarray(params.sigmas, dtype=np.float32)
+    cw = None if params.cum_weights is None else np.ascontiguousarray(params.cum_weights, dtype=np.float64)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().vqb_open_gmm(
+        _lib.ptr(m), _lib.ptr(sg), _lib.ptr(cw), m.shape[0], n, m.shape[1], row_offset,
+        row_offset + n if n_global is None else n_global, seed,
+        _device() if device is None else device, ctypes.byref(h)))
+    return TrainingSet._on_device(_Session.adopt(h, n, m.shape[1]))
+
+
+_MIXTURES = {  # cfg -> (dim, components, sigma_lo, sigma_hi, dirichlet)
+    "cfg2": (16, 1024, 2.0, 20.0, False),
+    "cfg4": (16, 4096, 1.0, 16.0, True),
+    "cfg5": (16, 1024, 2.0, 20.0, False),
+}
+
+
+def make_training_device(cfg: str, n: int | None = None, row_offset: int = 0,
+                         n_global: int | None = None, device: int | None = None):
+    """The device-drawn counterpart of ``make_training`` for the mixture
+    configs (cfg2, cfg4; cfg5's queries): the same mixture components (same
+    seed, same draws), rows from the counter-based device generator.  A shard
+    [row_offset, row_offset + n) is the same slice of the same set on any
+    number of devices.  Returns (TrainingSet, MixtureParams)."""
+    if cfg not in _MIXTURES:
+        raise ValueError(f"{cfg} is not a mixture workload")
+    spec = WORKLOADS[cfg]
+    params = mixture_params(np.random.default_rng(spec.seed), *_MIXTURES[cfg])
+    rows = spec.n if n is None else n
+    return device_mixture(params, rows, spec.seed, row_offset,
+                          rows + row_offset if n_global is None else n_global, device), params
