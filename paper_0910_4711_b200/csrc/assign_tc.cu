@@ -137,9 +137,9 @@ struct TcMisc {
   uint64_t xs_full[4];     // row tile landed in X stage i % kXsStages
   float qrow[4][kTcRows];  // ||y~||^2 per row of tile i (slot i & 3; -1: row out of fp16 range)
   union {
-    struct {               // kTcTop2: every part's (minimum, band count, index) per row
+    struct {               // kTcTop2: every part's (minimum, second minimum, index) per row
       float m1[P][kTcRows];
-      int cnt[P][kTcRows];
+      float m2[P][kTcRows];
       int i1[P][kTcRows];
       float q[kTcRows];
     } res[2];
@@ -392,12 +392,12 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       mbar_wait_sleep(&m->res_full[rb], (uint32_t)((i >> 1) & 1), kSleepNs);
     else
       pwait(&m->res_full[rb], (uint32_t)((i >> 1) & 1), 0);
-    float pm[C::kParts];
-    int pc[C::kParts], pi[C::kParts];
+    float pm[C::kParts], p2[C::kParts];
+    int pi[C::kParts];
 #pragma unroll
     for (int p = 0; p < C::kParts; ++p) {
       pm[p] = m->merge.res[rb].m1[p][r];
-      pc[p] = m->merge.res[rb].cnt[p][r];
+      p2[p] = m->merge.res[rb].m2[p][r];
       pi[p] = m->merge.res[rb].i1[p][r];
     }
     const float qcur = m->merge.res[rb].q[r];
@@ -406,30 +406,28 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
     const long long entry = t * kTcRows + r;
     const bool valid = entry < nitems;
     const long long row = a.r0 + entry;
-    // merge the parts: the band above the row's minimum; a part whose
-    // minimum lies above it has nothing inside
-    float M1 = pm[0];
+    // merge the parts' exact top-2: the row's minimum M1 (first part holding
+    // it), and its second minimum M2 = min(the winner part's second minimum,
+    // every other part's minimum); equal minima in two parts give M2 = M1
+    float M1 = pm[0], M2 = p2[0];
+    int i1 = pi[0];
 #pragma unroll
-    for (int p = 1; p < C::kParts; ++p) M1 = fminf(M1, pm[p]);
+    for (int p = 1; p < C::kParts; ++p) {
+      const bool lt = pm[p] < M1;
+      M2 = fminf(lt ? p2[p] : M2, lt ? M1 : pm[p]);
+      i1 = lt ? pi[p] : i1;
+      M1 = lt ? pm[p] : M1;
+    }
     const float E = tc_band<L>(M1 * inv, qcur, sqrtf(fmaxf(qcur, 0.f)), eyw);
-    // float64 rows: + the band of their float32 rounding (the epilogue's
-    // count used the same widened band)
+    // float64 rows: + the band of their float32 rounding
     const float band = 3.0f * E + input_band(valid ? rin_of(a, row) : 0.f, M1 * inv + qcur, 3.0f * E);
     const float thr_s = fmaf(band, dscale, M1);
-    int total = 0, i1 = 0;
-#pragma unroll
-    for (int p = 0; p < C::kParts; ++p) {
-      if (pm[p] <= thr_s && pc[p] > 0) {
-        total += pc[p];
-        i1 = pi[p];
-      }
-    }
     // certified iff the minimum is the only value within 3E of it (see the
     // header comment and assign_chunk in kernels.cu)
     bool flag = false;
     float thr = NAN;
     if (valid) {
-      flag = qcur < 0.f || total != 1;
+      flag = qcur < 0.f || !(M2 > thr_s);
       thr = M1 * inv + band;
       a.idx[row] = i1;
       if (!flag && a.dists) {
@@ -661,11 +659,13 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
 
     long long g = 0;
     for (long long i = 0; i < my_tiles; ++i) {
-      // kTcTop2: running minimum m1, the number of values inside the band
-      // above it (cnt) and the index of the last one (i1); kTcShortlist:
-      // candidate list
-      float m1 = INFINITY;
-      int i1 = 0, cnt = 0;
+      // kTcTop2: running top-2 of the block minima (b1, b2; blk = first block
+      // at b1) and the 16 class chains; kTcShortlist: candidate list
+      float b1 = INFINITY, b2 = INFINITY;
+      int blk = 0;
+      float ach[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) ach[t] = INFINITY;
       int nc = 0;
       int cand[kTcShort] = {0, 0, 0, 0, 0, 0, 0, 0};
       float thr_d = -INFINITY;
@@ -673,12 +673,12 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       bool valid;
       const long long row = row_of(i, entry, valid);
       if (MODE == kTcShortlist && valid) thr_d = a.flag_thr[entry] * dscale;  // NaN stays NaN -> overflow
-      float qcur = 0.f, yn = 0.f, rn = 0.f;
+      float qcur = 0.f;
       if constexpr (MODE == kTcTop2) {
-        pwait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1), 0);
-        qcur = m->qrow[i & 3][r];
-        yn = sqrtf(fmaxf(qcur, 0.f));
-        rn = valid ? rin_of(a, row) : 0.f;  // float64 rows: rounding band
+        if (h == 0) {
+          pwait(&m->q_full[i & 3], (uint32_t)((i >> 2) & 1), 0);
+          qcur = m->qrow[i & 3][r];
+        }
       }
       for (int c = 0; c < nch; ++c, ++g) {
         const int s = (int)(g & 1);
@@ -700,102 +700,47 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           }
           tmem_wait_ld();
         };
-        if constexpr (MODE == kTcTop2 && pipe_ld<L>()) {
-          // Same two reads, 16 columns per tcgen05.ld, software-pipelined:
-          // the load of group g+1 is in flight while group g is processed
-          // (ld(0) wait | ld(1) proc(0) wait | ld(2) proc(1) wait | ...), so the
-          // TMEM load latency overlaps the ALU chains with the same 32
-          // registers the unpipelined x32 form used.
-          const int ng = span / 16;
+        if constexpr (MODE == kTcTop2) {
+          // ONE read of the chunk, exact top-2 by minima only (half a 3-input
+          // FMNMX per value and partition, no per-value compare): the values
+          // of a part are covered by two partitions -- 16 persistent chains
+          // by column mod 16 (A) and blocks of 16 consecutive columns (B,
+          // folded into a running top-2 of the block minima).  Any two
+          // columns differ in class or in block, so the row's second minimum
+          // is min(second smallest A chain, second smallest block minimum);
+          // its minimum is at (first block holding it) + (class holding it).
           const uint32_t cbase = trow + (uint32_t)(s * kTcChunk + h * span);
-          float va[16], vb[16];
-          float c4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-          auto pmin = [&](const float (&v)[16]) {
-#pragma unroll
-            for (int t = 0; t < 16; t += 2) c4[(t >> 1) & 3] = fminf(c4[(t >> 1) & 3], fminf(v[t], v[t + 1]));
-          };
-          tmem_ld16(cbase, va);
-          tmem_wait_ld();
-#pragma unroll 1
-          for (int g2 = 0; g2 < ng; g2 += 2) {
-            if (g2 + 1 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 1) * 16), vb);
-            pmin(va);
-            tmem_wait_ld();
-            if (g2 + 2 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 2) * 16), va);
-            if (g2 + 1 < ng) pmin(vb);
-            tmem_wait_ld();
-          }
-          const float cm = fminf(fminf(c4[0], c4[1]), fminf(c4[2], c4[3]));
-          const float mnew = fminf(m1, cm);
-          const float e3 = 3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw);
-          const float thr = fmaf(e3 + input_band(rn, mnew * inv + qcur, e3), dscale, mnew);
-          if (cm < m1 && m1 > thr) cnt = 0;  // see the unpipelined form below
-          m1 = mnew;
           const int jb0 = c * kTcChunk + h * span;
-          auto pcount = [&](const float (&v)[16], int g) {
-            unsigned acc4[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-            for (int t = 0; t < 16; ++t)
-              asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
-                  : "+r"(acc4[t & 3])
-                  : "f"(v[t]), "f"(thr), "r"(0x10000u + (unsigned)t));
-            const unsigned acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-            if (acc) {
-              cnt += (int)(acc >> 16);
-              i1 = jb0 + g * 16 + (int)(acc & 0xffffu);  // exact when alone
-            }
+          auto fold = [&](float mu, int jb) {  // block minimum into the running top-2
+            const bool lt = mu < b1;
+            b2 = fminf(b2, fmaxf(b1, mu));
+            b1 = fminf(b1, mu);
+            blk = lt ? jb : blk;
           };
-          tmem_ld16(cbase, va);
-          tmem_wait_ld();
+          auto min16 = [&](const float* v) {
+            const float t0 = fminf(fminf(v[0], v[1]), v[2]), t1 = fminf(fminf(v[3], v[4]), v[5]);
+            const float t2 = fminf(fminf(v[6], v[7]), v[8]), t3 = fminf(fminf(v[9], v[10]), v[11]);
+            const float t4 = fminf(fminf(v[12], v[13]), v[14]);
+            return fminf(fminf(fminf(t0, t1), t2), fminf(fminf(t3, t4), v[15]));
+          };
+          if (span >= 32) {
 #pragma unroll 1
-          for (int g2 = 0; g2 < ng; g2 += 2) {
-            if (g2 + 1 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 1) * 16), vb);
-            pcount(va, g2);
-            tmem_wait_ld();
-            if (g2 + 2 < ng) tmem_ld16(cbase + (uint32_t)((g2 + 2) * 16), va);
-            if (g2 + 1 < ng) pcount(vb, g2 + 1);
-            tmem_wait_ld();
-          }
-        } else if constexpr (MODE == kTcTop2) {
-          // two reads of the chunk: its minimum (3-input FMNMX, 0.5 op per
-          // value), then one compare per value against the band above the
-          // running minimum (count + index packed in one predicated add)
-          float cm = INFINITY;
-#pragma unroll 1
-          for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
-            float v[32];
-            load(q4, v);
-            // four independent FMNMX3 chains (a single chain of 16 is
-            // latency-bound: the epilogue's top stall was the fixed-latency
-            // dependency wait)
-            float c4[4] = {cm, INFINITY, INFINITY, INFINITY};
+            for (int q4 = 0; q4 < span / 32; ++q4) {
+              float v[32];
+              tmem_ld32(cbase + (uint32_t)(q4 * 32), v);
+              tmem_wait_ld();
 #pragma unroll
-            for (int t = 0; t < 32; t += 2) c4[(t >> 1) & 3] = fminf(c4[(t >> 1) & 3], fminf(v[t], v[t + 1]));
-            cm = fminf(fminf(c4[0], c4[1]), fminf(c4[2], c4[3]));
-          }
-          const float mnew = fminf(m1, cm);
-          const float e3 = 3.0f * tc_band<L>(mnew * inv, qcur, yn, eyw);
-          const float thr = fmaf(e3 + input_band(rn, mnew * inv + qcur, e3), dscale, mnew);
-          // a new minimum far below the old one: every earlier value is >= the
-          // old minimum > thr, so the count restarts (otherwise it is kept,
-          // which can only over-count)
-          if (cm < m1 && m1 > thr) cnt = 0;
-          m1 = mnew;
-#pragma unroll 1
-          for (int q4 = 0; q4 < (span + 31) / 32; ++q4) {
-            float v[32];
-            load(q4, v);
-            unsigned acc4[4] = {0u, 0u, 0u, 0u};  // four chains
-#pragma unroll
-            for (int t = 0; t < 32; ++t)  // FSETP + predicated IADD
-              asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
-                  : "+r"(acc4[t & 3])
-                  : "f"(v[t]), "f"(thr), "r"(0x10000u + (unsigned)t));
-            const unsigned acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-            if (acc) {
-              cnt += (int)(acc >> 16);
-              i1 = c * kTcChunk + h * span + q4 * 32 + (int)(acc & 0xffffu);  // exact when alone
+              for (int t = 0; t < 16; ++t) ach[t] = fminf(fminf(v[t], v[t + 16]), ach[t]);
+              fold(min16(v), jb0 + q4 * 32);
+              fold(min16(v + 16), jb0 + q4 * 32 + 16);
             }
+          } else {
+            float v[16];
+            tmem_ld16(cbase, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 16; ++t) ach[t] = fminf(v[t], ach[t]);
+            fold(min16(v), jb0);
           }
         } else {
 #pragma unroll 1
@@ -834,11 +779,21 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       }
       if constexpr (MODE == kTcTop2) {
         // hand the tile's per-part results to the certification warps
+        // the part's top-2: the chains' second smallest (as a multiset: two
+        // classes at the minimum give s2 = s1) and the class of the minimum
+        float s1 = INFINITY, s2 = INFINITY;
+        int cls = 0;
+#pragma unroll
+        for (int t = 15; t >= 0; --t) {
+          s2 = fminf(s2, fmaxf(s1, ach[t]));
+          s1 = fminf(s1, ach[t]);
+          cls = ach[t] == b1 ? t : cls;
+        }
         const int rb = (int)(i & 1);
         pwait(&m->res_empty[rb], (uint32_t)(((i >> 1) & 1) ^ 1), 2);
-        m->merge.res[rb].m1[h][r] = m1;
-        m->merge.res[rb].cnt[h][r] = cnt;
-        m->merge.res[rb].i1[h][r] = i1;
+        m->merge.res[rb].m1[h][r] = b1;
+        m->merge.res[rb].m2[h][r] = fminf(b2, s2);
+        m->merge.res[rb].i1[h][r] = blk + cls;
         if (h == 0) m->merge.res[rb].q[r] = qcur;
         mbar_arrive(&m->res_full[rb]);
         if (!C::kCertWarps && h == 0) certify(i, r);

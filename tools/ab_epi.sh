@@ -1,0 +1,8 @@
+# A/B of two libvqb200.so builds (A = previous, B = current): step segments at cfg4 / cfg2 / cfg3 sizes,
+# per-level design times, then the GPU parity suite on B
+export A=${A:-paper_0910_4711_b200/libvqb200_prev.so} B=${B:-paper_0910_4711_b200/libvqb200.so}
+for c in "cfg4" "cfg4 1024" "cfg4 256" "cfg4 64" "cfg2" "cfg2 256" "cfg2 64" "cfg3" "cfg3 64"; do
+  for lib in $A $B $A $B; do echo -n "$c $lib: "; VQB200_LIB=$lib timeout 300 python tools/profile_step.py $c 2>&1 | tail -1; done
+done
+for lib in $A $B; do echo "== levels $lib"; VQB200_LIB=$lib python tools/design_levels.py cfg2; VQB200_LIB=$lib python tools/design_levels.py cfg3; VQB200_LIB=$lib python tools/design_levels.py cfg4; done
+if [ -n "$PARITY" ]; then timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu.log; fi
