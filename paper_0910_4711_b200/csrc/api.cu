@@ -127,6 +127,13 @@ struct vqb_session {
   bool fast = false;
   bool ordered = false;
   bool fused_ok = false;  // vqb_train on one device: the fused small-codebook pass leads every pass
+  // incremental cell sums of the training loop (kernels.cu moved_scan_kernel):
+  // previous cells, moved list, running local sums; allocated by the first design
+  int* idx_prev = nullptr;
+  int* mv = nullptr;
+  long long* acc = nullptr;
+  bool delta_on = false;
+  double delta_frac = 0.3;
   bool pending_init = false;
   long long lloyd_size = 0;  // vqb_lloyd_begin
   cudaEvent_t ev_batch[2] = {nullptr, nullptr};
@@ -204,6 +211,11 @@ struct vqb_session {
     a.obase = obase;
     a.oscan = oscan;
     a.oblocks = oblocks;
+    a.idx_prev = delta_on ? idx_prev : nullptr;
+    a.mv = delta_on ? mv : nullptr;
+    a.mv_cap = n + 32;
+    a.acc = delta_on ? acc : nullptr;
+    a.delta_max = (long long)((double)n * delta_frac);
     a.st = st;
     return a;
   }
@@ -219,6 +231,8 @@ struct vqb_session {
     cudaFree(partials);
     cudaFree(ord);
     cudaFree(tcb);
+    cudaFree(acc);
+    acc = nullptr;
     ord = nullptr;
     tcb = nullptr;
     cb[0] = cb[1] = nullptr;
@@ -271,6 +285,9 @@ struct vqb_session {
     cudaFree(operm);
     cudaFree(obase);
     cudaFree(oscan);
+    cudaFree(idx_prev);
+    cudaFree(mv);
+    cudaFree(acc);
     cudaFree(st);
     cudaFree(scratch);
     if (st_host) cudaFreeHost(st_host);
@@ -350,6 +367,30 @@ struct vqb_session {
     }
     CK(cudaStreamSynchronize(copy_stream));
     drained = upto;
+    return VQB_OK;
+  }
+
+  // buffers of the incremental cell sums (VQB_DELTA=0 turns them off;
+  // VQB_DELTA_FRAC: the moved fraction up to which a pass updates the running
+  // sums instead of summing every row)
+  int ensure_delta() {
+    const char* e = getenv("VQB_DELTA");
+    delta_on = !(e && strcmp(e, "0") == 0);
+    if (!delta_on) return VQB_OK;
+    const char* f = getenv("VQB_DELTA_FRAC");
+    const double v = f ? atof(f) : 0.3;
+    delta_frac = v >= 0.0 && v <= 1.0 ? v : 0.3;
+    if (!idx_prev) {
+      drop_graph();
+      CK(dalloc(&idx_prev, (size_t)n + 32));
+      CK(cudaMemsetAsync(idx_prev, 0xff, sizeof(int) * (n + 32), stream));
+    }
+    if (!mv) CK(dalloc(&mv, (size_t)(3 * (n + 32))));
+    if (!acc) {
+      drop_graph();
+      CK(dalloc(&acc, (size_t)(2 * kmax * dim + kmax)));
+      CK(cudaMemsetAsync(acc, 0, sizeof(long long) * (2 * kmax * dim + kmax), stream));
+    }
     return VQB_OK;
   }
 
@@ -810,6 +851,10 @@ int vqb_step_begin(vqb_session* s, const vqb_train_config* cfg) {
   if (s->ordered) {
     rc = s->ensure_ordered(cfg->target_size);
     if (rc) return rc;
+    s->delta_on = false;
+  } else {
+    rc = s->ensure_delta();
+    if (rc) return rc;
   }
   h->target = (int)cfg->target_size;
   h->max_iter = (int)cfg->max_iterations_per_level;
@@ -895,6 +940,7 @@ extern "C" int vqb_lloyd_begin(vqb_session* s, const double* codebook, int64_t s
     CK(cudaMemcpyAsync(&s->st->ordered, &s->st_host->ordered, sizeof(int), cudaMemcpyHostToDevice, s->stream));
   }
   s->lloyd_size = size;
+  s->delta_on = false;  // a stateless pass: every row is summed
   s->pending_init = false;
   KernelArgs a = s->args();
   CK(launch_clear(a, s->stream));
@@ -916,7 +962,7 @@ int vqb_session::batch_graph(int batch) {
     enabled = (e && strcmp(e, "0") == 0) ? 0 : 1;
   }
   if (!enabled || !own_stream) return VQB_OK;  // a caller's stream: plain launches
-  const int key = (fast ? 1 : 0) | (ordered ? 2 : 0) | (fused_ok ? 4 : 0) | (batch << 3);
+  const int key = (fast ? 1 : 0) | (ordered ? 2 : 0) | (fused_ok ? 4 : 0) | (delta_on ? 8 : 0) | (batch << 4);
   if (graph && graph_kmax == kmax && graph_key == key) return VQB_OK;
   drop_graph();
   cudaGraph_t g = nullptr;
@@ -967,6 +1013,7 @@ int vqb_step_result(vqb_session* s, double* codebook_out, vqb_level_iteration* h
   DevState* h = s->st_host;
   CK(cudaMemcpy(h, s->st, kStateHeader, cudaMemcpyDeviceToHost));
   if (!h->done) return fail(VQB_INTERNAL, "training loop has not finished");
+  s->delta_on = false;  // the running sums belong to the finished design
   const long long nh = h->n_hist;
   if (int rc = s->drain_hist(nh)) return rc;
   const std::vector<HistRec>& recs = s->hist_raw;

@@ -48,10 +48,11 @@ namespace vqb {
 #define VQB_SLEEP_NS 20000
 #endif
 constexpr uint32_t kSleepNs = VQB_SLEEP_NS;
-// epilogue TMEM reads: 16-column loads software-pipelined, or 32-column
-// loads waited on at once.  Pipelining pays with 8 epilogue warps (L >= 32:
-// cfg3 pass -8 %) and costs with 16 (L = 16: +14 %, the warps already hide
-// the load latency and the extra loop control is on the issue-bound path).
+// epilogue TMEM reads: 32-column loads double-buffered in registers (the next
+// group's load in flight while this one is scanned), or waited on at once.
+// Pipelining pays with 8 epilogue warps (L >= 32: cfg3 pass -5 %); with 16
+// (L = 16) the warps already hide the load latency and 64 value registers do
+// not fit.
 // VQB_PIPE_LD=0/1 forces one form (A/B builds).
 #ifndef VQB_PIPE_LD
 #define VQB_PIPE_LD -1
@@ -372,10 +373,20 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
 
   // certification of tile i's row r from the parts' results in res[i & 1]
   // (kTcTop2; run by a certification warp, or by epilogue part 0 at L = 64)
+  // loop invariants of the certification (the mbarrier waits are memory
+  // clobbers: inside the lambda they would be reloaded / recomputed per tile)
+  const float c_dscale = ldexpf(1.0f, st->tc_ey + st->tc_ew);
+  const float c_inv = 1.0f / c_dscale;
+  const float c_eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
+  const double* const c_cb = a.cb[st->cur];
+  const bool c_euclid = st->metric == kEuclidean;
+  constexpr bool kHoist = L >= 32;  // at L = 16 the registers they hold cost more (K = 4096: +3 % time)
   auto certify = [&](long long i, int r) {
-    const float dscale = ldexpf(1.0f, st->tc_ey + st->tc_ew);
-    const float inv = 1.0f / dscale;
-    const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
+    const float dscale = kHoist ? c_dscale : ldexpf(1.0f, st->tc_ey + st->tc_ew);
+    const float inv = kHoist ? c_inv : 1.0f / dscale;
+    const float eyw = kHoist ? c_eyw
+                             : sqrtf((float)L) * 5.9604645e-8f *
+                                   (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
     const int rb = (int)(i & 1);
     {
       // the row's coordinates for the FP64 winner distance are fetched into
@@ -430,11 +441,15 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       flag = qcur < 0.f || !(M2 > thr_s);
       thr = M1 * inv + band;
       a.idx[row] = i1;
+#ifdef VQB_EXP_NODIST
+      if (false) {
+#else
       if (!flag && a.dists) {
+#endif
         // exact FP64 distance to the certified winner (_kernels.py:25-34);
         // the row is L2-resident from its conversion
-        const double d = row_dist<L>(a, row, a.cb[st->cur], i1);
-        a.dists[row] = st->metric == kEuclidean ? sqrt(d) : d;
+        const double d = row_dist<L>(a, row, kHoist ? c_cb : a.cb[st->cur], i1);
+        a.dists[row] = (kHoist ? c_euclid : st->metric == kEuclidean) ? sqrt(d) : d;
       }
     }
     const int lane = threadIdx.x & 31;
@@ -534,6 +549,15 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           bulk_g2s(sA + b * C::kABytes, a.aimg + tg * (2LL * kTcRows * L), kImgBytes, &m->a_full[b]);
           mbar_arrive_expect_tx(&m->q_full[i & 3], kTcRows * 4u);
           bulk_g2s(&m->qrow[i & 3][0], a.aq + tg * kTcRows, kTcRows * 4u, &m->q_full[i & 3]);
+          // the certification warps read the tile's float32 rows for the FP64
+          // winner distances two tiles later: bring them into L2 now (with
+          // the image nothing else touches x32, and that HBM round trip per
+          // tile bounded the single-chunk passes)
+          if (L >= 32 && MODE == kTcTop2 && a.x32 && a.dim == L && a.dists) {  // (at L = 16: +1 % time)
+            const long long row0 = tg * kTcRows;
+            const long long rows = min((long long)kTcRows, a.n - row0);
+            if (rows > 0) bulk_prefetch_l2(a.x32 + row0 * L, (uint32_t)(rows * L * 4));
+          }
         }
       }
     } else {
@@ -723,16 +747,38 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
             const float t4 = fminf(fminf(v[12], v[13]), v[14]);
             return fminf(fminf(fminf(t0, t1), t2), fminf(fminf(t3, t4), v[15]));
           };
-          if (span >= 32) {
-#pragma unroll 1
-            for (int q4 = 0; q4 < span / 32; ++q4) {
-              float v[32];
-              tmem_ld32(cbase + (uint32_t)(q4 * 32), v);
-              tmem_wait_ld();
+          auto scan32 = [&](const float (&v)[32], int q4) {
 #pragma unroll
-              for (int t = 0; t < 16; ++t) ach[t] = fminf(fminf(v[t], v[t + 16]), ach[t]);
-              fold(min16(v), jb0 + q4 * 32);
-              fold(min16(v + 16), jb0 + q4 * 32 + 16);
+            for (int t = 0; t < 16; ++t) ach[t] = fminf(fminf(v[t], v[t + 16]), ach[t]);
+            fold(min16(v), jb0 + q4 * 32);
+            fold(min16(v + 16), jb0 + q4 * 32 + 16);
+          };
+          if (span >= 32) {
+            if (pipe_ld<L>() && span >= 64) {
+              // 8 epilogue warps (2 per scheduler): the load of group g + 1 is
+              // in flight while group g is scanned (two register buffers)
+              const int ng = span / 32;
+              float va[32], vb[32];
+              tmem_ld32(cbase, va);
+#pragma unroll 1
+              for (int q4 = 0; q4 < ng; q4 += 2) {
+                tmem_wait_ld();
+                if (q4 + 1 < ng) tmem_ld32(cbase + (uint32_t)((q4 + 1) * 32), vb);
+                scan32(va, q4);
+                if (q4 + 1 < ng) {
+                  tmem_wait_ld();
+                  if (q4 + 2 < ng) tmem_ld32(cbase + (uint32_t)((q4 + 2) * 32), va);
+                  scan32(vb, q4 + 1);
+                }
+              }
+            } else {
+#pragma unroll 1
+              for (int q4 = 0; q4 < span / 32; ++q4) {
+                float v[32];
+                tmem_ld32(cbase + (uint32_t)(q4 * 32), v);
+                tmem_wait_ld();
+                scan32(v, q4);
+              }
             }
           } else {
             float v[16];
@@ -783,12 +829,16 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         // classes at the minimum give s2 = s1) and the class of the minimum
         float s1 = INFINITY, s2 = INFINITY;
         int cls = 0;
+#ifdef VQB_EXP_NOTAIL
+        s2 = ach[0] + ach[7];
+#else
 #pragma unroll
         for (int t = 15; t >= 0; --t) {
           s2 = fminf(s2, fmaxf(s1, ach[t]));
           s1 = fminf(s1, ach[t]);
           cls = ach[t] == b1 ? t : cls;
         }
+#endif
         const int rb = (int)(i & 1);
         pwait(&m->res_empty[rb], (uint32_t)(((i >> 1) & 1) ^ 1), 2);
         m->merge.res[rb].m1[h][r] = b1;

@@ -1217,6 +1217,7 @@ __global__ void __launch_bounds__(sum_threads<DIM>(), 1) sums_kernel(KernelArgs 
   // small_only: launched beside sums_red_kernel (one graph serves every
   // level); this kernel takes the passes whose codebook fits warp tables
   if (small_only && !sums_warp_sink(K, dim, sum_threads<DIM>())) return;
+  if (delta_go(a, st)) return;  // the incremental branch updates the running sums instead
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) st->slabs = gridDim.x;
   const int t_lo = st->lo_shift;  // per-column shifts: a.cshift
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1490,6 +1491,9 @@ __device__ __forceinline__ void load4(const XT* __restrict__ p, int valid, bool 
 }
 
 template <typename XT, int LP, int M>
+__device__ __forceinline__ void sums_delta_body(const KernelArgs& a, const XT* __restrict__ X, const LimbPlan& pl);
+
+template <typename XT, int LP, int M>
 __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT* __restrict__ X, int zero_cells,
                                                           LimbPlan pl) {
   pdl_wait();
@@ -1497,6 +1501,10 @@ __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT
   if (pass_off(st)) return;
   const int K = zero_cells ? 1 : st->size;
   const int dim = a.dim;
+  if (delta_go(a, st)) {  // the incremental pass: only the rows that changed cell (same tables, same plan)
+    sums_delta_body<XT, LP, M>(a, X, pl);
+    return;
+  }
   if (pl.small_cut > 0 && K <= pl.small_cut) return;  // sums_kernel's warp tables take this pass
   if (blockIdx.x == 0 && threadIdx.x == 0) st->slabs = pl.chunks;
   const int t = st->lo_shift;  // == fixed_lo_shift(n_global), what the plan was made for
@@ -1507,9 +1515,12 @@ __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT
   const int d0 = piece * LP;
   constexpr int TPR = LP / 4;  // threads per row: 4 coordinates each
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned* tab = reinterpret_cast<unsigned*>(smem_raw);     // [K][LP][m]
-  unsigned* cnt = tab + (long long)K * LP * m;                // [K]
-  const long long twords = (long long)K * (LP * m + 1);
+  // one record per cell: LP x m limb counters + the row count.  The record
+  // length is odd, so the records of the random cells a warp touches spread
+  // over all 32 banks (LP x m alone is a multiple of 4: a quarter of them)
+  constexpr int kRec = LP * M + 1;
+  unsigned* tab = reinterpret_cast<unsigned*>(smem_raw);     // [K][LP x m | count]
+  const long long twords = (long long)K * kRec;
   for (long long i = threadIdx.x; i < twords; i += blockDim.x) tab[i] = 0;
   __syncthreads();
   const long long r0 = chunk * pl.rows;
@@ -1554,8 +1565,8 @@ __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT
     for (int u = 0; u < U; ++u) {
       const int c = cc[u];
       if (c < 0) continue;
-      if (g0 == 0) atomicAdd(cnt + c, 1u);
-      unsigned* e = tab + (unsigned)c * (unsigned)(LP * M) + (unsigned)(g0 * M);
+      if (g0 == 0) atomicAdd(tab + (unsigned)c * (unsigned)kRec + (unsigned)(LP * M), 1u);
+      unsigned* e = tab + (unsigned)c * (unsigned)kRec + (unsigned)(g0 * M);
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         long long h;
@@ -1579,13 +1590,13 @@ __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT
     const long long c = i / LP;
     const int ll = (int)(i % LP);
     if (d0 + ll >= dim) continue;
-    const unsigned* e = tab + i * m;
+    const unsigned* e = tab + c * kRec + ll * m;
     long long v = 0;
     for (int j = 0; j < m; ++j) v += (long long)e[j] << (w * j);
-    slab[c * dim + d0 + ll] = v - (long long)cnt[c] * bias;
+    slab[c * dim + d0 + ll] = v - (long long)tab[c * kRec + LP * M] * bias;
   }
   if (piece == 0)
-    for (long long c = threadIdx.x; c < K; c += blockDim.x) slab[(long long)K * dim + c] = cnt[c];
+    for (long long c = threadIdx.x; c < K; c += blockDim.x) slab[(long long)K * dim + c] = tab[c * kRec + LP * M];
 }
 
 // Launch the limb-RED sums when the plan fits (K large enough that the
@@ -1629,17 +1640,293 @@ static cudaError_t launch_sums_red(const KernelArgs& a, const XT* X, bool zero_c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Incremental cell sums of the training loop (vqb200_internal.h delta_go).
+// moved_scan_kernel compares the pass's cells with the previous pass's, lists
+// the rows that changed cell and brings idx_prev up to date; sums_delta_kernel
+// adds each listed row into its new cell and takes it out of its old one in
+// the limb tables of sums_red_kernel (a removal adds the negated limbs: the
+// 32-bit counters are read back as signed, so a CTA flushes before either
+// side of a counter can reach 2^31); reduce_partials_kernel adds the slabs to
+// the running sums `acc` and publishes them in the exchange buffer -- or,
+// after a pass that summed every row, keeps that pass's local sums as the new
+// running sums.  Reference: _kernels.update_rows (_kernels.py:39-66)
+// computes the same sums from scratch every pass.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) moved_scan_kernel(KernelArgs a) {
+  pdl_wait();
+  DevState* st = a.st;
+  if (pass_off(st) || !delta_track(a, st)) return;
+  const bool list = st->acc_size == st->size;  // else: this pass sums every row; only idx_prev is refreshed
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int wtot[kScanThreads / 32];
+  __shared__ int bbase;
+  const long long items = (a.n + 3) / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // whole blocks iterate (the list positions of a block's rows come from one
+  // global atomic per block and iteration)
+  for (long long b0 = (long long)blockIdx.x * blockDim.x; b0 < items; b0 += stride) {
+    const long long i = b0 + threadIdx.x;
+    int cur[4] = {0, 0, 0, 0}, prv[4] = {0, 0, 0, 0};
+    unsigned m = 0;
+    if (i < items) {
+      const long long r = 4 * i;
+      if (r + 3 < a.n) {
+        const int4 c = *reinterpret_cast<const int4*>(a.idx + r);
+        const int4 q = *reinterpret_cast<const int4*>(a.idx_prev + r);
+        cur[0] = c.x; cur[1] = c.y; cur[2] = c.z; cur[3] = c.w;
+        prv[0] = q.x; prv[1] = q.y; prv[2] = q.z; prv[3] = q.w;
+      } else {
+        for (int k = 0; k < 4; ++k)
+          if (r + k < a.n) {
+            cur[k] = a.idx[r + k];
+            prv[k] = a.idx_prev[r + k];
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) m |= (cur[k] != prv[k]) ? (1u << k) : 0u;
+      if (m) {
+        if (r + 3 < a.n) {
+          *reinterpret_cast<int4*>(a.idx_prev + r) = make_int4(cur[0], cur[1], cur[2], cur[3]);
+        } else {
+          for (int k = 0; k < 4; ++k)
+            if (r + k < a.n) a.idx_prev[r + k] = cur[k];
+        }
+      }
+    }
+    if (!list) continue;  // uniform over the grid
+    const int cnt = __popc(m);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int t = wtot[lane];
+      int ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += v;
+      }
+      wtot[lane] = ti - t;  // exclusive warp offsets
+      if (lane == 31) bbase = ti > 0 ? atomicAdd(&st->nmoved, ti) : 0;
+    }
+    __syncthreads();
+    long long pos = (long long)bbase + wtot[warp] + incl - cnt;
+    __syncthreads();  // wtot / bbase are rewritten by the next iteration
+    // past delta_max the pass sums every row anyway: the list is not read
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if ((m >> k) & 1u) {
+        if (pos < a.mv_cap) {
+          a.mv[pos] = (int)(4 * i + k);
+          a.mv[a.mv_cap + pos] = prv[k];
+          a.mv[2 * a.mv_cap + pos] = cur[k];
+        }
+        ++pos;
+      }
+  }
+}
+
+__device__ __forceinline__ void add_lo_acc(const KernelArgs& a, long long cell, int l, long long lo) {
+  long long* acc_lo = a.acc + a.kmax * a.dim + a.kmax;
+  if (lo) atomicAdd(reinterpret_cast<unsigned long long*>(acc_lo + cell * a.dim + l), (unsigned long long)lo);
+}
+
+constexpr long long kDeltaMinEntries = 1024;  // listed rows per CTA before another CTA (and slab) joins
+template <typename XT, int LP, int M>
+__device__ __forceinline__ void sums_delta_body(const KernelArgs& a, const XT* __restrict__ X, const LimbPlan& pl) {
+  DevState* st = a.st;
+  const long long nm = st->nmoved;
+  if (nm == 0) return;  // the slab reduction republishes the running sums
+  const int K = st->size;
+  const int dim = a.dim;
+  // few listed rows: few CTAs (and slabs to reduce afterwards)
+  long long used = (nm + kDeltaMinEntries - 1) / kDeltaMinEntries;
+  used = used < pl.chunks ? used : pl.chunks;
+  if (blockIdx.x / pl.pieces >= used) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->slabs = (int)used;
+  const int t = st->lo_shift;
+  constexpr int m = M;
+  const int w = pl.w;
+  const int piece = blockIdx.x % pl.pieces;
+  const long long chunk = blockIdx.x / pl.pieces;
+  const int d0 = piece * LP;
+  constexpr int TPR = LP / 4;
+  constexpr int kRec = LP * M + 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned* tab = reinterpret_cast<unsigned*>(smem_raw);  // [K][LP x m | count], signed mod 2^32
+  const long long twords = (long long)K * kRec;
+  const long long per = (nm + used - 1) / used;
+  const long long e0 = chunk * per;
+  const long long e1 = e0 + per < nm ? e0 + per : nm;
+  // a counter takes at most one limb (< 2^w) per entry on either side
+  const long long round = 1LL << (31 - w);
+  const int g0 = (threadIdx.x % TPR) * 4;
+  const int d = d0 + g0;
+  const int valid = dim - d >= 4 ? 4 : (dim - d > 0 ? dim - d : 0);
+  const bool vec = (dim & 3) == 0;
+  int sh[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) sh[g] = g < valid ? __ldg(a.cshift + d + g) : 0;
+  const long long bias = 1LL << (t - 1);
+  const unsigned long long mask = (1ull << w) - 1;
+  const int rstep = blockDim.x / TPR;
+  constexpr int U = 4;  // entries per thread per batch; the next batch is in flight meanwhile
+  long long* slab = a.partials + chunk * ((long long)a.kmax * dim + a.kmax);
+  bool first = true;
+  for (long long s0 = e0; first || s0 < e1; s0 += round) {
+    for (long long i = threadIdx.x; i < twords; i += blockDim.x) tab[i] = 0;
+    __syncthreads();
+    const long long s1 = s0 + round < e1 ? s0 + round : e1;
+    XT xv[U][4];
+    int cn[U], co[U];
+    auto fetch = [&](long long eb) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long e = eb + (long long)u * rstep;
+        const bool ok = e < s1;
+        const long long row = ok ? (long long)__ldg(a.mv + e) : 0;
+        co[u] = ok ? __ldg(a.mv + a.mv_cap + e) : -1;
+        cn[u] = ok ? __ldg(a.mv + 2 * a.mv_cap + e) : -1;
+        load4<XT>(X + row * dim + d, ok ? valid : 0, vec, xv[u]);
+      }
+    };
+    long long eb = s0 + threadIdx.x / TPR;
+    if (eb < s1) fetch(eb);
+    while (eb < s1) {
+      XT cx[U][4];
+      int ccn[U], cco[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ccn[u] = cn[u];
+        cco[u] = co[u];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) cx[u][g] = xv[u][g];
+      }
+      const long long nb = eb + (long long)rstep * U;
+      if (nb < s1) fetch(nb);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ccn[u] < 0) continue;
+        unsigned* en = tab + (unsigned)ccn[u] * (unsigned)kRec;
+        unsigned* eo = tab + (unsigned)cco[u] * (unsigned)kRec;
+        if (g0 == 0) {
+          atomicAdd(en + LP * M, 1u);
+          atomicAdd(eo + LP * M, 0xffffffffu);
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          long long h;
+          if (!split_fast(cx[u][g], sh[g], h)) {
+            long long lo;
+            split_fixed(cx[u][g], sh[g], t, h, lo);
+            if (g < valid) {
+              add_lo_acc(a, ccn[u], d + g, lo);
+              add_lo_acc(a, cco[u], d + g, -lo);
+            }
+          }
+          const unsigned long long uv = (unsigned long long)(h + bias);
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            const unsigned limb = (unsigned)((uv >> (w * j)) & mask);
+            atomicAdd(en + (g0 + g) * M + j, limb);
+            atomicAdd(eo + (g0 + g) * M + j, 0u - limb);
+          }
+        }
+      }
+      eb = nb;
+    }
+    __syncthreads();
+    // signed limb sums -> this chunk's slab (every word of cells < K written)
+    for (long long i = threadIdx.x; i < (long long)K * LP; i += blockDim.x) {
+      const long long c = i / LP;
+      const int ll = (int)(i % LP);
+      if (d0 + ll >= dim) continue;
+      const unsigned* e = tab + c * kRec + ll * m;
+      long long v = 0;
+      for (int j = 0; j < m; ++j) v += (long long)(int)e[j] << (w * j);
+      v -= (long long)(int)tab[c * kRec + LP * M] * bias;
+      long long* dst = slab + c * dim + d0 + ll;
+      *dst = first ? v : *dst + v;
+    }
+    if (piece == 0)
+      for (long long c = threadIdx.x; c < K; c += blockDim.x) {
+        long long* dst = slab + (long long)K * dim + c;
+        const long long v = (long long)(int)tab[c * kRec + LP * M];
+        *dst = first ? v : *dst + v;
+      }
+    __syncthreads();
+    first = false;
+  }
+}
+
+// the incremental sums as their own launch (codebooks whose every level fits
+// the warp tables have no sums_red_kernel in their pass; otherwise that
+// kernel takes the incremental branch itself)
+template <typename XT, int LP, int M>
+__global__ void __launch_bounds__(512, 1) sums_delta_kernel(KernelArgs a, const XT* __restrict__ X, LimbPlan pl) {
+  pdl_wait();
+  if (pass_off(a.st) || !delta_go(a, a.st)) return;
+  sums_delta_body<XT, LP, M>(a, X, pl);
+}
+
+template <typename XT, int LP>
+static cudaError_t launch_delta_lp(const KernelArgs& a, const XT* X, const LimbPlan& pl, cudaStream_t s) {
+  const unsigned grid = (unsigned)(pl.chunks * pl.pieces);
+#define VQB_DELTA_M(MM)                                                                                      \
+  {                                                                                                          \
+    const size_t smem = (size_t)a.kmax * (LP * MM + 1) * 4;                                                  \
+    cudaError_t e = cudaFuncSetAttribute(sums_delta_kernel<XT, LP, MM>,                                      \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    if (e != cudaSuccess) return e;                                                                          \
+    return launch_k(sums_delta_kernel<XT, LP, MM>, grid, 512, smem, s, a, X, pl);                            \
+  }
+  switch (pl.m) {
+    case 2: VQB_DELTA_M(2)
+    case 3: VQB_DELTA_M(3)
+    default: VQB_DELTA_M(4)
+  }
+#undef VQB_DELTA_M
+}
+
+// the incremental sums' own launch, for passes without a sums_red_kernel
+template <typename XT>
+static cudaError_t launch_delta(const KernelArgs& a, const XT* X, const LimbPlan& pl, cudaStream_t s) {
+  switch (pl.lp) {
+    case 32: return launch_delta_lp<XT, 32>(a, X, pl, s);
+    case 16: return launch_delta_lp<XT, 16>(a, X, pl, s);
+    case 8: return launch_delta_lp<XT, 8>(a, X, pl, s);
+    default: return launch_delta_lp<XT, 4>(a, X, pl, s);
+  }
+}
+
 // sum the per-block slabs into the exchange buffer: 32 words x 8 slab groups
 // per 256-thread block, int64 (any order is exact)
+// Incremental passes (delta_go): the slabs hold the moved rows' signed
+// contributions -- added to the running sums `acc`, which are then published;
+// a training pass that summed every row leaves its local sums in `acc`.
 __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int nblocks, int zero_cells) {
   pdl_wait();
   const DevState* st = a.st;
   if (pass_off(st)) return;
-  if (nblocks < 0) nblocks = st->slabs;  // whichever sums kernel ran this pass
+  const bool track = !zero_cells && delta_track(a, st);
+  const bool go = track && delta_go(a, st);
+  if (go)
+    nblocks = st->nmoved > 0 ? st->slabs : 0;
+  else if (nblocks < 0)
+    nblocks = st->slabs;  // whichever sums kernel ran this pass
   const int K = zero_cells ? 1 : st->size;
   const long long dim = a.dim;
   const long long words = (long long)K * dim + K;
   const long long stride = a.kmax * dim + a.kmax;
+  long long* acc_c = a.acc + a.kmax * dim;
+  long long* acc_l = acc_c + a.kmax;
   __shared__ long long part[8][32];
   const int wl = threadIdx.x & 31, g = threadIdx.x >> 5;
   for (long long w0 = (long long)blockIdx.x * 32; w0 < words; w0 += (long long)gridDim.x * 32) {
@@ -1660,19 +1947,42 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(KernelArgs a, int 
     if (g == 0 && w < words) {
       long long v = 0;
       for (int k = 0; k < 8; ++k) v += part[k][wl];
-      if (w < K * dim)
+      const bool is_sum = w < K * dim;
+      long long* accw = is_sum ? a.acc + w : acc_c + (w - K * dim);
+      if (go) v += *accw;
+      if (is_sum)
         a.ex.sums()[w] = v;
       else
         a.ex.counts()[w - K * dim] = v;
+      if (track) {
+        *accw = v;
+        if (is_sum) {
+          if (go)
+            a.ex.lo()[w] = acc_l[w];
+          else
+            acc_l[w] = a.ex.lo()[w];
+        }
+      }
     }
     __syncthreads();
   }
 }
 
 template <typename XT, int DIM>
-static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td, bool want_sums,
+static cudaError_t launch_full_sums(const KernelArgs& a, const XT* X, bool zero_cells, int sms, cudaStream_t s,
+                                    const LimbPlan& dpl);
+
+template <typename XT, int DIM>
+static cudaError_t launch_epi_dim(const KernelArgs& a_in, const XT* X, bool want_td, bool want_sums,
                                   bool zero_cells, int sms, cudaStream_t s) {
   cudaError_t e;
+  KernelArgs a = a_in;
+  // incremental sums: only where the limb tables of the largest codebook fit
+  LimbPlan dpl{};
+  if (a.acc) {
+    dpl = limb_plan(a.n, (int)a.kmax, a.dim, fixed_lo_shift(a.n_global), sms);
+    if (!want_sums || zero_cells || !limb_ok(dpl, (int)a.kmax)) a.acc = nullptr;
+  }
   if (want_td && !zero_cells) {
     // every assignment path stored the rows' exact distances (store_dist);
     // the same grid clears the low words the cell sums below add into
@@ -1686,6 +1996,22 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
     if (e != cudaSuccess) return e;
   }
   if (!want_sums) return cudaSuccess;
+  if (a.acc) {
+    e = launch_k(moved_scan_kernel, sms * 2, kScanThreads, 0, s, a);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_full_sums<XT, DIM>(a, X, zero_cells, sms, s, dpl);
+}
+
+// The sums kernels of a pass and the slab reduction.  Each reads the pass's
+// codebook size and mode from the device state and exactly one does the work:
+// sums_kernel (warp tables, small codebooks), sums_red_kernel (limb REDs; on
+// incremental passes its sums_delta branch) or, where a design has no
+// sums_red_kernel, sums_delta_kernel.
+template <typename XT, int DIM>
+static cudaError_t launch_full_sums(const KernelArgs& a, const XT* X, bool zero_cells, int sms, cudaStream_t s,
+                                    const LimbPlan& dpl) {
+  cudaError_t e;
   const long long kmax = zero_cells ? 1 : a.kmax;
   constexpr int kSumThreads = sum_threads<DIM>();
   const long long words = kmax * a.dim + kmax;
@@ -1723,6 +2049,10 @@ static cudaError_t launch_epi_dim(const KernelArgs& a, const XT* X, bool want_td
   if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (a.acc) {
+    e = launch_delta<XT>(a, X, dpl, s);
+    if (e != cudaSuccess) return e;
+  }
   e = launch_k(reduce_partials_kernel, rb, 256, 0, s, a, blocks, zero_cells ? 1 : 0);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -1783,7 +2113,7 @@ __device__ __forceinline__ void set_action(DevState* st, int act) {
 }
 
 // The decision step of a pass, one block of any size (<= 1024 threads).
-__device__ void finalize_body(const KernelArgs& a, int phase) {
+__device__ void finalize_body(const KernelArgs& a, int phase, bool track = true) {
   DevState* st = a.st;
   __shared__ double red[32];
   __shared__ long long s_empty[32];
@@ -1815,6 +2145,12 @@ __device__ void finalize_body(const KernelArgs& a, int phase) {
 
   // ---- distortion of this pass (fixed tree over tiles; in-order if ordered)
   const int K = st->size;
+  if (tid == 0) {
+    // the running sums / previous cells now describe this codebook size (the
+    // fused pass keeps neither)
+    st->acc_size = track && delta_track(a, st) ? K : 0;
+    st->nmoved = 0;
+  }
   if (st->mode != kModeUpdateOnly) {
     if (st->ordered) {
       if (tid == 0) {
@@ -2409,7 +2745,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1) pass_small_kernel(KernelArgs 
   }
   grid_sync(st);
   if (blockIdx.x == 0) {
-    finalize_body(a, 1);
+    finalize_body(a, 1, false);
     if (threadIdx.x == 0) st->skip = 1;  // the rest of this pass's kernels idle
   }
   grid_sync(st);

@@ -268,6 +268,35 @@ __global__ void __launch_bounds__(256) minmax_kernel(float* out, const float* in
 }
 
 
+// 3-input FMNMX3 with three register operands (the single-read top-2 epilogue
+// is ~80 % FMNMX3): MODE 0 = min3 / max3 chains, MODE 1 = the epilogue's mix
+// per 32 values (16 class chains + 2 block minima + 2 top-2 folds)
+template <int MODE>
+__global__ void __launch_bounds__(256) fmnmx3_kernel(float* out, const float* in, int iters) {
+  float fa[8], fb[8], fc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    fa[c] = in[(threadIdx.x + c) & 255];
+    fb[c] = in[(threadIdx.x * 3 + c) & 255];
+    fc[c] = in[(threadIdx.x * 5 + c) & 255];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        fa[c] = fminf(fminf(fb[c], fc[c]), fa[c]);
+        fb[c] = fmaxf(fmaxf(fc[c], fa[c]), fb[c]);
+        if (MODE == 1) fc[c] = fminf(fc[c], fmaxf(fa[c], fb[(c + 1) & 7]));
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += fa[c] + fb[c] + fc[c];
+  if (s == 123.456f) out[0] = s;
+}
+
 // shared-memory atomics for the cell tables: non-returning adds (RED) vs
 // returning adds whose result feeds a dependent add (the 64-bit carry idiom)
 template <int MODE>
@@ -408,6 +437,12 @@ extern "C" int vqb_pipe_microbench(int which, int blocks_per_sm, int iters, doub
         lane_ops = (mode == 2 ? 4.0 : 2.0) * blocks * threads * iters * 8 * 8;
         break;
       }
+      case 17:
+      case 18:
+        if (which == 17) fmnmx3_kernel<0><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        else fmnmx3_kernel<1><<<blocks, threads>>>((float*)buf, (const float*)inbuf, iters);
+        lane_ops = (which == 17 ? 2.0 : 4.0) * blocks * threads * iters * 4 * 8;  // instructions x lanes
+        break;
       case 11:
       case 12:
         if (which == 11) smem_atomic_kernel<0><<<sms, 512>>>((float*)buf, iters);

@@ -85,6 +85,11 @@ struct DevState {
   int act_src;         // buffer holding the source codebook of the action
   int act_k;           // source codebook size
   unsigned long long t0_ns;  // %globaltimer at the initial centroid
+  // incremental cell sums (training loop): the codebook size the running sums
+  // `acc` and the previous cells `idx_prev` describe (0: none), and the rows
+  // whose cell changed this pass (the moved list)
+  int acc_size;
+  int nmoved;
   int hist_cap;        // ring capacity: record i lives in hist[i % hist_cap]
   HistRec* hist;       // device ring, session-owned; the host drains it as passes complete
 };
@@ -189,8 +194,33 @@ struct KernelArgs {
   int* obase;           // ordered mode: per (cell, row block) offsets, kmax x oblocks
   int* oscan;           // ordered mode: scan scratch
   int oblocks;          // ordered mode: row blocks of the counting sort
+  // incremental cell sums of the training loop (nullable: every pass sums all
+  // rows): the previous pass's cells, the moved list [row | old cell | new
+  // cell] (3 x mv_cap ints), this shard's running two-word sums
+  // [hi kmax*dim | counts kmax | lo kmax*dim], and the moved-row count up to
+  // which a pass updates them instead of summing every row again
+  int* idx_prev;
+  int* mv;
+  long long mv_cap;
+  long long* acc;
+  long long delta_max;
   DevState* st;
 };
+
+// Incremental cell sums.  Integer fixed-point sums are exact, so a pass may
+// update the previous pass's sums by the rows that changed cell (+x into the
+// new cell, -x out of the old one) and get the very words a full pass over
+// every row would: late passes of a level move a few percent of the rows.
+// delta_track: this pass keeps idx_prev / acc current; delta_go: it also
+// takes the incremental path (acc describes this codebook size and few
+// enough rows moved) -- read by every sums kernel of the pass after
+// moved_scan_kernel has counted, so they all agree.
+__device__ __forceinline__ bool delta_track(const KernelArgs& a, const DevState* st) {
+  return a.acc != nullptr && st->mode == kModeTrain && !st->ordered;
+}
+__device__ __forceinline__ bool delta_go(const KernelArgs& a, const DevState* st) {
+  return delta_track(a, st) && st->acc_size == st->size && (long long)st->nmoved <= a.delta_max;
+}
 
 // The reference's distance (_kernels.py:25-29) of row `row` to codevector j
 // (FP64 master codebook cb), from the rows the reference sees: the float64

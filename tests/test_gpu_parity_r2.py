@@ -454,3 +454,95 @@ def test_float64_design_fast_path_matches_reference():
     ref = oracle.lbg_train(x, 64, epsilon=1e-3, workers=oracle.max_threads())
     assert stats.td_history() == [(s_, i, td) for s_, i, td, _ in ref.history]
     assert cb.codevectors.tobytes() == ref.codebook.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# incremental cell sums (kernels.cu moved_scan / sums_delta / reduce_delta):
+# every pass after a level's first updates the running two-word sums by the
+# rows that changed cell.  Integer sums are exact, so the design must equal
+# the one that sums every row in every pass (VQB_DELTA=0) bit for bit --
+# codebook, history (TD, empty cells), per-row distances -- and the oracle.
+# Reference: _kernels.update_rows (_kernels.py:39-66), core.py:384-415.
+# ---------------------------------------------------------------------------
+
+def _design_both(x, conf, fracs=("0.3", "1.0", "0.0")):
+    from paper_0910_4711_b200.core import _Session
+    s = _Session(x, None) if x.dtype == np.float32 else _Session(None, x)
+    old = {k: os.environ.get(k) for k in ("VQB_DELTA", "VQB_DELTA_FRAC")}
+    try:
+        os.environ["VQB_DELTA"] = "0"
+        ref = s.train(conf)
+        outs = []
+        for f in fracs:
+            os.environ["VQB_DELTA"] = "1"
+            os.environ["VQB_DELTA_FRAC"] = f
+            outs.append(s.train(conf))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return ref, outs
+
+
+def _same_design(a, b):
+    ha = [(h.codebook_size, h.iteration, h.td, h.empty_cells) for h in a[1]]
+    hb = [(h.codebook_size, h.iteration, h.td, h.empty_cells) for h in b[1]]
+    assert ha == hb
+    assert np.asarray(a[0]).tobytes() == np.asarray(b[0]).tobytes()
+    assert a[3] == b[3]
+    assert np.asarray(a[4]).tobytes() == np.asarray(b[4]).tobytes()
+
+
+@pytest.mark.parametrize("case", ["gmm16", "blocks64", "hetero16", "dim5", "tiny", "f64exact"])
+def test_incremental_sums_equal_full_sums(case):
+    rng = np.random.default_rng(123)
+    if case == "gmm16":
+        means = rng.uniform(0, 255, (64, 16))
+        x = (means[rng.integers(0, 64, 200001)] + rng.normal(0, 9, (200001, 16))).astype(np.float32)
+        conf = vq.LbgConfig(target_size=128, epsilon=1e-4, delta=0.01)
+    elif case == "blocks64":   # dimension pieces of the limb tables, integer rows
+        x = np.clip(rng.normal(128, 40, (60000, 64)) + rng.normal(0, 25, (60000, 1)), 0, 255)
+        x = np.floor(x).astype(np.float32)
+        conf = vq.LbgConfig(target_size=256, epsilon=1e-3, delta=0.01)
+    elif case == "hetero16":   # low words: columns spanning 1e6 .. 1e-4
+        x = _hetero(1 << 17, 16)
+        conf = vq.LbgConfig(target_size=32, epsilon=1e-4, delta=0.01)
+    elif case == "dim5":       # a dimension outside {16, 32, 64}, ragged row count
+        x = rng.normal(0, 1, (33333, 5)).astype(np.float32)
+        conf = vq.LbgConfig(target_size=64, epsilon=1e-3, delta=0.01)
+    elif case == "tiny":       # fewer rows than one tile, empty cells
+        x = rng.integers(0, 4, (37, 3)).astype(np.float32)
+        conf = vq.LbgConfig(target_size=16, epsilon=1e-3, delta=0.01)
+    else:                      # float64 rows float32 holds exactly
+        x = np.floor(rng.normal(0, 300, (40000, 8)))
+        conf = vq.LbgConfig(target_size=64, epsilon=1e-3, delta=0.01)
+    ref, outs = _design_both(x, conf)
+    for out in outs:
+        _same_design(ref, out)
+    # and the oracle, on the schedule (the codebook where the reference's own sums are exact)
+    if case in ("blocks64", "tiny", "f64exact"):
+        want = oracle.lbg_train(np.asarray(x, dtype=np.float64), conf.target_size, epsilon=conf.epsilon,
+                                delta=conf.delta, workers=oracle.max_threads())
+        assert [(h.codebook_size, h.iteration, h.empty_cells) for h in ref[1]] == \
+            [(s_, i, e) for s_, i, _, e in want.history]
+        assert np.asarray(outs[0][0]).tobytes() == want.codebook.tobytes()
+
+
+def test_incremental_sums_after_other_calls_on_the_session():
+    """assign / update / a second design between designs: the running sums and
+    previous cells of a finished design are never reused."""
+    from paper_0910_4711_b200.core import _Session
+    rng = np.random.default_rng(5)
+    x = np.floor(rng.normal(100, 30, (50000, 16))).astype(np.float32)
+    s = _Session(x, None)
+    conf = vq.LbgConfig(target_size=32, epsilon=1e-3, delta=0.01)
+    a = s.train(conf)
+    cells, _, _ = s.assign(np.asarray(a[0])[:7].copy(), 0)
+    s.update(cells, np.asarray(a[0])[:7].copy())
+    b = s.train(vq.LbgConfig(target_size=8, epsilon=1e-3, delta=0.01))
+    c = s.train(conf)
+    _same_design(a, c)
+    want = oracle.lbg_train(x.astype(np.float64), 8, epsilon=1e-3, delta=0.01, workers=oracle.max_threads())
+    assert np.asarray(b[0]).tobytes() == want.codebook.tobytes()
