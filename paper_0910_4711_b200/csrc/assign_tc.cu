@@ -441,11 +441,7 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       flag = qcur < 0.f || !(M2 > thr_s);
       thr = M1 * inv + band;
       a.idx[row] = i1;
-#ifdef VQB_EXP_NODIST
-      if (false) {
-#else
       if (!flag && a.dists) {
-#endif
         // exact FP64 distance to the certified winner (_kernels.py:25-34);
         // the row is L2-resident from its conversion
         const double d = row_dist<L>(a, row, kHoist ? c_cb : a.cb[st->cur], i1);
@@ -677,10 +673,12 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
       return a.r0 + entry;
     };
 
-
-    const float inv = 1.0f / dscale;
-    const float eyw = sqrtf((float)L) * 5.9604645e-8f * (ldexpf(1.0f, -st->tc_ey) + ldexpf(1.0f, -st->tc_ew));
-
+    auto min16 = [](const float* v) {
+      const float t0 = fminf(fminf(v[0], v[1]), v[2]), t1 = fminf(fminf(v[3], v[4]), v[5]);
+      const float t2 = fminf(fminf(v[6], v[7]), v[8]), t3 = fminf(fminf(v[9], v[10]), v[11]);
+      const float t4 = fminf(fminf(v[12], v[13]), v[14]);
+      return fminf(fminf(fminf(t0, t1), t2), fminf(fminf(t3, t4), v[15]));
+    };
     long long g = 0;
     for (long long i = 0; i < my_tiles; ++i) {
       // kTcTop2: running top-2 of the block minima (b1, b2; blk = first block
@@ -740,12 +738,6 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
             b2 = fminf(b2, fmaxf(b1, mu));
             b1 = fminf(b1, mu);
             blk = lt ? jb : blk;
-          };
-          auto min16 = [&](const float* v) {
-            const float t0 = fminf(fminf(v[0], v[1]), v[2]), t1 = fminf(fminf(v[3], v[4]), v[5]);
-            const float t2 = fminf(fminf(v[6], v[7]), v[8]), t3 = fminf(fminf(v[9], v[10]), v[11]);
-            const float t4 = fminf(fminf(v[12], v[13]), v[14]);
-            return fminf(fminf(fminf(t0, t1), t2), fminf(fminf(t3, t4), v[15]));
           };
           auto scan32 = [&](const float (&v)[32], int q4) {
 #pragma unroll
@@ -827,18 +819,21 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
         // hand the tile's per-part results to the certification warps
         // the part's top-2: the chains' second smallest (as a multiset: two
         // classes at the minimum give s2 = s1) and the class of the minimum
-        float s1 = INFINITY, s2 = INFINITY;
-        int cls = 0;
-#ifdef VQB_EXP_NOTAIL
-        s2 = ach[0] + ach[7];
-#else
+        // The chains' minimum is b1 itself (both are the minimum of the part's
+        // values), so: mark the chains equal to b1 (one FSETP each, feeding a
+        // predicated OR into the mask and the select that takes the chain out
+        // of the second-minimum tree); cls = the first marked chain; two
+        // marked chains make the second minimum b1.
+        unsigned eqm = 0u;
+        float rest[16];
 #pragma unroll
-        for (int t = 15; t >= 0; --t) {
-          s2 = fminf(s2, fmaxf(s1, ach[t]));
-          s1 = fminf(s1, ach[t]);
-          cls = ach[t] == b1 ? t : cls;
-        }
-#endif
+        for (int t = 0; t < 16; ++t)
+          asm("{\n\t.reg .pred p;\n\tsetp.eq.f32 p, %2, %3;\n\t@p or.b32 %0, %0, %4;\n\t"
+              "selp.f32 %1, 0f7F800000, %2, p;\n\t}"
+              : "+r"(eqm), "=f"(rest[t])
+              : "f"(ach[t]), "f"(b1), "r"(1u << t));
+        const int cls = eqm ? __ffs(eqm) - 1 : 0;
+        const float s2 = (eqm & (eqm - 1u)) ? b1 : min16(rest);
         const int rb = (int)(i & 1);
         pwait(&m->res_empty[rb], (uint32_t)(((i >> 1) & 1) ^ 1), 2);
         m->merge.res[rb].m1[h][r] = b1;

@@ -1490,6 +1490,13 @@ __device__ __forceinline__ void load4(const XT* __restrict__ p, int valid, bool 
   }
 }
 
+// incremental branch inside sums_red_kernel (1) or as its own launch (0).
+// Merged it saves one idle launch per pass (design -1 %), but the larger
+// kernel's full-sum path ran 12-15 us slower at cfg2 / cfg3 (the stateless
+// Lloyd step: +4 %), so it is its own launch.
+#ifndef VQB_DELTA_MERGE
+#define VQB_DELTA_MERGE 0
+#endif
 template <typename XT, int LP, int M>
 __device__ __forceinline__ void sums_delta_body(const KernelArgs& a, const XT* __restrict__ X, const LimbPlan& pl);
 
@@ -1501,10 +1508,14 @@ __global__ void __launch_bounds__(512, 1) sums_red_kernel(KernelArgs a, const XT
   if (pass_off(st)) return;
   const int K = zero_cells ? 1 : st->size;
   const int dim = a.dim;
+#if VQB_DELTA_MERGE
   if (delta_go(a, st)) {  // the incremental pass: only the rows that changed cell (same tables, same plan)
     sums_delta_body<XT, LP, M>(a, X, pl);
     return;
   }
+#else
+  if (delta_go(a, st)) return;
+#endif
   if (pl.small_cut > 0 && K <= pl.small_cut) return;  // sums_kernel's warp tables take this pass
   if (blockIdx.x == 0 && threadIdx.x == 0) st->slabs = pl.chunks;
   const int t = st->lo_shift;  // == fixed_lo_shift(n_global), what the plan was made for
@@ -2040,6 +2051,12 @@ static cudaError_t launch_full_sums(const KernelArgs& a, const XT* X, bool zero_
                      X, 0, 1);
         if (e != cudaSuccess) return e;
       }
+#if !VQB_DELTA_MERGE
+      if (a.acc) {
+        e = launch_delta<XT>(a, X, dpl, s);
+        if (e != cudaSuccess) return e;
+      }
+#endif
       return launch_k(reduce_partials_kernel, rb, 256, 0, s, a, -1, 0);
     }
   }
