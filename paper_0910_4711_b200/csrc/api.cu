@@ -216,6 +216,11 @@ struct vqb_session {
     a.mv_cap = n + 32;
     a.acc = delta_on ? acc : nullptr;
     a.delta_max = (long long)((double)n * delta_frac);
+    static const int small = [] {
+      const char* e = getenv("VQB_SMALL");
+      return e ? atoi(e) : 1;
+    }();
+    a.small_on = small;
     a.st = st;
     return a;
   }

@@ -258,6 +258,11 @@ static int getenv_flag(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// candidate widths with a small-codebook kernel (assign_small_kernel), which
+// takes the passes with K < kSmallK
+constexpr int kSmallK = 64;
+__host__ __device__ constexpr bool small_dim(int L) { return L == 16; }
+
 template <int L, int TK>
 struct TileStream {
   // W tile [TK][L] then norms [TK]; two buffers.
@@ -458,6 +463,7 @@ __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelAr
   if (pass_off(st)) return;
   const int K = st->size;
   if (a.tcb && tc_handles(st, K)) return;  // assign_tc runs this pass
+  if (small_dim(L) && a.small_on && K < kSmallK) return;  // assign_small_kernel runs this pass
   const int ntiles = (K + TK - 1) / TK;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
@@ -518,6 +524,208 @@ __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelAr
     else
       assign_chunk<L, NT, TK, 1, PACKED>(a, row0, hi, K, ntiles, smem, bars, seq, seq_total);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Small codebooks (K < kSmallK, the sizes the tensor-core pass leaves to the
+// FP32 kernels): candidate pass with ONE ROW PER THREAD, rows staged through
+// shared memory.  assign_fast_kernel reads a row per lane straight from
+// global memory (4 x LDG.128 at a 64-byte stride: 16 cache lines per warp
+// instruction), reads it again for the FP64 winner distance and gathers the
+// winner's codevector from global memory; at K = 2..32 that load pattern --
+// not the arithmetic -- set its time (cfg4: 0.46-0.89 ms against 0.18 ms of
+// HBM time; more CTAs per SM, L1 / L2 prefetches did not move it).  Here a
+// tile of 256 rows is fetched with fully coalesced 16-byte loads one tile
+// ahead (registers), parked in shared memory with a padded row stride (each
+// thread then reads its own row in 4-wavefront LDS.128s, again for the exact
+// FP64 distance), and the FP64 codebook (<= 63 rows) sits in shared memory
+// too.  Distances as FFMA2 over dimension pairs; assign_chunk's band and
+// re-rank queue.
+// Reference: _kernels.assign_range (_kernels.py:18-36).
+// ---------------------------------------------------------------------------
+constexpr int kSmallNT = 256;
+#ifndef VQB_SMALL_MINB
+#define VQB_SMALL_MINB 3
+#endif
+constexpr int kSmallMinB = VQB_SMALL_MINB;  // CTAs per SM the kernel is compiled for (A/B builds: 4)
+template <int L>
+struct SmallSmem {
+  static constexpr int XS = L + 4;  // row stride (words): a quarter-warp's LDS.128s hit 8 distinct bank groups
+  static constexpr int CS = L + 2;  // FP64 codevector stride (doubles): <= 2-way conflicts across winners
+  float x[2][kSmallNT * XS];
+  double cb[kSmallK * CS];
+  float w[kSmallK * L];
+  float nrm[kSmallK];
+  float mu[L];
+};
+
+template <int L>
+__global__ void __launch_bounds__(kSmallNT, L == 16 ? kSmallMinB : 2) assign_small_kernel(KernelArgs a) {
+  pdl_wait();
+  DevState* st = a.st;
+  if (pass_off(st)) return;
+  const int K = st->size;
+  if (K >= kSmallK || (a.tcb && tc_handles(st, K))) return;  // assign_fast / assign_tc take this pass
+  using SM = SmallSmem<L>;
+  constexpr int NT = kSmallNT, XS = SM::XS, CS = SM::CS, CH = L / 4;  // CH: 16-byte chunks per row
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31;
+  // the staged row serves the winner distance when the candidate rows ARE
+  // the rows the reference sees (float32 rows of width L)
+  const bool regs_exact = a.x32 != nullptr && a.x64 == nullptr && a.dim == L && a.xc == a.x32;
+  const double* cbg = a.cb[st->cur];
+  const bool euclid = st->metric == kEuclidean;
+  for (int e = tid; e < K * L; e += NT) sm.w[e] = a.w[e];
+  for (int e = tid; e < K; e += NT) sm.nrm[e] = a.nrm[e];
+  if (tid < L) sm.mu[tid] = a.mu[tid];
+  if (regs_exact)
+    for (int e = tid; e < K * L; e += NT) sm.cb[(e / L) * CS + e % L] = cbg[e];
+
+  const long long n = a.r1 - a.r0;
+  const long long lo = a.r0 + n * blockIdx.x / gridDim.x;
+  const long long hi = a.r0 + n * (blockIdx.x + 1) / gridDim.x;
+  const long long ntile = (hi - lo + NT - 1) / NT;
+  float4 nxt[CH];
+  auto fetch = [&](long long t) {  // tile t's chunks tid, tid + NT, ...: consecutive lanes, consecutive 16 bytes
+    const long long r0 = lo + t * NT;
+    const float4* src = reinterpret_cast<const float4*>(a.xc + r0 * L);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int q = tid + k * NT;
+      nxt[k] = (t < ntile && r0 + q / CH < hi) ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto park = [&](int buf) {
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int q = tid + k * NT;
+      *reinterpret_cast<float4*>(&sm.x[buf][(q / CH) * XS + (q % CH) * 4]) = nxt[k];
+    }
+  };
+  if (ntile > 0) {
+    fetch(0);
+    park(0);
+    fetch(1);
+  }
+  __syncthreads();
+  const float u = 5.9604645e-8f;
+  for (long long t = 0; t < ntile; ++t) {
+    const int buf = (int)(t & 1);
+    const long long row = lo + t * NT + tid;
+    const bool valid = row < hi;
+    // y~ = fl(x - mu) packed in dimension pairs for FFMA2, ||y~||^2 as an
+    // ascending FMA chain (assign_chunk's)
+    const float* xrow = &sm.x[buf][tid * XS];
+    unsigned long long y2[L / 2];
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const float4 v = *reinterpret_cast<const float4*>(xrow + c * 4);
+      const float4 mu4 = *reinterpret_cast<const float4*>(sm.mu + c * 4);
+      const float y0 = __fsub_rn(v.x, mu4.x), y1 = __fsub_rn(v.y, mu4.y);
+      const float y2f = __fsub_rn(v.z, mu4.z), y3 = __fsub_rn(v.w, mu4.w);
+      q = fmaf(y0, y0, q);
+      q = fmaf(y1, y1, q);
+      q = fmaf(y2f, y2f, q);
+      q = fmaf(y3, y3, q);
+      y2[2 * c] = pack2(y0, y1);
+      y2[2 * c + 1] = pack2(y2f, y3);
+    }
+    // tile t + 1 into the other buffer (its readers passed the barrier that
+    // ended iteration t - 1), tile t + 2 into registers; this tile's rows
+    // stay in their buffer for the winner distance below
+    park(buf ^ 1);
+    fetch(t + 2);
+    float m1 = INFINITY, m2 = INFINITY;
+    int i1 = 0;
+#pragma unroll 2
+    for (int j = 0; j < K; ++j) {
+      // v_j = ||c~_j||^2 - 2 y~.c~_j as two interleaved FMA chains (even / odd
+      // dimensions, one FFMA2 per pair) added at the end: at most L/2 + 2
+      // roundings on a path, inside the band's (L + 3) u S^2
+      unsigned long long v2 = pack2(sm.nrm[j], 0.f);
+      const float4* wj = reinterpret_cast<const float4*>(sm.w + j * L);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const float4 w4 = wj[c];  // one address for the whole warp: a broadcast
+        v2 = ffma2(pack2(w4.x, w4.y), y2[2 * c], v2);
+        v2 = ffma2(pack2(w4.z, w4.w), y2[2 * c + 1], v2);
+      }
+      float va, vb;
+      unpack2(v2, va, vb);
+      const float v = __fadd_rn(va, vb);
+      const float n2 = fminf(m2, fmaxf(m1, v));
+      const bool pr = v < m1;
+      m1 = fminf(m1, v);
+      i1 = pr ? j : i1;
+      m2 = n2;
+    }
+    // certification: assign_chunk's band (FMA chain of L terms + norm)
+    bool ok = false;
+    float thr = NAN;
+    if (valid) {
+      const float yn = sqrtf(q);
+      const float d2 = fmaxf(m2 + q, 0.f);
+      const float sd = sqrtf(d2) * 1.01f + 1.0f;
+      const float S = 2.02f * yn + sd;
+      const float E = (float)(L + 3) * u * S * S + 2.5f * u * sd * S + 1e-14f * S * S;
+      const float band = 3.0f * E + input_band(rin_of(a, row), m1 + q, 3.0f * E);
+      ok = (m2 - m1) > band;
+      thr = m1 + band;
+      a.idx[row] = i1;
+      if (ok && a.dists) {
+        double d = 0.0;
+        if (regs_exact) {
+          // the reference's arithmetic (_kernels.py:25-29) on the registers' row
+          const double2* c2 = reinterpret_cast<const double2*>(sm.cb + i1 * CS);
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const float4 xv = *reinterpret_cast<const float4*>(xrow + c * 4);
+            const double2 ca = c2[2 * c], cb2 = c2[2 * c + 1];
+            const double d0 = __dsub_rn((double)xv.x, ca.x);
+            d = __dadd_rn(d, __dmul_rn(d0, d0));
+            const double d1 = __dsub_rn((double)xv.y, ca.y);
+            d = __dadd_rn(d, __dmul_rn(d1, d1));
+            const double d2 = __dsub_rn((double)xv.z, cb2.x);
+            d = __dadd_rn(d, __dmul_rn(d2, d2));
+            const double d3 = __dsub_rn((double)xv.w, cb2.y);
+            d = __dadd_rn(d, __dmul_rn(d3, d3));
+          }
+        } else {
+          d = row_dist<L>(a, row, cbg, i1);
+        }
+        a.dists[row] = euclid ? sqrt(d) : d;
+      }
+    }
+    const bool flag = valid && !ok;
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    if (mask) {
+      int base = 0;
+      const int leader = __ffs(mask) - 1;
+      if (lane == leader) base = atomicAdd(&st->flag_count, __popc(mask));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (flag) {
+        const int pos = base + __popc(mask & ((1u << lane) - 1u));
+        a.flags[pos] = (int)row;
+        a.flag_thr[pos] = thr;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int L>
+static cudaError_t launch_small_L(const KernelArgs& a, int sms, cudaStream_t s) {
+  const size_t smem = sizeof(SmallSmem<L>);
+  cudaError_t e = cudaFuncSetAttribute(assign_small_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long n = a.r1 - a.r0;
+  long long grid = (long long)sms * (L == 16 ? kSmallMinB : 2);
+  const long long tiles = (n + kSmallNT - 1) / kSmallNT;
+  if (grid > tiles) grid = tiles > 0 ? tiles : 1;
+  return launch_k(assign_small_kernel<L>, (unsigned)grid, kSmallNT, smem, s, a);
 }
 
 static bool packed_default() {
@@ -1046,7 +1254,12 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
       case 64: e = launch_fast_L<64>(a, sms, s); break;
       default: return cudaErrorInvalidValue;
     }
-    if (e != cudaSuccess || !a.tcb) return e;
+    if (e != cudaSuccess) return e;
+    if (a.small_on && a.cdim == 16) {
+      e = launch_small_L<16>(a, sms, s);
+      if (e != cudaSuccess) return e;
+    }
+    if (!a.tcb) return e;
     return launch_assign_tc(a, sms, s);
   }
   return launch_exact_rows(a, 0, sms, s);
