@@ -519,10 +519,11 @@ def run_b200(args):
         # ---- CPU baseline: oracle on a bounded sample, all host cores
         cpu_rate, rows, threads, secs = cpu_iteration_rate(x, cb, target_s=4.0)
         cores, model = _cpu_info()
-        # per step: reset, assign_fast + assign_tc (one of them exits at once),
-        # TC shortlist + FP32 shortlist + exact re-rank, td_tiles (+ low-word
-        # clear) + sums + reduce_partials, finalize + apply
-        launches_per_step = 11
+        # per step: reset, assign_fast + assign_small + assign_tc (two of them
+        # exit at once), TC shortlist + FP32 shortlist + exact re-rank, td_tiles
+        # (+ low-word clear) + sums_red + sums (one exits) + reduce_partials,
+        # finalize + apply (profiles/r02_launch_summary_cfg4_step.txt)
+        launches_per_step = 13
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
