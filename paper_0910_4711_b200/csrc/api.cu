@@ -221,6 +221,11 @@ struct vqb_session {
       return e ? atoi(e) : 1;
     }();
     a.small_on = small;
+    static const int diff = [] {
+      const char* e = getenv("VQB_DIFF");
+      return e ? atoi(e) : 1;
+    }();
+    a.diff_on = diff;
     a.st = st;
     return a;
   }

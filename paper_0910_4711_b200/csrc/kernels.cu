@@ -261,6 +261,9 @@ static int getenv_flag(const char* name, int dflt) {
 // candidate widths with a small-codebook kernel (assign_small_kernel), which
 // takes the passes with K < kSmallK
 constexpr int kSmallK = 64;
+// (the kernel is written for T = L / 16 lanes per row; at L = 64 it measured no
+// faster than assign_fast_kernel at K = 2 and 1.6x slower at K = 32 -- cfg3,
+// profiles/r02_assign_small_ab.txt -- so only L = 16 takes it)
 __host__ __device__ constexpr bool small_dim(int L) { return L == 16; }
 
 template <int L, int TK>
@@ -271,7 +274,14 @@ struct TileStream {
 };
 
 // Process rows assigned to this thread in one chunk: R rows, strided by NT.
-template <int L, int NT, int TK, int R, bool PACKED>
+// DIFF: candidate values in DIFFERENCE form, v_j = sum_l (y~_l - c~_l)^2 (the
+// distance itself, two FMA-pipe operations per dimension), instead of the
+// expanded ||c~_j||^2 - 2 y~.c~_j.  Its error is relative to the distance, not
+// to ||y~||^2, so rows whose distance is small against their norm (image
+// blocks with a large mean) certify instead of queueing: the kernel takes it
+// for K < kSmallK at L >= 32, where the extra FMAs are cheap and the expanded
+// form queued ~30 % of cfg3's rows.
+template <int L, int NT, int TK, int R, bool PACKED, bool DIFF = false>
 __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0, long long row_end,
                                              int K, int ntiles, float* smem, uint64_t* bars,
                                              long long& seq, long long seq_total) {
@@ -328,7 +338,8 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
         const unsigned long long n2 = pack2(nj, nj);
         unsigned long long v2[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) v2[p] = n2;
+        for (int p = 0; p < P; ++p) v2[p] = DIFF ? pack2(0.f, 0.f) : n2;
+        const unsigned long long half2 = pack2(0.5f, 0.5f);
 #pragma unroll
         for (int c = 0; c < L / 4; ++c) {
           const float4 t4 = wj[c];
@@ -337,7 +348,15 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
           for (int q = 0; q < 4; ++q) {
             const unsigned long long w2 = pack2(w[q], w[q]);
 #pragma unroll
-            for (int p = 0; p < P; ++p) v2[p] = ffma2(y2[p][c * 4 + q], w2, v2[p]);
+            for (int p = 0; p < P; ++p) {
+              if constexpr (DIFF) {
+                // y~ - c~ = y~ + 0.5 w (w = -2 c~: the halving is exact, one rounding)
+                const unsigned long long d2 = ffma2(half2, w2, y2[p][c * 4 + q]);
+                v2[p] = ffma2(d2, d2, v2[p]);
+              } else {
+                v2[p] = ffma2(y2[p][c * 4 + q], w2, v2[p]);
+              }
+            }
           }
         }
 #pragma unroll
@@ -363,7 +382,7 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
       float v[R];
       const float nj = sN[j];
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = nj;
+      for (int r = 0; r < R; ++r) v[r] = DIFF ? 0.f : nj;
 #pragma unroll
       for (int c = 0; c < L / 16; ++c) {
         float w[16];
@@ -378,7 +397,14 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
 #pragma unroll
         for (int r = 0; r < R; ++r) {
 #pragma unroll
-          for (int l = 0; l < 16; ++l) v[r] = fmaf(w[l], y[r][c * 16 + l], v[r]);
+          for (int l = 0; l < 16; ++l) {
+            if constexpr (DIFF) {
+              const float d = fmaf(0.5f, w[l], y[r][c * 16 + l]);
+              v[r] = fmaf(d, d, v[r]);
+            } else {
+              v[r] = fmaf(w[l], y[r][c * 16 + l], v[r]);
+            }
+          }
         }
       }
 #pragma unroll
@@ -427,14 +453,34 @@ __device__ __forceinline__ void assign_chunk(const KernelArgs& a, long long row0
     float thr = NAN;
     if (valid[r]) {
       const float yn = sqrtf(q[r]);
-      const float d2 = fmaxf(m2[r] + q[r], 0.f);
+      // distance of the runner-up: m2 itself in difference form
+      const float d2 = fmaxf(DIFF ? m2[r] : m2[r] + q[r], 0.f);
       const float sd = sqrtf(d2) * 1.01f + 1.0f;
       const float S = 2.02f * yn + sd;
       const float E = (float)(L + 3) * u * S * S + 2.5f * u * sd * S + 1e-14f * S * S;
+      if constexpr (DIFF) {
+        // t_l = fl(y~_l - c~_l) differs from x_l - c_l by e_l, |e_l| <= u (|y~_l|
+        // + |c~_l| + |t_l|) (centring, FP32 codebook rounding, the difference),
+        // so ||e|| <= 2 u (||y~|| + sqrt T) with T = sum t^2, and the FMA chain
+        // of L non-negative terms adds at most (L + 1) u T:
+        //   |v - d| <= (L + 3) u sd^2 + 4.1 u sd (yn + sd) =: Ed   (sd >= sqrt of
+        // every distance up to the runner-up's; v - Ed(v) grows with v, so the
+        // runner-up's bound covers every farther codevector).  Certified iff
+        // the gap exceeds 3 Ed (two values' worth x 1.5, as above).
+        const float Ed = (float)(L + 3) * u * sd * sd + 4.1f * u * sd * (yn + sd) + 1e-14f * S * S;
+        const float bandd = 3.0f * Ed + input_band(rin_of(a, row), m1[r], 3.0f * Ed);
+        ok = (m2[r] - m1[r]) > bandd;
+        // the re-rank rescans in the EXPANDED arithmetic (v = d - ||y~||^2 up
+        // to E): the reference's winner has d <= m1 + Ed, hence v <= m1 - q +
+        // Ed + E (+ the rounding of q and of the subtraction)
+        const float bande = 3.0f * E + input_band(rin_of(a, row), m1[r], 3.0f * E);
+        thr = (m1[r] - q[r]) + bande + bandd + (float)(L + 8) * u * (q[r] + fabsf(m1[r]));
+      } else {
       // float64 rows: + the band of their float32 rounding (input_band)
       const float band = 3.0f * E + input_band(rin_of(a, row), m1[r] + q[r], 3.0f * E);
       ok = (m2[r] - m1[r]) > band;
       thr = m1[r] + band;  // shortlist band (shortlist_kernel)
+      }
       a.idx[row] = i1[r];
       if (ok && a.dists) store_dist(a, row, row_dist<L>(a, row, a.cb[a.st->cur], i1[r]));
     }
@@ -504,10 +550,21 @@ __global__ void __launch_bounds__(FastCfg<L>::NT, 1) assign_fast_kernel(KernelAr
   if (ntiles == 1) mbar_wait(&bars[0], 0);
 
   long long seq = 0;
-  for (long long c = 0; c < full; ++c)
-    assign_chunk<L, NT, TK, R, PACKED>(a, lo + c * per_chunk, hi, K, ntiles, smem, bars, seq,
-                                       seq_total);
-  if (rem > 0) {
+  const bool diff = L >= 32 && K < kSmallK && a.diff_on;  // difference-form values (assign_chunk)
+  for (long long c = 0; c < full; ++c) {
+    if (diff)
+      assign_chunk<L, NT, TK, R, PACKED, (L >= 32)>(a, lo + c * per_chunk, hi, K, ntiles, smem, bars, seq,
+                                                    seq_total);
+    else
+      assign_chunk<L, NT, TK, R, PACKED>(a, lo + c * per_chunk, hi, K, ntiles, smem, bars, seq,
+                                         seq_total);
+  }
+  if (rem > 0 && diff) {
+    // tail chunk in difference form: the full row count per thread (rows past
+    // the range are masked)
+    assign_chunk<L, NT, TK, R, PACKED, (L >= 32)>(a, lo + full * per_chunk, hi, K, ntiles, smem, bars, seq,
+                                                  seq_total);
+  } else if (rem > 0) {
     // tail chunk: only as many rows per thread as needed (no wave tail)
     const long long row0 = lo + full * per_chunk;
     int rr = (int)((rem + NT - 1) / NT);
@@ -548,13 +605,25 @@ constexpr int kSmallNT = 256;
 #define VQB_SMALL_MINB 3
 #endif
 constexpr int kSmallMinB = VQB_SMALL_MINB;  // CTAs per SM the kernel is compiled for (A/B builds: 4)
+// T = L / 16 adjacent lanes share a row, 16 dimensions each (a row of 64
+// dimensions in one thread's registers would leave 8 warps per SM); their
+// partial sums meet in a butterfly, so every lane of a row holds the same
+// value bits and takes the same top-2 decisions.  Shared-memory layouts are
+// chosen so that a quarter-warp's LDS.128s fall on distinct bank groups: the
+// row tile as T sub-tiles (16 dimensions of every row, 20-word row stride,
+// sub-tiles skewed by 32 / T words), the FP32 codebook with a 20-word stride
+// per 16-dimension slice.
 template <int L>
 struct SmallSmem {
-  static constexpr int XS = L + 4;  // row stride (words): a quarter-warp's LDS.128s hit 8 distinct bank groups
+  static constexpr int T = L / 16;           // lanes per row
+  static constexpr int RT = kSmallNT / T;    // rows per tile
+  static constexpr int SUB = RT * 20 + (T > 1 ? 32 / T : 0);  // sub-tile stride (words)
+  static constexpr int WSS = T > 1 ? 20 : 16;                 // codebook slice stride (words)
+  static constexpr int WSJ = T * WSS;                         // codevector stride (words)
   static constexpr int CS = L + 2;  // FP64 codevector stride (doubles): <= 2-way conflicts across winners
-  float x[2][kSmallNT * XS];
+  float x[2][T * SUB];
   double cb[kSmallK * CS];
-  float w[kSmallK * L];
+  float w[kSmallK * WSJ];
   float nrm[kSmallK];
   float mu[L];
 };
@@ -567,16 +636,23 @@ __global__ void __launch_bounds__(kSmallNT, L == 16 ? kSmallMinB : 2) assign_sma
   const int K = st->size;
   if (K >= kSmallK || (a.tcb && tc_handles(st, K))) return;  // assign_fast / assign_tc take this pass
   using SM = SmallSmem<L>;
-  constexpr int NT = kSmallNT, XS = SM::XS, CS = SM::CS, CH = L / 4;  // CH: 16-byte chunks per row
+  constexpr int NT = kSmallNT, T = SM::T, RT = SM::RT, CS = SM::CS, CH = L / 4;  // CH: 16-byte chunks per row
+  // difference-form values at L >= 32 (assign_chunk's DIFF: image blocks with a
+  // large mean certify instead of queueing)
+  constexpr bool DIFF = L >= 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
+  const int rloc = tid / T, sub = tid % T;  // this lane's row of the tile and its 16-dimension slice
   // the staged row serves the winner distance when the candidate rows ARE
   // the rows the reference sees (float32 rows of width L)
   const bool regs_exact = a.x32 != nullptr && a.x64 == nullptr && a.dim == L && a.xc == a.x32;
   const double* cbg = a.cb[st->cur];
   const bool euclid = st->metric == kEuclidean;
-  for (int e = tid; e < K * L; e += NT) sm.w[e] = a.w[e];
+  for (int e = tid; e < K * L; e += NT) {
+    const int j = e / L, l = e % L;
+    sm.w[j * SM::WSJ + (l / 16) * SM::WSS + l % 16] = a.w[e];
+  }
   for (int e = tid; e < K; e += NT) sm.nrm[e] = a.nrm[e];
   if (tid < L) sm.mu[tid] = a.mu[tid];
   if (regs_exact)
@@ -585,22 +661,25 @@ __global__ void __launch_bounds__(kSmallNT, L == 16 ? kSmallMinB : 2) assign_sma
   const long long n = a.r1 - a.r0;
   const long long lo = a.r0 + n * blockIdx.x / gridDim.x;
   const long long hi = a.r0 + n * (blockIdx.x + 1) / gridDim.x;
-  const long long ntile = (hi - lo + NT - 1) / NT;
-  float4 nxt[CH];
+  const long long ntile = (hi - lo + RT - 1) / RT;
+  float4 nxt[4];  // RT * CH = 4 * NT chunks per tile for every L
   auto fetch = [&](long long t) {  // tile t's chunks tid, tid + NT, ...: consecutive lanes, consecutive 16 bytes
-    const long long r0 = lo + t * NT;
+    const long long r0 = lo + t * RT;
     const float4* src = reinterpret_cast<const float4*>(a.xc + r0 * L);
 #pragma unroll
-    for (int k = 0; k < CH; ++k) {
+    for (int k = 0; k < 4; ++k) {
       const int q = tid + k * NT;
       nxt[k] = (t < ntile && r0 + q / CH < hi) ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
+  auto xaddr = [&](int buf, int r, int cc) -> float* {  // chunk cc of row r of the staged tile
+    return &sm.x[buf][(cc / 4) * SM::SUB + r * 20 + (cc % 4) * 4];
+  };
   auto park = [&](int buf) {
 #pragma unroll
-    for (int k = 0; k < CH; ++k) {
+    for (int k = 0; k < 4; ++k) {
       const int q = tid + k * NT;
-      *reinterpret_cast<float4*>(&sm.x[buf][(q / CH) * XS + (q % CH) * 4]) = nxt[k];
+      *reinterpret_cast<float4*>(xaddr(buf, q / CH, q % CH)) = nxt[k];
     }
   };
   if (ntile > 0) {
@@ -612,17 +691,16 @@ __global__ void __launch_bounds__(kSmallNT, L == 16 ? kSmallMinB : 2) assign_sma
   const float u = 5.9604645e-8f;
   for (long long t = 0; t < ntile; ++t) {
     const int buf = (int)(t & 1);
-    const long long row = lo + t * NT + tid;
-    const bool valid = row < hi;
-    // y~ = fl(x - mu) packed in dimension pairs for FFMA2, ||y~||^2 as an
-    // ascending FMA chain (assign_chunk's)
-    const float* xrow = &sm.x[buf][tid * XS];
-    unsigned long long y2[L / 2];
+    const long long row = lo + t * RT + rloc;
+    const bool valid = row < hi && sub == 0;  // one lane per row certifies and stores
+    // y~ = fl(x - mu) packed in dimension pairs for FFMA2, ||y~||^2 as FMA
+    // chains (per slice, then the butterfly)
+    unsigned long long y2[8];
     float q = 0.f;
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const float4 v = *reinterpret_cast<const float4*>(xrow + c * 4);
-      const float4 mu4 = *reinterpret_cast<const float4*>(sm.mu + c * 4);
+    for (int c = 0; c < 4; ++c) {
+      const float4 v = *reinterpret_cast<const float4*>(xaddr(buf, rloc, sub * 4 + c));
+      const float4 mu4 = *reinterpret_cast<const float4*>(sm.mu + sub * 16 + c * 4);
       const float y0 = __fsub_rn(v.x, mu4.x), y1 = __fsub_rn(v.y, mu4.y);
       const float y2f = __fsub_rn(v.z, mu4.z), y3 = __fsub_rn(v.w, mu4.w);
       q = fmaf(y0, y0, q);
@@ -632,6 +710,8 @@ __global__ void __launch_bounds__(kSmallNT, L == 16 ? kSmallMinB : 2) assign_sma
       y2[2 * c] = pack2(y0, y1);
       y2[2 * c + 1] = pack2(y2f, y3);
     }
+#pragma unroll
+    for (int o = 1; o < T; o <<= 1) q = __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
     // tile t + 1 into the other buffer (its readers passed the barrier that
     // ended iteration t - 1), tile t + 2 into registers; this tile's rows
     // stay in their buffer for the winner distance below
@@ -639,56 +719,77 @@ __global__ void __launch_bounds__(kSmallNT, L == 16 ? kSmallMinB : 2) assign_sma
     fetch(t + 2);
     float m1 = INFINITY, m2 = INFINITY;
     int i1 = 0;
+    const unsigned long long half2 = pack2(0.5f, 0.5f);
 #pragma unroll 2
     for (int j = 0; j < K; ++j) {
-      // v_j = ||c~_j||^2 - 2 y~.c~_j as two interleaved FMA chains (even / odd
-      // dimensions, one FFMA2 per pair) added at the end: at most L/2 + 2
-      // roundings on a path, inside the band's (L + 3) u S^2
-      unsigned long long v2 = pack2(sm.nrm[j], 0.f);
-      const float4* wj = reinterpret_cast<const float4*>(sm.w + j * L);
+      // expanded form: v_j = ||c~_j||^2 - 2 y~.c~_j; difference form:
+      // sum (y~ - c~_j)^2 -- two interleaved FMA chains per slice (even / odd
+      // dimensions, one FFMA2 per pair), added, then the butterfly over the
+      // row's lanes: at most 8 + 1 + log2 T + 1 roundings on a path, inside
+      // the band's (L + 3) u term
+      unsigned long long v2 = pack2(DIFF || sub != 0 ? 0.f : sm.nrm[j], 0.f);
+      const float4* wj = reinterpret_cast<const float4*>(sm.w + j * SM::WSJ + sub * SM::WSS);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const float4 w4 = wj[c];  // one address for the whole warp: a broadcast
-        v2 = ffma2(pack2(w4.x, w4.y), y2[2 * c], v2);
-        v2 = ffma2(pack2(w4.z, w4.w), y2[2 * c + 1], v2);
+      for (int c = 0; c < 4; ++c) {
+        const float4 w4 = wj[c];  // one address per slice: a broadcast
+        if constexpr (DIFF) {
+          // y~ - c~ = y~ + 0.5 w (w = -2 c~: the halving is exact, one rounding)
+          const unsigned long long da = ffma2(half2, pack2(w4.x, w4.y), y2[2 * c]);
+          const unsigned long long db = ffma2(half2, pack2(w4.z, w4.w), y2[2 * c + 1]);
+          v2 = ffma2(da, da, v2);
+          v2 = ffma2(db, db, v2);
+        } else {
+          v2 = ffma2(pack2(w4.x, w4.y), y2[2 * c], v2);
+          v2 = ffma2(pack2(w4.z, w4.w), y2[2 * c + 1], v2);
+        }
       }
       float va, vb;
       unpack2(v2, va, vb);
-      const float v = __fadd_rn(va, vb);
+      float v = __fadd_rn(va, vb);
+#pragma unroll
+      for (int o = 1; o < T; o <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
       const float n2 = fminf(m2, fmaxf(m1, v));
       const bool pr = v < m1;
       m1 = fminf(m1, v);
       i1 = pr ? j : i1;
       m2 = n2;
     }
-    // certification: assign_chunk's band (FMA chain of L terms + norm)
+    // certification: assign_chunk's bands (expanded / difference form)
     bool ok = false;
     float thr = NAN;
     if (valid) {
       const float yn = sqrtf(q);
-      const float d2 = fmaxf(m2 + q, 0.f);
+      const float d2 = fmaxf(DIFF ? m2 : m2 + q, 0.f);
       const float sd = sqrtf(d2) * 1.01f + 1.0f;
       const float S = 2.02f * yn + sd;
       const float E = (float)(L + 3) * u * S * S + 2.5f * u * sd * S + 1e-14f * S * S;
-      const float band = 3.0f * E + input_band(rin_of(a, row), m1 + q, 3.0f * E);
-      ok = (m2 - m1) > band;
-      thr = m1 + band;
+      if constexpr (DIFF) {
+        const float Ed = (float)(L + 3) * u * sd * sd + 4.1f * u * sd * (yn + sd) + 1e-14f * S * S;
+        const float bandd = 3.0f * Ed + input_band(rin_of(a, row), m1, 3.0f * Ed);
+        ok = (m2 - m1) > bandd;
+        const float bande = 3.0f * E + input_band(rin_of(a, row), m1, 3.0f * E);
+        thr = (m1 - q) + bande + bandd + (float)(L + 8) * u * (q + fabsf(m1));
+      } else {
+        const float band = 3.0f * E + input_band(rin_of(a, row), m1 + q, 3.0f * E);
+        ok = (m2 - m1) > band;
+        thr = m1 + band;
+      }
       a.idx[row] = i1;
       if (ok && a.dists) {
         double d = 0.0;
         if (regs_exact) {
-          // the reference's arithmetic (_kernels.py:25-29) on the registers' row
+          // the reference's arithmetic (_kernels.py:25-29) on the staged row
           const double2* c2 = reinterpret_cast<const double2*>(sm.cb + i1 * CS);
-#pragma unroll
+#pragma unroll 4
           for (int c = 0; c < CH; ++c) {
-            const float4 xv = *reinterpret_cast<const float4*>(xrow + c * 4);
+            const float4 xv = *reinterpret_cast<const float4*>(xaddr(buf, rloc, c));
             const double2 ca = c2[2 * c], cb2 = c2[2 * c + 1];
             const double d0 = __dsub_rn((double)xv.x, ca.x);
             d = __dadd_rn(d, __dmul_rn(d0, d0));
             const double d1 = __dsub_rn((double)xv.y, ca.y);
             d = __dadd_rn(d, __dmul_rn(d1, d1));
-            const double d2 = __dsub_rn((double)xv.z, cb2.x);
-            d = __dadd_rn(d, __dmul_rn(d2, d2));
+            const double d2v = __dsub_rn((double)xv.z, cb2.x);
+            d = __dadd_rn(d, __dmul_rn(d2v, d2v));
             const double d3 = __dsub_rn((double)xv.w, cb2.y);
             d = __dadd_rn(d, __dmul_rn(d3, d3));
           }
@@ -723,7 +824,7 @@ static cudaError_t launch_small_L(const KernelArgs& a, int sms, cudaStream_t s) 
   if (e != cudaSuccess) return e;
   const long long n = a.r1 - a.r0;
   long long grid = (long long)sms * (L == 16 ? kSmallMinB : 2);
-  const long long tiles = (n + kSmallNT - 1) / kSmallNT;
+  const long long tiles = (n + SmallSmem<L>::RT - 1) / SmallSmem<L>::RT;
   if (grid > tiles) grid = tiles > 0 ? tiles : 1;
   return launch_k(assign_small_kernel<L>, (unsigned)grid, kSmallNT, smem, s, a);
 }
@@ -1255,7 +1356,7 @@ cudaError_t launch_assign(const KernelArgs& a, bool fast, int sms, cudaStream_t 
       default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
-    if (a.small_on && a.cdim == 16) {
+    if (a.small_on && small_dim(a.cdim)) {
       e = launch_small_L<16>(a, sms, s);
       if (e != cudaSuccess) return e;
     }

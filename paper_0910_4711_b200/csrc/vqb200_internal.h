@@ -204,6 +204,7 @@ struct KernelArgs {
   long long mv_cap;
   long long* acc;
   long long delta_max;
+  int diff_on;          // FFMA pass at L >= 32, K < 64: difference-form candidate values (VQB_DIFF=0: expanded)
   int small_on;         // candidate pass: assign_small_kernel takes K < 64 (VQB_SMALL=0: assign_fast_kernel does)
   DevState* st;
 };
