@@ -546,3 +546,64 @@ def test_incremental_sums_after_other_calls_on_the_session():
     _same_design(a, c)
     want = oracle.lbg_train(x.astype(np.float64), 8, epsilon=1e-3, delta=0.01, workers=oracle.max_threads())
     assert np.asarray(b[0]).tobytes() == want.codebook.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# small codebooks (K < 64): assign_small_kernel at W = 16 (rows staged through
+# shared memory) and the difference-form values at W = 32 / 64.  Indices and
+# per-row distances must stay the oracle's bit for bit on data built to sit on
+# the band's edges.  Reference: _kernels.assign_range (_kernels.py:18-36).
+# ---------------------------------------------------------------------------
+
+import functools
+
+
+@functools.lru_cache(maxsize=1)
+def _small_k_cases():
+    rng = np.random.default_rng(77)
+    out = []
+    for dim in (16, 32, 64, 11, 48):
+        n = 20011
+        # image-like rows: a large mean per row, a small texture on top
+        base = rng.integers(20, 236, (n, 1)).astype(np.float64)
+        x = np.clip(base + rng.normal(0, 3.0, (n, dim)), 0, 255).round().astype(np.float32)
+        for k in (2, 7, 33, 63):
+            cb = x[rng.choice(n, k, replace=False)].astype(np.float64)
+            cb[k // 2] = cb[0]                     # an exact duplicate: lowest index must win
+            cb[-1] = cb[1] + 1e-9                  # a near-duplicate far inside any FP32 band
+            out.append((f"blocks_d{dim}_k{k}", x, cb))
+        # rows exactly on codevectors (zero distances) and exact two-way ties
+        cb = np.zeros((4, dim))
+        cb[1, 0], cb[2, 0], cb[3, 1] = 2.0, -2.0, 2.0
+        t = rng.integers(-3, 4, (4099, dim)).astype(np.float32) * 0
+        t[:, 0] = rng.integers(-3, 4, 4099)
+        t[:, 1] = rng.integers(-3, 4, 4099)
+        out.append((f"ties_d{dim}", t, cb))
+        # a common offset of 1e5 and magnitudes of 1e-3
+        out.append((f"offset_d{dim}", (x + 1e5).astype(np.float32), x[:37].astype(np.float64) + 1e5 + 0.25))
+        out.append((f"tiny_d{dim}", (x * 1e-5).astype(np.float32), x[:21].astype(np.float64) * 1e-5))
+    return out
+
+
+@pytest.mark.parametrize("i", range(35))  # 5 widths x (4 codebook sizes + ties + offset + tiny)
+def test_small_codebook_paths_vs_oracle(i):
+    from paper_0910_4711_b200.core import _session_of, _matrix_keep_f32
+    name, x, cb = _small_k_cases()[i]
+    cells, dists = oracle.assign_all(x.astype(np.float64), cb, workers=oracle.max_threads())
+    got_cells, got_d, total = _session_of(_matrix_keep_f32(x)).assign(cb, 0)
+    assert np.array_equal(got_cells, cells), name
+    assert got_d.tobytes() == dists.tobytes(), name
+
+
+def test_small_codebook_float64_rows_vs_oracle():
+    """float64 rows float32 cannot hold (the candidate rows are rounded copies,
+    the winner distance reads the float64 rows) through both small-K paths."""
+    from paper_0910_4711_b200.core import _Session
+    rng = np.random.default_rng(78)
+    for dim, k in ((16, 9), (64, 31), (5, 40)):
+        x = rng.normal(100.0, 30.0, (30011, dim)) + rng.normal(0, 1e-7, (30011, dim))
+        cb = x[rng.choice(30011, k, replace=False)] + 0.125
+        cells, dists = oracle.assign_all(x, cb, workers=oracle.max_threads())
+        got_cells, got_d, _ = _Session(None, x).assign(cb, 0)
+        assert np.array_equal(got_cells, cells), (dim, k)
+        assert got_d.tobytes() == dists.tobytes(), (dim, k)
