@@ -742,8 +742,19 @@ __global__ void __launch_bounds__(TcCfg<L>::threads(MODE), 1) assign_tc_kernel(K
           auto scan32 = [&](const float (&v)[32], int q4) {
 #pragma unroll
             for (int t = 0; t < 16; ++t) ach[t] = fminf(fminf(v[t], v[t + 16]), ach[t]);
-            fold(min16(v), jb0 + q4 * 32);
-            fold(min16(v + 16), jb0 + q4 * 32 + 16);
+            // both block minima in one step: the pair sorted (lo <= hi), then
+            // the two smallest of {b1, b2, lo, hi} = min(b1, lo) and
+            // min3(b2, hi, max(b1, lo)) -- one half-rate FMNMX less than two
+            // single folds; the first block at the minimum keeps its index
+            // (lo < b1 strictly, and block 0 on mu0 == mu1)
+            const float mu0 = min16(v), mu1 = min16(v + 16);
+            const int jb = jb0 + q4 * 32;
+            const float lo = fminf(mu0, mu1), hi = fmaxf(mu0, mu1);
+            const int jlo = mu1 < mu0 ? jb + 16 : jb;
+            const bool lt = lo < b1;
+            b2 = fminf(fminf(b2, hi), fmaxf(b1, lo));
+            b1 = fminf(b1, lo);
+            blk = lt ? jlo : blk;
           };
           if (span >= 32) {
             if (pipe_ld<L>() && span >= 64) {
