@@ -162,7 +162,12 @@ struct TcMisc {
 template <int L>
 __device__ __forceinline__ float tc_band(float m1v, float q, float yn, float eyw) {
   constexpr float u = 5.9604645e-8f;
-  constexpr float cacc = (float)(2 * (3 * L / 16 + 1) + 4) * 2.3841858e-7f + 1e-14f;
+  // accumulation term per MMA in units of 2^-22 (A/B builds only: the measured
+  // worst on band-edge operands is 0.29 of the default 2)
+#ifndef VQB_TC_ACC_TERM
+#define VQB_TC_ACC_TERM 2
+#endif
+  constexpr float cacc = (float)(VQB_TC_ACC_TERM * (3 * L / 16 + 1) + 4) * 2.3841858e-7f + 1e-14f;
   const float d1 = fmaxf(m1v + fmaxf(q, 0.f), 0.f);
   auto poly = [&](float sd) {
     const float S = fmaf(2.02f, yn, sd);
